@@ -1,0 +1,464 @@
+"""Benchmark: TSDF voxel-updates/s and frames/s of the multi-volume mapper.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], the configuration the metric is quoted
+on "at 1/2/4/8 B200"): 8 fixed 512^3 volumes tiling a 4.08 m cube at 4 mm
+(init_grid(4.08, 1020, 510)), 640x480 frames of the demo scene (sphere +
+floor + box) along orbit_trajectory((0,0,1.5), 1.5, 64), ground-truth poses.
+One step = one frame through the hot path: fused integration of every
+volume + fused raycast of every volume (+ all-gather / _hit_wins merge of
+the partial ray maps across ranks when N > 1).  With N GPUs the 8 volumes
+are owned round-robin by the ranks (total work fixed -> "strong").
+
+value  = voxel updates per frame x frames/s, inputs resident in HBM, CUDA
+         events on the launching stream, L2 flushed (256 MiB write) between
+         timed steps, max over ranks.
+e2e    = the same through the public FusionPipeline.step API with the frame
+         read from pinned host memory each step (H2D inside the timed region)
+         and the step's counters read back (D2H).
+config2 (secondary): BASELINE configs[1] — one 256^3 volume with ICP
+         tracking on (integrate + raycast + projective ICP per frame).
+
+--impl reference times the reference algorithm on the host CPU (the C
+restatement in oracle/, all host threads) on the same workload and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "TSDF voxel-updates/sec and frames/sec at 1/2/4/8 B200; % HBM roofline"
+BYTES_PER_UPDATE = 16  # read + write of f32 tsdf and f32 weight
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-config2", action="store_true")
+    p.add_argument("--frames", type=int, default=64, help="distinct frames cycled through")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+
+def workload(nframes: int):
+    import paper_1511_07106_b200 as tf
+    from paper_1511_07106_b200.synth import demo_scene
+
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(4.08, 1020, 510)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)[:nframes]
+    scene = demo_scene()
+    return intr, spec, params, poses, scene
+
+
+def config_desc(n_gpus: int) -> dict:
+    return {"workload": "configs[2]: 8 fixed 512^3 TSDF volumes at 4 mm (init_grid(4.08, 1020, "
+                        "510)), 640x480 demo-scene orbit frames, ground-truth poses; step = "
+                        "integrate + raycast of every volume",
+            "volumes": 8, "voxels_per_side": 512, "voxel_size_m": 0.004, "image": "640x480",
+            "ownership": f"round-robin over {n_gpus} rank(s)",
+            "l2": "flushed between timed steps (256 MiB write); volumes 8.6 GB > L2"}
+
+
+def peak_hbm() -> tuple[float, str]:
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        try:
+            return float(json.loads(f.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int) -> None:
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self._t.join(timeout=2)
+
+    def summary(self) -> dict | None:
+        rows = []
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) == 6:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[2:]))
+                except ValueError:
+                    pass
+        if not rows:
+            return None
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        active = sorted({names[i] for _, _, flags in rows for i, f in enumerate(flags)
+                         if f.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(r[0] for r in rows),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": active, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1511_07106_b200 as tf
+    from paper_1511_07106_b200 import _native as nat
+    from paper_1511_07106_b200.distributed import ShardedFusion, broadcast_frame
+
+    lib = nat.load_library()
+    intr, spec, params, poses, scene = workload(args.frames)
+    nframes = len(poses)
+    host_frames = [scene.render_depth(p, intr).data for p in poses]
+    dev_frames = torch.stack([torch.from_numpy(f) for f in host_frames]).cuda()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: int) -> int:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return int(t.item())
+
+    shard = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length, params,
+                          intr, rank, world)
+
+    # ---- warm-up (also the per-frame work cycle starts here) ----
+    for i in range(args.warmup):
+        shard.step(dev_frames[i % nframes], poses[i % nframes])
+    barrier()
+
+    # ---- timed region: resident inputs, per-step events, L2 flushed between ----
+    shard.stats.zero_()
+    nat.profile_read()  # drop warm-up records
+    lib.tf_profile_enable(1)
+    launches0 = lib.tf_launch_count()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        barrier()
+        for s in range(args.steps):
+            flush.zero_()
+            i = (args.warmup + s) % nframes
+            starts[s].record()
+            shard.step(dev_frames[i], poses[i])
+            stops[s].record()
+        barrier()
+    lib.tf_profile_enable(0)
+    launches = lib.tf_launch_count() - launches0
+    ms_total = sum(a.elapsed_time(b) for a, b in zip(starts, stops))
+    prof = nat.profile_read()
+    st = shard.stats.cpu().numpy()
+    updates_local = int(st[nat.STAT_VOXEL_UPDATES])
+    ms_total = max_over_ranks(ms_total)
+    updates = sum_over_ranks(updates_local)
+    samples = sum_over_ranks(int(st[nat.STAT_RAY_SAMPLES]))
+    ms_per_step = ms_total / args.steps
+    fps = 1000.0 / ms_per_step
+    updates_per_frame = updates / args.steps
+    value = updates_per_frame * fps
+
+    # roofline of the dominant kernel (the voxel-update kernel), this rank
+    upd_ms, upd_launches = prof["integrate_update"]
+    int_ms, _ = prof["integrate_all"]
+    ray_ms, ray_launches = prof["raycast"]
+    peak, peak_src = peak_hbm()
+    achieved = (BYTES_PER_UPDATE * updates_local / max(upd_launches, 1)) / (
+        upd_ms / max(upd_launches, 1) / 1e3) / 1e9 if upd_ms > 0 else 0.0
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic_r01.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get("brick_update_kernel_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    result = {
+        "metric": METRIC, "value": value, "unit": "voxel-updates/s",
+        "frames_per_s": fps, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_desc(world),
+        "voxel_updates_per_frame": updates_per_frame,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "kernel": "brick_update_kernel", "peak_source": peak_src,
+                     "bytes_per_update": BYTES_PER_UPDATE,
+                     "launches": upd_launches, "kernel_ms_per_launch": upd_ms / max(upd_launches, 1),
+                     "updates_per_launch": updates_local / max(upd_launches, 1)},
+        "breakdown_ms_per_step": {"integrate_update_kernel": upd_ms / args.steps,
+                                  "integrate_total": int_ms / args.steps,
+                                  "raycast": ray_ms / args.steps},
+        "raycast": {"samples_per_frame": samples / args.steps,
+                    "samples_per_s": samples / (ms_total / 1e3)},
+        "gpu_launches": int(launches),
+    }
+    cs = clocks.summary()
+    result["clocks"] = cs
+
+    # ---- e2e through the public pipeline API, frames from pinned host memory ----
+    if not args.no_e2e:
+        result["e2e"] = run_e2e(args, tf, nat, torch, dist, rank, world, intr, spec, params,
+                                poses, host_frames, barrier, max_over_ranks, sum_over_ranks)
+    del shard, dev_frames
+    torch.cuda.empty_cache()
+
+    if not args.no_config2:
+        result["config2"] = run_config2(args, tf, nat, torch, barrier, max_over_ranks)
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(intr, spec, params, poses, host_frames)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, tf, nat, torch, dist, rank, world, intr, spec, params, poses, host_frames,
+            barrier, max_over_ranks, sum_over_ranks) -> dict:
+    from paper_1511_07106_b200.distributed import ShardedFusion, broadcast_frame
+
+    nframes = len(poses)
+    pinned = [torch.from_numpy(f).pin_memory() for f in host_frames]
+    steps = min(args.steps, 50)
+    if world == 1:
+        cfg = tf.RunConfig(side_length=4.08, resolution=1020, resident_resolution=510,
+                           use_groundtruth=True, max_resident=8)
+        spill = tempfile.mkdtemp(prefix="tfb200_spill_")
+        pipe = tf.FusionPipeline(cfg, spill)
+
+        def step(i):
+            pipe.step(pinned[i], poses[i])          # public API: H2D inside step()
+            return pipe.stats.cpu()                 # D2H of the step's counters
+    else:
+        shard = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length,
+                              params, intr, rank, world)
+        buf = torch.empty(host_frames[0].shape, dtype=torch.float64, device="cuda")
+
+        def step(i):
+            if rank == 0:
+                buf.copy_(pinned[i], non_blocking=True)
+            broadcast_frame(buf)
+            shard.step(buf, poses[i])
+            return shard.stats.cpu()
+
+    for i in range(args.warmup):
+        out = step(i % nframes)
+    barrier()
+    before = int(out[nat.STAT_VOXEL_UPDATES])
+    t0 = time.perf_counter()
+    for s in range(steps):
+        out = step((args.warmup + s) % nframes)
+    barrier()
+    sec = max_over_ranks(time.perf_counter() - t0)
+    updates = sum_over_ranks(int(out[nat.STAT_VOXEL_UPDATES]) - before)
+    return {"value": updates / sec, "unit": "voxel-updates/s", "frames_per_s": steps / sec,
+            "h2d_bytes_per_step": int(host_frames[0].nbytes) if rank == 0 else 0,
+            "d2h_bytes_per_step": 64, "steps": steps,
+            "path": "FusionPipeline.step(pinned host frame)" if world == 1 else
+                    "rank-0 H2D + NCCL broadcast + ShardedFusion.step"}
+
+
+def run_config2(args, tf, nat, torch, barrier, max_over_ranks) -> dict:
+    """BASELINE configs[1]: one 256^3 volume, ICP tracking on, 1.5-degree orbit."""
+    from paper_1511_07106_b200.synth import demo_scene
+
+    cfg = tf.RunConfig(side_length=3.0, resolution=254, resident_resolution=254,
+                       use_groundtruth=False)
+    intr = cfg.intrinsics()
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 240)[:64]
+    scene = demo_scene()
+    steps = min(args.steps, 63)
+    frames = [torch.from_numpy(scene.render_depth(p, intr).data).cuda() for p in poses[:steps + 1]]
+    pipe = tf.FusionPipeline(cfg, tempfile.mkdtemp(prefix="tfb200_c2_"))
+    pipe.step(frames[0], poses[0])   # frame 0 defines the world frame (warm-up)
+    barrier()
+    pipe.stats.zero_()
+    t0 = time.perf_counter()
+    for i in range(1, steps + 1):
+        pipe.step(frames[i])
+    barrier()
+    sec = max_over_ranks(time.perf_counter() - t0)
+    ks = pipe.kernel_stats()
+    lost = sum(1 for r in pipe.records[1:] if not r.tracked)
+    err = max(float(np.abs(p.translation - q.translation).max())
+              for p, q in zip(pipe.poses, poses[:steps + 1]))
+    return {"workload": "configs[1]: one 256^3 volume (init_grid(3.0, 254, 254)), 640x480, "
+                        "1.5-degree orbit, ICP tracking on", "frames": steps,
+            "frames_per_s": steps / sec, "voxel_updates_per_s": ks["voxel_updates"] / sec,
+            "lost_frames": lost, "max_translation_error_m": err}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle restatement of the reference kernels, all host threads)
+# ---------------------------------------------------------------------------
+
+def cpu_frame_sample(intr, spec, params, poses, host_frames, volumes: int, threads: int) -> dict:
+    import oracle
+
+    n = spec.voxels_per_side
+    vs = spec.voxel_size
+    coarse = max(2, int(round(0.5 * params.truncation / vs)))
+    keys = spec.keys[:volumes]
+    tiles = [(np.zeros((n, n, n), np.float32), np.zeros((n, n, n), np.float32)) for _ in keys]
+    p0, p1 = poses[0], poses[1]
+    for (t, w), k in zip(tiles, keys):
+        inv = p0.invert()
+        oracle.integrate(t, w, k, vs, host_frames[0], inv.rotation, inv.translation,
+                         p0.translation, intr.fx, intr.fy, intr.cx, intr.cy, params.truncation,
+                         params.max_weight, params.sample_weight, threads=threads)
+    inv = p1.invert()
+    t0 = time.perf_counter()
+    updates = 0
+    for (t, w), k in zip(tiles, keys):
+        updates += oracle.integrate(t, w, k, vs, host_frames[1], inv.rotation, inv.translation,
+                                    p1.translation, intr.fx, intr.fy, intr.cx, intr.cy,
+                                    params.truncation, params.max_weight, params.sample_weight,
+                                    threads=threads)
+    t_int = time.perf_counter() - t0
+    d = np.full((intr.height, intr.width), np.inf)
+    v = np.zeros((intr.height, intr.width, 3))
+    nn = np.zeros_like(v)
+    t0 = time.perf_counter()
+    for (t, w), k in zip(tiles, keys):
+        oracle.raycast(t, w, k, vs, params.truncation, coarse, p1.rotation, p1.translation,
+                       intr.fx, intr.fy, intr.cx, intr.cy, d, v, nn, threads=threads)
+    t_ray = time.perf_counter() - t0
+    return {"updates": updates, "t_integrate": t_int, "t_raycast": t_ray, "volumes": volumes}
+
+
+def cpu_baseline(intr, spec, params, poses, host_frames) -> dict:
+    import oracle
+
+    threads = oracle.default_threads()
+    vols = 8 if threads >= 16 else 2
+    s = cpu_frame_sample(intr, spec, params, poses, host_frames, vols, threads)
+    frame_s = (s["t_integrate"] + s["t_raycast"]) * 8 / vols
+    updates_frame = s["updates"] * 8 / vols
+    return {"value": updates_frame / frame_s, "unit": "voxel-updates/s", "cores": threads,
+            "kind": "port", "frames_per_s": 1.0 / frame_s,
+            "sample": f"frame 1 of the same workload, {vols} of 8 volumes (integrate + raycast, "
+                      f"C oracle on {threads} host threads), scaled to 8 volumes",
+            "integrate_s_per_volume": s["t_integrate"] / vols,
+            "raycast_s_per_volume": s["t_raycast"] / vols}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # the CPU reference runs once, on rank 0
+    import oracle
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    threads = oracle.default_threads()
+    intr, spec, params, poses, scene = workload(2)
+    host_frames = [scene.render_depth(p, intr).data for p in poses]
+    vols = 8 if threads >= 32 else (4 if threads >= 8 else 1)
+    steps, warmup = max(1, min(args.steps, 5)), min(args.warmup, 1)
+    for _ in range(warmup):
+        cpu_frame_sample(intr, spec, params, poses, host_frames, vols, threads)
+    times, ups = [], []
+    for _ in range(steps):
+        s = cpu_frame_sample(intr, spec, params, poses, host_frames, vols, threads)
+        times.append((s["t_integrate"] + s["t_raycast"]) * 8 / vols)
+        ups.append(s["updates"] * 8 / vols)
+    frame_s = sum(times) / len(times)
+    value = (sum(ups) / len(ups)) / frame_s
+    sample = (f"per step: frame 1 of the workload on {vols} of 8 volumes (integrate + raycast), "
+              f"C restatement of the reference kernels on {threads} host threads, scaled to 8")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "voxel-updates/s",
+        "frames_per_s": 1.0 / frame_s, "n_gpus": world, "steps": steps, "warmup": warmup,
+        "ms_per_step": frame_s * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_desc(world),
+        "cpu_baseline": {"value": value, "unit": "voxel-updates/s", "cores": threads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "voxel-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def main() -> None:
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,170 @@
+/*
+ * tfb200 — C ABI of the B200-native tilefusion hot path (libtfb200.so).
+ *
+ * Each entry point replaces one operator of the reference package
+ * (/root/reference/pkg/src/tilefusion, cited file:line) and is what a
+ * ctypes / cffi binding of that operator binds (INTEGRATION.md shows the
+ * stubs).  Conventions:
+ *
+ *   - every pointer named *_dev is caller-owned device memory on the current
+ *     device (PyTorch tensors' data_ptr()); small matrices / vectors
+ *     (r_*[9], t_*[3]) and descriptors are HOST memory read during the call;
+ *   - calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and never synchronise the device, allocate, or copy
+ *     device->host; scratch comes from a caller workspace sized by the
+ *     matching *_workspace_size() call;
+ *   - the return value is 0 on success, a negative TF_E* code otherwise, with
+ *     a message available from tf_last_error() (thread-local).  No C++
+ *     exception crosses the ABI;
+ *   - voxels are AoS float2 (tsdf, weight) [n][n][n] with x fastest — the
+ *     interleaved body of the reference spill format (volumes.py:43-66), so a
+ *     spill is one raw copy;
+ *   - results are bit-identical to the reference kernels: the exact paths use
+ *     IEEE round-to-nearest FP64 ops in the reference's evaluation order with
+ *     no contraction, and float32 where numba types the reference's
+ *     arithmetic as float32.
+ */
+#ifndef TFB200_H
+#define TFB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TFB200_ABI_VERSION 1
+#define TFB200_MAX_VOLUMES_PER_LAUNCH 64
+
+enum {
+    TF_OK = 0,
+    TF_EINVAL = -1,  /* bad argument (sizes, null pointers, workspace too small) */
+    TF_ECUDA = -2,   /* CUDA launch / runtime error */
+};
+
+/* One TSDF subvolume resident on the device (tsdf.py:41-107). */
+typedef struct TfVolume {
+    void *voxels_dev;    /* float2[n][n][n]: (tsdf, weight), x fastest */
+    int64_t n;           /* voxels_per_side */
+    int64_t origin[3];   /* origin_voxel: global voxel of local (0,0,0) */
+    double voxel_size;   /* side_length / voxels_per_side (tsdf.py:80-82) */
+} TfVolume;
+
+/* Pinhole intrinsics of one pyramid level (geometry.py:27-57). */
+typedef struct TfCamera {
+    double fx, fy, cx, cy;
+    int64_t width, height;
+} TfCamera;
+
+/* Per-call counters written (accumulated) to a device uint64[8]. */
+enum {
+    TF_STAT_VOXEL_UPDATES = 0, /* voxels passing every integration gate */
+    TF_STAT_SWEPT_VOXELS = 1,  /* voxels evaluated after brick culling */
+    TF_STAT_ACTIVE_BRICKS = 2,
+    TF_STAT_TOTAL_BRICKS = 3,
+    TF_STAT_RAY_SAMPLES = 4,   /* trilinear _sample calls (_kernels.py:28) */
+    TF_STAT_RAY_HITS = 5,      /* hits merged by this raycast call */
+    TF_STAT_COUNT = 8
+};
+
+int tf_abi_version(void);
+const char *tf_last_error(void);
+
+/* Measurement hooks.  tf_launch_count: kernels launched by this library so
+ * far.  With tf_profile_enable(1), each tf_integrate / tf_raycast brackets its
+ * kernels with CUDA events on the caller's stream; tf_profile_read waits for
+ * them and returns summed milliseconds and launch counts per kind:
+ * 0 = integration voxel-update kernel, 1 = whole tf_integrate, 2 = raycast. */
+enum { TF_PROF_INTEGRATE_UPDATE = 0, TF_PROF_INTEGRATE_ALL = 1, TF_PROF_RAYCAST = 2,
+       TF_PROF_KINDS = 3 };
+uint64_t tf_launch_count(void);
+void tf_profile_enable(int on);
+int tf_profile_read(double *ms_by_kind, int64_t *launches_by_kind, int nkinds);
+
+/* Test hook: TF_DEBUG_NO_CULL makes tf_integrate sweep every brick, so tests
+ * can prove culling never drops an update (bitwise equality at full size). */
+enum { TF_DEBUG_NO_CULL = 1u };
+void tf_set_debug_flags(uint32_t flags);
+uint32_t tf_debug_flags(void);
+
+/* ---- integration: replaces _kernels.integrate_kernel (_kernels.py:71-133),
+ * called by tsdf.integrate (tsdf.py:110-144), fused over `nvol` volumes.
+ * r_cw / t_cw: Pose.invert() of the camera pose, cam_center its translation
+ * (tsdf.py:126-135). `depth_dev`: f64 [height][width] z-depth, 0 = invalid.
+ * stats_dev may be NULL. */
+size_t tf_integrate_workspace_size(const TfVolume *vols, int nvol, const TfCamera *cam);
+int tf_integrate(const TfVolume *vols, int nvol, const double *depth_dev,
+                 const TfCamera *cam, const double r_cw[9], const double t_cw[3],
+                 const double cam_center[3], double tau, double max_weight,
+                 double sample_weight, void *workspace_dev, size_t workspace_bytes,
+                 uint64_t *stats_dev, void *stream);
+
+/* ---- raycast: replaces _kernels.raycast_kernel (_kernels.py:266-451) with
+ * its helpers _sample / _scan_crossing / _hit_wins, called by tsdf.raycast
+ * (tsdf.py:193-225), fused over `nvol` volumes sharing one voxel size.
+ * Merges into existing maps with the _hit_wins total order, exactly like
+ * calling the reference once per volume in any order.
+ * dist_dev f64 [H][W] (+inf = none), vert_dev / norm_dev f64 [H][W][3]. */
+int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
+               int64_t coarse_step, const double r_wc[9], const double cam_center[3],
+               double *dist_dev, double *vert_dev, double *norm_dev,
+               uint64_t *stats_dev, void *stream);
+
+/* ---- trilinear_sample (tsdf.py:147-153 / _kernels._sample :28-68) for
+ * `npoints` world points (f64 [N][3]); writes value and validity per point. */
+int tf_trilinear_sample(const TfVolume *vol, const double *points_dev, int64_t npoints,
+                        double *values_dev, uint8_t *valid_dev, void *stream);
+
+/* ---- raymap merge: _hit_wins (_kernels.py:246-263) of a partial map into
+ * `dst` (the cross-GPU reduction of DESIGN.md "Multi-GPU"). */
+int tf_raymap_merge(double *dst_dist_dev, double *dst_vert_dev, double *dst_norm_dev,
+                    const double *src_dist_dev, const double *src_vert_dev,
+                    const double *src_norm_dev, int64_t npixels, void *stream);
+
+/* ---- ICP source maps: geometry.depth_to_vertices + compute_normals
+ * (geometry.py:261-302) of pyramid level `level` (stride 2^level subsampling of
+ * the full-resolution depth, geometry.py:256-258), with that level's camera.
+ * Outputs are dense level-sized arrays; valid = vertex_ok & normal_ok. */
+int tf_vertex_normal_map(const double *depth_dev, int64_t full_width, int64_t full_height,
+                         int level, const TfCamera *level_cam, double *verts_dev,
+                         double *norms_dev, uint8_t *valid_dev, void *stream);
+
+/* ---- ICP normal equations: the per-pixel part of tracking._solve_step
+ * (tracking.py:76-108) with a deterministic FP64 tree reduction.  The model
+ * maps are the full-resolution RayMap viewed at stride 2^level
+ * (RayMap.downsampled, tsdf.py:185-190).  out29_dev (device, 29 doubles):
+ * upper triangle of A^T A (21, row major), A^T r (6), sum r^2, count. */
+size_t tf_icp_workspace_size(int64_t src_pixels);
+int tf_icp_reduce(const double *src_verts_dev, const double *src_norms_dev,
+                  const uint8_t *src_valid_dev, int64_t src_width, int64_t src_height,
+                  const double *mdl_dist_dev, const double *mdl_vert_dev,
+                  const double *mdl_norm_dev, int64_t mdl_full_width,
+                  int64_t mdl_full_height, int level, const TfCamera *level_cam,
+                  const double r_est[9], const double t_est[3], const double r_ref[9],
+                  const double t_ref[3], double max_dist_sq, double cos_min,
+                  void *workspace_dev, size_t workspace_bytes, double *out29_dev,
+                  void *stream);
+
+/* ---- extraction: _kernels.extract_bound / extract_kernel
+ * (_kernels.py:454-578), called by tsdf.extract_points (tsdf.py:261-280).
+ * Two calls: tf_extract_count writes the vertex count (device int64) after an
+ * order-preserving scan kept in the workspace; tf_extract_emit then writes
+ * the vertices in the reference's (z, y, x) voxel order. */
+size_t tf_extract_workspace_size(int64_t n);
+int tf_extract_count(const TfVolume *vol, void *workspace_dev, size_t workspace_bytes,
+                     int64_t *count_dev, void *stream);
+int tf_extract_emit(const TfVolume *vol, const void *workspace_dev, size_t workspace_bytes,
+                    double *verts_dev, double *norms_dev, void *stream);
+
+/* ---- endpoint cells: volumes.bin_endpoints (volumes.py:305-331): per valid
+ * pixel the tile-lattice cell of its endpoint, as int64 [H*W][3] with
+ * cells of invalid pixels set to INT64_MIN. */
+int tf_endpoint_cells(const double *depth_dev, const TfCamera *cam, const double r_wc[9],
+                      const double t_wc[3], double block_side, int64_t *cells_dev,
+                      void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TFB200_H */

@@ -1,0 +1,209 @@
+"""ctypes binding of libtfb200.so (include/tfb200.h) and device plumbing.
+
+There is no fallback: if the library or a CUDA device is missing, every
+entry point raises.  PyTorch supplies device memory, the current stream and
+the device index only; all arithmetic of the hot path runs in libtfb200.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+import torch
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libtfb200.so"
+ABI_VERSION = 1
+
+_c_d = ctypes.c_double
+_c_i64 = ctypes.c_int64
+_c_int = ctypes.c_int
+_c_p = ctypes.c_void_p
+_c_sz = ctypes.c_size_t
+
+
+class TfVolume(ctypes.Structure):
+    _fields_ = [("voxels_dev", _c_p), ("n", _c_i64), ("origin", _c_i64 * 3),
+                ("voxel_size", _c_d)]
+
+
+class TfCamera(ctypes.Structure):
+    _fields_ = [("fx", _c_d), ("fy", _c_d), ("cx", _c_d), ("cy", _c_d), ("width", _c_i64),
+                ("height", _c_i64)]
+
+
+DEBUG_NO_CULL = 1
+PROF_INTEGRATE_UPDATE, PROF_INTEGRATE_ALL, PROF_RAYCAST, PROF_KINDS = 0, 1, 2, 3
+
+
+def profile_read() -> dict:
+    """Summed device ms / launches per profiled kind since the last read."""
+    ms = (ctypes.c_double * PROF_KINDS)()
+    cnt = (ctypes.c_int64 * PROF_KINDS)()
+    check(lib().tf_profile_read(ms, cnt, PROF_KINDS), "tf_profile_read")
+    names = ("integrate_update", "integrate_all", "raycast")
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(names)}
+
+# TF_STAT_* slots (tfb200.h)
+STAT_VOXEL_UPDATES, STAT_SWEPT_VOXELS, STAT_ACTIVE_BRICKS, STAT_TOTAL_BRICKS = 0, 1, 2, 3
+STAT_RAY_SAMPLES, STAT_RAY_HITS = 4, 5
+STAT_COUNT = 8
+
+_SIGNATURES = {
+    "tf_abi_version": (_c_int, []),
+    "tf_last_error": (ctypes.c_char_p, []),
+    "tf_set_debug_flags": (None, [ctypes.c_uint32]),
+    "tf_launch_count": (ctypes.c_uint64, []),
+    "tf_profile_enable": (None, [_c_int]),
+    "tf_profile_read": (_c_int, [_c_p, _c_p, _c_int]),
+    "tf_debug_flags": (ctypes.c_uint32, []),
+    "tf_integrate_workspace_size": (_c_sz, [_c_p, _c_int, _c_p]),
+    "tf_integrate": (_c_int, [_c_p, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_d, _c_d, _c_d,
+                              _c_p, _c_sz, _c_p, _c_p]),
+    "tf_raycast": (_c_int, [_c_p, _c_int, _c_p, _c_d, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
+                            _c_p, _c_p]),
+    "tf_trilinear_sample": (_c_int, [_c_p, _c_p, _c_i64, _c_p, _c_p, _c_p]),
+    "tf_raymap_merge": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p]),
+    "tf_vertex_normal_map": (_c_int, [_c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p,
+                                      _c_p]),
+    "tf_icp_workspace_size": (_c_sz, [_c_i64]),
+    "tf_icp_reduce": (_c_int, [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_i64,
+                               _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_d, _c_d, _c_p,
+                               _c_sz, _c_p, _c_p]),
+    "tf_extract_workspace_size": (_c_sz, [_c_i64]),
+    "tf_extract_count": (_c_int, [_c_p, _c_p, _c_sz, _c_p, _c_p]),
+    "tf_extract_emit": (_c_int, [_c_p, _c_p, _c_sz, _c_p, _c_p, _c_p]),
+    "tf_endpoint_cells": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_d, _c_p, _c_p]),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: Path | str | None = None) -> ctypes.CDLL:
+    """Load libtfb200.so (no CUDA device needed just to load and bind)."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path is not None else LIB_PATH
+        if not p.exists():
+            raise RuntimeError(
+                f"{p} is missing: build it with `python -m paper_1511_07106_b200.build` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.tf_abi_version() != ABI_VERSION:
+            raise RuntimeError(f"libtfb200 ABI {lib.tf_abi_version()} != {ABI_VERSION}")
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def lib() -> ctypes.CDLL:
+    return load_library()
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = lib().tf_last_error().decode(errors="replace")
+        raise RuntimeError(f"{what} failed ({rc}): {msg}")
+
+
+# ---------------------------------------------------------------------------
+# device plumbing
+# ---------------------------------------------------------------------------
+
+def device() -> torch.device:
+    """The CUDA device the hot path runs on (torch's current device)."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1511_07106_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    assert t.is_cuda and t.is_contiguous(), "device buffers must be contiguous CUDA tensors"
+    return t.data_ptr()
+
+
+def mat9(m) -> ctypes.Array:
+    a = np.ascontiguousarray(m, dtype=np.float64).reshape(9)
+    return (_c_d * 9)(*a.tolist())
+
+
+def vec3(v) -> ctypes.Array:
+    a = np.ascontiguousarray(v, dtype=np.float64).reshape(3)
+    return (_c_d * 3)(*a.tolist())
+
+
+def camera(intr) -> TfCamera:
+    return TfCamera(float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy),
+                    int(intr.width), int(intr.height))
+
+
+def volume_struct(voxels: torch.Tensor, n: int, origin, voxel_size: float) -> TfVolume:
+    o = np.asarray(origin, dtype=np.int64)
+    return TfVolume(ptr(voxels), int(n), (_c_i64 * 3)(int(o[0]), int(o[1]), int(o[2])),
+                    float(voxel_size))
+
+
+class _Workspace:
+    """Per-device grow-only scratch buffer handed to the C ABI."""
+
+    def __init__(self) -> None:
+        self._bufs: dict[int, torch.Tensor] = {}
+
+    def get(self, nbytes: int, slot: str = "main") -> torch.Tensor:
+        dev = device()
+        key = (dev.index, slot)
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+            self._bufs[key] = buf
+        return buf
+
+
+workspace = _Workspace()
+
+
+class _Stats:
+    """Per-device uint64[8] counter block accumulated by the kernels."""
+
+    def __init__(self) -> None:
+        self._bufs: dict[int, torch.Tensor] = {}
+
+    def buffer(self) -> torch.Tensor:
+        dev = device()
+        buf = self._bufs.get(dev.index)
+        if buf is None:
+            buf = torch.zeros(STAT_COUNT, dtype=torch.int64, device=dev)
+            self._bufs[dev.index] = buf
+        return buf
+
+    def read(self) -> np.ndarray:
+        return self.buffer().cpu().numpy().astype(np.uint64)
+
+    def reset(self) -> None:
+        self.buffer().zero_()
+
+
+stats = _Stats()
+
+
+def env_flag(name: str) -> bool:
+    return os.environ.get(name, "").lower() in ("1", "true", "yes", "on")

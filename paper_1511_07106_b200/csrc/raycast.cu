@@ -1,0 +1,474 @@
+// Multi-volume truncated-SDF raycast with nearest-surface merge (sm_100a).
+//
+// Replaces _kernels.raycast_kernel + _sample + _scan_crossing + _hit_wins
+// (reference _kernels.py:28-68, :136-451).  One thread per pixel marches the
+// camera-anchored lattice through every volume of the launch, keeps the best
+// hit under the _hit_wins total order in registers, and writes the pixel once.
+//
+// Because _hit_wins is a strict total order, the merged result does not
+// depend on the order volumes are visited (the reference's own invariant,
+// test_acceptance.py:349-361).  The kernel therefore visits a ray's volumes
+// nearest-entry first and skips a volume outright when no hit inside it can
+// beat the current best: every hit of a volume whose first lattice index is
+// j0 has tstar >= (j0 - 1) * delta (_kernels.py:170-171), so a volume with
+// (j0 - 1) * delta > best is provably irrelevant.  Everything else — the
+// sample positions, the coarse/fine stepping, both re-walk rules, the
+// crossing interpolation and the analytic normal — is the reference's
+// arithmetic in the reference's order.
+#include <math.h>
+
+#include "tf_common.cuh"
+
+namespace tf {
+
+struct RayGeom {
+    Mat3 r_wc;
+    Vec3 cam;
+    double fx, fy, cx, cy;
+    int64_t width, height;
+    double near_thresh;  // NEAR_SURFACE_FRACTION * tau (_kernels.py:25, :298)
+    int64_t coarse;
+};
+
+struct Hit {
+    double t, hx, hy, hz, nx, ny, nz;
+};
+
+// _hit_wins (_kernels.py:246-263)
+__device__ __forceinline__ bool hit_wins(const Hit &h, const Hit &cur) {
+    if (h.t < cur.t) return true;
+    if (h.t > cur.t) return false;
+    if (h.nx != cur.nx) return h.nx > cur.nx;
+    if (h.ny != cur.ny) return h.ny > cur.ny;
+    return h.nz > cur.nz;
+}
+
+// 8 corners of the cell with minimum corner (ix, iy, iz): c[z][y][x] order
+struct Cell {
+    float2 c[8];
+};
+
+__device__ __forceinline__ void load_cell(const float2 *__restrict__ vox, int64_t n, int64_t ix,
+                                          int64_t iy, int64_t iz, Cell &cell) {
+    const float2 *b = vox + vox_index(n, iz, iy, ix);
+    const int64_t sy = n, sz = n * n;
+    cell.c[0] = __ldg(b);
+    cell.c[1] = __ldg(b + 1);
+    cell.c[2] = __ldg(b + sy);
+    cell.c[3] = __ldg(b + sy + 1);
+    cell.c[4] = __ldg(b + sz);
+    cell.c[5] = __ldg(b + sz + 1);
+    cell.c[6] = __ldg(b + sz + sy);
+    cell.c[7] = __ldg(b + sz + sy + 1);
+}
+
+__device__ __forceinline__ bool cell_observed(const Cell &cell) {
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ok &= !(cell.c[k].y <= 0.0f);  // :40-50
+    return ok;
+}
+
+// _sample (_kernels.py:28-68)
+__device__ __forceinline__ bool sample(const float2 *__restrict__ vox, int64_t n, double qx,
+                                       double qy, double qz, double &value) {
+    const double flx = floor(qx), fly = floor(qy), flz = floor(qz);
+    const double hi = (double)(n - 2);
+    if (!(flx >= 0.0 && fly >= 0.0 && flz >= 0.0 && flx <= hi && fly <= hi && flz <= hi))
+        return false;
+    const int64_t ix = (int64_t)flx, iy = (int64_t)fly, iz = (int64_t)flz;
+    Cell cell;
+    load_cell(vox, n, ix, iy, iz, cell);
+    if (!cell_observed(cell)) return false;
+    const double fx = dsub(qx, flx), fy = dsub(qy, fly), fz = dsub(qz, flz);
+    const double gx = dsub(1.0, fx), gy = dsub(1.0, fy), gz = dsub(1.0, fz);
+    const double c00 = dadd(dmul((double)cell.c[0].x, gx), dmul((double)cell.c[1].x, fx));
+    const double c10 = dadd(dmul((double)cell.c[2].x, gx), dmul((double)cell.c[3].x, fx));
+    const double c01 = dadd(dmul((double)cell.c[4].x, gx), dmul((double)cell.c[5].x, fx));
+    const double c11 = dadd(dmul((double)cell.c[6].x, gx), dmul((double)cell.c[7].x, fx));
+    const double c0 = dadd(dmul(c00, gy), dmul(c10, fy));
+    const double c1 = dadd(dmul(c01, gy), dmul(c11, fy));
+    value = dadd(dmul(c0, gz), dmul(c1, fz));
+    return true;
+}
+
+struct Ray {
+    const float2 *vox;
+    int64_t n;
+    double htx, hty, htz, vs;
+    double ox, oy, oz, dx, dy, dz;
+    unsigned long long samples;
+};
+
+// fine lattice point k in local voxel coordinates (:164-167, :357-359)
+__device__ __forceinline__ bool sample_at(Ray &r, int64_t k, double &value) {
+    const double tk = dmul((double)k, r.vs);
+    const double kx = dsub(ddiv(dadd(r.ox, dmul(tk, r.dx)), r.vs), r.htx);
+    const double ky = dsub(ddiv(dadd(r.oy, dmul(tk, r.dy)), r.vs), r.hty);
+    const double kz = dsub(ddiv(dadd(r.oz, dmul(tk, r.dz)), r.vs), r.htz);
+    r.samples++;
+    return sample(r.vox, r.n, kx, ky, kz, value);
+}
+
+// (edge * a) * b with the edge a float32 difference (numba types the corners
+// float32, _kernels.py:201-226)
+__device__ __forceinline__ double gterm(float hi, float lo, double a, double b) {
+    return dmul(dmul((double)fsubr(hi, lo), a), b);
+}
+
+// _scan_crossing (_kernels.py:136-243)
+__device__ bool scan_crossing(Ray &r, int64_t scan_from, int64_t scan_end, bool sp_valid,
+                              double sp_v, Hit &hit) {
+    const double delta = r.vs;
+    const double hi = (double)(r.n - 2);
+    for (int64_t k = scan_from; k <= scan_end; ++k) {
+        double s = 0.0;
+        const bool sv = sample_at(r, k, s);
+        if (sp_valid && sp_v > 0.0 && sv && s <= 0.0) {
+            const double ta = dmul((double)(k - 1), delta);
+            const double tstar = dadd(ta, dmul(delta, ddiv(sp_v, dsub(sp_v, s))));  // :171
+            if (tstar >= 0.0) {
+                const double hx = dadd(r.ox, dmul(tstar, r.dx));
+                const double hy = dadd(r.oy, dmul(tstar, r.dy));
+                const double hz = dadd(r.oz, dmul(tstar, r.dz));
+                const double qx = dsub(ddiv(hx, r.vs), r.htx);
+                const double qy = dsub(ddiv(hy, r.vs), r.hty);
+                const double qz = dsub(ddiv(hz, r.vs), r.htz);
+                const double fcx = floor(qx), fcy = floor(qy), fcz = floor(qz);
+                if (fcx >= 0.0 && fcy >= 0.0 && fcz >= 0.0 && fcx <= hi && fcy <= hi && fcz <= hi) {
+                    Cell cell;
+                    load_cell(r.vox, r.n, (int64_t)fcx, (int64_t)fcy, (int64_t)fcz, cell);
+                    bool observed = true;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) observed &= cell.c[q].y > 0.0f;  // :189-196
+                    if (observed) {
+                        const double gfx = dsub(qx, fcx), gfy = dsub(qy, fcy), gfz = dsub(qz, fcz);
+                        const double ofx = dsub(1.0, gfx), ofy = dsub(1.0, gfy), ofz = dsub(1.0, gfz);
+                        const float c000 = cell.c[0].x, c100 = cell.c[1].x, c010 = cell.c[2].x,
+                                    c110 = cell.c[3].x, c001 = cell.c[4].x, c101 = cell.c[5].x,
+                                    c011 = cell.c[6].x, c111 = cell.c[7].x;
+                        double gx = dadd(dadd(dadd(gterm(c100, c000, ofy, ofz),
+                                                   gterm(c110, c010, gfy, ofz)),
+                                              gterm(c101, c001, ofy, gfz)),
+                                         gterm(c111, c011, gfy, gfz));                 // :209-214
+                        double gy = dadd(dadd(dadd(gterm(c010, c000, ofx, ofz),
+                                                   gterm(c110, c100, gfx, ofz)),
+                                              gterm(c011, c001, ofx, gfz)),
+                                         gterm(c111, c101, gfx, gfz));                 // :215-220
+                        double gz = dadd(dadd(dadd(gterm(c001, c000, ofx, ofy),
+                                                   gterm(c011, c010, ofx, gfy)),
+                                              gterm(c101, c100, gfx, ofy)),
+                                         gterm(c111, c110, gfx, gfy));                 // :221-226
+                        const double gnorm =
+                            dsqrt(dadd(dadd(dmul(gx, gx), dmul(gy, gy)), dmul(gz, gz)));
+                        if (gnorm > 0.0) {
+                            if (dadd(dadd(dmul(gx, r.dx), dmul(gy, r.dy)), dmul(gz, r.dz)) > 0.0) {
+                                gx = -gx;
+                                gy = -gy;
+                                gz = -gz;
+                            }
+                            hit.t = tstar;
+                            hit.hx = hx;
+                            hit.hy = hy;
+                            hit.hz = hz;
+                            hit.nx = ddiv(gx, gnorm);
+                            hit.ny = ddiv(gy, gnorm);
+                            hit.nz = ddiv(gz, gnorm);
+                            return true;
+                        }
+                    }
+                }
+            }
+        }
+        sp_valid = sv;
+        sp_v = s;
+    }
+    return false;
+}
+
+// Entry lattice interval of the ray in one volume's sampleable box
+// (_kernels.py:299-348); false on a miss.
+__device__ __forceinline__ bool ray_interval(const TfVolume &vol, const double o[3],
+                                             const double d[3], int64_t &j0, int64_t &j_end) {
+    double t_lo = 0.0, t_hi = 1.0e30;
+    const double vs = vol.voxel_size;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double mn = dmul((double)vol.origin[a], vs);
+        const double mx = dmul((double)(vol.origin[a] + vol.n - 1), vs);
+        if (fabs(d[a]) < 1.0e-15) {
+            if (o[a] < mn || o[a] > mx) return false;
+        } else {
+            double t1 = ddiv(dsub(mn, o[a]), d[a]);
+            double t2 = ddiv(dsub(mx, o[a]), d[a]);
+            if (t1 > t2) {
+                const double tmp = t1;
+                t1 = t2;
+                t2 = tmp;
+            }
+            if (t1 > t_lo) t_lo = t1;
+            if (t2 < t_hi) t_hi = t2;
+        }
+    }
+    if (t_lo > t_hi) return false;
+    j0 = (int64_t)ceil(ddiv(t_lo, vs));
+    if (j0 < 0) j0 = 0;
+    j_end = (int64_t)floor(ddiv(t_hi, vs));
+    return true;
+}
+
+// The per-volume march of raycast_kernel (_kernels.py:349-451), merging into
+// `best`.  Returns whether `best` changed.
+__device__ bool march_volume(Ray &r, int64_t j, int64_t j_end, int64_t coarse,
+                             double near_thresh, Hit &best) {
+    bool prev_has = false;
+    double prev_v = 0.0;
+    int64_t prev_j = -1, last_j = j - 1, swept_j = j - 1;
+    while (j <= j_end) {
+        double value = 0.0;
+        const bool valid = sample_at(r, j, value);
+        bool do_scan = false;
+        if (!valid || value <= 0.0) {                                   // :362-369
+            if (prev_has && prev_v > 0.0)
+                do_scan = true;
+            else if (swept_j < j - 1 && (valid || coarse > 2))
+                do_scan = true;
+        }
+        if (do_scan) {
+            const int64_t scan_from = (prev_j > swept_j ? prev_j : swept_j) + 1;
+            const int64_t k0 = scan_from - 1;
+            bool sp_valid;
+            double sp_v = 0.0;
+            if (prev_has && k0 == prev_j) {
+                sp_valid = true;
+                sp_v = prev_v;
+            } else {
+                sp_valid = sample_at(r, k0, sp_v);
+            }
+            Hit h;
+            const bool found = scan_crossing(r, scan_from, j, sp_valid, sp_v, h);
+            swept_j = j;
+            if (found) {
+                if (hit_wins(h, best)) {
+                    best = h;
+                    return true;
+                }
+                return false;                                           // finished
+            }
+        }
+        last_j = j;
+        if (valid) {
+            prev_has = true;
+            prev_v = value;
+            prev_j = j;
+            if (fabs(value) < near_thresh)
+                j += 1;
+            else
+                j = (j / coarse + 1) * coarse;
+        } else {
+            j = (j / coarse + 1) * coarse;
+        }
+    }
+    // exit re-walk (:417-451)
+    const int64_t scan_from = (last_j > swept_j ? last_j : swept_j) + 1;
+    if (scan_from <= j_end) {
+        const int64_t k0 = scan_from - 1;
+        bool sp_valid;
+        double sp_v = 0.0;
+        if (prev_has && k0 == prev_j) {
+            sp_valid = true;
+            sp_v = prev_v;
+        } else {
+            sp_valid = sample_at(r, k0, sp_v);
+        }
+        Hit h;
+        if (scan_crossing(r, scan_from, j_end, sp_valid, sp_v, h) && hit_wins(h, best)) {
+            best = h;
+            return true;
+        }
+    }
+    return false;
+}
+
+constexpr int kRayBlockX = 8, kRayBlockY = 16;  // 128 threads; warp = 8x4 pixels
+
+__global__ void __launch_bounds__(128) raycast_kernel(
+    const __grid_constant__ VolumeTable vt, const __grid_constant__ RayGeom g,
+    double *__restrict__ out_dist, double *__restrict__ out_vert, double *__restrict__ out_norm,
+    unsigned long long *__restrict__ stats) {
+    // warp w of the block covers rows 4w..4w+3 of the 8x16 block tile
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t px = (int64_t)blockIdx.x * kRayBlockX + (lane & 7);
+    const int64_t py = (int64_t)blockIdx.y * kRayBlockY + w * 4 + (lane >> 3);
+    unsigned long long samples = 0, hits = 0;
+    if (px < g.width && py < g.height) {
+        const int64_t p = py * g.width + px;
+        Hit best;
+        best.t = out_dist[p];
+        best.hx = out_vert[3 * p + 0];
+        best.hy = out_vert[3 * p + 1];
+        best.hz = out_vert[3 * p + 2];
+        best.nx = out_norm[3 * p + 0];
+        best.ny = out_norm[3 * p + 1];
+        best.nz = out_norm[3 * p + 2];
+        // ray direction (_kernels.py:307-315)
+        const double *R = g.r_wc.m;
+        const double rx = ddiv(dsub((double)px, g.cx), g.fx);
+        const double ry = ddiv(dsub((double)py, g.cy), g.fy);
+        double d[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) d[a] = dadd(dadd(dmul(R[3 * a], rx), dmul(R[3 * a + 1], ry)), R[3 * a + 2]);
+        const double dn = dsqrt(dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2])));
+        d[0] = ddiv(d[0], dn);
+        d[1] = ddiv(d[1], dn);
+        d[2] = ddiv(d[2], dn);
+        const double o[3] = {g.cam.v[0], g.cam.v[1], g.cam.v[2]};
+
+        // entry intervals of every volume, visited nearest-entry first
+        int64_t jlo[TFB200_MAX_VOLUMES_PER_LAUNCH], jhi[TFB200_MAX_VOLUMES_PER_LAUNCH];
+        uint64_t pending = 0;  // bit v set = volume v still to march
+        for (int v = 0; v < vt.count; ++v)
+            if (ray_interval(vt.vol[v], o, d, jlo[v], jhi[v])) pending |= 1ull << v;
+        bool changed = false;
+        while (pending) {
+            int pick = -1;
+            for (int v = 0; v < vt.count; ++v)
+                if (((pending >> v) & 1ull) &&
+                    (pick < 0 || dmul((double)(jlo[v] - 1), vt.vol[v].voxel_size) <
+                                     dmul((double)(jlo[pick] - 1), vt.vol[pick].voxel_size)))
+                    pick = v;
+            pending &= ~(1ull << pick);
+            const TfVolume &vol = vt.vol[pick];
+            // no hit of this volume can have tstar below (j0 - 1) * delta
+            if (dmul((double)(jlo[pick] - 1), vol.voxel_size) > best.t) continue;
+            Ray r;
+            r.vox = (const float2 *)vol.voxels_dev;
+            r.n = vol.n;
+            r.htx = (double)vol.origin[0];
+            r.hty = (double)vol.origin[1];
+            r.htz = (double)vol.origin[2];
+            r.vs = vol.voxel_size;
+            r.ox = o[0];
+            r.oy = o[1];
+            r.oz = o[2];
+            r.dx = d[0];
+            r.dy = d[1];
+            r.dz = d[2];
+            r.samples = 0;
+            changed |= march_volume(r, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
+            samples += r.samples;
+        }
+        if (changed) {
+            hits = 1;
+            out_dist[p] = best.t;
+            out_vert[3 * p + 0] = best.hx;
+            out_vert[3 * p + 1] = best.hy;
+            out_vert[3 * p + 2] = best.hz;
+            out_norm[3 * p + 0] = best.nx;
+            out_norm[3 * p + 1] = best.ny;
+            out_norm[3 * p + 2] = best.nz;
+        }
+    }
+    if (stats) {
+        warp_count_add(&stats[TF_STAT_RAY_SAMPLES], samples);
+        warp_count_add(&stats[TF_STAT_RAY_HITS], hits);
+    }
+}
+
+__global__ void raymap_merge_kernel(double *__restrict__ dd, double *__restrict__ dv,
+                                    double *__restrict__ dn, const double *__restrict__ sd,
+                                    const double *__restrict__ sv, const double *__restrict__ sn,
+                                    int64_t npix) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= npix) return;
+    Hit h{sd[p], 0, 0, 0, sn[3 * p], sn[3 * p + 1], sn[3 * p + 2]};
+    Hit cur{dd[p], 0, 0, 0, dn[3 * p], dn[3 * p + 1], dn[3 * p + 2]};
+    if (hit_wins(h, cur)) {
+        dd[p] = sd[p];
+        for (int a = 0; a < 3; ++a) {
+            dv[3 * p + a] = sv[3 * p + a];
+            dn[3 * p + a] = sn[3 * p + a];
+        }
+    }
+}
+
+__global__ void trilinear_sample_kernel(const TfVolume vol, const double *__restrict__ pts,
+                                        int64_t npts, double *__restrict__ values,
+                                        uint8_t *__restrict__ valid) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npts) return;
+    // q = point / voxel_size - origin_voxel (tsdf.py:149)
+    const double qx = dsub(ddiv(pts[3 * i + 0], vol.voxel_size), (double)vol.origin[0]);
+    const double qy = dsub(ddiv(pts[3 * i + 1], vol.voxel_size), (double)vol.origin[1]);
+    const double qz = dsub(ddiv(pts[3 * i + 2], vol.voxel_size), (double)vol.origin[2]);
+    double v = 0.0;
+    const bool ok = sample((const float2 *)vol.voxels_dev, vol.n, qx, qy, qz, v);
+    values[i] = ok ? v : 0.0;
+    valid[i] = ok ? 1 : 0;
+}
+
+}  // namespace tf
+
+using namespace tf;
+
+extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
+                          int64_t coarse_step, const double r_wc[9], const double cam_center[3],
+                          double *dist, double *vert, double *norm, uint64_t *stats,
+                          void *stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (nvol == 0) return TF_OK;
+    if (!vols || nvol < 0 || !cam || !r_wc || !cam_center || !dist || !vert || !norm)
+        return tf_set_error(TF_EINVAL, "tf_raycast: null argument");
+    if (cam->width <= 0 || cam->height <= 0 || coarse_step < 1)
+        return tf_set_error(TF_EINVAL, "tf_raycast: bad image size or coarse step");
+    RayGeom g{};
+    for (int i = 0; i < 9; ++i) g.r_wc.m[i] = r_wc[i];
+    for (int i = 0; i < 3; ++i) g.cam.v[i] = cam_center[i];
+    g.fx = cam->fx;
+    g.fy = cam->fy;
+    g.cx = cam->cx;
+    g.cy = cam->cy;
+    g.width = cam->width;
+    g.height = cam->height;
+    g.near_thresh = 0.99 * tau;
+    g.coarse = coarse_step;
+    dim3 grid((unsigned)((cam->width + kRayBlockX - 1) / kRayBlockX),
+              (unsigned)((cam->height + kRayBlockY - 1) / kRayBlockY));
+    for (int first = 0; first < nvol; first += TFB200_MAX_VOLUMES_PER_LAUNCH) {
+        VolumeTable vt{};
+        vt.count = nvol - first < TFB200_MAX_VOLUMES_PER_LAUNCH ? nvol - first
+                                                                : TFB200_MAX_VOLUMES_PER_LAUNCH;
+        for (int v = 0; v < vt.count; ++v) {
+            vt.vol[v] = vols[first + v];
+            if (!vt.vol[v].voxels_dev || vt.vol[v].n < 2 || !(vt.vol[v].voxel_size > 0.0))
+                return tf_set_error(TF_EINVAL, "tf_raycast: bad volume %d", first + v);
+        }
+        void *prof = tf_profile_begin(TF_PROF_RAYCAST, stream);
+        raycast_kernel<<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm,
+                                                 (unsigned long long *)stats);
+        tf_profile_end(prof, stream);
+        int rc = tf_check_launch("raycast_kernel");
+        if (rc) return rc;
+    }
+    return TF_OK;
+}
+
+extern "C" int tf_raymap_merge(double *dd, double *dv, double *dn, const double *sd,
+                               const double *sv, const double *sn, int64_t npix, void *stream_) {
+    if (npix <= 0) return TF_OK;
+    if (!dd || !dv || !dn || !sd || !sv || !sn)
+        return tf_set_error(TF_EINVAL, "tf_raymap_merge: null argument");
+    raymap_merge_kernel<<<(unsigned)((npix + 255) / 256), 256, 0, (cudaStream_t)stream_>>>(
+        dd, dv, dn, sd, sv, sn, npix);
+    return tf_check_launch("raymap_merge_kernel");
+}
+
+extern "C" int tf_trilinear_sample(const TfVolume *vol, const double *pts, int64_t npts,
+                                   double *values, uint8_t *valid, void *stream_) {
+    if (npts <= 0) return TF_OK;
+    if (!vol || !pts || !values || !valid || !vol->voxels_dev)
+        return tf_set_error(TF_EINVAL, "tf_trilinear_sample: null argument");
+    trilinear_sample_kernel<<<(unsigned)((npts + 127) / 128), 128, 0, (cudaStream_t)stream_>>>(
+        *vol, pts, npts, values, valid);
+    return tf_check_launch("trilinear_sample_kernel");
+}

@@ -1,0 +1,65 @@
+// Shared device helpers for libtfb200 (sm_100a).
+//
+// Exactness: the reference kernels are numba-compiled scalar FP64 with no
+// FMA contraction.  Every arithmetic step on an exact path
+// goes through the round-to-nearest intrinsics below, which the compiler
+// never fuses or reorders, so results do not depend on -fmad.  The library
+// is additionally built with --fmad=false.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tfb200.h"
+
+namespace tf {
+
+// ---- exact IEEE round-to-nearest building blocks -------------------------
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float fmulr(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fsubr(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fdivr(float a, float b) { return __fdiv_rn(a, b); }
+
+// Python's left-to-right a*b + c*d + e*f + g without contraction.
+__device__ __forceinline__ double dot3_plus(double a0, double b0, double a1, double b1,
+                                            double a2, double b2, double c) {
+    return dadd(dadd(dadd(dmul(a0, b0), dmul(a1, b1)), dmul(a2, b2)), c);
+}
+
+// ---- small POD parameter blocks passed by value ---------------------------
+struct Mat3 {
+    double m[9];
+};
+struct Vec3 {
+    double v[3];
+};
+
+struct VolumeTable {
+    int count;
+    TfVolume vol[TFB200_MAX_VOLUMES_PER_LAUNCH];
+};
+
+__device__ __forceinline__ int64_t vox_index(int64_t n, int64_t z, int64_t y, int64_t x) {
+    return (z * n + y) * n + x;
+}
+
+// Warp-aggregated 64-bit counter add (integer: order-independent, exact).
+__device__ __forceinline__ void warp_count_add(unsigned long long *dst, unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+}  // namespace tf
+
+// ---- host-side error plumbing (api.cu) --------------------------------------
+int tf_set_error(int code, const char *fmt, ...);
+int tf_check_launch(const char *what);
+void tf_count_launch(unsigned n);
+void *tf_profile_begin(int kind, cudaStream_t stream);
+void tf_profile_end(void *token, cudaStream_t stream);

@@ -1,0 +1,218 @@
+"""Generate the golden fixtures from the REFERENCE package itself.
+
+Run in the build container (needs /root/reference and numba):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+Every array in the fixtures is produced by the reference tilefusion code
+(its numba kernels, its numpy tracking, its renderer); nothing here calls
+the oracle or the CUDA path.  The fixtures pin both of them:
+tests/test_oracle_golden.py (CPU) and tests/test_gpu_parity.py (GPU).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path(os.environ.get("TILEFUSION_REF", "/root/reference/pkg/src"))
+sys.path.insert(0, str(REF))
+
+import tilefusion as tf  # noqa: E402
+from tilefusion import tracking as tr  # noqa: E402
+from tilefusion.geometry import rotation_from_axis_angle  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def anchored_scene():
+    # tests/conftest.py:13-23 (same as the CLI demo scene)
+    return tf.Scene((
+        tf.Sphere(np.array([0.1, 0.05, 1.5]), 0.35),
+        tf.Plane(np.array([0.0, 0.5, 0.0]), np.array([0.0, -1.0, 0.0])),
+        tf.Box(np.array([-0.75, 0.1, 1.3]), np.array([-0.35, 0.5, 1.75])),
+    ))
+
+
+def intr_arr(intr):
+    return np.array([intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height], np.float64)
+
+
+def pose_arr(poses):
+    return np.stack([p.matrix for p in poses])
+
+
+def fusion_fixture():
+    """Integrate + raycast + extract on one 48^3 volume (and a 2x1x1 tiling)."""
+    intr = tf.CameraIntrinsics(fx=90.0, fy=90.0, cx=47.5, cy=35.5, width=96, height=72)
+    scene = anchored_scene()
+    poses = tf.orbit_trajectory(np.array([0.0, 0.0, 1.5]), 1.5, 40)[:5]
+    frames = [scene.render_depth(p, intr) for p in poses]
+    vol = tf.TsdfSubvolume.empty(np.array([-24, -24, 8]), 48, 48 * 0.03)
+    params = tf.FusionParams.for_voxel_size(vol.voxel_size)
+    snaps_t, snaps_w = [], []
+    for f, p in zip(frames, poses):
+        tf.integrate(vol, f, p, intr, params)
+        snaps_t.append(vol.tsdf.copy())
+        snaps_w.append(vol.weight.copy())
+    raymaps = []
+    for p in (poses[0], poses[4]):
+        rm = tf.RayMap.empty(intr)
+        tf.raycast(vol, p, intr, rm, params)
+        raymaps.append(rm)
+    cloud = tf.extract_points(vol)
+    np.savez_compressed(
+        OUT / "fusion_small.npz",
+        intr=intr_arr(intr), poses=pose_arr(poses), frames=np.stack([f.data for f in frames]),
+        origin=vol.origin_voxel, n=np.int64(48), side=np.float64(48 * 0.03),
+        tau=np.float64(params.truncation), max_weight=np.float64(params.max_weight),
+        sample_weight=np.float64(params.sample_weight),
+        tsdf_after=np.stack(snaps_t), weight_after=np.stack(snaps_w),
+        ray_pose_index=np.array([0, 4]),
+        ray_dist=np.stack([r.distance for r in raymaps]),
+        ray_vert=np.stack([r.vertices for r in raymaps]),
+        ray_norm=np.stack([r.normals for r in raymaps]),
+        cloud_verts=cloud.vertices, cloud_norms=cloud.normals,
+    )
+    print("fusion_small:", len(cloud), "points,", int(np.isfinite(raymaps[1].distance).sum()), "hits")
+
+
+def tiled_fixture():
+    """Tiled-vs-single (evaluation.equivalence_check, test_evaluation.py:59-67 sizes)."""
+    intr = tf.CameraIntrinsics(fx=65.625, fy=65.625, cx=40.0, cy=30.0, width=80, height=60)
+    scene = tf.Scene((tf.Sphere(np.array([0.0, 0.0, 0.9]), 0.5),))
+    poses = tf.orbit_trajectory(np.array([0.0, 0.0, 0.9]), 0.9, 3)
+    frames = [scene.render_depth(p, intr) for p in poses]
+    spec_t = tf.init_grid(1.8, 28, 14)
+    params = tf.FusionParams.for_voxel_size(spec_t.voxel_size)
+    tiles = [tf.TsdfSubvolume.empty(np.array(k), spec_t.voxels_per_side, spec_t.subvolume_side_length)
+             for k in spec_t.keys]
+    dists, verts, norms = [], [], []
+    for f, p in zip(frames, poses):
+        for v in tiles:
+            tf.integrate(v, f, p, intr, params)
+        rm = tf.RayMap.empty(intr)
+        for v in tiles:
+            tf.raycast(v, p, intr, rm, params)
+        dists.append(rm.distance)
+        verts.append(rm.vertices)
+        norms.append(rm.normals)
+    np.savez_compressed(
+        OUT / "tiled_small.npz",
+        intr=intr_arr(intr), poses=pose_arr(poses), frames=np.stack([f.data for f in frames]),
+        keys=np.array(spec_t.keys, np.int64), n=np.int64(spec_t.voxels_per_side),
+        side=np.float64(spec_t.subvolume_side_length), tau=np.float64(params.truncation),
+        tsdf=np.stack([v.tsdf for v in tiles]), weight=np.stack([v.weight for v in tiles]),
+        ray_dist=np.stack(dists), ray_vert=np.stack(verts), ray_norm=np.stack(norms),
+    )
+    print("tiled_small:", len(tiles), "tiles")
+
+
+def icp_fixture():
+    """track() against a fused model with a perturbed seed; every _solve_step recorded."""
+    intr = tf.CameraIntrinsics(fx=100.0, fy=100.0, cx=40.0, cy=30.0, width=80, height=60)
+    scene = anchored_scene()
+    pose = tf.Pose.identity()
+    vol = tf.TsdfSubvolume.empty(np.array([-50, -50, 24]), 100, 2.5)
+    params = tf.FusionParams.for_voxel_size(0.025)
+    integ_frame = scene.render_depth(pose, intr)
+    tf.integrate(vol, integ_frame, pose, intr, params)
+    model = tf.RayMap.empty(intr)
+    tf.raycast(vol, pose, intr, model, params)
+    frame = scene.render_depth(pose, intr)
+    bump = tf.Pose(rotation_from_axis_angle(np.array([1.0, 0.0, 0.0]), np.radians(1.0)),
+                   np.array([0.0, 0.01, 0.0]))
+    seed = pose.compose(bump)
+    tparams = tf.TrackingParams(min_correspondences=200)
+
+    steps = []
+    real = tr._solve_step
+
+    def spy(src_pts, src_nrm, src_valid, model_pts, model_nrm, model_valid, estimate,
+            ref_inv, intr_l, params_l, min_pairs):
+        out = real(src_pts, src_nrm, src_valid, model_pts, model_nrm, model_valid,
+                   estimate, ref_inv, intr_l, params_l, min_pairs)
+        rec = {"level_w": intr_l.width, "estimate": estimate.matrix.copy(),
+               "min_pairs": min_pairs}
+        if out is None:
+            rec.update(count=-1, delta=np.full(6, np.nan), rms=np.nan)
+        else:
+            rec.update(count=out[1], delta=out[0].copy(), rms=out[2])
+        steps.append(rec)
+        return out
+
+    tr._solve_step = spy
+    try:
+        result = tf.track(frame, intr, model, pose, tparams, init=seed)
+    finally:
+        tr._solve_step = real
+    # vertex/normal maps of the three pyramid levels (geometry.py:313-317)
+    levels = []
+    f, i = frame, intr
+    for _ in range(3):
+        vm = tf.VertexNormalMap.from_depth(i, f)
+        levels.append(vm)
+        f, i = f.downsampled(), i.scaled(0.5)
+    np.savez_compressed(
+        OUT / "icp_small.npz",
+        intr=intr_arr(intr), frame=frame.data, model_dist=model.distance,
+        model_vert=model.vertices, model_norm=model.normals,
+        ref_pose=pose.matrix, seed_pose=seed.matrix,
+        max_distance=np.float64(tparams.max_distance), max_angle_deg=np.float64(tparams.max_angle_deg),
+        iterations=np.array(tparams.iterations), min_correspondences=np.int64(tparams.min_correspondences),
+        step_level_w=np.array([s["level_w"] for s in steps]),
+        step_estimate=np.stack([s["estimate"] for s in steps]),
+        step_min_pairs=np.array([s["min_pairs"] for s in steps]),
+        step_count=np.array([s["count"] for s in steps]),
+        step_delta=np.stack([s["delta"] for s in steps]),
+        step_rms=np.array([s["rms"] for s in steps]),
+        result_pose=result.pose.matrix, result_lost=np.bool_(result.lost),
+        result_count=np.int64(result.correspondences), result_rms=np.float64(result.residual_rms),
+        **{f"vn{l}_verts": levels[l].vertices for l in range(3)},
+        **{f"vn{l}_norms": levels[l].normals for l in range(3)},
+        **{f"vn{l}_valid": levels[l].valid for l in range(3)},
+    )
+    print("icp_small:", len(steps), "steps, lost", result.lost, "count", result.correspondences)
+
+
+def endpoints_fixture():
+    """bin_endpoints known answers on a corridor (volumes.py:305-331)."""
+    intr = tf.CameraIntrinsics(fx=65.625, fy=65.625, cx=40.0, cy=30.0, width=80, height=60)
+    scene = tf.Scene((
+        tf.Plane(np.array([0.9, 0.0, 0.0]), np.array([-1.0, 0.0, 0.0])),
+        tf.Plane(np.array([-0.9, 0.0, 0.0]), np.array([1.0, 0.0, 0.0])),
+        tf.Plane(np.array([0.0, 0.5, 0.0]), np.array([0.0, -1.0, 0.0])),
+    ))
+    poses = tf.corridor_trajectory(4.0, 6)
+    yaw = tf.Pose(rotation_from_axis_angle(np.array([0.0, 1.0, 0.0]), 0.3), np.zeros(3))
+    poses = [p.compose(yaw) if k % 2 else p for k, p in enumerate(poses)]
+    frames, keys, counts, offsets = [], [], [], [0]
+    for p in poses:
+        d = scene.render_depth(p, intr).data.copy()
+        d[d > 4.0] = 0.0
+        frames.append(d)
+        c = tf.bin_endpoints(tf.DepthFrame(d), intr, p, 30, 0.02)
+        for k in sorted(c):
+            keys.append(k)
+            counts.append(c[k])
+        offsets.append(len(keys))
+    np.savez_compressed(
+        OUT / "endpoints_small.npz",
+        intr=intr_arr(intr), poses=pose_arr(poses), frames=np.stack(frames),
+        spacing=np.int64(30), voxel_size=np.float64(0.02),
+        keys=np.array(keys, np.int64), counts=np.array(counts, np.int64),
+        offsets=np.array(offsets, np.int64),
+    )
+    print("endpoints_small:", len(keys), "cells")
+
+
+if __name__ == "__main__":
+    fusion_fixture()
+    tiled_fixture()
+    icp_fixture()
+    endpoints_fixture()
+    for p in sorted(OUT.glob("*.npz")):
+        print(p.name, p.stat().st_size, "bytes")

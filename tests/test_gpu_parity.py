@@ -1,0 +1,247 @@
+"""CUDA path (libtfb200 through the package API) vs the golden vectors and the
+oracle.  Bit-exact for integration (tsdf AND weights), raycast maps,
+extraction, vertex/normal maps and endpoint cells; ICP inlier counts exact,
+pose increments within 1e-5 m / 1e-6 rad."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1511_07106_b200 as tf
+from paper_1511_07106_b200 import _native as nat
+from paper_1511_07106_b200 import tracking as trk
+from paper_1511_07106_b200.geometry import CameraIntrinsics, Pose
+from paper_1511_07106_b200.synth import demo_scene
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _intr(a) -> CameraIntrinsics:
+    return CameraIntrinsics(float(a[0]), float(a[1]), float(a[2]), float(a[3]), int(a[4]), int(a[5]))
+
+
+def _pose(m) -> Pose:
+    return Pose(m[:3, :3], m[:3, 3])
+
+
+def test_native_library_is_the_one_loaded():
+    lib = nat.load_library()
+    assert lib.tf_abi_version() == nat.ABI_VERSION
+    assert torch.cuda.is_available()
+
+
+def test_fusion_fixture_bit_exact():
+    g = load_golden("fusion_small.npz")
+    intr = _intr(g["intr"])
+    n = int(g["n"])
+    vol = tf.TsdfSubvolume.empty(g["origin"], n, float(g["side"]))
+    params = tf.FusionParams(float(g["tau"]), float(g["max_weight"]), float(g["sample_weight"]))
+    for k, (frame, m) in enumerate(zip(g["frames"], g["poses"])):
+        tf.integrate(vol, tf.DepthFrame(frame), _pose(m), intr, params)
+        pair = vol.voxels.cpu().numpy()
+        assert np.array_equal(pair[..., 0], g["tsdf_after"][k]), f"tsdf after frame {k}"
+        assert np.array_equal(pair[..., 1], g["weight_after"][k]), f"weight after frame {k}"
+    for i, pi in enumerate(g["ray_pose_index"]):
+        rm = tf.RayMap.empty(intr)
+        tf.raycast(vol, _pose(g["poses"][pi]), intr, rm, params)
+        assert np.array_equal(rm.distance, g["ray_dist"][i])
+        assert np.array_equal(rm.vertices, g["ray_vert"][i])
+        assert np.array_equal(rm.normals, g["ray_norm"][i])
+    cloud = tf.extract_points(vol)
+    assert np.array_equal(cloud.vertices, g["cloud_verts"])
+    assert np.array_equal(cloud.normals, g["cloud_norms"])
+
+
+def test_tiled_fixture_fused_launch_bit_exact():
+    g = load_golden("tiled_small.npz")
+    intr = _intr(g["intr"])
+    n = int(g["n"])
+    params = tf.FusionParams.for_voxel_size(float(g["side"]) / n)
+    assert params.truncation == float(g["tau"])
+    tiles = [tf.TsdfSubvolume.empty(k, n, float(g["side"])) for k in g["keys"]]
+    for f, (frame, m) in enumerate(zip(g["frames"], g["poses"])):
+        pose = _pose(m)
+        tf.integrate_volumes(tiles, tf.DepthFrame(frame), pose, intr, params)
+        rm = tf.RayMap.empty(intr)
+        tf.raycast_volumes(tiles, pose, intr, rm, params)
+        assert np.array_equal(rm.distance, g["ray_dist"][f])
+        assert np.array_equal(rm.vertices, g["ray_vert"][f])
+        assert np.array_equal(rm.normals, g["ray_norm"][f])
+    for i, t in enumerate(tiles):
+        assert np.array_equal(t.tsdf, g["tsdf"][i])
+        assert np.array_equal(t.weight, g["weight"][i])
+
+
+def test_vertex_normal_maps_bit_exact():
+    g = load_golden("icp_small.npz")
+    intr = _intr(g["intr"])
+    depth = torch.as_tensor(g["frame"], device="cuda")
+    for level in range(3):
+        lv = trk.source_level(depth, intr, level)
+        assert np.array_equal(lv.verts.cpu().numpy(), g[f"vn{level}_verts"])
+        assert np.array_equal(lv.norms.cpu().numpy(), g[f"vn{level}_norms"])
+        assert np.array_equal(lv.valid.cpu().numpy().astype(bool), g[f"vn{level}_valid"])
+        intr = intr.scaled(0.5)
+
+
+def test_icp_steps_match_reference():
+    g = load_golden("icp_small.npz")
+    intr0 = _intr(g["intr"])
+    model = tf.RayMap(g["model_vert"], g["model_norm"], g["model_dist"])
+    depth = torch.as_tensor(g["frame"], device="cuda")
+    params = tf.TrackingParams(max_distance=float(g["max_distance"]),
+                               max_angle_deg=float(g["max_angle_deg"]),
+                               iterations=tuple(int(i) for i in g["iterations"]),
+                               min_correspondences=int(g["min_correspondences"]))
+    levels = {}
+    intr = intr0
+    for level in range(3):
+        levels[intr.width] = trk.source_level(depth, intr, level)
+        intr = intr.scaled(0.5)
+    ref_inv = _pose(g["ref_pose"]).invert()
+    for k in range(len(g["step_count"])):
+        src = levels[int(g["step_level_w"][k])]
+        step = trk.solve_step(src, model, _pose(g["step_estimate"][k]), ref_inv, params,
+                              int(g["step_min_pairs"][k]))
+        if g["step_count"][k] < 0:
+            assert step is None
+            continue
+        delta, count, rms = step
+        assert count == g["step_count"][k], f"step {k}"
+        assert np.abs(delta[:3] - g["step_delta"][k][:3]).max() <= 1e-6
+        assert np.abs(delta[3:] - g["step_delta"][k][3:]).max() <= 1e-5
+    res = tf.track(tf.DepthFrame(g["frame"]), intr0, model, _pose(g["ref_pose"]), params,
+                   init=_pose(g["seed_pose"]))
+    assert res.lost == bool(g["result_lost"])
+    assert res.correspondences == int(g["result_count"])
+    assert np.abs(res.pose.matrix - g["result_pose"]).max() < 1e-9
+
+
+def test_bin_endpoints_match_reference():
+    g = load_golden("endpoints_small.npz")
+    intr = _intr(g["intr"])
+    for f in range(len(g["frames"])):
+        got = tf.bin_endpoints(tf.DepthFrame(g["frames"][f]), intr, _pose(g["poses"][f]),
+                               int(g["spacing"]), float(g["voxel_size"]))
+        lo, hi = g["offsets"][f], g["offsets"][f + 1]
+        want = {tuple(int(x) for x in g["keys"][i]): int(g["counts"][i]) for i in range(lo, hi)}
+        assert got == want
+
+
+# ---------------------------------------------------------------------------
+# the CUDA path vs the oracle at the benchmark camera and volume sizes
+# ---------------------------------------------------------------------------
+
+def _oracle_integrate(tsdf, weight, vol, frame, pose, intr, params, threads=8):
+    inv = pose.invert()
+    return oracle.integrate(tsdf, weight, vol.origin_voxel, vol.voxel_size, frame, inv.rotation,
+                            inv.translation, pose.translation, intr.fx, intr.fy, intr.cx,
+                            intr.cy, params.truncation, params.max_weight, params.sample_weight,
+                            threads=threads)
+
+
+def test_config1_volume_256_bit_exact_vs_oracle():
+    """Config 1 geometry (one 256^3 tile, 640x480, demo orbit), 4 frames."""
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(3.0, 254, 254)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    vol = tf.TsdfSubvolume.empty(spec.keys[0], spec.voxels_per_side, spec.subvolume_side_length)
+    n = spec.voxels_per_side
+    t = np.zeros((n, n, n), np.float32)
+    w = np.zeros((n, n, n), np.float32)
+    scene = demo_scene()
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)[:4]
+    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    for pose in poses:
+        frame = scene.render_depth(pose, intr)
+        stats.zero_()
+        tf.integrate_volumes([vol], frame, pose, intr, params, stats)
+        want = _oracle_integrate(t, w, vol, frame.data, pose, intr, params)
+        got = int(stats[nat.STAT_VOXEL_UPDATES].item())
+        assert got == want
+        pair = vol.voxels.cpu().numpy()
+        assert np.array_equal(pair[..., 0], t)
+        assert np.array_equal(pair[..., 1], w)
+    rm = tf.RayMap.empty(intr)
+    tf.raycast(vol, poses[-1], intr, rm, params)
+    d = np.full((intr.height, intr.width), np.inf)
+    v = np.zeros((intr.height, intr.width, 3))
+    nn = np.zeros_like(v)
+    oracle.raycast(t, w, vol.origin_voxel, vol.voxel_size, params.truncation,
+                   tf.tsdf.coarse_step(params, vol.voxel_size), poses[-1].rotation,
+                   poses[-1].translation, intr.fx, intr.fy, intr.cx, intr.cy, d, v, nn, threads=8)
+    assert np.isfinite(d).sum() > 100000
+    assert np.array_equal(rm.distance, d)
+    assert np.array_equal(rm.vertices, v)
+    assert np.array_equal(rm.normals, nn)
+
+
+def test_culling_never_drops_an_update():
+    """Full-size property: culled and unculled sweeps are bitwise identical."""
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(4.08, 1020, 510)  # config 3: 8 x 512^3 at 4 mm
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    keys = spec.keys[:2]
+    a = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in keys]
+    b = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in keys]
+    scene = demo_scene()
+    lib = nat.load_library()
+    sa = torch.zeros(8, dtype=torch.int64, device="cuda")
+    sb = torch.zeros(8, dtype=torch.int64, device="cuda")
+    try:
+        for pose in tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)[:3]:
+            frame = scene.render_depth(pose, intr)
+            lib.tf_set_debug_flags(0)
+            tf.integrate_volumes(a, frame, pose, intr, params, sa)
+            lib.tf_set_debug_flags(nat.DEBUG_NO_CULL)
+            tf.integrate_volumes(b, frame, pose, intr, params, sb)
+    finally:
+        lib.tf_set_debug_flags(0)
+    assert sa[nat.STAT_VOXEL_UPDATES].item() == sb[nat.STAT_VOXEL_UPDATES].item() > 0
+    assert sa[nat.STAT_SWEPT_VOXELS].item() < sb[nat.STAT_SWEPT_VOXELS].item()
+    for x, y in zip(a, b):
+        assert torch.equal(x.voxels, y.voxels)
+
+
+def test_fused_raycast_equals_per_volume_any_order():
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(3.0, 124, 62)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    tiles = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length)
+             for k in spec.keys]
+    scene = demo_scene()
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 16)
+    for pose in poses[:4]:
+        tf.integrate_volumes(tiles, scene.render_depth(pose, intr), pose, intr, params)
+    fused = tf.RayMap.empty(intr)
+    tf.raycast_volumes(tiles, poses[1], intr, fused, params)
+    order = np.random.default_rng(7).permutation(len(tiles))
+    single = tf.RayMap.empty(intr)
+    for i in order:
+        tf.raycast(tiles[i], poses[1], intr, single, params)
+    assert np.isfinite(fused.distance).sum() > 50000
+    assert torch.equal(fused.distance_dev, single.distance_dev)
+    assert torch.equal(fused.vertices_dev, single.vertices_dev)
+    assert torch.equal(fused.normals_dev, single.normals_dev)
+
+
+def test_trilinear_sample_and_merge():
+    g = load_golden("fusion_small.npz")
+    n = int(g["n"])
+    vol = tf.TsdfSubvolume(g["origin"], n, float(g["side"]), g["tsdf_after"][-1],
+                           g["weight_after"][-1])
+    rng = np.random.default_rng(0)
+    lo = vol.world_min
+    hi = vol.world_max
+    t = g["tsdf_after"][-1]
+    w = g["weight_after"][-1]
+    for p in rng.uniform(lo, hi, size=(200, 3)):
+        got = tf.trilinear_sample(vol, p)
+        q = p / vol.voxel_size - vol.origin_voxel
+        ok, val = oracle.sample(t, w, q[0], q[1], q[2])
+        assert (got is not None) == ok
+        if ok:
+            assert got == val
