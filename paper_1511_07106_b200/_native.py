@@ -53,31 +53,34 @@ STAT_VOXEL_UPDATES, STAT_SWEPT_VOXELS, STAT_ACTIVE_BRICKS, STAT_TOTAL_BRICKS = 0
 STAT_RAY_SAMPLES, STAT_RAY_HITS = 4, 5
 STAT_COUNT = 8
 
+_VOL = ctypes.POINTER(TfVolume)
+_CAM = ctypes.POINTER(TfCamera)
+
 _SIGNATURES = {
     "tf_abi_version": (_c_int, []),
     "tf_last_error": (ctypes.c_char_p, []),
     "tf_set_debug_flags": (None, [ctypes.c_uint32]),
+    "tf_debug_flags": (ctypes.c_uint32, []),
     "tf_launch_count": (ctypes.c_uint64, []),
     "tf_profile_enable": (None, [_c_int]),
     "tf_profile_read": (_c_int, [_c_p, _c_p, _c_int]),
-    "tf_debug_flags": (ctypes.c_uint32, []),
-    "tf_integrate_workspace_size": (_c_sz, [_c_p, _c_int, _c_p]),
-    "tf_integrate": (_c_int, [_c_p, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_d, _c_d, _c_d,
+    "tf_integrate_workspace_size": (_c_sz, [_VOL, _c_int, _CAM]),
+    "tf_integrate": (_c_int, [_VOL, _c_int, _c_p, _CAM, _c_p, _c_p, _c_p, _c_d, _c_d, _c_d,
                               _c_p, _c_sz, _c_p, _c_p]),
-    "tf_raycast": (_c_int, [_c_p, _c_int, _c_p, _c_d, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
+    "tf_raycast": (_c_int, [_VOL, _c_int, _CAM, _c_d, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
                             _c_p, _c_p]),
-    "tf_trilinear_sample": (_c_int, [_c_p, _c_p, _c_i64, _c_p, _c_p, _c_p]),
+    "tf_trilinear_sample": (_c_int, [_VOL, _c_p, _c_i64, _c_p, _c_p, _c_p]),
     "tf_raymap_merge": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p]),
-    "tf_vertex_normal_map": (_c_int, [_c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p,
+    "tf_vertex_normal_map": (_c_int, [_c_p, _c_i64, _c_i64, _c_int, _CAM, _c_p, _c_p, _c_p,
                                       _c_p]),
     "tf_icp_workspace_size": (_c_sz, [_c_i64]),
     "tf_icp_reduce": (_c_int, [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_i64,
-                               _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_d, _c_d, _c_p,
+                               _c_i64, _c_int, _CAM, _c_p, _c_p, _c_p, _c_p, _c_d, _c_d, _c_p,
                                _c_sz, _c_p, _c_p]),
     "tf_extract_workspace_size": (_c_sz, [_c_i64]),
-    "tf_extract_count": (_c_int, [_c_p, _c_p, _c_sz, _c_p, _c_p]),
-    "tf_extract_emit": (_c_int, [_c_p, _c_p, _c_sz, _c_p, _c_p, _c_p]),
-    "tf_endpoint_cells": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_d, _c_p, _c_p]),
+    "tf_extract_count": (_c_int, [_VOL, _c_p, _c_sz, _c_p, _c_p]),
+    "tf_extract_emit": (_c_int, [_VOL, _c_p, _c_sz, _c_p, _c_p, _c_p]),
+    "tf_endpoint_cells": (_c_int, [_c_p, _CAM, _c_p, _c_p, _c_d, _c_p, _c_p]),
 }
 
 EXPORTED = tuple(_SIGNATURES)
