@@ -82,9 +82,11 @@ uint64_t tf_launch_count(void);
 void tf_profile_enable(int on);
 int tf_profile_read(double *ms_by_kind, int64_t *launches_by_kind, int nkinds);
 
-/* Test hook: TF_DEBUG_NO_CULL makes tf_integrate sweep every brick, so tests
- * can prove culling never drops an update (bitwise equality at full size). */
-enum { TF_DEBUG_NO_CULL = 1u };
+/* Test hooks (bitwise-equality proofs at full size): TF_DEBUG_NO_CULL makes
+ * tf_integrate sweep every brick (culling never drops an update);
+ * TF_DEBUG_EXACT_ONLY runs the plain reference-order float64 arithmetic for
+ * every voxel instead of the float32-screened fast path. */
+enum { TF_DEBUG_NO_CULL = 1u, TF_DEBUG_EXACT_ONLY = 2u };
 void tf_set_debug_flags(uint32_t flags);
 uint32_t tf_debug_flags(void);
 

@@ -37,6 +37,7 @@ class TfCamera(ctypes.Structure):
 
 
 DEBUG_NO_CULL = 1
+DEBUG_EXACT_ONLY = 2
 PROF_INTEGRATE_UPDATE, PROF_INTEGRATE_ALL, PROF_RAYCAST, PROF_KINDS = 0, 1, 2, 3
 
 

@@ -3,19 +3,31 @@
 // Replaces _kernels.integrate_kernel (reference _kernels.py:71-133).  Three
 // launches per frame, all on the caller's stream:
 //
-//   1. frame_prep   — per pixel {depth, ray_scale} table (ray_scale is a pure
+//   1. frame_prep   — per pixel {depth, ray_scale} tables (ray_scale is a pure
 //                     function of the rounded pixel, :118-120, so it is
-//                     computed once per pixel instead of once per voxel) and a
-//                     max-depth mip over 16x16-pixel tiles for culling;
+//                     computed once per pixel instead of once per voxel): an
+//                     exact float64 table and a float32 copy for screening,
+//                     plus a max-depth mip over 16x16-pixel tiles for culling;
 //   2. brick_cull   — one thread per 8^3 brick of every volume; a brick is
 //                     dropped only when NO voxel in it can pass the
 //                     reference's gates (behind the camera, projecting outside
 //                     the image, no valid depth, or more than tau behind every
 //                     depth it can see), with explicit rounding margins;
-//   3. brick_update — persistent warps walk the surviving bricks and run the
-//                     reference's per-voxel arithmetic exactly (same op order,
-//                     round-to-nearest intrinsics, f32 where numba types it
-//                     f32), reading/writing each voxel's float2 once.
+//   3. brick_update — persistent warps walk the surviving bricks.  Each voxel
+//                     is first SCREENED in float32 with rigorous error bounds:
+//                     its pixel is decided when u+0.5 / v+0.5 are not within
+//                     the bound of an integer, and its class (skip / free
+//                     space, i.e. sdf >= tau so the clamped value is exactly
+//                     tau / near the surface) when the float32 sdf is not within
+//                     the bound of +-tau.  Free-space voxels (the large
+//                     majority) then need only the exact running-mean update;
+//                     every undecided voxel runs the reference's full float64
+//                     arithmetic (same op order, round-to-nearest intrinsics,
+//                     float32 where numba types it float32).  Results are
+//                     bit-identical to the exact path for every voxel
+//                     (tests: TF_DEBUG_EXACT_ONLY and TF_DEBUG_NO_CULL runs).
+//                     Voxel pairs move as 16-byte loads / stores and each
+//                     thread keeps 8 voxels in flight to cover HBM latency.
 //
 // Work therefore scales with voxels near the camera frustum, not with n^3,
 // and the only HBM traffic per voxel update is its 8-byte read + 8-byte write.
@@ -48,6 +60,10 @@ struct FrameGeom {
     double fx, fy, cx, cy;
     int64_t width, height;
     double tau, max_w, sw;
+    double sw_tau;  // RN(sample_weight * tau): the free-space numerator term (:132)
+    // float32 copies for the conservative screen
+    float r32[9];
+    float fx32, fy32, cx32, cy32, tau32, w32, h32;
 };
 
 static MipDesc make_mip(int64_t width, int64_t height) {
@@ -78,7 +94,7 @@ static MipDesc make_mip(int64_t width, int64_t height) {
 // patterns order like the values and the coarser levels use atomicMax on the
 // bits (exact; order-independent).
 __global__ void __launch_bounds__(256) frame_prep_kernel(
-    const double *__restrict__ depth, double2 *__restrict__ table,
+    const double *__restrict__ depth, double2 *__restrict__ table, float2 *__restrict__ table32,
     unsigned long long *__restrict__ mip, const MipDesc m, const double fx,
     const double fy, const double cx, const double cy, const int64_t width,
     const int64_t height) {
@@ -92,6 +108,9 @@ __global__ void __launch_bounds__(256) frame_prep_kernel(
         const double ry = ddiv(dsub((double)vi, cy), fy);
         const double rs = dsqrt(dadd(dadd(dmul(rx, rx), dmul(ry, ry)), 1.0));
         table[vi * width + ui] = make_double2(d, rs);
+        // screening copy: d32 > 0 exactly when d > 0 (tiny depths clamp up)
+        const float d32 = d > 0.0 ? fmaxf(__double2float_rn(d), 1.17549435e-38f) : 0.0f;
+        table32[vi * width + ui] = make_float2(d32, __double2float_rn(rs));
     }
     // block max of the (non-negative) depths
     double v = d > 0.0 ? d : 0.0;
@@ -144,82 +163,99 @@ __device__ __forceinline__ int find_volume(const BrickTable &bt, int64_t g) {
 }
 
 // Returns true when some voxel of the brick may pass every gate of
-// _kernels.py:107-127.  All margins are orders of magnitude above the FP64
-// rounding of the reference's per-voxel arithmetic (relative ~1e-15).
+// _kernels.py:107-127.  Evaluated in float32 around a float64 brick origin;
+// every comparison carries an explicit bound on the float32 error plus a wide
+// safety factor, so a brick is dropped only if no voxel can be updated.
 __device__ bool brick_may_update(const TfVolume &vol, int64_t bx, int64_t by, int64_t bz,
                                  const FrameGeom &f, const unsigned long long *__restrict__ mip,
                                  const MipDesc &m) {
     const int64_t n = vol.n;
     const int64_t i0[3] = {bx * kBrick, by * kBrick, bz * kBrick};
-    double gmin[3], gmax[3], gabs = 0.0;
+    double g0[3];
+    float ext[3], gmin[3], gmax[3];
+    float gabs = 0.f;
     for (int a = 0; a < 3; ++a) {
         const int64_t i1 = min(i0[a] + kBrick - 1, n - 1);
         // the reference's voxel centres (i + ht) * vs are monotone in i
-        gmin[a] = (double)(i0[a] + vol.origin[a]) * vol.voxel_size;
-        gmax[a] = (double)(i1 + vol.origin[a]) * vol.voxel_size;
-        gabs += fmax(fabs(gmin[a]), fabs(gmax[a]));
+        g0[a] = (double)(i0[a] + vol.origin[a]) * vol.voxel_size;
+        const double g1 = (double)(i1 + vol.origin[a]) * vol.voxel_size;
+        ext[a] = (float)(g1 - g0[a]);
+        gmin[a] = (float)g0[a];
+        gmax[a] = (float)g1;
+        gabs += fmaxf(fabsf(gmin[a]), fabsf(gmax[a]));
     }
-    const double *R = f.r_cw.m, *T = f.t_cw.v;
-    const double tabs = fabs(T[0]) + fabs(T[1]) + fabs(T[2]);
-    const double err = 1e-12 * (gabs + tabs + 1.0);  // bound on pc rounding, meters
-    double zmin = 1e300, zmax = -1e300, xabs = 0.0, yabs = 0.0;
-    double pcs[8][3];
+    const double *R = f.r_cw.m;
+    float pc0[3];
+    float pabs = 0.f;
+    for (int r = 0; r < 3; ++r) {
+        pc0[r] = (float)(R[3 * r] * g0[0] + R[3 * r + 1] * g0[1] + R[3 * r + 2] * g0[2] + f.t_cw.v[r]);
+        pabs += fabsf(pc0[r]);
+    }
+    // float32 error of corner camera coordinates (origin rounding, column
+    // products, three adds) — 2^-19 of the magnitudes is > 8x the true bound
+    const float err = 1.9073486e-6f * (pabs + ext[0] + ext[1] + ext[2]) + 1e-30f;
+    float zmin = 3e38f, zmax = -3e38f, xabs = 0.f, yabs = 0.f;
+    float pcs[8][3];
+#pragma unroll
     for (int c = 0; c < 8; ++c) {
-        const double g[3] = {(c & 1) ? gmax[0] : gmin[0], (c & 2) ? gmax[1] : gmin[1],
-                             (c & 4) ? gmax[2] : gmin[2]};
+        const float e0 = (c & 1) ? ext[0] : 0.f, e1 = (c & 2) ? ext[1] : 0.f, e2 = (c & 4) ? ext[2] : 0.f;
+#pragma unroll
         for (int r = 0; r < 3; ++r)
-            pcs[c][r] = R[r * 3 + 0] * g[0] + R[r * 3 + 1] * g[1] + R[r * 3 + 2] * g[2] + T[r];
-        zmin = fmin(zmin, pcs[c][2]);
-        zmax = fmax(zmax, pcs[c][2]);
-        xabs = fmax(xabs, fabs(pcs[c][0]));
-        yabs = fmax(yabs, fabs(pcs[c][1]));
+            pcs[c][r] = pc0[r] + f.r32[3 * r] * e0 + f.r32[3 * r + 1] * e1 + f.r32[3 * r + 2] * e2;
+        zmin = fminf(zmin, pcs[c][2]);
+        zmax = fmaxf(zmax, pcs[c][2]);
+        xabs = fmaxf(xabs, fabsf(pcs[c][0]));
+        yabs = fmaxf(yabs, fabsf(pcs[c][1]));
     }
-    if (zmax <= -2.0 * err) return false;  // every voxel has pcz <= 0 (:107)
+    if (zmax < -2.f * err) return false;  // every voxel has pcz <= 0 (:107)
 
     int64_t u0 = 0, u1 = f.width - 1, v0 = 0, v1 = f.height - 1;
-    if (zmin > 0.01 + 2.0 * err) {
-        // in front of the camera: the projections of all voxels lie inside the
+    if (zmin > 0.01f + 2.f * err) {
+        // in front of the camera: all voxel projections lie inside the
         // projected corners' bounding box (convexity), up to rounding
-        double umin = 1e300, umax = -1e300, vmin = 1e300, vmax = -1e300;
+        float umin = 3e38f, umax = -3e38f, vmin = 3e38f, vmax = -3e38f;
+#pragma unroll
         for (int c = 0; c < 8; ++c) {
-            const double u = f.fx * pcs[c][0] / pcs[c][2] + f.cx;
-            const double v = f.fy * pcs[c][1] / pcs[c][2] + f.cy;
-            umin = fmin(umin, u);
-            umax = fmax(umax, u);
-            vmin = fmin(vmin, v);
-            vmax = fmax(vmax, v);
+            const float rz = 1.0f / pcs[c][2];
+            const float u = f.fx32 * (pcs[c][0] * rz) + f.cx32;
+            const float v = f.fy32 * (pcs[c][1] * rz) + f.cy32;
+            umin = fminf(umin, u);
+            umax = fmaxf(umax, u);
+            vmin = fminf(vmin, v);
+            vmax = fmaxf(vmax, v);
         }
-        const double zl = zmin - 2.0 * err;
-        const double mu = f.fx * (2.0 * err / zl + xabs * 2.0 * err / (zl * zl)) +
-                          1e-9 * (fabs(umin) + fabs(umax) + fabs(f.cx)) + 1e-6;
-        const double mv = f.fy * (2.0 * err / zl + yabs * 2.0 * err / (zl * zl)) +
-                          1e-9 * (fabs(vmin) + fabs(vmax) + fabs(f.cy)) + 1e-6;
-        const double fu0 = floor(umin - mu + 0.5), fu1 = floor(umax + mu + 0.5);
-        const double fv0 = floor(vmin - mv + 0.5), fv1 = floor(vmax + mv + 0.5);
-        if (fu1 < 0.0 || fv1 < 0.0 || fu0 > (double)(f.width - 1) || fv0 > (double)(f.height - 1))
+        const float zl = zmin - 2.f * err;
+        const float mu = f.fx32 * (2.f * err / zl) * (1.f + xabs / zl) * 1.5f +
+                         3.8e-6f * (fabsf(umin) + fabsf(umax) + fabsf(f.cx32)) + 1e-3f;
+        const float mv = f.fy32 * (2.f * err / zl) * (1.f + yabs / zl) * 1.5f +
+                         3.8e-6f * (fabsf(vmin) + fabsf(vmax) + fabsf(f.cy32)) + 1e-3f;
+        const float fu0 = floorf(umin - mu + 0.5f), fu1 = floorf(umax + mu + 0.5f);
+        const float fv0 = floorf(vmin - mv + 0.5f), fv1 = floorf(vmax + mv + 0.5f);
+        if (fu1 < 0.f || fv1 < 0.f || fu0 > f.w32 - 1.f || fv0 > f.h32 - 1.f)
             return false;  // outside the image (:113)
-        u0 = fu0 < 0.0 ? 0 : (int64_t)fu0;
-        v0 = fv0 < 0.0 ? 0 : (int64_t)fv0;
-        u1 = fu1 > (double)(f.width - 1) ? f.width - 1 : (int64_t)fu1;
-        v1 = fv1 > (double)(f.height - 1) ? f.height - 1 : (int64_t)fv1;
+        u0 = fu0 < 0.f ? 0 : (int64_t)fu0;
+        v0 = fv0 < 0.f ? 0 : (int64_t)fv0;
+        u1 = fu1 > f.w32 - 1.f ? f.width - 1 : (int64_t)fu1;
+        v1 = fv1 > f.h32 - 1.f ? f.height - 1 : (int64_t)fv1;
     }
-    const double dmax = rect_max_depth(mip, m, u0, u1, v0, v1);
-    if (!(dmax > 0.0)) return false;  // no valid depth reachable (:116)
+    const float dmax = __double2float_ru(rect_max_depth(mip, m, u0, u1, v0, v1));
+    if (!(dmax > 0.f)) return false;  // no valid depth reachable (:116)
 
     // sdf = d - dist / ray_scale < -tau for every voxel (:125-127)?
-    double dd2 = 0.0;
+    float dd2 = 0.f, cabs = 0.f;
     for (int a = 0; a < 3; ++a) {
-        const double lo = gmin[a] - f.cam.v[a], hi = f.cam.v[a] - gmax[a];
-        const double s = fmax(fmax(lo, hi), 0.0);
+        const float c = (float)f.cam.v[a];
+        const float s = fmaxf(fmaxf(gmin[a] - c, c - gmax[a]), 0.f);
         dd2 += s * s;
+        cabs += fabsf(c);
     }
-    const double dist_lb = sqrt(dd2) * (1.0 - 1e-12);
-    const double ax = fmax(fabs((double)u0 - f.cx), fabs((double)u1 - f.cx)) / f.fx;
-    const double ay = fmax(fabs((double)v0 - f.cy), fabs((double)v1 - f.cy)) / f.fy;
-    const double rs_ub = sqrt(ax * ax + ay * ay + 1.0) * (1.0 + 1e-12);
-    const double q_lb = dist_lb / rs_ub;
-    const double margin = 1e-9 * (dmax + q_lb + f.tau) + 1e-12;
-    if (dmax - q_lb < -f.tau - margin) return false;
+    const float dist_lb = sqrtf(dd2) * (1.f - 1e-5f) - 1.9073486e-6f * (gabs + cabs);
+    const float ax = fmaxf(fabsf((float)u0 - f.cx32), fabsf((float)u1 - f.cx32)) / f.fx32;
+    const float ay = fmaxf(fabsf((float)v0 - f.cy32), fabsf((float)v1 - f.cy32)) / f.fy32;
+    const float rs_ub = sqrtf(ax * ax + ay * ay + 1.f) * (1.f + 1e-5f);
+    const float q_lb = dist_lb / rs_ub;
+    const float margin = 1e-5f * (dmax + fabsf(q_lb) + f.tau32) + 1e-6f;
+    if (dmax - q_lb < -f.tau32 - margin) return false;
     return true;
 }
 
@@ -286,7 +322,9 @@ __device__ __forceinline__ int update_voxel(float2 *__restrict__ vox, int64_t li
     return 1;
 }
 
-__global__ void __launch_bounds__(256) brick_update_kernel(
+// Reference-order exact update of every voxel of every surviving brick
+// (TF_DEBUG_EXACT_ONLY; the fast kernel below must match it bit for bit).
+__global__ void __launch_bounds__(256) brick_update_exact_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const double2 *__restrict__ table,
     const uint32_t *__restrict__ active, const unsigned int *__restrict__ active_count,
@@ -330,6 +368,208 @@ __global__ void __launch_bounds__(256) brick_update_kernel(
     (void)lane;
 }
 
+
+// ---- float32 screening (decides what the exact arithmetic would decide, or
+// defers to it) ---------------------------------------------------------------
+
+enum : int { kSkip = 0, kFree = 1, kExact = 2 };
+
+// Pixel of a voxel from float32 camera coordinates with absolute error <= epc
+// per component.  Returns kSkip (pcz <= 0 or outside the image), kExact
+// (too close to call) or kFree with *pix set (the caller still screens sdf).
+__device__ __forceinline__ int screen_pixel(const FrameGeom &f, float pcx, float pcy, float pcz,
+                                            float epc, int64_t &pix) {
+    if (pcz + epc < 0.f) return kSkip;          // pcz < 0 for sure (:107)
+    if (pcz <= 64.f * epc) return kExact;       // near the camera plane
+    const float rz = __frcp_rn(pcz);
+    const float xn = pcx * rz, yn = pcy * rz;
+    const float u = fmaf(f.fx32, xn, f.cx32), v = fmaf(f.fy32, yn, f.cy32);
+    // |u - u_ref| bound: propagated epc (pcz >= 64 epc keeps 1/pcz within
+    // 1/63 of 1/pcz32) plus float32 rounding of the rounded inputs and ops
+    const float q = epc * rz * 1.05f;
+    const float du = f.fx32 * q * (1.f + fabsf(xn)) + 9.6e-7f * (fabsf(u) + fabsf(f.cx32) + 1.f);
+    const float dv = f.fy32 * q * (1.f + fabsf(yn)) + 9.6e-7f * (fabsf(v) + fabsf(f.cy32) + 1.f);
+    const float a = u + 0.5f, b = v + 0.5f;
+    if (a + du < 0.f || a - du >= f.w32 || b + dv < 0.f || b - dv >= f.h32) return kSkip;  // :113
+    const float fa = floorf(a), fb = floorf(b);
+    const float ra = a - fa, rb = b - fb;
+    if (ra <= du || ra >= 1.f - du || rb <= dv || rb >= 1.f - dv) return kExact;  // :111-112
+    if (fa < 0.f || fa >= f.w32 || fb < 0.f || fb >= f.h32) return kSkip;
+    pix = (int64_t)fb * f.width + (int64_t)fa;
+    return kFree;
+}
+
+// Class of a voxel whose pixel is known: kSkip (d <= 0 or sdf < -tau for
+// sure), kFree (sdf >= tau for sure -> clamped value is exactly tau) or
+// kExact.  dd* are float32 voxel-minus-camera offsets with error <= epd.
+__device__ __forceinline__ int screen_sdf(const FrameGeom &f, float2 px, float ddx, float ddy,
+                                          float ddz, float epd) {
+    const float d = px.x, rs = px.y;
+    if (!(d > 0.f)) return kSkip;  // d32 > 0 exactly when d > 0 (frame_prep)
+    const float dist2 = fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz));
+    const float m_abs = 8.f * epd * (fabsf(ddx) + fabsf(ddy) + fabsf(ddz) + epd);
+    const float ea = 2.4e-7f * (d + f.tau32);  // d / tau float32 rounding
+    const float A = d - f.tau32 - ea;            // dist <= A * rs  <=>  sdf >= tau
+    if (A > 0.f) {
+        const float lim = A * rs;
+        if (dist2 * (1.f + 1e-5f) + m_abs <= lim * lim * (1.f - 1e-5f)) return kFree;
+    }
+    const float B = d + f.tau32 + ea;            // dist > B * rs    <=>  sdf < -tau
+    const float lim = B * rs;
+    if (dist2 * (1.f - 1e-5f) - m_abs > lim * lim * (1.f + 1e-5f)) return kSkip;
+    return kExact;
+}
+
+// running weighted mean with clamped == tau (_kernels.py:129-133)
+__device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f) {
+    const float wv = fmulr(old.y, old.x);
+    const double w_sum = dadd((double)old.y, f.sw);
+    const double t_new = ddiv(dadd((double)wv, f.sw_tau), w_sum);
+    const double w_new = f.max_w < w_sum ? f.max_w : w_sum;
+    return make_float2(__double2float_rn(t_new), __double2float_rn(w_new));
+}
+
+constexpr int kZBatch = 4;  // z slices per batch: 2 voxels x 4 slices in flight per thread
+
+// Lane layout per warp and brick: lane = 4 * y + xp, each lane owns the voxel
+// pair (x, x+1), x = 2 * xp, of row y, for all 8 z: a warp instruction moves
+// eight 64-byte rows.  Bricks come from the cull's active list.
+__global__ void __launch_bounds__(256, 2) brick_update_kernel(
+    const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
+    const __grid_constant__ FrameGeom f, const double2 *__restrict__ table,
+    const float2 *__restrict__ table32, const uint32_t *__restrict__ active,
+    const unsigned int *__restrict__ active_count, unsigned long long *__restrict__ stats) {
+    const unsigned count = *active_count;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lx = 2 * (lane & 3), ly = lane >> 2;
+    unsigned long long updates = 0, swept = 0;
+    for (int64_t i = warp; i < count; i += nwarps) {
+        const int64_t g = active[i];
+        const int vi = find_volume(bt, g);
+        const TfVolume vol = vt.vol[vi];
+        const int64_t n = vol.n, nb = bt.nb[vi], local = g - bt.offset[vi];
+        const int64_t x0 = (local % nb) * kBrick + lx;
+        const int64_t y = ((local / nb) % nb) * kBrick + ly;
+        const int64_t z0 = (local / (nb * nb)) * kBrick;
+        float2 *vox = (float2 *)vol.voxels_dev;
+        const double vs = vol.voxel_size;
+        const bool in_y = y < n;
+        const bool in_x0 = x0 < n, in_x1 = x0 + 1 < n;
+        const bool pair_ok = ((n & 1) == 0);  // 16-byte aligned pairs, never split
+        // exact float64 voxel centres (:99-103) and float32 screening bases at z0
+        const double gx[2] = {dmul((double)(x0 + vol.origin[0]), vs),
+                              dmul((double)(x0 + 1 + vol.origin[0]), vs)};
+        const double gy = dmul((double)(y + vol.origin[1]), vs);
+        const double gz0 = dmul((double)(z0 + vol.origin[2]), vs);
+        const double *R = f.r_cw.m;
+        float pb[2][3], db[2][3], epc[2], epd[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            float pa = 0.f, da = 0.f;
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                pb[k][r] = (float)(R[3 * r] * gx[k] + R[3 * r + 1] * gy + R[3 * r + 2] * gz0 +
+                                   f.t_cw.v[r]);
+                pa += fabsf(pb[k][r]);
+            }
+            db[k][0] = (float)(gx[k] - f.cam.v[0]);
+            db[k][1] = (float)(gy - f.cam.v[1]);
+            db[k][2] = (float)(gz0 - f.cam.v[2]);
+            da = fabsf(db[k][0]) + fabsf(db[k][1]) + fabsf(db[k][2]);
+            // 2^-20 of the magnitudes (+ the z walk of <= 8 voxels) bounds the
+            // float32 error of the screened coordinates with > 4x margin
+            const float walk = 8.f * (float)vs * 1.75f;
+            epc[k] = 9.5367432e-7f * (pa + walk) + 1e-30f;
+            epd[k] = 9.5367432e-7f * (da + walk) + 1e-30f;
+        }
+        const float vs32 = (float)vs;
+        const float sz[3] = {f.r32[2] * vs32, f.r32[5] * vs32, f.r32[8] * vs32};
+#pragma unroll
+        for (int zb = 0; zb < kBrick; zb += kZBatch) {
+            int cls[kZBatch][2];
+            int64_t pix[kZBatch][2];
+            // A: pixel of every voxel of the batch
+#pragma unroll
+            for (int j = 0; j < kZBatch; ++j) {
+                const int64_t z = z0 + zb + j;
+                const float kz = (float)(zb + j);
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    pix[j][k] = 0;
+                    const bool in = in_y && z < n && (k ? in_x1 : in_x0);
+                    cls[j][k] = in ? screen_pixel(f, fmaf(kz, sz[0], pb[k][0]), fmaf(kz, sz[1], pb[k][1]),
+                                                  fmaf(kz, sz[2], pb[k][2]), epc[k], pix[j][k])
+                                   : -1;
+                }
+            }
+            // B: screening depth / ray scale of the decided pixels
+            float2 px[kZBatch][2];
+#pragma unroll
+            for (int j = 0; j < kZBatch; ++j)
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+                    px[j][k] = cls[j][k] == kFree ? __ldg(&table32[pix[j][k]]) : make_float2(0.f, 0.f);
+            // C: sdf class
+#pragma unroll
+            for (int j = 0; j < kZBatch; ++j) {
+                const float kz = (float)(zb + j) * vs32;
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+                    if (cls[j][k] == kFree)
+                        cls[j][k] = screen_sdf(f, px[j][k], db[k][0], db[k][1], db[k][2] + kz, epd[k]);
+            }
+            // D: load the voxel pairs that have a free-space update
+            float4 old[kZBatch];
+#pragma unroll
+            for (int j = 0; j < kZBatch; ++j) {
+                const int64_t lin = vox_index(n, z0 + zb + j, y, x0);
+                const bool any = cls[j][0] == kFree || cls[j][1] == kFree;
+                old[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (any) {
+                    if (pair_ok) {
+                        old[j] = *reinterpret_cast<const float4 *>(vox + lin);
+                    } else {
+                        if (cls[j][0] == kFree) { const float2 a = vox[lin]; old[j].x = a.x; old[j].y = a.y; }
+                        if (cls[j][1] == kFree) { const float2 b = vox[lin + 1]; old[j].z = b.x; old[j].w = b.y; }
+                    }
+                }
+            }
+            // E: free-space updates (pairs written back whole; an untouched
+            // neighbour is rewritten unchanged), then the exact voxels
+#pragma unroll
+            for (int j = 0; j < kZBatch; ++j) {
+                const int64_t z = z0 + zb + j;
+                const int64_t lin = vox_index(n, z, y, x0);
+                const bool f0 = cls[j][0] == kFree, f1 = cls[j][1] == kFree;
+                if (f0 || f1) {
+                    float2 a = make_float2(old[j].x, old[j].y), b = make_float2(old[j].z, old[j].w);
+                    if (f0) a = free_update(a, f);
+                    if (f1) b = free_update(b, f);
+                    if (pair_ok) {
+                        *reinterpret_cast<float4 *>(vox + lin) = make_float4(a.x, a.y, b.x, b.y);
+                    } else {
+                        if (f0) vox[lin] = a;
+                        if (f1) vox[lin + 1] = b;
+                    }
+                }
+                updates += (unsigned)f0 + (unsigned)f1;
+                swept += (unsigned)(cls[j][0] >= 0) + (unsigned)(cls[j][1] >= 0);
+                if (cls[j][0] == kExact || cls[j][1] == kExact) {
+                    const double gz = dmul((double)(z + vol.origin[2]), vs);
+                    if (cls[j][0] == kExact) updates += update_voxel(vox, lin, gx[0], gy, gz, table, f);
+                    if (cls[j][1] == kExact) updates += update_voxel(vox, lin + 1, gx[1], gy, gz, table, f);
+                }
+            }
+        }
+    }
+    if (stats) {
+        warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
+        warp_count_add(&stats[TF_STAT_SWEPT_VOXELS], swept);
+    }
+}
+
 __global__ void brick_stats_kernel(const unsigned int *__restrict__ active_count,
                                    unsigned long long total, unsigned long long *stats) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -343,7 +583,7 @@ __global__ void brick_stats_kernel(const unsigned int *__restrict__ active_count
 // ---------------------------------------------------------------------------
 
 struct IntegrateLayout {
-    size_t table_off, mip_off, count_off, active_off, total;
+    size_t table_off, table32_off, mip_off, count_off, active_off, total;
 };
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -354,6 +594,8 @@ static IntegrateLayout layout_for(int64_t total_bricks_max, const TfCamera *cam)
     size_t off = 0;
     L.table_off = off;
     off = align_up(off + (size_t)(cam->width * cam->height) * sizeof(double2), 256);
+    L.table32_off = off;
+    off = align_up(off + (size_t)(cam->width * cam->height) * sizeof(float2), 256);
     L.mip_off = off;
     off = align_up(off + (size_t)m.total * sizeof(unsigned long long), 256);
     L.count_off = off;
@@ -414,6 +656,7 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
                             L.total);
     char *ws = (char *)workspace;
     double2 *table = (double2 *)(ws + L.table_off);
+    float2 *table32 = (float2 *)(ws + L.table32_off);
     unsigned long long *mip = (unsigned long long *)(ws + L.mip_off);
     unsigned int *count = (unsigned int *)(ws + L.count_off);
     uint32_t *active = (uint32_t *)(ws + L.active_off);
@@ -424,8 +667,9 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
         return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
     dim3 pblock(kTile, kTile);
     dim3 pgrid((unsigned)m.tiles_x[0], (unsigned)m.tiles_y[0]);
-    frame_prep_kernel<<<pgrid, pblock, 0, stream>>>(depth, table, mip, m, cam->fx, cam->fy,
-                                                    cam->cx, cam->cy, cam->width, cam->height);
+    frame_prep_kernel<<<pgrid, pblock, 0, stream>>>(depth, table, table32, mip, m, cam->fx,
+                                                    cam->fy, cam->cx, cam->cy, cam->width,
+                                                    cam->height);
     int rc = tf_check_launch("frame_prep_kernel");
     if (rc) return rc;
 
@@ -444,6 +688,15 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
     f.tau = tau;
     f.max_w = max_weight;
     f.sw = sample_weight;
+    f.sw_tau = sample_weight * tau;  // IEEE double product, as the reference's sw * clamped
+    for (int i = 0; i < 9; ++i) f.r32[i] = (float)r_cw[i];
+    f.fx32 = (float)cam->fx;
+    f.fy32 = (float)cam->fy;
+    f.cx32 = (float)cam->cx;
+    f.cy32 = (float)cam->cy;
+    f.tau32 = (float)tau;
+    f.w32 = (float)cam->width;
+    f.h32 = (float)cam->height;
 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -472,8 +725,13 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
                                                            (tf_debug_flags() & TF_DEBUG_NO_CULL) ? 1 : 0);
         if ((rc = tf_check_launch("brick_cull_kernel"))) return rc;
         void *prof = tf_profile_begin(TF_PROF_INTEGRATE_UPDATE, stream);
-        brick_update_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(
-            vt, bt, f, table, active, count, (unsigned long long *)stats);
+        if (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) {
+            brick_update_exact_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(
+                vt, bt, f, table, active, count, (unsigned long long *)stats);
+        } else {
+            brick_update_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(
+                vt, bt, f, table, table32, active, count, (unsigned long long *)stats);
+        }
         tf_profile_end(prof, stream);
         if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
         if (stats) {

@@ -245,3 +245,51 @@ def test_trilinear_sample_and_merge():
         assert (got is not None) == ok
         if ok:
             assert got == val
+
+
+def test_fast_screen_equals_exact_path_full_size():
+    """Config-3 volumes: the float32-screened kernel == reference-order float64 kernel."""
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(4.08, 1020, 510)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    keys = [spec.keys[0], spec.keys[5]]
+    a = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in keys]
+    b = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in keys]
+    scene = demo_scene()
+    lib = nat.load_library()
+    sa = torch.zeros(8, dtype=torch.int64, device="cuda")
+    sb = torch.zeros(8, dtype=torch.int64, device="cuda")
+    try:
+        for pose in tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)[::9]:
+            frame = scene.render_depth(pose, intr)
+            lib.tf_set_debug_flags(0)
+            tf.integrate_volumes(a, frame, pose, intr, params, sa)
+            lib.tf_set_debug_flags(nat.DEBUG_EXACT_ONLY)
+            tf.integrate_volumes(b, frame, pose, intr, params, sb)
+    finally:
+        lib.tf_set_debug_flags(0)
+    assert sa[nat.STAT_VOXEL_UPDATES].item() == sb[nat.STAT_VOXEL_UPDATES].item() > 0
+    for x, y in zip(a, b):
+        assert torch.equal(x.voxels, y.voxels)
+
+
+@pytest.mark.parametrize("n", [49, 50])
+def test_odd_and_even_sizes_vs_oracle(n):
+    """Partial bricks and the unpaired (odd n) voxel path against the oracle."""
+    g = load_golden("fusion_small.npz")
+    intr = _intr(g["intr"])
+    vs = 0.03
+    vol = tf.TsdfSubvolume.empty([-25, -23, 7], n, n * vs)
+    params = tf.FusionParams(float(g["tau"]))
+    t = np.zeros((n, n, n), np.float32)
+    w = np.zeros((n, n, n), np.float32)
+    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    for frame, m in zip(g["frames"], g["poses"]):
+        pose = _pose(m)
+        stats.zero_()
+        tf.integrate_volumes([vol], tf.DepthFrame(frame), pose, intr, params, stats)
+        want = _oracle_integrate(t, w, vol, frame, pose, intr, params, threads=2)
+        assert stats[nat.STAT_VOXEL_UPDATES].item() == want
+    pair = vol.voxels.cpu().numpy()
+    assert np.array_equal(pair[..., 0], t)
+    assert np.array_equal(pair[..., 1], w)
