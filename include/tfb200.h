@@ -65,6 +65,7 @@ enum {
     TF_STAT_TOTAL_BRICKS = 3,
     TF_STAT_RAY_SAMPLES = 4,   /* trilinear _sample calls (_kernels.py:28) */
     TF_STAT_RAY_HITS = 5,      /* hits merged by this raycast call */
+    TF_STAT_EXACT_VOXELS = 6,  /* voxels the float32 screen deferred to the exact path */
     TF_STAT_COUNT = 8
 };
 

@@ -51,7 +51,7 @@ def profile_read() -> dict:
 
 # TF_STAT_* slots (tfb200.h)
 STAT_VOXEL_UPDATES, STAT_SWEPT_VOXELS, STAT_ACTIVE_BRICKS, STAT_TOTAL_BRICKS = 0, 1, 2, 3
-STAT_RAY_SAMPLES, STAT_RAY_HITS = 4, 5
+STAT_RAY_SAMPLES, STAT_RAY_HITS, STAT_EXACT_VOXELS = 4, 5, 6
 STAT_COUNT = 8
 
 _VOL = ctypes.POINTER(TfVolume)

@@ -369,6 +369,14 @@ __global__ void __launch_bounds__(256) brick_update_exact_kernel(
 }
 
 
+// out-of-line copy for the rare queue-overflow path of the fast kernel
+__device__ __noinline__ int update_voxel_slow(float2 *__restrict__ vox, int64_t lin, double gx,
+                                              double gy, double gz,
+                                              const double2 *__restrict__ table,
+                                              const FrameGeom &f) {
+    return update_voxel(vox, lin, gx, gy, gz, table, f);
+}
+
 // ---- float32 screening (decides what the exact arithmetic would decide, or
 // defers to it) ---------------------------------------------------------------
 
@@ -438,7 +446,9 @@ __global__ void __launch_bounds__(256, 2) brick_update_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const double2 *__restrict__ table,
     const float2 *__restrict__ table32, const uint32_t *__restrict__ active,
-    const unsigned int *__restrict__ active_count, unsigned long long *__restrict__ stats) {
+    const unsigned int *__restrict__ active_count, unsigned long long *__restrict__ queue,
+    unsigned long long *__restrict__ queue_count, const unsigned long long queue_cap,
+    unsigned long long *__restrict__ stats) {
     const unsigned count = *active_count;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -556,10 +566,24 @@ __global__ void __launch_bounds__(256, 2) brick_update_kernel(
                 }
                 updates += (unsigned)f0 + (unsigned)f1;
                 swept += (unsigned)(cls[j][0] >= 0) + (unsigned)(cls[j][1] >= 0);
-                if (cls[j][0] == kExact || cls[j][1] == kExact) {
-                    const double gz = dmul((double)(z + vol.origin[2]), vs);
-                    if (cls[j][0] == kExact) updates += update_voxel(vox, lin, gx[0], gy, gz, table, f);
-                    if (cls[j][1] == kExact) updates += update_voxel(vox, lin + 1, gx[1], gy, gz, table, f);
+                // undecided voxels go to the exact kernel (no warp divergence here)
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const bool ex = cls[j][k] == kExact;
+                    const unsigned m = __ballot_sync(0xffffffffu, ex);
+                    if (m) {
+                        unsigned long long base = 0;
+                        if (lane == 0) base = atomicAdd(queue_count, (unsigned long long)__popc(m));
+                        base = __shfl_sync(0xffffffffu, base, 0) + __popc(m & ((1u << lane) - 1u));
+                        if (ex) {
+                            if (base < queue_cap) {
+                                queue[base] = ((unsigned long long)vi << 40) | (unsigned long long)(lin + k);
+                            } else {  // queue full: exact update in place
+                                const double gz = dmul((double)(z + vol.origin[2]), vs);
+                                updates += update_voxel_slow(vox, lin + k, gx[k], gy, gz, table, f);
+                            }
+                        }
+                    }
                 }
             }
         }
@@ -567,6 +591,34 @@ __global__ void __launch_bounds__(256, 2) brick_update_kernel(
     if (stats) {
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
         warp_count_add(&stats[TF_STAT_SWEPT_VOXELS], swept);
+    }
+}
+
+// The exact reference arithmetic for every queued (undecided) voxel; one
+// thread per voxel, so the float64 path runs without divergence.
+__global__ void __launch_bounds__(256) exact_queue_kernel(
+    const __grid_constant__ VolumeTable vt, const __grid_constant__ FrameGeom f,
+    const double2 *__restrict__ table, const unsigned long long *__restrict__ queue,
+    const unsigned long long *__restrict__ queue_count, const unsigned long long queue_cap,
+    unsigned long long *__restrict__ stats) {
+    const unsigned long long total = min(*queue_count, queue_cap);
+    unsigned long long updates = 0;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long e = queue[i];
+        const int v = (int)(e >> 40);
+        const int64_t lin = (int64_t)(e & ((1ull << 40) - 1));
+        const TfVolume vol = vt.vol[v];
+        const int64_t n = vol.n;
+        const int64_t x = lin % n, y = (lin / n) % n, z = lin / (n * n);
+        const double vs = vol.voxel_size;
+        updates += update_voxel((float2 *)vol.voxels_dev, lin, dmul((double)(x + vol.origin[0]), vs),
+                                dmul((double)(y + vol.origin[1]), vs),
+                                dmul((double)(z + vol.origin[2]), vs), table, f);
+    }
+    if (stats) {
+        warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
+        if (blockIdx.x == 0 && threadIdx.x == 0) stats[TF_STAT_EXACT_VOXELS] += *queue_count;
     }
 }
 
@@ -583,8 +635,12 @@ __global__ void brick_stats_kernel(const unsigned int *__restrict__ active_count
 // ---------------------------------------------------------------------------
 
 struct IntegrateLayout {
-    size_t table_off, table32_off, mip_off, count_off, active_off, total;
+    size_t table_off, table32_off, mip_off, count_off, active_off, queue_off, total;
+    unsigned long long queue_cap;
 };
+
+// capacity of the exact-voxel queue; overflow is handled inline (still exact)
+constexpr unsigned long long kQueueCap = 8ull << 20;
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -602,6 +658,9 @@ static IntegrateLayout layout_for(int64_t total_bricks_max, const TfCamera *cam)
     off = align_up(off + 256, 256);
     L.active_off = off;
     off = align_up(off + (size_t)total_bricks_max * sizeof(uint32_t), 256);
+    L.queue_off = off;
+    L.queue_cap = kQueueCap;
+    off = align_up(off + (size_t)L.queue_cap * sizeof(unsigned long long), 256);
     L.total = off;
     return L;
 }
@@ -659,6 +718,8 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
     float2 *table32 = (float2 *)(ws + L.table32_off);
     unsigned long long *mip = (unsigned long long *)(ws + L.mip_off);
     unsigned int *count = (unsigned int *)(ws + L.count_off);
+    unsigned long long *qcount = (unsigned long long *)(ws + L.count_off + 64);
+    unsigned long long *queue = (unsigned long long *)(ws + L.queue_off);
     uint32_t *active = (uint32_t *)(ws + L.active_off);
     const MipDesc m = make_mip(cam->width, cam->height);
 
@@ -718,7 +779,7 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
             off += nb * nb * nb;
         }
         bt.offset[cnt] = off;
-        if (cudaMemsetAsync(count, 0, sizeof(unsigned int), stream) != cudaSuccess)
+        if (cudaMemsetAsync(count, 0, 128, stream) != cudaSuccess)  // brick + queue counters
             return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
         const unsigned cull_blocks = (unsigned)((off + 255) / 256);
         brick_cull_kernel<<<cull_blocks, 256, 0, stream>>>(vt, bt, f, m, mip, active, count,
@@ -730,7 +791,12 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
                 vt, bt, f, table, active, count, (unsigned long long *)stats);
         } else {
             brick_update_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(
-                vt, bt, f, table, table32, active, count, (unsigned long long *)stats);
+                vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap,
+                (unsigned long long *)stats);
+            if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
+            exact_queue_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, f, table, queue, qcount,
+                                                                     L.queue_cap,
+                                                                     (unsigned long long *)stats);
         }
         tf_profile_end(prof, stream);
         if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
