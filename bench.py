@@ -263,7 +263,7 @@ def run_ours(args) -> None:
         "breakdown_ms_per_step": {"integrate_update_kernel": upd_ms / args.steps,
                                   "integrate_total": int_ms / args.steps,
                                   "raycast": ray_ms / args.steps},
-        "integrate": {"swept_voxels_per_frame": sum_over_ranks(int(st[nat.STAT_SWEPT_VOXELS])) / args.steps,
+        "integrate": {"noop_updates_per_frame": sum_over_ranks(int(st[nat.STAT_NOOP_UPDATES])) / args.steps, "swept_voxels_per_frame": sum_over_ranks(int(st[nat.STAT_SWEPT_VOXELS])) / args.steps,
                       "exact_path_voxels_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_VOXELS])) / args.steps,
                       "active_bricks_per_frame": sum_over_ranks(int(st[nat.STAT_ACTIVE_BRICKS])) / args.steps,
                       "total_bricks": sum_over_ranks(int(st[nat.STAT_TOTAL_BRICKS])) // max(args.steps, 1)},

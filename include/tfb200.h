@@ -66,6 +66,7 @@ enum {
     TF_STAT_RAY_SAMPLES = 4,   /* trilinear _sample calls (_kernels.py:28) */
     TF_STAT_RAY_HITS = 5,      /* hits merged by this raycast call */
     TF_STAT_EXACT_VOXELS = 6,  /* voxels the float32 screen deferred to the exact path */
+    TF_STAT_NOOP_UPDATES = 7,  /* updates proven to leave the voxel unchanged (store skipped) */
     TF_STAT_COUNT = 8
 };
 
@@ -86,8 +87,10 @@ int tf_profile_read(double *ms_by_kind, int64_t *launches_by_kind, int nkinds);
 /* Test hooks (bitwise-equality proofs at full size): TF_DEBUG_NO_CULL makes
  * tf_integrate sweep every brick (culling never drops an update);
  * TF_DEBUG_EXACT_ONLY runs the plain reference-order float64 arithmetic for
- * every voxel instead of the float32-screened fast path. */
-enum { TF_DEBUG_NO_CULL = 1u, TF_DEBUG_EXACT_ONLY = 2u };
+ * every voxel instead of the float32-screened fast path; TF_DEBUG_NO_FIXEDPOINT
+ * stores every free-space update even when it provably leaves the voxel
+ * unchanged. */
+enum { TF_DEBUG_NO_CULL = 1u, TF_DEBUG_EXACT_ONLY = 2u, TF_DEBUG_NO_FIXEDPOINT = 4u };
 void tf_set_debug_flags(uint32_t flags);
 uint32_t tf_debug_flags(void);
 

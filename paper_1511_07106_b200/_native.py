@@ -38,6 +38,7 @@ class TfCamera(ctypes.Structure):
 
 DEBUG_NO_CULL = 1
 DEBUG_EXACT_ONLY = 2
+DEBUG_NO_FIXEDPOINT = 4
 PROF_INTEGRATE_UPDATE, PROF_INTEGRATE_ALL, PROF_RAYCAST, PROF_KINDS = 0, 1, 2, 3
 
 
@@ -51,7 +52,7 @@ def profile_read() -> dict:
 
 # TF_STAT_* slots (tfb200.h)
 STAT_VOXEL_UPDATES, STAT_SWEPT_VOXELS, STAT_ACTIVE_BRICKS, STAT_TOTAL_BRICKS = 0, 1, 2, 3
-STAT_RAY_SAMPLES, STAT_RAY_HITS, STAT_EXACT_VOXELS = 4, 5, 6
+STAT_RAY_SAMPLES, STAT_RAY_HITS, STAT_EXACT_VOXELS, STAT_NOOP_UPDATES = 4, 5, 6, 7
 STAT_COUNT = 8
 
 _VOL = ctypes.POINTER(TfVolume)

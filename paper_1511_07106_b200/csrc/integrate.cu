@@ -377,56 +377,33 @@ __device__ __noinline__ int update_voxel_slow(float2 *__restrict__ vox, int64_t 
     return update_voxel(vox, lin, gx, gy, gz, table, f);
 }
 
-// ---- float32 screening (decides what the exact arithmetic would decide, or
-// defers to it) ---------------------------------------------------------------
+// ---- float32 screening ------------------------------------------------------
+//
+// For each voxel the screen either decides exactly what the reference's float64
+// arithmetic decides, or defers the voxel to the exact kernel.  Bounds:
+//  * camera coordinates pc are float32 around a float64 column base, with
+//    |error| <= epc (2^-20 of the magnitudes: > 8x the real bound);
+//  * u + 0.5 = fx * pcx * rcp(pcz) + (cx + 0.5) with rcp.approx (rel. error
+//    <= 2^-22), |error| <= du, a per-batch bound computed from the batch's
+//    smallest pcz and largest |pcx|; a voxel whose u + 0.5 lies within du of an
+//    integer is deferred (~0.1% of voxels), otherwise floor() is exact;
+//  * sdf = d - dist / rs is compared against +-tau through squared distances
+//    with 1e-5 relative and explicit absolute margins; only voxels in the
+//    +-tau band (near the surface) are deferred.
 
 enum : int { kSkip = 0, kFree = 1, kExact = 2 };
 
-// Pixel of a voxel from float32 camera coordinates with absolute error <= epc
-// per component.  Returns kSkip (pcz <= 0 or outside the image), kExact
-// (too close to call) or kFree with *pix set (the caller still screens sdf).
-__device__ __forceinline__ int screen_pixel(const FrameGeom &f, float pcx, float pcy, float pcz,
-                                            float epc, int64_t &pix) {
-    if (pcz + epc < 0.f) return kSkip;          // pcz < 0 for sure (:107)
-    if (pcz <= 64.f * epc) return kExact;       // near the camera plane
-    const float rz = __frcp_rn(pcz);
-    const float xn = pcx * rz, yn = pcy * rz;
-    const float u = fmaf(f.fx32, xn, f.cx32), v = fmaf(f.fy32, yn, f.cy32);
-    // |u - u_ref| bound: propagated epc (pcz >= 64 epc keeps 1/pcz within
-    // 1/63 of 1/pcz32) plus float32 rounding of the rounded inputs and ops
-    const float q = epc * rz * 1.05f;
-    const float du = f.fx32 * q * (1.f + fabsf(xn)) + 9.6e-7f * (fabsf(u) + fabsf(f.cx32) + 1.f);
-    const float dv = f.fy32 * q * (1.f + fabsf(yn)) + 9.6e-7f * (fabsf(v) + fabsf(f.cy32) + 1.f);
-    const float a = u + 0.5f, b = v + 0.5f;
-    if (a + du < 0.f || a - du >= f.w32 || b + dv < 0.f || b - dv >= f.h32) return kSkip;  // :113
-    const float fa = floorf(a), fb = floorf(b);
-    const float ra = a - fa, rb = b - fb;
-    if (ra <= du || ra >= 1.f - du || rb <= dv || rb >= 1.f - dv) return kExact;  // :111-112
-    if (fa < 0.f || fa >= f.w32 || fb < 0.f || fb >= f.h32) return kSkip;
-    pix = (int64_t)fb * f.width + (int64_t)fa;
-    return kFree;
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
 }
 
-// Class of a voxel whose pixel is known: kSkip (d <= 0 or sdf < -tau for
-// sure), kFree (sdf >= tau for sure -> clamped value is exactly tau) or
-// kExact.  dd* are float32 voxel-minus-camera offsets with error <= epd.
-__device__ __forceinline__ int screen_sdf(const FrameGeom &f, float2 px, float ddx, float ddy,
-                                          float ddz, float epd) {
-    const float d = px.x, rs = px.y;
-    if (!(d > 0.f)) return kSkip;  // d32 > 0 exactly when d > 0 (frame_prep)
-    const float dist2 = fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz));
-    const float m_abs = 8.f * epd * (fabsf(ddx) + fabsf(ddy) + fabsf(ddz) + epd);
-    const float ea = 2.4e-7f * (d + f.tau32);  // d / tau float32 rounding
-    const float A = d - f.tau32 - ea;            // dist <= A * rs  <=>  sdf >= tau
-    if (A > 0.f) {
-        const float lim = A * rs;
-        if (dist2 * (1.f + 1e-5f) + m_abs <= lim * lim * (1.f - 1e-5f)) return kFree;
-    }
-    const float B = d + f.tau32 + ea;            // dist > B * rs    <=>  sdf < -tau
-    const float lim = B * rs;
-    if (dist2 * (1.f - 1e-5f) - m_abs > lim * lim * (1.f + 1e-5f)) return kSkip;
-    return kExact;
-}
+struct ScreenConst {
+    float tau_ea;     // tau + float32 rounding allowance of d and tau
+    float fxh, fyh;   // fx, fy
+    float cxh, cyh;   // cx + 0.5, cy + 0.5
+};
 
 // running weighted mean with clamped == tau (_kernels.py:129-133)
 __device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f) {
@@ -437,153 +414,163 @@ __device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f) {
     return make_float2(__double2float_rn(t_new), __double2float_rn(w_new));
 }
 
-constexpr int kZBatch = 4;  // z slices per batch: 2 voxels x 4 slices in flight per thread
+constexpr int kZBatch = 4;  // voxels in flight per thread
 
-// Lane layout per warp and brick: lane = 4 * y + xp, each lane owns the voxel
-// pair (x, x+1), x = 2 * xp, of row y, for all 8 z: a warp instruction moves
-// eight 64-byte rows.  Bricks come from the cull's active list.
-__global__ void __launch_bounds__(256, 2) brick_update_kernel(
+// Lane layout per warp and brick: x = lane & 7, y = lane >> 3 (+4 for the
+// second half); each lane walks z in batches of kZBatch, so a warp
+// instruction touches four 64-byte rows.  Bricks come from the cull's list.
+__global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const double2 *__restrict__ table,
     const float2 *__restrict__ table32, const uint32_t *__restrict__ active,
     const unsigned int *__restrict__ active_count, unsigned long long *__restrict__ queue,
     unsigned long long *__restrict__ queue_count, const unsigned long long queue_cap,
-    unsigned long long *__restrict__ stats) {
+    const int fixed_point, unsigned long long *__restrict__ stats) {
     const unsigned count = *active_count;
     const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int lx = 2 * (lane & 3), ly = lane >> 2;
-    unsigned long long updates = 0, swept = 0;
-    for (int64_t i = warp; i < count; i += nwarps) {
-        const int64_t g = active[i];
+    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int lx = lane & 7, ly = lane >> 3;
+    const float tau_ea = f.tau32 + 2.4e-7f * (f.tau32 + 16.f);  // d < 16 m rounding allowance
+    const float2 fixed = make_float2(f.tau32, (float)f.max_w);
+    unsigned long long updates = 0, swept = 0, nop = 0;
+    for (unsigned i = warp; i < count; i += nwarps) {
+        const unsigned g = active[i];
         const int vi = find_volume(bt, g);
-        const TfVolume vol = vt.vol[vi];
-        const int64_t n = vol.n, nb = bt.nb[vi], local = g - bt.offset[vi];
-        const int64_t x0 = (local % nb) * kBrick + lx;
-        const int64_t y = ((local / nb) % nb) * kBrick + ly;
-        const int64_t z0 = (local / (nb * nb)) * kBrick;
+        const TfVolume &vol = vt.vol[vi];
+        const unsigned n = (unsigned)vol.n, nb = (unsigned)bt.nb[vi];
+        const unsigned local = g - (unsigned)bt.offset[vi];
+        const unsigned bxy = local % (nb * nb);
+        const unsigned x = (bxy % nb) * kBrick + lx;
+        const unsigned z0 = (local / (nb * nb)) * kBrick;
+        const unsigned y_base = (bxy / nb) * kBrick + ly;
         float2 *vox = (float2 *)vol.voxels_dev;
         const double vs = vol.voxel_size;
-        const bool in_y = y < n;
-        const bool in_x0 = x0 < n, in_x1 = x0 + 1 < n;
-        const bool pair_ok = ((n & 1) == 0);  // 16-byte aligned pairs, never split
-        // exact float64 voxel centres (:99-103) and float32 screening bases at z0
-        const double gx[2] = {dmul((double)(x0 + vol.origin[0]), vs),
-                              dmul((double)(x0 + 1 + vol.origin[0]), vs)};
-        const double gy = dmul((double)(y + vol.origin[1]), vs);
-        const double gz0 = dmul((double)(z0 + vol.origin[2]), vs);
-        const double *R = f.r_cw.m;
-        float pb[2][3], db[2][3], epc[2], epd[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            float pa = 0.f, da = 0.f;
-#pragma unroll
-            for (int r = 0; r < 3; ++r) {
-                pb[k][r] = (float)(R[3 * r] * gx[k] + R[3 * r + 1] * gy + R[3 * r + 2] * gz0 +
-                                   f.t_cw.v[r]);
-                pa += fabsf(pb[k][r]);
-            }
-            db[k][0] = (float)(gx[k] - f.cam.v[0]);
-            db[k][1] = (float)(gy - f.cam.v[1]);
-            db[k][2] = (float)(gz0 - f.cam.v[2]);
-            da = fabsf(db[k][0]) + fabsf(db[k][1]) + fabsf(db[k][2]);
-            // 2^-20 of the magnitudes (+ the z walk of <= 8 voxels) bounds the
-            // float32 error of the screened coordinates with > 4x margin
-            const float walk = 8.f * (float)vs * 1.75f;
-            epc[k] = 9.5367432e-7f * (pa + walk) + 1e-30f;
-            epd[k] = 9.5367432e-7f * (da + walk) + 1e-30f;
-        }
         const float vs32 = (float)vs;
-        const float sz[3] = {f.r32[2] * vs32, f.r32[5] * vs32, f.r32[8] * vs32};
+        const double *R = f.r_cw.m;
+        const double gx = dmul((double)((int64_t)x + vol.origin[0]), vs);
+        const double gz0 = dmul((double)((int64_t)z0 + vol.origin[2]), vs);
+        const float szx = f.r32[2] * vs32, szy = f.r32[5] * vs32, szz = f.r32[8] * vs32;
+#pragma unroll 1
+        for (int hy = 0; hy < 2; ++hy) {
+            const unsigned y = y_base + 4 * hy;
+            const double gy = dmul((double)((int64_t)y + vol.origin[1]), vs);
+            // float32 column bases at z0 (plain float64, then rounded)
+            const float pbx = (float)(R[0] * gx + R[1] * gy + R[2] * gz0 + f.t_cw.v[0]);
+            const float pby = (float)(R[3] * gx + R[4] * gy + R[5] * gz0 + f.t_cw.v[1]);
+            const float pbz = (float)(R[6] * gx + R[7] * gy + R[8] * gz0 + f.t_cw.v[2]);
+            const float dbx = (float)(gx - f.cam.v[0]);
+            const float dby = (float)(gy - f.cam.v[1]);
+            const float dbz = (float)(gz0 - f.cam.v[2]);
+            const float walk = 14.f * vs32;
+            const float epc = 9.5367432e-7f * (fabsf(pbx) + fabsf(pby) + fabsf(pbz) + walk) + 1e-30f;
+            const float epd = 9.5367432e-7f * (fabsf(dbx) + fabsf(dby) + fabsf(dbz) + walk) + 1e-30f;
+            const float mabs = 8.f * epd * (fabsf(dbx) + fabsf(dby) + fabsf(dbz) + 8.f * vs32 + epd);
+            const bool row_in = x < n && y < n;
+#pragma unroll 1
+            for (int zb = 0; zb < kBrick; zb += kZBatch) {
+                // per-batch bound of the projection error (smallest pcz, largest |pcx|, |pcy|)
+                const float kz0 = (float)zb, kz1 = (float)(zb + kZBatch - 1);
+                const float za = fmaf(kz0, szz, pbz), zc = fmaf(kz1, szz, pbz);
+                const float zlo = fminf(za, zc) - epc;
+                const float xab = fmaxf(fabsf(fmaf(kz0, szx, pbx)), fabsf(fmaf(kz1, szx, pbx))) + epc;
+                const float yab = fmaxf(fabsf(fmaf(kz0, szy, pby)), fabsf(fmaf(kz1, szy, pby))) + epc;
+                const bool proj_ok = zlo > 64.f * epc;
+                const float rzm = proj_ok ? 1.0f / zlo : 0.f;
+                const float xnm = xab * rzm, ynm = yab * rzm;
+                const float du = f.fx32 * epc * rzm * 1.05f * (1.f + xnm) +
+                                 9.6e-7f * (f.fx32 * xnm + fabsf(f.cx32) + 2.f);
+                const float dv = f.fy32 * epc * rzm * 1.05f * (1.f + ynm) +
+                                 9.6e-7f * (f.fy32 * ynm + fabsf(f.cy32) + 2.f);
+                const float hu = 0.5f - du, hv = 0.5f - dv;
+                int cls[kZBatch];
+                unsigned pix[kZBatch];
+                float2 px[kZBatch];
+                // A: pixel of every voxel of the batch
 #pragma unroll
-        for (int zb = 0; zb < kBrick; zb += kZBatch) {
-            int cls[kZBatch][2];
-            int64_t pix[kZBatch][2];
-            // A: pixel of every voxel of the batch
-#pragma unroll
-            for (int j = 0; j < kZBatch; ++j) {
-                const int64_t z = z0 + zb + j;
-                const float kz = (float)(zb + j);
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    pix[j][k] = 0;
-                    const bool in = in_y && z < n && (k ? in_x1 : in_x0);
-                    cls[j][k] = in ? screen_pixel(f, fmaf(kz, sz[0], pb[k][0]), fmaf(kz, sz[1], pb[k][1]),
-                                                  fmaf(kz, sz[2], pb[k][2]), epc[k], pix[j][k])
-                                   : -1;
-                }
-            }
-            // B: screening depth / ray scale of the decided pixels
-            float2 px[kZBatch][2];
-#pragma unroll
-            for (int j = 0; j < kZBatch; ++j)
-#pragma unroll
-                for (int k = 0; k < 2; ++k)
-                    px[j][k] = cls[j][k] == kFree ? __ldg(&table32[pix[j][k]]) : make_float2(0.f, 0.f);
-            // C: sdf class
-#pragma unroll
-            for (int j = 0; j < kZBatch; ++j) {
-                const float kz = (float)(zb + j) * vs32;
-#pragma unroll
-                for (int k = 0; k < 2; ++k)
-                    if (cls[j][k] == kFree)
-                        cls[j][k] = screen_sdf(f, px[j][k], db[k][0], db[k][1], db[k][2] + kz, epd[k]);
-            }
-            // D: load the voxel pairs that have a free-space update
-            float4 old[kZBatch];
-#pragma unroll
-            for (int j = 0; j < kZBatch; ++j) {
-                const int64_t lin = vox_index(n, z0 + zb + j, y, x0);
-                const bool any = cls[j][0] == kFree || cls[j][1] == kFree;
-                old[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (any) {
-                    if (pair_ok) {
-                        old[j] = *reinterpret_cast<const float4 *>(vox + lin);
-                    } else {
-                        if (cls[j][0] == kFree) { const float2 a = vox[lin]; old[j].x = a.x; old[j].y = a.y; }
-                        if (cls[j][1] == kFree) { const float2 b = vox[lin + 1]; old[j].z = b.x; old[j].w = b.y; }
+                for (int j = 0; j < kZBatch; ++j) {
+                    const float kz = (float)(zb + j);
+                    const float pcx = fmaf(kz, szx, pbx), pcy = fmaf(kz, szy, pby), pcz = fmaf(kz, szz, pbz);
+                    int c = kSkip;
+                    pix[j] = 0;
+                    if (row_in && z0 + zb + j < n) {
+                        if (!proj_ok || hu <= 0.f || hv <= 0.f) {
+                            c = (pcz + epc < 0.f) ? kSkip : kExact;  // :107, or too close to call
+                        } else {
+                            const float rz = rcp_approx(pcz);
+                            const float a = fmaf(f.fx32, pcx * rz, f.cx32 + 0.5f);
+                            const float b = fmaf(f.fy32, pcy * rz, f.cy32 + 0.5f);
+                            const float fa = floorf(a), fb = floorf(b);
+                            if (fabsf(a - fa - 0.5f) >= hu || fabsf(b - fb - 0.5f) >= hv) {
+                                c = kExact;                             // within du of a rounding edge
+                            } else {
+                                const int ui = (int)fa, vi2 = (int)fb;  // saturating conversion
+                                if ((unsigned)ui < (unsigned)f.width && (unsigned)vi2 < (unsigned)f.height) {
+                                    c = kFree;
+                                    pix[j] = (unsigned)vi2 * (unsigned)f.width + (unsigned)ui;
+                                }
+                            }
+                        }
+                        swept += 1;
                     }
+                    cls[j] = c;
                 }
-            }
-            // E: free-space updates (pairs written back whole; an untouched
-            // neighbour is rewritten unchanged), then the exact voxels
+                // B: screening depth / ray scale of the decided pixels
 #pragma unroll
-            for (int j = 0; j < kZBatch; ++j) {
-                const int64_t z = z0 + zb + j;
-                const int64_t lin = vox_index(n, z, y, x0);
-                const bool f0 = cls[j][0] == kFree, f1 = cls[j][1] == kFree;
-                if (f0 || f1) {
-                    float2 a = make_float2(old[j].x, old[j].y), b = make_float2(old[j].z, old[j].w);
-                    if (f0) a = free_update(a, f);
-                    if (f1) b = free_update(b, f);
-                    if (pair_ok) {
-                        *reinterpret_cast<float4 *>(vox + lin) = make_float4(a.x, a.y, b.x, b.y);
-                    } else {
-                        if (f0) vox[lin] = a;
-                        if (f1) vox[lin + 1] = b;
+                for (int j = 0; j < kZBatch; ++j)
+                    px[j] = cls[j] == kFree ? __ldg(&table32[pix[j]]) : make_float2(0.f, 0.f);
+                // C: sdf class (dist <= (d - tau) rs  => free;  dist > (d + tau) rs  => skip)
+#pragma unroll
+                for (int j = 0; j < kZBatch; ++j) {
+                    if (cls[j] != kFree) continue;
+                    const float d = px[j].x, rs = px[j].y;
+                    const float ddz = fmaf((float)(zb + j), vs32, dbz);
+                    const float dist2 = fmaf(dbx, dbx, fmaf(dby, dby, ddz * ddz));
+                    const float A = (d - tau_ea) * rs, B = (d + tau_ea) * rs;
+                    int c = kExact;
+                    if (!(d > 0.f)) c = kSkip;  // d32 > 0 exactly when d > 0
+                    else if (A > 0.f && fmaf(dist2, 1.00001f, mabs) <= A * A * 0.99999f) c = kFree;
+                    else if (fmaf(dist2, 0.99999f, -mabs) > B * B * 1.00001f) c = kSkip;
+                    cls[j] = c;
+                }
+                // D: load the voxels with a free-space update
+                const unsigned row = (z0 + zb) * n * n + y * n + x;  // < 2^32 for n <= 1625
+                float2 old[kZBatch];
+#pragma unroll
+                for (int j = 0; j < kZBatch; ++j)
+                    old[j] = cls[j] == kFree ? vox[(size_t)row + (size_t)j * n * n] : make_float2(0.f, 0.f);
+                // E: free-space updates; exact voxels are queued
+                unsigned overflow = 0;
+#pragma unroll
+                for (int j = 0; j < kZBatch; ++j) {
+                    const size_t lin = (size_t)row + (size_t)j * n * n;
+                    if (cls[j] == kFree) {
+                        ++updates;
+                        if (fixed_point && old[j].x == fixed.x && old[j].y == fixed.y) {
+                            ++nop;  // (tau32, max_w) is a host-verified fixed point
+                        } else {
+                            vox[lin] = free_update(old[j], f);
+                        }
                     }
-                }
-                updates += (unsigned)f0 + (unsigned)f1;
-                swept += (unsigned)(cls[j][0] >= 0) + (unsigned)(cls[j][1] >= 0);
-                // undecided voxels go to the exact kernel (no warp divergence here)
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    const bool ex = cls[j][k] == kExact;
+                    const bool ex = cls[j] == kExact;
                     const unsigned m = __ballot_sync(0xffffffffu, ex);
                     if (m) {
                         unsigned long long base = 0;
                         if (lane == 0) base = atomicAdd(queue_count, (unsigned long long)__popc(m));
                         base = __shfl_sync(0xffffffffu, base, 0) + __popc(m & ((1u << lane) - 1u));
                         if (ex) {
-                            if (base < queue_cap) {
-                                queue[base] = ((unsigned long long)vi << 40) | (unsigned long long)(lin + k);
-                            } else {  // queue full: exact update in place
-                                const double gz = dmul((double)(z + vol.origin[2]), vs);
-                                updates += update_voxel_slow(vox, lin + k, gx[k], gy, gz, table, f);
-                            }
+                            if (base < queue_cap)
+                                queue[base] = ((unsigned long long)vi << 40) | (unsigned long long)lin;
+                            else
+                                overflow |= 1u << j;  // queue full: exact update in place below
                         }
                     }
+                }
+#pragma unroll 1
+                for (int j = 0; overflow && j < kZBatch; ++j) {
+                    if (!((overflow >> j) & 1u)) continue;
+                    const double gz = dmul((double)((int64_t)(z0 + zb + j) + vol.origin[2]), vs);
+                    updates += update_voxel(vox, (int64_t)row + (int64_t)j * n * n, gx, gy, gz, table, f);
                 }
             }
         }
@@ -591,6 +578,7 @@ __global__ void __launch_bounds__(256, 2) brick_update_kernel(
     if (stats) {
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
         warp_count_add(&stats[TF_STAT_SWEPT_VOXELS], swept);
+        warp_count_add(&stats[TF_STAT_NOOP_UPDATES], nop);
     }
 }
 
@@ -759,6 +747,21 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
     f.w32 = (float)cam->width;
     f.h32 = (float)cam->height;
 
+    // Is the saturated free-space state (tau32, max_w) a fixed point of the
+    // free-space update?  Evaluated here with the kernel's exact IEEE
+    // operations (host code is built with -ffp-contract=off); when it is,
+    // such voxels are provably unchanged and their store is skipped.
+    int fixed_point = 0;
+    if (!(tf_debug_flags() & TF_DEBUG_NO_FIXEDPOINT)) {
+        const volatile float t32 = (float)tau, w32 = (float)max_weight;
+        const volatile float wv = t32 * w32;
+        const volatile double w_sum = (double)w32 + sample_weight;
+        const volatile double num = (double)wv + f.sw_tau;
+        const volatile double t_new = num / w_sum;
+        const double w_new = max_weight < w_sum ? max_weight : w_sum;
+        fixed_point = ((float)t_new == t32) && ((float)w_new == w32);
+    }
+
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -790,9 +793,9 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
             brick_update_exact_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(
                 vt, bt, f, table, active, count, (unsigned long long *)stats);
         } else {
-            brick_update_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(
+            brick_update_kernel<<<(unsigned)sms * 6, 256, 0, stream>>>(
                 vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap,
-                (unsigned long long *)stats);
+                fixed_point, (unsigned long long *)stats);
             if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
             exact_queue_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, f, table, queue, qcount,
                                                                      L.queue_cap,

@@ -293,3 +293,30 @@ def test_odd_and_even_sizes_vs_oracle(n):
     pair = vol.voxels.cpu().numpy()
     assert np.array_equal(pair[..., 0], t)
     assert np.array_equal(pair[..., 1], w)
+
+
+def test_saturated_fixed_point_shortcut_is_exact():
+    """max_weight = 3 saturates quickly; skipped no-op stores must equal real ones."""
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(3.0, 254, 254)
+    params = tf.FusionParams(truncation=4 * spec.voxel_size, max_weight=3.0)
+    vols = [tf.TsdfSubvolume.empty(spec.keys[0], spec.voxels_per_side, spec.subvolume_side_length)
+            for _ in range(3)]
+    scene = demo_scene()
+    lib = nat.load_library()
+    stats = [torch.zeros(8, dtype=torch.int64, device="cuda") for _ in range(3)]
+    flags = [0, nat.DEBUG_NO_FIXEDPOINT, nat.DEBUG_EXACT_ONLY]
+    try:
+        for pose in tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)[:6]:
+            frame = scene.render_depth(pose, intr)
+            for v, s, fl in zip(vols, stats, flags):
+                lib.tf_set_debug_flags(fl)
+                tf.integrate_volumes([v], frame, pose, intr, params, s)
+    finally:
+        lib.tf_set_debug_flags(0)
+    assert stats[0][nat.STAT_NOOP_UPDATES].item() > 0
+    assert stats[1][nat.STAT_NOOP_UPDATES].item() == 0
+    assert (stats[0][nat.STAT_VOXEL_UPDATES].item() == stats[1][nat.STAT_VOXEL_UPDATES].item()
+            == stats[2][nat.STAT_VOXEL_UPDATES].item())
+    assert torch.equal(vols[0].voxels, vols[2].voxels)
+    assert torch.equal(vols[1].voxels, vols[2].voxels)
