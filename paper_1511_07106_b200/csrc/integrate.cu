@@ -466,27 +466,18 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
             const float epc = 9.5367432e-7f * (fabsf(pbx) + fabsf(pby) + fabsf(pbz) + walk) + 1e-30f;
             const float epd = 9.5367432e-7f * (fabsf(dbx) + fabsf(dby) + fabsf(dbz) + walk) + 1e-30f;
             const float mabs = 8.f * epd * (fabsf(dbx) + fabsf(dby) + fabsf(dbz) + 8.f * vs32 + epd);
+            const float k1u = f.fx32 * epc * 1.05f, k1v = f.fy32 * epc * 1.05f;
+            const float k3u = 9.6e-7f * f.fx32, k3v = 9.6e-7f * f.fy32;
+            const float k2u = 9.6e-7f * (fabsf(f.cx32) + 2.f), k2v = 9.6e-7f * (fabsf(f.cy32) + 2.f);
             const bool row_in = x < n && y < n;
 #pragma unroll 1
             for (int zb = 0; zb < kBrick; zb += kZBatch) {
-                // per-batch bound of the projection error (smallest pcz, largest |pcx|, |pcy|)
-                const float kz0 = (float)zb, kz1 = (float)(zb + kZBatch - 1);
-                const float za = fmaf(kz0, szz, pbz), zc = fmaf(kz1, szz, pbz);
-                const float zlo = fminf(za, zc) - epc;
-                const float xab = fmaxf(fabsf(fmaf(kz0, szx, pbx)), fabsf(fmaf(kz1, szx, pbx))) + epc;
-                const float yab = fmaxf(fabsf(fmaf(kz0, szy, pby)), fabsf(fmaf(kz1, szy, pby))) + epc;
-                const bool proj_ok = zlo > 64.f * epc;
-                const float rzm = proj_ok ? 1.0f / zlo : 0.f;
-                const float xnm = xab * rzm, ynm = yab * rzm;
-                const float du = f.fx32 * epc * rzm * 1.05f * (1.f + xnm) +
-                                 9.6e-7f * (f.fx32 * xnm + fabsf(f.cx32) + 2.f);
-                const float dv = f.fy32 * epc * rzm * 1.05f * (1.f + ynm) +
-                                 9.6e-7f * (f.fy32 * ynm + fabsf(f.cy32) + 2.f);
-                const float hu = 0.5f - du, hv = 0.5f - dv;
                 int cls[kZBatch];
                 unsigned pix[kZBatch];
                 float2 px[kZBatch];
-                // A: pixel of every voxel of the batch
+                // A: pixel of every voxel of the batch.  |u+0.5 error| <= du with
+                // du = fx epc 1.05 rz (1 + |xn|) + 2^-20 (fx |xn| + |cx| + 2)
+                // (propagated column error + float32 rounding of inputs and ops)
 #pragma unroll
                 for (int j = 0; j < kZBatch; ++j) {
                     const float kz = (float)(zb + j);
@@ -494,14 +485,15 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                     int c = kSkip;
                     pix[j] = 0;
                     if (row_in && z0 + zb + j < n) {
-                        if (!proj_ok || hu <= 0.f || hv <= 0.f) {
-                            c = (pcz + epc < 0.f) ? kSkip : kExact;  // :107, or too close to call
-                        } else {
+                        if (pcz > 64.f * epc) {
                             const float rz = rcp_approx(pcz);
-                            const float a = fmaf(f.fx32, pcx * rz, f.cx32 + 0.5f);
-                            const float b = fmaf(f.fy32, pcy * rz, f.cy32 + 0.5f);
+                            const float xn = pcx * rz, yn = pcy * rz;
+                            const float a = fmaf(f.fx32, xn, f.cx32 + 0.5f);
+                            const float b = fmaf(f.fy32, yn, f.cy32 + 0.5f);
+                            const float du = fmaf(k1u, rz * (1.f + fabsf(xn)), fmaf(k3u, fabsf(xn), k2u));
+                            const float dv = fmaf(k1v, rz * (1.f + fabsf(yn)), fmaf(k3v, fabsf(yn), k2v));
                             const float fa = floorf(a), fb = floorf(b);
-                            if (fabsf(a - fa - 0.5f) >= hu || fabsf(b - fb - 0.5f) >= hv) {
+                            if (fabsf(a - fa - 0.5f) >= 0.5f - du || fabsf(b - fb - 0.5f) >= 0.5f - dv) {
                                 c = kExact;                             // within du of a rounding edge
                             } else {
                                 const int ui = (int)fa, vi2 = (int)fb;  // saturating conversion
@@ -510,6 +502,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                                     pix[j] = (unsigned)vi2 * (unsigned)f.width + (unsigned)ui;
                                 }
                             }
+                        } else {
+                            c = (pcz + epc < 0.f) ? kSkip : kExact;  // behind (:107) / on the plane
                         }
                         swept += 1;
                     }
