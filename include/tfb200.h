@@ -57,7 +57,7 @@ typedef struct TfCamera {
     int64_t width, height;
 } TfCamera;
 
-/* Per-call counters written (accumulated) to a device uint64[8]. */
+/* Per-call counters written (accumulated) to a device uint64[16]. */
 enum {
     TF_STAT_VOXEL_UPDATES = 0, /* voxels passing every integration gate */
     TF_STAT_SWEPT_VOXELS = 1,  /* voxels evaluated after brick culling */
@@ -67,7 +67,10 @@ enum {
     TF_STAT_RAY_HITS = 5,      /* hits merged by this raycast call */
     TF_STAT_EXACT_VOXELS = 6,  /* voxels the float32 screen deferred to the exact path */
     TF_STAT_NOOP_UPDATES = 7,  /* updates proven to leave the voxel unchanged (store skipped) */
-    TF_STAT_COUNT = 8
+    TF_STAT_EXACT_PROJ = 8,    /* ... deferred: pixel rounding too close to call */
+    TF_STAT_EXACT_PLANE = 9,   /* ... deferred: on the camera plane */
+    TF_STAT_EXACT_SDF = 10,    /* ... deferred: sdf within the +-tau band */
+    TF_STAT_COUNT = 16
 };
 
 int tf_abi_version(void);

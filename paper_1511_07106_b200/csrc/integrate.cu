@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const int lx = lane & 7, ly = lane >> 3;
     const float tau_ea = f.tau32 + 2.4e-7f * (f.tau32 + 16.f);  // d < 16 m rounding allowance
     const float2 fixed = make_float2(f.tau32, (float)f.max_w);
-    unsigned long long updates = 0, swept = 0, nop = 0;
+    unsigned long long updates = 0, swept = 0, nop = 0, ex_proj = 0, ex_plane = 0, ex_sdf = 0;
     for (unsigned i = warp; i < count; i += nwarps) {
         const unsigned g = active[i];
         const int vi = find_volume(bt, g);
@@ -495,6 +495,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                             const float fa = floorf(a), fb = floorf(b);
                             if (fabsf(a - fa - 0.5f) >= 0.5f - du || fabsf(b - fb - 0.5f) >= 0.5f - dv) {
                                 c = kExact;                             // within du of a rounding edge
+                                ++ex_proj;
                             } else {
                                 const int ui = (int)fa, vi2 = (int)fb;  // saturating conversion
                                 if ((unsigned)ui < (unsigned)f.width && (unsigned)vi2 < (unsigned)f.height) {
@@ -504,6 +505,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                             }
                         } else {
                             c = (pcz + epc < 0.f) ? kSkip : kExact;  // behind (:107) / on the plane
+                            ex_plane += c == kExact;
                         }
                         swept += 1;
                     }
@@ -525,6 +527,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                     if (!(d > 0.f)) c = kSkip;  // d32 > 0 exactly when d > 0
                     else if (A > 0.f && fmaf(dist2, 1.00001f, mabs) <= A * A * 0.99999f) c = kFree;
                     else if (fmaf(dist2, 0.99999f, -mabs) > B * B * 1.00001f) c = kSkip;
+                    ex_sdf += c == kExact;
                     cls[j] = c;
                 }
                 // D: load the voxels with a free-space update
@@ -573,6 +576,9 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
         warp_count_add(&stats[TF_STAT_SWEPT_VOXELS], swept);
         warp_count_add(&stats[TF_STAT_NOOP_UPDATES], nop);
+        warp_count_add(&stats[TF_STAT_EXACT_PROJ], ex_proj);
+        warp_count_add(&stats[TF_STAT_EXACT_PLANE], ex_plane);
+        warp_count_add(&stats[TF_STAT_EXACT_SDF], ex_sdf);
     }
 }
 

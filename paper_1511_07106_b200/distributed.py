@@ -28,6 +28,7 @@ from typing import Callable, Sequence
 import torch
 import torch.distributed as dist
 
+from . import _native as nat
 from .geometry import CameraIntrinsics, Pose
 from .tsdf import FusionParams, RayMap, TsdfSubvolume, integrate_volumes, raycast_volumes
 
@@ -83,7 +84,7 @@ class ShardedFusion:
         self.tiles = [TsdfSubvolume.empty(k, voxels_per_side, side_length) for k in self.keys]
         self.partial = RayMap.empty(intr)
         self.model = RayMap.empty(intr)
-        self.stats = torch.zeros(8, dtype=torch.int64, device=self.partial.distance_dev.device)
+        self.stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device=self.partial.distance_dev.device)
 
     def step(self, depth: torch.Tensor, pose: Pose) -> RayMap:
         integrate_volumes(self.tiles, depth, pose, self.intr, self.params, self.stats)

@@ -154,7 +154,7 @@ def test_config1_volume_256_bit_exact_vs_oracle():
     w = np.zeros((n, n, n), np.float32)
     scene = demo_scene()
     poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)[:4]
-    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
     for pose in poses:
         frame = scene.render_depth(pose, intr)
         stats.zero_()
@@ -189,8 +189,8 @@ def test_culling_never_drops_an_update():
     b = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in keys]
     scene = demo_scene()
     lib = nat.load_library()
-    sa = torch.zeros(8, dtype=torch.int64, device="cuda")
-    sb = torch.zeros(8, dtype=torch.int64, device="cuda")
+    sa = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
+    sb = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
     try:
         for pose in tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)[:3]:
             frame = scene.render_depth(pose, intr)
@@ -257,8 +257,8 @@ def test_fast_screen_equals_exact_path_full_size():
     b = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in keys]
     scene = demo_scene()
     lib = nat.load_library()
-    sa = torch.zeros(8, dtype=torch.int64, device="cuda")
-    sb = torch.zeros(8, dtype=torch.int64, device="cuda")
+    sa = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
+    sb = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
     try:
         for pose in tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)[::9]:
             frame = scene.render_depth(pose, intr)
@@ -283,7 +283,7 @@ def test_odd_and_even_sizes_vs_oracle(n):
     params = tf.FusionParams(float(g["tau"]))
     t = np.zeros((n, n, n), np.float32)
     w = np.zeros((n, n, n), np.float32)
-    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
     for frame, m in zip(g["frames"], g["poses"]):
         pose = _pose(m)
         stats.zero_()
@@ -304,7 +304,7 @@ def test_saturated_fixed_point_shortcut_is_exact():
             for _ in range(3)]
     scene = demo_scene()
     lib = nat.load_library()
-    stats = [torch.zeros(8, dtype=torch.int64, device="cuda") for _ in range(3)]
+    stats = [torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda") for _ in range(3)]
     flags = [0, nat.DEBUG_NO_FIXEDPOINT, nat.DEBUG_EXACT_ONLY]
     try:
         for pose in tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)[:6]:
