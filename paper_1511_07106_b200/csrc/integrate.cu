@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
             const float k3u = 9.6e-7f * f.fx32, k3v = 9.6e-7f * f.fy32;
             const float k2u = 9.6e-7f * (fabsf(f.cx32) + 2.f), k2v = 9.6e-7f * (fabsf(f.cy32) + 2.f);
             const bool row_in = x < n && y < n;
+            const float hw = 0.5f * f.w32, hh = 0.5f * f.h32;
 #pragma unroll 1
             for (int zb = 0; zb < kBrick; zb += kZBatch) {
                 int cls[kZBatch];
@@ -493,7 +494,9 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                             const float du = fmaf(k1u, rz * (1.f + fabsf(xn)), fmaf(k3u, fabsf(xn), k2u));
                             const float dv = fmaf(k1v, rz * (1.f + fabsf(yn)), fmaf(k3v, fabsf(yn), k2v));
                             const float fa = floorf(a), fb = floorf(b);
-                            if (fabsf(a - fa - 0.5f) >= 0.5f - du || fabsf(b - fb - 0.5f) >= 0.5f - dv) {
+                            if (fabsf(a - hw) >= hw + du || fabsf(b - hh) >= hh + dv) {
+                                c = kSkip;  // clearly outside the image (:113)
+                            } else if (fabsf(a - fa - 0.5f) >= 0.5f - du || fabsf(b - fb - 0.5f) >= 0.5f - dv) {
                                 c = kExact;                             // within du of a rounding edge
                                 ++ex_proj;
                             } else {
