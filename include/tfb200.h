@@ -70,6 +70,7 @@ enum {
     TF_STAT_EXACT_PROJ = 8,    /* ... deferred: pixel rounding too close to call */
     TF_STAT_EXACT_PLANE = 9,   /* ... deferred: on the camera plane */
     TF_STAT_EXACT_SDF = 10,    /* ... deferred: sdf within the +-tau band */
+    TF_STAT_EXACT_MARCHES = 11, /* ray-volume marches redone with the exact arithmetic */
     TF_STAT_COUNT = 16
 };
 
@@ -90,7 +91,7 @@ int tf_profile_read(double *ms_by_kind, int64_t *launches_by_kind, int nkinds);
 /* Test hooks (bitwise-equality proofs at full size): TF_DEBUG_NO_CULL makes
  * tf_integrate sweep every brick (culling never drops an update);
  * TF_DEBUG_EXACT_ONLY runs the plain reference-order float64 arithmetic for
- * every voxel instead of the float32-screened fast path; TF_DEBUG_NO_FIXEDPOINT
+ * every voxel / ray instead of the float32-screened / certified fast paths; TF_DEBUG_NO_FIXEDPOINT
  * stores every free-space update even when it provably leaves the voxel
  * unchanged. */
 enum { TF_DEBUG_NO_CULL = 1u, TF_DEBUG_EXACT_ONLY = 2u, TF_DEBUG_NO_FIXEDPOINT = 4u };

@@ -28,6 +28,7 @@ struct RayGeom {
     int64_t width, height;
     double near_thresh;  // NEAR_SURFACE_FRACTION * tau (_kernels.py:25, :298)
     int64_t coarse;
+    int exact_only;      // TF_DEBUG_EXACT_ONLY: plain reference march for every ray
 };
 
 struct Hit {
@@ -116,70 +117,66 @@ __device__ __forceinline__ double gterm(float hi, float lo, double a, double b) 
     return dmul(dmul((double)fsubr(hi, lo), a), b);
 }
 
+// Crossing acceptance of _scan_crossing (_kernels.py:170-240) for the
+// consecutive samples (k-1, k) with exact values sp_v > 0 >= s.
+__device__ bool accept_crossing(const Ray &r, int64_t k, double sp_v, double s, Hit &hit) {
+    const double delta = r.vs;
+    const double hi = (double)(r.n - 2);
+    const double ta = dmul((double)(k - 1), delta);
+    const double tstar = dadd(ta, dmul(delta, ddiv(sp_v, dsub(sp_v, s))));  // :171
+    if (!(tstar >= 0.0)) return false;
+    const double hx = dadd(r.ox, dmul(tstar, r.dx));
+    const double hy = dadd(r.oy, dmul(tstar, r.dy));
+    const double hz = dadd(r.oz, dmul(tstar, r.dz));
+    const double qx = dsub(ddiv(hx, r.vs), r.htx);
+    const double qy = dsub(ddiv(hy, r.vs), r.hty);
+    const double qz = dsub(ddiv(hz, r.vs), r.htz);
+    const double fcx = floor(qx), fcy = floor(qy), fcz = floor(qz);
+    if (!(fcx >= 0.0 && fcy >= 0.0 && fcz >= 0.0 && fcx <= hi && fcy <= hi && fcz <= hi)) return false;
+    Cell cell;
+    load_cell(r.vox, r.n, (int64_t)fcx, (int64_t)fcy, (int64_t)fcz, cell);
+    bool observed = true;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) observed &= cell.c[q].y > 0.0f;  // :189-196
+    if (!observed) return false;
+    const double gfx = dsub(qx, fcx), gfy = dsub(qy, fcy), gfz = dsub(qz, fcz);
+    const double ofx = dsub(1.0, gfx), ofy = dsub(1.0, gfy), ofz = dsub(1.0, gfz);
+    const float c000 = cell.c[0].x, c100 = cell.c[1].x, c010 = cell.c[2].x, c110 = cell.c[3].x,
+                c001 = cell.c[4].x, c101 = cell.c[5].x, c011 = cell.c[6].x, c111 = cell.c[7].x;
+    double gx = dadd(dadd(dadd(gterm(c100, c000, ofy, ofz), gterm(c110, c010, gfy, ofz)),
+                          gterm(c101, c001, ofy, gfz)),
+                     gterm(c111, c011, gfy, gfz));                          // :209-214
+    double gy = dadd(dadd(dadd(gterm(c010, c000, ofx, ofz), gterm(c110, c100, gfx, ofz)),
+                          gterm(c011, c001, ofx, gfz)),
+                     gterm(c111, c101, gfx, gfz));                          // :215-220
+    double gz = dadd(dadd(dadd(gterm(c001, c000, ofx, ofy), gterm(c011, c010, ofx, gfy)),
+                          gterm(c101, c100, gfx, ofy)),
+                     gterm(c111, c110, gfx, gfy));                          // :221-226
+    const double gnorm = dsqrt(dadd(dadd(dmul(gx, gx), dmul(gy, gy)), dmul(gz, gz)));
+    if (!(gnorm > 0.0)) return false;
+    if (dadd(dadd(dmul(gx, r.dx), dmul(gy, r.dy)), dmul(gz, r.dz)) > 0.0) {
+        gx = -gx;
+        gy = -gy;
+        gz = -gz;
+    }
+    hit.t = tstar;
+    hit.hx = hx;
+    hit.hy = hy;
+    hit.hz = hz;
+    hit.nx = ddiv(gx, gnorm);
+    hit.ny = ddiv(gy, gnorm);
+    hit.nz = ddiv(gz, gnorm);
+    return true;
+}
+
 // _scan_crossing (_kernels.py:136-243)
 __device__ bool scan_crossing(Ray &r, int64_t scan_from, int64_t scan_end, bool sp_valid,
                               double sp_v, Hit &hit) {
-    const double delta = r.vs;
-    const double hi = (double)(r.n - 2);
     for (int64_t k = scan_from; k <= scan_end; ++k) {
         double s = 0.0;
         const bool sv = sample_at(r, k, s);
-        if (sp_valid && sp_v > 0.0 && sv && s <= 0.0) {
-            const double ta = dmul((double)(k - 1), delta);
-            const double tstar = dadd(ta, dmul(delta, ddiv(sp_v, dsub(sp_v, s))));  // :171
-            if (tstar >= 0.0) {
-                const double hx = dadd(r.ox, dmul(tstar, r.dx));
-                const double hy = dadd(r.oy, dmul(tstar, r.dy));
-                const double hz = dadd(r.oz, dmul(tstar, r.dz));
-                const double qx = dsub(ddiv(hx, r.vs), r.htx);
-                const double qy = dsub(ddiv(hy, r.vs), r.hty);
-                const double qz = dsub(ddiv(hz, r.vs), r.htz);
-                const double fcx = floor(qx), fcy = floor(qy), fcz = floor(qz);
-                if (fcx >= 0.0 && fcy >= 0.0 && fcz >= 0.0 && fcx <= hi && fcy <= hi && fcz <= hi) {
-                    Cell cell;
-                    load_cell(r.vox, r.n, (int64_t)fcx, (int64_t)fcy, (int64_t)fcz, cell);
-                    bool observed = true;
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) observed &= cell.c[q].y > 0.0f;  // :189-196
-                    if (observed) {
-                        const double gfx = dsub(qx, fcx), gfy = dsub(qy, fcy), gfz = dsub(qz, fcz);
-                        const double ofx = dsub(1.0, gfx), ofy = dsub(1.0, gfy), ofz = dsub(1.0, gfz);
-                        const float c000 = cell.c[0].x, c100 = cell.c[1].x, c010 = cell.c[2].x,
-                                    c110 = cell.c[3].x, c001 = cell.c[4].x, c101 = cell.c[5].x,
-                                    c011 = cell.c[6].x, c111 = cell.c[7].x;
-                        double gx = dadd(dadd(dadd(gterm(c100, c000, ofy, ofz),
-                                                   gterm(c110, c010, gfy, ofz)),
-                                              gterm(c101, c001, ofy, gfz)),
-                                         gterm(c111, c011, gfy, gfz));                 // :209-214
-                        double gy = dadd(dadd(dadd(gterm(c010, c000, ofx, ofz),
-                                                   gterm(c110, c100, gfx, ofz)),
-                                              gterm(c011, c001, ofx, gfz)),
-                                         gterm(c111, c101, gfx, gfz));                 // :215-220
-                        double gz = dadd(dadd(dadd(gterm(c001, c000, ofx, ofy),
-                                                   gterm(c011, c010, ofx, gfy)),
-                                              gterm(c101, c100, gfx, ofy)),
-                                         gterm(c111, c110, gfx, gfy));                 // :221-226
-                        const double gnorm =
-                            dsqrt(dadd(dadd(dmul(gx, gx), dmul(gy, gy)), dmul(gz, gz)));
-                        if (gnorm > 0.0) {
-                            if (dadd(dadd(dmul(gx, r.dx), dmul(gy, r.dy)), dmul(gz, r.dz)) > 0.0) {
-                                gx = -gx;
-                                gy = -gy;
-                                gz = -gz;
-                            }
-                            hit.t = tstar;
-                            hit.hx = hx;
-                            hit.hy = hy;
-                            hit.hz = hz;
-                            hit.nx = ddiv(gx, gnorm);
-                            hit.ny = ddiv(gy, gnorm);
-                            hit.nz = ddiv(gz, gnorm);
-                            return true;
-                        }
-                    }
-                }
-            }
-        }
+        if (sp_valid && sp_v > 0.0 && sv && s <= 0.0 && accept_crossing(r, k, sp_v, s, hit))
+            return true;                                               // :169-240
         sp_valid = sv;
         sp_v = s;
     }
@@ -219,7 +216,7 @@ __device__ __forceinline__ bool ray_interval(const TfVolume &vol, const double o
 
 // The per-volume march of raycast_kernel (_kernels.py:349-451), merging into
 // `best`.  Returns whether `best` changed.
-__device__ bool march_volume(Ray &r, int64_t j, int64_t j_end, int64_t coarse,
+__device__ __noinline__ bool march_volume(Ray &r, int64_t j, int64_t j_end, int64_t coarse,
                              double near_thresh, Hit &best) {
     bool prev_has = false;
     double prev_v = 0.0;
@@ -290,6 +287,171 @@ __device__ bool march_volume(Ray &r, int64_t j, int64_t j_end, int64_t coarse,
     return false;
 }
 
+
+// ---- certified fast march -------------------------------------------------
+//
+// The reference samples the lattice point k at q = (o + (k vs) d) / vs - ht,
+// i.e. q ~= q0 + k d with q0 = o / vs - ht; the difference between the
+// reference's rounded q and fma(k, d, q0) is < 1e-9 voxel here (|q|, k,
+// |o / vs|, |ht| < 1e6).  fast_sample() takes floor(q) from a 20-bit fixed
+// point of q and evaluates the trilinear value in float32, then CERTIFIES
+// every decision the march takes from the sample: the cell index (q farther
+// than 4 * 2^-20 from an integer), validity (exact weights), the sign
+// (|value| > 2e-5 max|corner|, > 5x the float32 + fixed-point error) and the
+// near-surface test (| |value| - 0.99 tau | above the same bound).  An
+// uncertain sample makes the caller redo the whole ray-volume march with the
+// exact reference arithmetic; a crossing is recomputed from the two exact
+// samples (k-1, k) and accepted with the reference's exact arithmetic.  So
+// every output bit is the reference's, at ~6 float64 ops per sample instead
+// of 3 divisions and 11 conversions.
+
+enum : int { kInvalid = 0, kValid = 1, kUnsure = 2 };
+
+struct FastRay {
+    const float2 *vox;
+    int n;
+    double q0x, q0y, q0z, dx, dy, dz;
+    float near, near_tol;
+};
+
+__device__ __forceinline__ bool fixed_cell(double q, unsigned &i, float &fr) {
+    const double t = dadd(q, 6442450944.0);  // 1.5 * 2^32: ulp(t) = 2^-20
+    const unsigned lo = (unsigned)__double2loint(t);
+    const unsigned fq = lo & 0xFFFFFu;
+    i = lo >> 20;
+    fr = (float)fq * 9.5367431640625e-07f;  // 2^-20
+    return fq - 4u <= (1u << 20) - 9u;       // 4 <= fq <= 2^20 - 5: floor is certain
+}
+
+__device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
+
+__device__ __forceinline__ int fast_sample(const FastRay &r, int64_t k, float &value) {
+    const double kd = (double)k;
+    unsigned ix, iy, iz;
+    float fx, fy, fz;
+    const bool cx = fixed_cell(dfma(kd, r.dx, r.q0x), ix, fx);
+    const bool cy = fixed_cell(dfma(kd, r.dy, r.q0y), iy, fy);
+    const bool cz = fixed_cell(dfma(kd, r.dz, r.q0z), iz, fz);
+    if (!(cx && cy && cz)) return kUnsure;
+    const unsigned hi = (unsigned)(r.n - 2);
+    if (ix > hi || iy > hi || iz > hi) return kInvalid;              // :38
+    const unsigned n = (unsigned)r.n;
+    const float2 *b = r.vox + ((size_t)(iz * n + iy) * n + ix);
+    const float2 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + n), c110 = __ldg(b + n + 1);
+    const float2 c001 = __ldg(b + n * n), c101 = __ldg(b + n * n + 1);
+    const float2 c011 = __ldg(b + n * n + n), c111 = __ldg(b + n * n + n + 1);
+    const float wmin = fminf(fminf(fminf(c000.y, c100.y), fminf(c010.y, c110.y)),
+                             fminf(fminf(c001.y, c101.y), fminf(c011.y, c111.y)));
+    if (wmin <= 0.0f) return kInvalid;                                // :40-50
+    const float v = lerpf(lerpf(lerpf(c000.x, c100.x, fx), lerpf(c010.x, c110.x, fx), fy),
+                          lerpf(lerpf(c001.x, c101.x, fx), lerpf(c011.x, c111.x, fx), fy), fz);
+    const float cmax = fmaxf(fmaxf(fmaxf(fabsf(c000.x), fabsf(c100.x)), fmaxf(fabsf(c010.x), fabsf(c110.x))),
+                             fmaxf(fmaxf(fabsf(c001.x), fabsf(c101.x)), fmaxf(fabsf(c011.x), fabsf(c111.x))));
+    const float ev = 2e-5f * cmax + 1e-30f;
+    const float av = fabsf(v);
+    if (av <= ev || fabsf(av - r.near) <= ev + r.near_tol) return kUnsure;
+    value = v;
+    return kValid;
+}
+
+// _scan_crossing with certified samples; the crossing itself is exact.
+// Returns 1 (hit in `hit`), 0 (none) or -1 (uncertain: redo exactly).
+__device__ __forceinline__ int scan_fast(const FastRay &fr, const Ray &er, int64_t from, int64_t end,
+                                         bool sp_valid, float sp_v, Hit &hit,
+                                         unsigned long long &samples) {
+    for (int64_t k = from; k <= end; ++k) {
+        float s = 0.f;
+        const int st = fast_sample(fr, k, s);
+        ++samples;
+        if (st == kUnsure) return -1;
+        const bool sv = st == kValid;
+        if (sp_valid && sp_v > 0.f && sv && s <= 0.f) {
+            Ray r = er;
+            double e0 = 0.0, e1 = 0.0;
+            const bool v0 = sample_at(r, k - 1, e0), v1 = sample_at(r, k, e1);
+            if (!v0 || !v1 || !(e0 > 0.0) || !(e1 <= 0.0)) return -1;  // never, if certified
+            if (accept_crossing(r, k, e0, e1, hit)) return 1;
+        }
+        sp_valid = sv;
+        sp_v = s;
+    }
+    return 0;
+}
+
+// march_volume with certified samples: 1 = best changed, 0 = not, -1 = redo exactly.
+__device__ int march_fast(const FastRay &fr, const Ray &er, int64_t j, int64_t j_end, int64_t coarse,
+                          Hit &best, unsigned long long &samples) {
+    bool prev_has = false;
+    float prev_v = 0.f;
+    int64_t prev_j = -1, last_j = j - 1, swept_j = j - 1;
+    while (j <= j_end) {
+        float value = 0.f;
+        const int st = fast_sample(fr, j, value);
+        ++samples;
+        if (st == kUnsure) return -1;
+        const bool valid = st == kValid;
+        bool do_scan = false;
+        if (!valid || value <= 0.f) {                                   // :362-369
+            if (prev_has && prev_v > 0.f)
+                do_scan = true;
+            else if (swept_j < j - 1 && (valid || coarse > 2))
+                do_scan = true;
+        }
+        if (do_scan) {
+            const int64_t scan_from = (prev_j > swept_j ? prev_j : swept_j) + 1;
+            const int64_t k0 = scan_from - 1;
+            bool sp_valid = true;
+            float sp_v = prev_v;
+            if (!(prev_has && k0 == prev_j)) {
+                const int s0 = fast_sample(fr, k0, sp_v);
+                ++samples;
+                if (s0 == kUnsure) return -1;
+                sp_valid = s0 == kValid;
+            }
+            Hit h;
+            const int found = scan_fast(fr, er, scan_from, j, sp_valid, sp_v, h, samples);
+            if (found < 0) return -1;
+            swept_j = j;
+            if (found) {
+                if (hit_wins(h, best)) {
+                    best = h;
+                    return 1;
+                }
+                return 0;
+            }
+        }
+        last_j = j;
+        if (valid) {
+            prev_has = true;
+            prev_v = value;
+            prev_j = j;
+            j = fabsf(value) < fr.near ? j + 1 : (j / coarse + 1) * coarse;
+        } else {
+            j = (j / coarse + 1) * coarse;
+        }
+    }
+    const int64_t scan_from = (last_j > swept_j ? last_j : swept_j) + 1;  // :417-451
+    if (scan_from <= j_end) {
+        const int64_t k0 = scan_from - 1;
+        bool sp_valid = true;
+        float sp_v = prev_v;
+        if (!(prev_has && k0 == prev_j)) {
+            const int s0 = fast_sample(fr, k0, sp_v);
+            ++samples;
+            if (s0 == kUnsure) return -1;
+            sp_valid = s0 == kValid;
+        }
+        Hit h;
+        const int found = scan_fast(fr, er, scan_from, j_end, sp_valid, sp_v, h, samples);
+        if (found < 0) return -1;
+        if (found && hit_wins(h, best)) {
+            best = h;
+            return 1;
+        }
+    }
+    return 0;
+}
+
 constexpr int kRayBlockX = 8, kRayBlockY = 16;  // 128 threads; warp = 8x4 pixels
 
 __global__ void __launch_bounds__(128) raycast_kernel(
@@ -300,7 +462,7 @@ __global__ void __launch_bounds__(128) raycast_kernel(
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t px = (int64_t)blockIdx.x * kRayBlockX + (lane & 7);
     const int64_t py = (int64_t)blockIdx.y * kRayBlockY + w * 4 + (lane >> 3);
-    unsigned long long samples = 0, hits = 0;
+    unsigned long long samples = 0, hits = 0, exact_marches = 0;
     if (px < g.width && py < g.height) {
         const int64_t p = py * g.width + px;
         Hit best;
@@ -355,8 +517,24 @@ __global__ void __launch_bounds__(128) raycast_kernel(
             r.dy = d[1];
             r.dz = d[2];
             r.samples = 0;
-            changed |= march_volume(r, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
-            samples += r.samples;
+            int res = -1;
+            const double q0x = dsub(ddiv(o[0], r.vs), r.htx);
+            const double q0y = dsub(ddiv(o[1], r.vs), r.hty);
+            const double q0z = dsub(ddiv(o[2], r.vs), r.htz);
+            const double mag = fabs(q0x) + fabs(q0y) + fabs(q0z) + fabs(r.htx) + fabs(r.hty) +
+                               fabs(r.htz) + (double)jhi[pick];
+            if (!g.exact_only && vol.n <= 4000 && mag < 1e6) {
+                FastRay fr{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
+                           (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f};
+                res = march_fast(fr, r, jlo[pick], jhi[pick], g.coarse, best, samples);
+            }
+            if (res < 0) {  // uncertain somewhere (or forced): the exact reference march
+                changed |= march_volume(r, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
+                samples += r.samples;
+                exact_marches += 1;
+            } else {
+                changed |= res > 0;
+            }
         }
         if (changed) {
             hits = 1;
@@ -372,6 +550,7 @@ __global__ void __launch_bounds__(128) raycast_kernel(
     if (stats) {
         warp_count_add(&stats[TF_STAT_RAY_SAMPLES], samples);
         warp_count_add(&stats[TF_STAT_RAY_HITS], hits);
+        warp_count_add(&stats[TF_STAT_EXACT_MARCHES], exact_marches);
     }
 }
 
@@ -432,6 +611,7 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
     g.height = cam->height;
     g.near_thresh = 0.99 * tau;
     g.coarse = coarse_step;
+    g.exact_only = (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) ? 1 : 0;
     dim3 grid((unsigned)((cam->width + kRayBlockX - 1) / kRayBlockX),
               (unsigned)((cam->height + kRayBlockY - 1) / kRayBlockY));
     for (int first = 0; first < nvol; first += TFB200_MAX_VOLUMES_PER_LAUNCH) {

@@ -320,3 +320,34 @@ def test_saturated_fixed_point_shortcut_is_exact():
             == stats[2][nat.STAT_VOXEL_UPDATES].item())
     assert torch.equal(vols[0].voxels, vols[2].voxels)
     assert torch.equal(vols[1].voxels, vols[2].voxels)
+
+
+def test_certified_raycast_equals_exact_march_full_size():
+    """Config-3 volumes, several views: certified fast march == exact reference march."""
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(4.08, 1020, 510)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    tiles = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length)
+             for k in spec.keys]
+    scene = demo_scene()
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)
+    for pose in poses[:8]:
+        tf.integrate_volumes(tiles, scene.render_depth(pose, intr), pose, intr, params)
+    lib = nat.load_library()
+    stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
+    try:
+        for pose in (poses[3], poses[7], poses[20]):
+            fast = tf.RayMap.empty(intr)
+            lib.tf_set_debug_flags(0)
+            tf.raycast_volumes(tiles, pose, intr, fast, params, stats)
+            exact = tf.RayMap.empty(intr)
+            lib.tf_set_debug_flags(nat.DEBUG_EXACT_ONLY)
+            tf.raycast_volumes(tiles, pose, intr, exact, params)
+            assert torch.isfinite(exact.distance_dev).sum().item() > 100000
+            assert torch.equal(fast.distance_dev, exact.distance_dev)
+            assert torch.equal(fast.vertices_dev, exact.vertices_dev)
+            assert torch.equal(fast.normals_dev, exact.normals_dev)
+    finally:
+        lib.tf_set_debug_flags(0)
+    # the certified path must carry the bulk of the work
+    assert stats[nat.STAT_EXACT_MARCHES].item() < 0.01 * 3 * intr.width * intr.height
