@@ -269,7 +269,8 @@ def run_ours(args) -> None:
                                                   (("pixel_rounding", nat.STAT_EXACT_PROJ), ("camera_plane", nat.STAT_EXACT_PLANE), ("sdf_band", nat.STAT_EXACT_SDF))},
                       "active_bricks_per_frame": sum_over_ranks(int(st[nat.STAT_ACTIVE_BRICKS])) / args.steps,
                       "total_bricks": sum_over_ranks(int(st[nat.STAT_TOTAL_BRICKS])) // max(args.steps, 1)},
-        "raycast": {"exact_marches_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_MARCHES])) / args.steps,
+        "raycast": {"exact_samples_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_SAMPLES])) / args.steps,
+                    "certification_failures": sum_over_ranks(int(st[nat.STAT_CERT_FAILURES])),
                     "samples_per_frame": samples / args.steps,
                     "samples_per_s": samples / (ms_total / 1e3)},
         "gpu_launches": int(launches),

@@ -70,7 +70,8 @@ enum {
     TF_STAT_EXACT_PROJ = 8,    /* ... deferred: pixel rounding too close to call */
     TF_STAT_EXACT_PLANE = 9,   /* ... deferred: on the camera plane */
     TF_STAT_EXACT_SDF = 10,    /* ... deferred: sdf within the +-tau band */
-    TF_STAT_EXACT_MARCHES = 11, /* ray-volume marches redone with the exact arithmetic */
+    TF_STAT_EXACT_SAMPLES = 11, /* ray samples evaluated with the exact arithmetic */
+    TF_STAT_CERT_FAILURES = 12, /* certified decisions contradicted by exact ones (must be 0) */
     TF_STAT_COUNT = 16
 };
 

@@ -305,13 +305,19 @@ __device__ __noinline__ bool march_volume(Ray &r, int64_t j, int64_t j_end, int6
 // every output bit is the reference's, at ~6 float64 ops per sample instead
 // of 3 divisions and 11 conversions.
 
-enum : int { kInvalid = 0, kValid = 1, kUnsure = 2 };
+// The march only ever consumes three facts about a sample: valid, value > 0
+// and |value| < 0.99 tau.  fast_sample() returns them certified, or kUnsure
+// when any of them is too close to call; an unsure sample is then evaluated
+// with the exact reference arithmetic (sample_at), so every decision is the
+// reference's.
+enum : unsigned { kValidBit = 1u, kPosBit = 2u, kNearBit = 4u, kUnsure = 8u };
 
 struct FastRay {
     const float2 *vox;
     int n;
     double q0x, q0y, q0z, dx, dy, dz;
     float near, near_tol;
+    double near_thresh;
 };
 
 __device__ __forceinline__ bool fixed_cell(double q, unsigned &i, float &fr) {
@@ -325,7 +331,7 @@ __device__ __forceinline__ bool fixed_cell(double q, unsigned &i, float &fr) {
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 
-__device__ __forceinline__ int fast_sample(const FastRay &r, int64_t k, float &value) {
+__device__ __forceinline__ unsigned fast_sample(const FastRay &r, int64_t k) {
     const double kd = (double)k;
     unsigned ix, iy, iz;
     float fx, fy, fz;
@@ -334,7 +340,7 @@ __device__ __forceinline__ int fast_sample(const FastRay &r, int64_t k, float &v
     const bool cz = fixed_cell(dfma(kd, r.dz, r.q0z), iz, fz);
     if (!(cx && cy && cz)) return kUnsure;
     const unsigned hi = (unsigned)(r.n - 2);
-    if (ix > hi || iy > hi || iz > hi) return kInvalid;              // :38
+    if (ix > hi || iy > hi || iz > hi) return 0u;                     // invalid (:38)
     const unsigned n = (unsigned)r.n;
     const float2 *b = r.vox + ((size_t)(iz * n + iy) * n + ix);
     const float2 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + n), c110 = __ldg(b + n + 1);
@@ -342,7 +348,7 @@ __device__ __forceinline__ int fast_sample(const FastRay &r, int64_t k, float &v
     const float2 c011 = __ldg(b + n * n + n), c111 = __ldg(b + n * n + n + 1);
     const float wmin = fminf(fminf(fminf(c000.y, c100.y), fminf(c010.y, c110.y)),
                              fminf(fminf(c001.y, c101.y), fminf(c011.y, c111.y)));
-    if (wmin <= 0.0f) return kInvalid;                                // :40-50
+    if (wmin <= 0.0f) return 0u;                                      // invalid (:40-50)
     const float v = lerpf(lerpf(lerpf(c000.x, c100.x, fx), lerpf(c010.x, c110.x, fx), fy),
                           lerpf(lerpf(c001.x, c101.x, fx), lerpf(c011.x, c111.x, fx), fy), fz);
     const float cmax = fmaxf(fmaxf(fmaxf(fabsf(c000.x), fabsf(c100.x)), fmaxf(fabsf(c010.x), fabsf(c110.x))),
@@ -350,49 +356,62 @@ __device__ __forceinline__ int fast_sample(const FastRay &r, int64_t k, float &v
     const float ev = 2e-5f * cmax + 1e-30f;
     const float av = fabsf(v);
     if (av <= ev || fabsf(av - r.near) <= ev + r.near_tol) return kUnsure;
-    value = v;
-    return kValid;
+    return kValidBit | (v > 0.f ? kPosBit : 0u) | (av < r.near ? kNearBit : 0u);
 }
 
-// _scan_crossing with certified samples; the crossing itself is exact.
-// Returns 1 (hit in `hit`), 0 (none) or -1 (uncertain: redo exactly).
-__device__ __forceinline__ int scan_fast(const FastRay &fr, const Ray &er, int64_t from, int64_t end,
-                                         bool sp_valid, float sp_v, Hit &hit,
-                                         unsigned long long &samples) {
+// certified decisions of lattice point k (exact fallback when unsure)
+__device__ __forceinline__ unsigned cert_sample(const FastRay &fr, const Ray &er, int64_t k,
+                                                unsigned long long &samples,
+                                                unsigned long long &exact_samples) {
+    ++samples;
+    const unsigned s = fast_sample(fr, k);
+    if (!(s & kUnsure)) return s;
+    ++exact_samples;
+    Ray r = er;
+    double v = 0.0;
+    if (!sample_at(r, k, v)) return 0u;
+    return kValidBit | (v > 0.0 ? kPosBit : 0u) | (fabs(v) < fr.near_thresh ? kNearBit : 0u);
+}
+
+// _scan_crossing on certified decisions; the crossing itself is exact.
+// Returns whether a crossing was accepted (into `hit`).
+__device__ __forceinline__ bool scan_fast(const FastRay &fr, const Ray &er, int64_t from, int64_t end,
+                                          unsigned sp, Hit &hit, unsigned long long &samples,
+                                          unsigned long long &exact_samples) {
     for (int64_t k = from; k <= end; ++k) {
-        float s = 0.f;
-        const int st = fast_sample(fr, k, s);
-        ++samples;
-        if (st == kUnsure) return -1;
-        const bool sv = st == kValid;
-        if (sp_valid && sp_v > 0.f && sv && s <= 0.f) {
+        const unsigned s = cert_sample(fr, er, k, samples, exact_samples);
+        // sp_valid and sp_v > 0 and sv and s <= 0 (:169)
+        if ((sp & (kValidBit | kPosBit)) == (kValidBit | kPosBit) && (s & (kValidBit | kPosBit)) == kValidBit) {
             Ray r = er;
             double e0 = 0.0, e1 = 0.0;
             const bool v0 = sample_at(r, k - 1, e0), v1 = sample_at(r, k, e1);
-            if (!v0 || !v1 || !(e0 > 0.0) || !(e1 <= 0.0)) return -1;  // never, if certified
-            if (accept_crossing(r, k, e0, e1, hit)) return 1;
+            exact_samples += 2;
+            if (!v0 || !v1 || !(e0 > 0.0) || !(e1 <= 0.0)) {
+                // a certified decision disagreed with the exact arithmetic: never
+                // expected; counted (TF_STAT_CERT_FAILURES) so tests catch it
+                exact_samples += 1ull << 40;
+            } else if (accept_crossing(r, k, e0, e1, hit)) {
+                return true;
+            }
         }
-        sp_valid = sv;
-        sp_v = s;
+        sp = s;
     }
-    return 0;
+    return false;
 }
 
-// march_volume with certified samples: 1 = best changed, 0 = not, -1 = redo exactly.
-__device__ int march_fast(const FastRay &fr, const Ray &er, int64_t j, int64_t j_end, int64_t coarse,
-                          Hit &best, unsigned long long &samples) {
+// march_volume on certified decisions (_kernels.py:349-451); same control flow.
+// Returns whether `best` changed.
+__device__ bool march_fast(const FastRay &fr, const Ray &er, int64_t j, int64_t j_end, int64_t coarse,
+                           Hit &best, unsigned long long &samples, unsigned long long &exact_samples) {
+    unsigned prev = 0u;  // decisions of the last valid march sample
     bool prev_has = false;
-    float prev_v = 0.f;
     int64_t prev_j = -1, last_j = j - 1, swept_j = j - 1;
     while (j <= j_end) {
-        float value = 0.f;
-        const int st = fast_sample(fr, j, value);
-        ++samples;
-        if (st == kUnsure) return -1;
-        const bool valid = st == kValid;
+        const unsigned s = cert_sample(fr, er, j, samples, exact_samples);
+        const bool valid = s & kValidBit;
         bool do_scan = false;
-        if (!valid || value <= 0.f) {                                   // :362-369
-            if (prev_has && prev_v > 0.f)
+        if (!valid || !(s & kPosBit)) {                                 // :362-369
+            if (prev_has && (prev & kPosBit))
                 do_scan = true;
             else if (swept_j < j - 1 && (valid || coarse > 2))
                 do_scan = true;
@@ -400,32 +419,24 @@ __device__ int march_fast(const FastRay &fr, const Ray &er, int64_t j, int64_t j
         if (do_scan) {
             const int64_t scan_from = (prev_j > swept_j ? prev_j : swept_j) + 1;
             const int64_t k0 = scan_from - 1;
-            bool sp_valid = true;
-            float sp_v = prev_v;
-            if (!(prev_has && k0 == prev_j)) {
-                const int s0 = fast_sample(fr, k0, sp_v);
-                ++samples;
-                if (s0 == kUnsure) return -1;
-                sp_valid = s0 == kValid;
-            }
+            const unsigned sp = (prev_has && k0 == prev_j) ? prev : cert_sample(fr, er, k0, samples, exact_samples);
             Hit h;
-            const int found = scan_fast(fr, er, scan_from, j, sp_valid, sp_v, h, samples);
-            if (found < 0) return -1;
+            const bool found = scan_fast(fr, er, scan_from, j, sp, h, samples, exact_samples);
             swept_j = j;
             if (found) {
                 if (hit_wins(h, best)) {
                     best = h;
-                    return 1;
+                    return true;
                 }
-                return 0;
+                return false;
             }
         }
         last_j = j;
         if (valid) {
             prev_has = true;
-            prev_v = value;
+            prev = s;
             prev_j = j;
-            j = fabsf(value) < fr.near ? j + 1 : (j / coarse + 1) * coarse;
+            j = (s & kNearBit) ? j + 1 : (j / coarse + 1) * coarse;
         } else {
             j = (j / coarse + 1) * coarse;
         }
@@ -433,23 +444,14 @@ __device__ int march_fast(const FastRay &fr, const Ray &er, int64_t j, int64_t j
     const int64_t scan_from = (last_j > swept_j ? last_j : swept_j) + 1;  // :417-451
     if (scan_from <= j_end) {
         const int64_t k0 = scan_from - 1;
-        bool sp_valid = true;
-        float sp_v = prev_v;
-        if (!(prev_has && k0 == prev_j)) {
-            const int s0 = fast_sample(fr, k0, sp_v);
-            ++samples;
-            if (s0 == kUnsure) return -1;
-            sp_valid = s0 == kValid;
-        }
+        const unsigned sp = (prev_has && k0 == prev_j) ? prev : cert_sample(fr, er, k0, samples, exact_samples);
         Hit h;
-        const int found = scan_fast(fr, er, scan_from, j_end, sp_valid, sp_v, h, samples);
-        if (found < 0) return -1;
-        if (found && hit_wins(h, best)) {
+        if (scan_fast(fr, er, scan_from, j_end, sp, h, samples, exact_samples) && hit_wins(h, best)) {
             best = h;
-            return 1;
+            return true;
         }
     }
-    return 0;
+    return false;
 }
 
 constexpr int kRayBlockX = 8, kRayBlockY = 16;  // 128 threads; warp = 8x4 pixels
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(128) raycast_kernel(
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t px = (int64_t)blockIdx.x * kRayBlockX + (lane & 7);
     const int64_t py = (int64_t)blockIdx.y * kRayBlockY + w * 4 + (lane >> 3);
-    unsigned long long samples = 0, hits = 0, exact_marches = 0;
+    unsigned long long samples = 0, hits = 0, exact_samples = 0;
     if (px < g.width && py < g.height) {
         const int64_t p = py * g.width + px;
         Hit best;
@@ -517,7 +519,6 @@ __global__ void __launch_bounds__(128) raycast_kernel(
             r.dy = d[1];
             r.dz = d[2];
             r.samples = 0;
-            int res = -1;
             const double q0x = dsub(ddiv(o[0], r.vs), r.htx);
             const double q0y = dsub(ddiv(o[1], r.vs), r.hty);
             const double q0z = dsub(ddiv(o[2], r.vs), r.htz);
@@ -525,15 +526,12 @@ __global__ void __launch_bounds__(128) raycast_kernel(
                                fabs(r.htz) + (double)jhi[pick];
             if (!g.exact_only && vol.n <= 4000 && mag < 1e6) {
                 FastRay fr{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
-                           (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f};
-                res = march_fast(fr, r, jlo[pick], jhi[pick], g.coarse, best, samples);
-            }
-            if (res < 0) {  // uncertain somewhere (or forced): the exact reference march
+                           (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh};
+                changed |= march_fast(fr, r, jlo[pick], jhi[pick], g.coarse, best, samples, exact_samples);
+            } else {  // forced, or coordinates too large to certify: the exact reference march
                 changed |= march_volume(r, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
                 samples += r.samples;
-                exact_marches += 1;
-            } else {
-                changed |= res > 0;
+                exact_samples += r.samples;
             }
         }
         if (changed) {
@@ -550,7 +548,8 @@ __global__ void __launch_bounds__(128) raycast_kernel(
     if (stats) {
         warp_count_add(&stats[TF_STAT_RAY_SAMPLES], samples);
         warp_count_add(&stats[TF_STAT_RAY_HITS], hits);
-        warp_count_add(&stats[TF_STAT_EXACT_MARCHES], exact_marches);
+        warp_count_add(&stats[TF_STAT_EXACT_SAMPLES], exact_samples & ((1ull << 40) - 1));
+        warp_count_add(&stats[TF_STAT_CERT_FAILURES], exact_samples >> 40);
     }
 }
 

@@ -343,11 +343,12 @@ def test_certified_raycast_equals_exact_march_full_size():
             exact = tf.RayMap.empty(intr)
             lib.tf_set_debug_flags(nat.DEBUG_EXACT_ONLY)
             tf.raycast_volumes(tiles, pose, intr, exact, params)
-            assert torch.isfinite(exact.distance_dev).sum().item() > 100000
+            assert torch.isfinite(exact.distance_dev).sum().item() > 30000
             assert torch.equal(fast.distance_dev, exact.distance_dev)
             assert torch.equal(fast.vertices_dev, exact.vertices_dev)
             assert torch.equal(fast.normals_dev, exact.normals_dev)
     finally:
         lib.tf_set_debug_flags(0)
     # the certified path must carry the bulk of the work
-    assert stats[nat.STAT_EXACT_MARCHES].item() < 0.01 * 3 * intr.width * intr.height
+    assert stats[nat.STAT_EXACT_SAMPLES].item() < 0.02 * stats[nat.STAT_RAY_SAMPLES].item()
+    assert stats[nat.STAT_CERT_FAILURES].item() == 0
