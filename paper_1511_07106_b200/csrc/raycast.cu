@@ -16,6 +16,7 @@
 // crossing interpolation and the analytic normal — is the reference's
 // arithmetic in the reference's order.
 #include <math.h>
+#include <stdlib.h>
 
 #include "tf_common.cuh"
 
@@ -102,7 +103,7 @@ struct Ray {
 };
 
 // fine lattice point k in local voxel coordinates (:164-167, :357-359)
-__device__ __forceinline__ bool sample_at(Ray &r, int64_t k, double &value) {
+__device__ __noinline__ bool sample_at(Ray &r, int64_t k, double &value) {
     const double tk = dmul((double)k, r.vs);
     const double kx = dsub(ddiv(dadd(r.ox, dmul(tk, r.dx)), r.vs), r.htx);
     const double ky = dsub(ddiv(dadd(r.oy, dmul(tk, r.dy)), r.vs), r.hty);
@@ -119,7 +120,7 @@ __device__ __forceinline__ double gterm(float hi, float lo, double a, double b) 
 
 // Crossing acceptance of _scan_crossing (_kernels.py:170-240) for the
 // consecutive samples (k-1, k) with exact values sp_v > 0 >= s.
-__device__ bool accept_crossing(const Ray &r, int64_t k, double sp_v, double s, Hit &hit) {
+__device__ __noinline__ bool accept_crossing(const Ray &r, int64_t k, double sp_v, double s, Hit &hit) {
     const double delta = r.vs;
     const double hi = (double)(r.n - 2);
     const double ta = dmul((double)(k - 1), delta);
@@ -331,7 +332,7 @@ __device__ __forceinline__ bool fixed_cell(double q, unsigned &i, float &fr) {
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 
-__device__ __forceinline__ unsigned fast_sample(const FastRay &r, int64_t k) {
+__device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k) {
     const double kd = (double)k;
     unsigned ix, iy, iz;
     float fx, fy, fz;
@@ -360,7 +361,7 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int64_t k) {
 }
 
 // certified decisions of lattice point k (exact fallback when unsure)
-__device__ __forceinline__ unsigned cert_sample(const FastRay &fr, const Ray &er, int64_t k,
+__device__ __forceinline__ unsigned cert_sample(const FastRay &fr, const Ray &er, int k,
                                                 unsigned long long &samples,
                                                 unsigned long long &exact_samples) {
     ++samples;
@@ -375,10 +376,10 @@ __device__ __forceinline__ unsigned cert_sample(const FastRay &fr, const Ray &er
 
 // _scan_crossing on certified decisions; the crossing itself is exact.
 // Returns whether a crossing was accepted (into `hit`).
-__device__ __forceinline__ bool scan_fast(const FastRay &fr, const Ray &er, int64_t from, int64_t end,
+__device__ __forceinline__ bool scan_fast(const FastRay &fr, const Ray &er, int from, int end,
                                           unsigned sp, Hit &hit, unsigned long long &samples,
                                           unsigned long long &exact_samples) {
-    for (int64_t k = from; k <= end; ++k) {
+    for (int k = from; k <= end; ++k) {
         const unsigned s = cert_sample(fr, er, k, samples, exact_samples);
         // sp_valid and sp_v > 0 and sv and s <= 0 (:169)
         if ((sp & (kValidBit | kPosBit)) == (kValidBit | kPosBit) && (s & (kValidBit | kPosBit)) == kValidBit) {
@@ -401,11 +402,12 @@ __device__ __forceinline__ bool scan_fast(const FastRay &fr, const Ray &er, int6
 
 // march_volume on certified decisions (_kernels.py:349-451); same control flow.
 // Returns whether `best` changed.
-__device__ bool march_fast(const FastRay &fr, const Ray &er, int64_t j, int64_t j_end, int64_t coarse,
+__device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_end, const int coarse,
                            Hit &best, unsigned long long &samples, unsigned long long &exact_samples) {
     unsigned prev = 0u;  // decisions of the last valid march sample
     bool prev_has = false;
-    int64_t prev_j = -1, last_j = j - 1, swept_j = j - 1;
+    int prev_j = -1, last_j = j - 1, swept_j = j - 1;
+    int phase = j % coarse;  // j mod coarse, tracked so no division runs per step
     while (j <= j_end) {
         const unsigned s = cert_sample(fr, er, j, samples, exact_samples);
         const bool valid = s & kValidBit;
@@ -417,8 +419,8 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int64_t j, int64_t 
                 do_scan = true;
         }
         if (do_scan) {
-            const int64_t scan_from = (prev_j > swept_j ? prev_j : swept_j) + 1;
-            const int64_t k0 = scan_from - 1;
+            const int scan_from = (prev_j > swept_j ? prev_j : swept_j) + 1;
+            const int k0 = scan_from - 1;
             const unsigned sp = (prev_has && k0 == prev_j) ? prev : cert_sample(fr, er, k0, samples, exact_samples);
             Hit h;
             const bool found = scan_fast(fr, er, scan_from, j, sp, h, samples, exact_samples);
@@ -436,14 +438,18 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int64_t j, int64_t 
             prev_has = true;
             prev = s;
             prev_j = j;
-            j = (s & kNearBit) ? j + 1 : (j / coarse + 1) * coarse;
-        } else {
-            j = (j / coarse + 1) * coarse;
+        }
+        if (valid && (s & kNearBit)) {  // fine step
+            ++j;
+            phase = phase + 1 == coarse ? 0 : phase + 1;
+        } else {                         // next multiple of coarse
+            j += coarse - phase;
+            phase = 0;
         }
     }
-    const int64_t scan_from = (last_j > swept_j ? last_j : swept_j) + 1;  // :417-451
+    const int scan_from = (last_j > swept_j ? last_j : swept_j) + 1;  // :417-451
     if (scan_from <= j_end) {
-        const int64_t k0 = scan_from - 1;
+        const int k0 = scan_from - 1;
         const unsigned sp = (prev_has && k0 == prev_j) ? prev : cert_sample(fr, er, k0, samples, exact_samples);
         Hit h;
         if (scan_fast(fr, er, scan_from, j_end, sp, h, samples, exact_samples) && hit_wins(h, best)) {
@@ -456,7 +462,8 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int64_t j, int64_t 
 
 constexpr int kRayBlockX = 8, kRayBlockY = 16;  // 128 threads; warp = 8x4 pixels
 
-__global__ void __launch_bounds__(128) raycast_kernel(
+template <int kMinBlocks>
+__global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ RayGeom g,
     double *__restrict__ out_dist, double *__restrict__ out_vert, double *__restrict__ out_norm,
     unsigned long long *__restrict__ stats) {
@@ -524,10 +531,11 @@ __global__ void __launch_bounds__(128) raycast_kernel(
             const double q0z = dsub(ddiv(o[2], r.vs), r.htz);
             const double mag = fabs(q0x) + fabs(q0y) + fabs(q0z) + fabs(r.htx) + fabs(r.hty) +
                                fabs(r.htz) + (double)jhi[pick];
-            if (!g.exact_only && vol.n <= 4000 && mag < 1e6) {
+            if (!g.exact_only && vol.n <= 4000 && mag < 1e6 && jhi[pick] < (1 << 30) && g.coarse < (1 << 20)) {
                 FastRay fr{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
                            (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh};
-                changed |= march_fast(fr, r, jlo[pick], jhi[pick], g.coarse, best, samples, exact_samples);
+                changed |= march_fast(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
+                                      exact_samples);
             } else {  // forced, or coordinates too large to certify: the exact reference march
                 changed |= march_volume(r, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
                 samples += r.samples;
@@ -623,8 +631,16 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
                 return tf_set_error(TF_EINVAL, "tf_raycast: bad volume %d", first + v);
         }
         void *prof = tf_profile_begin(TF_PROF_RAYCAST, stream);
-        raycast_kernel<<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm,
-                                                 (unsigned long long *)stats);
+        static const int minb = [] {
+            const char *e = getenv("TFB200_RAY_MINBLOCKS");  // tuning knob
+            return e ? atoi(e) : 5;
+        }();
+        if (minb == 4)
+            raycast_kernel<4><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats);
+        else if (minb == 6)
+            raycast_kernel<6><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats);
+        else
+            raycast_kernel<5><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats);
         tf_profile_end(prof, stream);
         int rc = tf_check_launch("raycast_kernel");
         if (rc) return rc;
