@@ -43,12 +43,23 @@ enum {
     TF_ECUDA = -2,   /* CUDA launch / runtime error */
 };
 
-/* One TSDF subvolume resident on the device (tsdf.py:41-107). */
+/* One TSDF subvolume resident on the device (tsdf.py:41-107).
+ *
+ * brick_bad_dev (optional, may be NULL): uint32 per 8^3 brick (x fastest,
+ * ceil(n/8)^3 entries) counting the brick's voxels that are NOT "observed and
+ * >= summary_threshold".  Built by tf_brick_summary for a truncation tau
+ * (summary_threshold = tf_good_threshold(tau)) and kept exact by
+ * tf_integrate; tf_raycast uses it to certify free-space samples without
+ * gathering voxels.  Ignored (not used, not maintained) when NULL or when
+ * summary_threshold does not match the call's tau. */
 typedef struct TfVolume {
     void *voxels_dev;    /* float2[n][n][n]: (tsdf, weight), x fastest */
     int64_t n;           /* voxels_per_side */
     int64_t origin[3];   /* origin_voxel: global voxel of local (0,0,0) */
     double voxel_size;   /* side_length / voxels_per_side (tsdf.py:80-82) */
+    uint32_t *brick_bad_dev;
+    float summary_threshold;
+    int32_t reserved;
 } TfVolume;
 
 /* Pinhole intrinsics of one pyramid level (geometry.py:27-57). */
@@ -126,6 +137,10 @@ int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
  * `npoints` world points (f64 [N][3]); writes value and validity per point. */
 int tf_trilinear_sample(const TfVolume *vol, const double *points_dev, int64_t npoints,
                         double *values_dev, uint8_t *valid_dev, void *stream);
+
+/* ---- free-space brick summaries (see TfVolume.brick_bad_dev). */
+float tf_good_threshold(double tau);
+int tf_brick_summary(const TfVolume *vol, void *stream);
 
 /* ---- raymap merge: _hit_wins (_kernels.py:246-263) of a partial map into
  * `dst` (the cross-GPU reduction of DESIGN.md "Multi-GPU"). */

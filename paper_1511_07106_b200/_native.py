@@ -28,7 +28,8 @@ _c_sz = ctypes.c_size_t
 
 class TfVolume(ctypes.Structure):
     _fields_ = [("voxels_dev", _c_p), ("n", _c_i64), ("origin", _c_i64 * 3),
-                ("voxel_size", _c_d)]
+                ("voxel_size", _c_d), ("brick_bad_dev", _c_p), ("summary_threshold", ctypes.c_float),
+                ("reserved", ctypes.c_int32)]
 
 
 class TfCamera(ctypes.Structure):
@@ -74,6 +75,8 @@ _SIGNATURES = {
     "tf_raycast": (_c_int, [_VOL, _c_int, _CAM, _c_d, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
                             _c_p, _c_p]),
     "tf_trilinear_sample": (_c_int, [_VOL, _c_p, _c_i64, _c_p, _c_p, _c_p]),
+    "tf_good_threshold": (ctypes.c_float, [_c_d]),
+    "tf_brick_summary": (_c_int, [_VOL, _c_p]),
     "tf_raymap_merge": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p]),
     "tf_vertex_normal_map": (_c_int, [_c_p, _c_i64, _c_i64, _c_int, _CAM, _c_p, _c_p, _c_p,
                                       _c_p]),
@@ -163,10 +166,12 @@ def camera(intr) -> TfCamera:
                     int(intr.width), int(intr.height))
 
 
-def volume_struct(voxels: torch.Tensor, n: int, origin, voxel_size: float) -> TfVolume:
+def volume_struct(voxels: torch.Tensor, n: int, origin, voxel_size: float,
+                  brick_bad: torch.Tensor | None = None, threshold: float = 0.0) -> TfVolume:
     o = np.asarray(origin, dtype=np.int64)
     return TfVolume(ptr(voxels), int(n), (_c_i64 * 3)(int(o[0]), int(o[1]), int(o[2])),
-                    float(voxel_size))
+                    float(voxel_size), ptr(brick_bad) if brick_bad is not None else None,
+                    float(threshold), 0)
 
 
 class _Workspace:

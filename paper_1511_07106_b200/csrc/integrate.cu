@@ -64,7 +64,19 @@ struct FrameGeom {
     // float32 copies for the conservative screen
     float r32[9];
     float fx32, fy32, cx32, cy32, tau32, w32, h32;
+    float good_t;  // free-space summary threshold for this tau
 };
+
+// brick summary maintained by this call for volume `vol`?
+__device__ __forceinline__ bool keeps_summary(const TfVolume &vol, const FrameGeom &f) {
+    return vol.brick_bad_dev != nullptr && vol.summary_threshold == f.good_t;
+}
+
+__device__ __forceinline__ void summary_add(const TfVolume &vol, int64_t lin, int delta) {
+    const int64_t n = vol.n, nb = (n + 7) / 8;
+    const int64_t x = lin % n, y = (lin / n) % n, z = lin / (n * n);
+    atomicAdd(&vol.brick_bad_dev[((z >> 3) * nb + (y >> 3)) * nb + (x >> 3)], (unsigned)delta);
+}
 
 static MipDesc make_mip(int64_t width, int64_t height) {
     MipDesc m{};
@@ -292,7 +304,7 @@ __global__ void __launch_bounds__(256) brick_cull_kernel(
 __device__ __forceinline__ int update_voxel(float2 *__restrict__ vox, int64_t lin, double gx,
                                             double gy, double gz,
                                             const double2 *__restrict__ table,
-                                            const FrameGeom &f) {
+                                            const FrameGeom &f, int *dbad = nullptr) {
     const double *R = f.r_cw.m;
     const double pcx = dot3_plus(R[0], gx, R[1], gy, R[2], gz, f.t_cw.v[0]);  // :104
     const double pcy = dot3_plus(R[3], gx, R[4], gy, R[5], gz, f.t_cw.v[1]);  // :105
@@ -318,7 +330,9 @@ __device__ __forceinline__ int update_voxel(float2 *__restrict__ vox, int64_t li
     const double w_sum = dadd((double)old.y, f.sw);                             // :131
     const double t_new = ddiv(dadd((double)wv, dmul(f.sw, clamped)), w_sum);    // :132
     const double w_new = f.max_w < w_sum ? f.max_w : w_sum;                     // :133
-    vox[lin] = make_float2(__double2float_rn(t_new), __double2float_rn(w_new));
+    const float2 nv = make_float2(__double2float_rn(t_new), __double2float_rn(w_new));
+    vox[lin] = nv;
+    if (dbad) *dbad = voxel_bad(nv, f.good_t) - voxel_bad(old, f.good_t);
     return 1;
 }
 
@@ -356,7 +370,10 @@ __global__ void __launch_bounds__(256) brick_update_exact_kernel(
                 if (x < n && y < n && z < n) {
                     const double gz = dmul((double)(z + vol.origin[2]), vs);    // :99
                     swept += 1;
-                    updates += update_voxel(vox, vox_index(n, z, y, x), gx, gy, gz, table, f);
+                    int db = 0;
+                    const int64_t lin = vox_index(n, z, y, x);
+                    updates += update_voxel(vox, lin, gx, gy, gz, table, f, &db);
+                    if (db && keeps_summary(vol, f)) summary_add(vol, lin, db);
                 }
             }
         }
@@ -373,8 +390,8 @@ __global__ void __launch_bounds__(256) brick_update_exact_kernel(
 __device__ __noinline__ int update_voxel_slow(float2 *__restrict__ vox, int64_t lin, double gx,
                                               double gy, double gz,
                                               const double2 *__restrict__ table,
-                                              const FrameGeom &f) {
-    return update_voxel(vox, lin, gx, gy, gz, table, f);
+                                              const FrameGeom &f, int *dbad) {
+    return update_voxel(vox, lin, gx, gy, gz, table, f, dbad);
 }
 
 // ---- float32 screening ------------------------------------------------------
@@ -451,6 +468,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         const double gx = dmul((double)((int64_t)x + vol.origin[0]), vs);
         const double gz0 = dmul((double)((int64_t)z0 + vol.origin[2]), vs);
         const float szx = f.r32[2] * vs32, szy = f.r32[5] * vs32, szz = f.r32[8] * vs32;
+        const bool keep = keeps_summary(vol, f);
+        int dbad = 0;  // change of this brick's bad-voxel count (summary)
 #pragma unroll 1
         for (int hy = 0; hy < 2; ++hy) {
             const unsigned y = y_base + 4 * hy;
@@ -549,7 +568,9 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                         if (fixed_point && old[j].x == fixed.x && old[j].y == fixed.y) {
                             ++nop;  // (tau32, max_w) is a host-verified fixed point
                         } else {
-                            vox[lin] = free_update(old[j], f);
+                            const float2 nv = free_update(old[j], f);
+                            vox[lin] = nv;
+                            dbad += voxel_bad(nv, f.good_t) - voxel_bad(old[j], f.good_t);
                         }
                     }
                     const bool ex = cls[j] == kExact;
@@ -570,9 +591,16 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                 for (int j = 0; overflow && j < kZBatch; ++j) {
                     if (!((overflow >> j) & 1u)) continue;
                     const double gz = dmul((double)((int64_t)(z0 + zb + j) + vol.origin[2]), vs);
-                    updates += update_voxel(vox, (int64_t)row + (int64_t)j * n * n, gx, gy, gz, table, f);
+                    int db = 0;
+                    updates += update_voxel(vox, (int64_t)row + (int64_t)j * n * n, gx, gy, gz, table, f, &db);
+                    dbad += db;
                 }
             }
+        }
+        if (keep) {  // one atomic per brick and warp
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
+            if (lane == 0 && dbad) atomicAdd(&vol.brick_bad_dev[local], (unsigned)dbad);
         }
     }
     if (stats) {
@@ -603,9 +631,11 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
         const int64_t n = vol.n;
         const int64_t x = lin % n, y = (lin / n) % n, z = lin / (n * n);
         const double vs = vol.voxel_size;
+        int db = 0;
         updates += update_voxel((float2 *)vol.voxels_dev, lin, dmul((double)(x + vol.origin[0]), vs),
                                 dmul((double)(y + vol.origin[1]), vs),
-                                dmul((double)(z + vol.origin[2]), vs), table, f);
+                                dmul((double)(z + vol.origin[2]), vs), table, f, &db);
+        if (db && keeps_summary(vol, f)) summary_add(vol, lin, db);
     }
     if (stats) {
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
@@ -618,6 +648,27 @@ __global__ void brick_stats_kernel(const unsigned int *__restrict__ active_count
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         stats[TF_STAT_ACTIVE_BRICKS] += *active_count;
         stats[TF_STAT_TOTAL_BRICKS] += total;
+    }
+}
+
+// bad-voxel count of every brick from scratch (one warp per brick)
+__global__ void __launch_bounds__(256) brick_summary_kernel(const TfVolume vol) {
+    const int64_t n = vol.n, nb = (n + 7) / 8, total = nb * nb * nb;
+    const int lane = threadIdx.x & 31;
+    const float2 *vox = (const float2 *)vol.voxels_dev;
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < total;
+         b += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t x = (b % nb) * 8 + (lane & 7), y0 = ((b / nb) % nb) * 8 + (lane >> 3);
+        const int64_t z0 = (b / (nb * nb)) * 8;
+        unsigned bad = 0;
+        for (int hy = 0; hy < 2; ++hy)
+            for (int k = 0; k < 8; ++k) {
+                const int64_t y = y0 + 4 * hy, z = z0 + k;
+                if (x < n && y < n && z < n) bad += voxel_bad(vox[vox_index(n, z, y, x)], vol.summary_threshold);
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+        if (lane == 0) vol.brick_bad_dev[b] = bad;
     }
 }
 
@@ -749,6 +800,7 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
     f.tau32 = (float)tau;
     f.w32 = (float)cam->width;
     f.h32 = (float)cam->height;
+    f.good_t = good_threshold(tau);
 
     // Is the saturated free-space state (tau32, max_w) a fixed point of the
     // free-space update?  Evaluated here with the kernel's exact IEEE
@@ -814,4 +866,16 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
     }
     tf_profile_end(prof_all, stream);
     return TF_OK;
+}
+
+extern "C" float tf_good_threshold(double tau) { return good_threshold(tau); }
+
+extern "C" int tf_brick_summary(const TfVolume *vol, void *stream_) {
+    if (!vol || !vol->voxels_dev || !vol->brick_bad_dev || vol->n < 2)
+        return tf_set_error(TF_EINVAL, "tf_brick_summary: bad argument");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    brick_summary_kernel<<<(unsigned)sms * 8, 256, 0, (cudaStream_t)stream_>>>(*vol);
+    return tf_check_launch("brick_summary_kernel");
 }

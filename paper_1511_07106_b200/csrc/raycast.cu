@@ -30,6 +30,7 @@ struct RayGeom {
     double near_thresh;  // NEAR_SURFACE_FRACTION * tau (_kernels.py:25, :298)
     int64_t coarse;
     int exact_only;      // TF_DEBUG_EXACT_ONLY: plain reference march for every ray
+    float good_t;        // brick-summary threshold for this tau
 };
 
 struct Hit {
@@ -319,6 +320,8 @@ struct FastRay {
     double q0x, q0y, q0z, dx, dy, dz;
     float near, near_tol;
     double near_thresh;
+    const unsigned *bad;  // brick summary (NULL: not usable for this tau)
+    unsigned nb;
 };
 
 __device__ __forceinline__ bool fixed_cell(double q, unsigned &i, float &fr) {
@@ -342,6 +345,11 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k) {
     if (!(cx && cy && cz)) return kUnsure;
     const unsigned hi = (unsigned)(r.n - 2);
     if (ix > hi || iy > hi || iz > hi) return 0u;                     // invalid (:38)
+    // a cell inside one brick whose voxels are all observed and >= T is
+    // certainly valid, positive and not near the surface
+    if (r.bad && (ix & 7u) != 7u && (iy & 7u) != 7u && (iz & 7u) != 7u &&
+        __ldg(&r.bad[((iz >> 3) * r.nb + (iy >> 3)) * r.nb + (ix >> 3)]) == 0u)
+        return kValidBit | kPosBit;
     const unsigned n = (unsigned)r.n;
     const float2 *b = r.vox + ((size_t)(iz * n + iy) * n + ix);
     const float2 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + n), c110 = __ldg(b + n + 1);
@@ -532,8 +540,10 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
             const double mag = fabs(q0x) + fabs(q0y) + fabs(q0z) + fabs(r.htx) + fabs(r.hty) +
                                fabs(r.htz) + (double)jhi[pick];
             if (!g.exact_only && vol.n <= 4000 && mag < 1e6 && jhi[pick] < (1 << 30) && g.coarse < (1 << 20)) {
+                const bool summ = vol.brick_bad_dev != nullptr && vol.summary_threshold == g.good_t;
                 FastRay fr{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
-                           (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh};
+                           (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh,
+                           summ ? vol.brick_bad_dev : nullptr, (unsigned)((vol.n + 7) / 8)};
                 changed |= march_fast(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
                                       exact_samples);
             } else {  // forced, or coordinates too large to certify: the exact reference march
@@ -619,6 +629,7 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
     g.near_thresh = 0.99 * tau;
     g.coarse = coarse_step;
     g.exact_only = (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) ? 1 : 0;
+    g.good_t = good_threshold(tau);
     dim3 grid((unsigned)((cam->width + kRayBlockX - 1) / kRayBlockX),
               (unsigned)((cam->height + kRayBlockY - 1) / kRayBlockY));
     for (int first = 0; first < nvol; first += TFB200_MAX_VOLUMES_PER_LAUNCH) {
@@ -633,7 +644,7 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
         void *prof = tf_profile_begin(TF_PROF_RAYCAST, stream);
         static const int minb = [] {
             const char *e = getenv("TFB200_RAY_MINBLOCKS");  // tuning knob
-            return e ? atoi(e) : 5;
+            return e ? atoi(e) : 4;
         }();
         if (minb == 4)
             raycast_kernel<4><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats);

@@ -48,6 +48,20 @@ __device__ __forceinline__ int64_t vox_index(int64_t n, int64_t z, int64_t y, in
     return (z * n + y) * n + x;
 }
 
+// Free-space summary threshold: a voxel is "good" when observed and its tsdf
+// >= T, T = 0.99 tau (1 + 4e-6) rounded up to float32.  Any trilinear value of
+// good corners is then > 0.99 tau (the reference's near-surface threshold,
+// _kernels.py:25, :298) with margin far above float64 rounding.
+__host__ __device__ inline float good_threshold(double tau) {
+    const double near = 0.99 * tau;
+    const double want = near * (1.0 + 4e-6);
+    float t = (float)want;
+    if ((double)t < want) t = nextafterf(t, 3.0e38f);
+    return t;
+}
+
+__device__ __forceinline__ int voxel_bad(float2 v, float t) { return !(v.y > 0.0f && v.x >= t); }
+
 // Warp-aggregated 64-bit counter add (integer: order-independent, exact).
 __device__ __forceinline__ void warp_count_add(unsigned long long *dst, unsigned long long v) {
 #pragma unroll

@@ -127,6 +127,15 @@ class TsdfSubvolume:
             pair = np.stack([t.astype(np.float32, copy=False), w.astype(np.float32, copy=False)], -1)
             self.voxels = torch.from_numpy(np.ascontiguousarray(pair)).to(nat.device())
         self._mirror = _Mirror(self._download, self._upload)
+        # free-space brick summary (TfVolume.brick_bad_dev): built lazily for a
+        # truncation, kept exact by tf_integrate, dropped when the voxels are
+        # replaced from the host
+        self.brick_bad: torch.Tensor | None = None
+        self._summary_t: float | None = None
+
+    def invalidate_summary(self) -> None:
+        """Call after writing ``voxels`` directly (outside the package's kernels)."""
+        self._summary_t = None
 
     # ---- host mirrors --------------------------------------------------------
     def _download(self) -> dict:
@@ -147,10 +156,25 @@ class TsdfSubvolume:
         return self._mirror.fetch()["weight"]
 
     def _device_read(self) -> None:
+        if self._mirror.exposed and self._mirror.host is not None:
+            self._summary_t = None  # host copies are about to be uploaded
         self._mirror.before_read()
 
     def _device_written(self) -> None:
         self._mirror.after_write()
+
+    def _summary_for(self, tau: float) -> tuple[torch.Tensor, float]:
+        L = nat.lib()
+        thr = float(L.tf_good_threshold(float(tau)))
+        if self._summary_t != thr:
+            nb = (self.voxels_per_side + 7) // 8
+            if self.brick_bad is None:
+                self.brick_bad = torch.empty(nb ** 3, dtype=torch.int32, device=self.voxels.device)
+            vol = nat.volume_struct(self.voxels, self.voxels_per_side, self.origin_voxel,
+                                    self.voxel_size, self.brick_bad, thr)
+            nat.check(L.tf_brick_summary(vol, nat.stream_handle()), "tf_brick_summary")
+            self._summary_t = thr
+        return self.brick_bad, thr
 
     # ---- reference API ---------------------------------------------------------
     @classmethod
@@ -185,9 +209,14 @@ class TsdfSubvolume:
         return TsdfSubvolume(self.origin_voxel.copy(), self.voxels_per_side, self.side_length,
                              voxels=self.voxels.clone())
 
-    def native(self) -> nat.TfVolume:
+    def native(self, tau: float | None = None) -> nat.TfVolume:
+        """ABI descriptor; with ``tau`` it carries the brick summary for that truncation."""
+        if tau is None:
+            return nat.volume_struct(self.voxels, self.voxels_per_side, self.origin_voxel,
+                                     self.voxel_size)
+        bad, thr = self._summary_for(tau)
         return nat.volume_struct(self.voxels, self.voxels_per_side, self.origin_voxel,
-                                 self.voxel_size)
+                                 self.voxel_size, bad, thr)
 
     def __repr__(self) -> str:
         return (f"TsdfSubvolume(origin_voxel={self.origin_voxel!r}, "
@@ -213,10 +242,10 @@ def device_depth(frame) -> torch.Tensor:
     return host.to(nat.device())
 
 
-def _vol_array(vols: Sequence[TsdfSubvolume]):
+def _vol_array(vols: Sequence[TsdfSubvolume], tau: float | None = None):
     arr = (nat.TfVolume * max(1, len(vols)))()
     for i, v in enumerate(vols):
-        arr[i] = v.native()
+        arr[i] = v.native(tau)
     return arr
 
 
@@ -237,7 +266,7 @@ def integrate_volumes(volumes: Sequence[TsdfSubvolume], frame, pose: Pose,
     for v in volumes:
         v._device_read()
     inverse = pose.invert()
-    arr = _vol_array(volumes)
+    arr = _vol_array(volumes, params.truncation)
     cam = nat.camera(intr)
     L = nat.lib()
     need = L.tf_integrate_workspace_size(arr, len(volumes), cam)
@@ -403,7 +432,7 @@ def raycast_volumes(volumes: Sequence[TsdfSubvolume], pose: Pose, intr: CameraIn
     c = nat.vec3(pose.translation)
     st = stats if stats is not None else nat.stats.buffer()
     for coarse, vols in groups.items():
-        arr = _vol_array(vols)
+        arr = _vol_array(vols, params.truncation)
         nat.check(nat.lib().tf_raycast(arr, len(vols), cam, float(params.truncation), int(coarse),
                                        r, c, nat.ptr(raymap.distance_dev),
                                        nat.ptr(raymap.vertices_dev), nat.ptr(raymap.normals_dev),

@@ -352,3 +352,26 @@ def test_certified_raycast_equals_exact_march_full_size():
     # the certified path must carry the bulk of the work
     assert stats[nat.STAT_EXACT_SAMPLES].item() < 0.02 * stats[nat.STAT_RAY_SAMPLES].item()
     assert stats[nat.STAT_CERT_FAILURES].item() == 0
+
+
+def test_brick_summary_stays_exact_under_integration():
+    """The incrementally maintained free-space summary equals a rebuild."""
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(4.08, 1020, 510)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    tiles = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length)
+             for k in spec.keys[:4]]
+    scene = demo_scene()
+    for pose in tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)[:6]:
+        tf.integrate_volumes(tiles, scene.render_depth(pose, intr), pose, intr, params)
+    lib = nat.load_library()
+    for t in tiles:
+        maintained = t.brick_bad.clone()
+        t.invalidate_summary()
+        t._summary_for(params.truncation)
+        assert torch.equal(maintained, t.brick_bad)
+        nb = (spec.voxels_per_side + 7) // 8
+        assert int((t.brick_bad == 0).sum().item()) > 0 or t is not tiles[0]
+    good = sum(int((t.brick_bad == 0).sum().item()) for t in tiles)
+    assert good > 1000  # free-space bricks exist to be skipped
+    assert lib.tf_good_threshold(params.truncation) > 0.99 * params.truncation
