@@ -271,6 +271,7 @@ def run_ours(args) -> None:
                       "total_bricks": sum_over_ranks(int(st[nat.STAT_TOTAL_BRICKS])) // max(args.steps, 1)},
         "raycast": {"exact_samples_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_SAMPLES])) / args.steps,
                     "certification_failures": sum_over_ranks(int(st[nat.STAT_CERT_FAILURES])),
+                    "summary_certified_samples_per_frame": sum_over_ranks(int(st[nat.STAT_SUMMARY_SAMPLES])) / args.steps,
                     "samples_per_frame": samples / args.steps,
                     "samples_per_s": samples / (ms_total / 1e3)},
         "gpu_launches": int(launches),

@@ -56,6 +56,7 @@ STAT_VOXEL_UPDATES, STAT_SWEPT_VOXELS, STAT_ACTIVE_BRICKS, STAT_TOTAL_BRICKS = 0
 STAT_RAY_SAMPLES, STAT_RAY_HITS, STAT_EXACT_VOXELS, STAT_NOOP_UPDATES = 4, 5, 6, 7
 STAT_EXACT_PROJ, STAT_EXACT_PLANE, STAT_EXACT_SDF, STAT_EXACT_SAMPLES = 8, 9, 10, 11
 STAT_CERT_FAILURES = 12
+STAT_SUMMARY_SAMPLES = 13
 STAT_COUNT = 16
 
 _VOL = ctypes.POINTER(TfVolume)

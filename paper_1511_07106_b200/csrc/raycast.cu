@@ -312,7 +312,7 @@ __device__ __noinline__ bool march_volume(Ray &r, int64_t j, int64_t j_end, int6
 // when any of them is too close to call; an unsure sample is then evaluated
 // with the exact reference arithmetic (sample_at), so every decision is the
 // reference's.
-enum : unsigned { kValidBit = 1u, kPosBit = 2u, kNearBit = 4u, kUnsure = 8u };
+enum : unsigned { kValidBit = 1u, kPosBit = 2u, kNearBit = 4u, kUnsure = 8u, kSummaryBit = 16u };
 
 struct FastRay {
     const float2 *vox;
@@ -349,7 +349,7 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k) {
     // certainly valid, positive and not near the surface
     if (r.bad && (ix & 7u) != 7u && (iy & 7u) != 7u && (iz & 7u) != 7u &&
         __ldg(&r.bad[((iz >> 3) * r.nb + (iy >> 3)) * r.nb + (ix >> 3)]) == 0u)
-        return kValidBit | kPosBit;
+        return kValidBit | kPosBit | kSummaryBit;
     const unsigned n = (unsigned)r.n;
     const float2 *b = r.vox + ((size_t)(iz * n + iy) * n + ix);
     const float2 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + n), c110 = __ldg(b + n + 1);
@@ -374,7 +374,8 @@ __device__ __forceinline__ unsigned cert_sample(const FastRay &fr, const Ray &er
                                                 unsigned long long &exact_samples) {
     ++samples;
     const unsigned s = fast_sample(fr, k);
-    if (!(s & kUnsure)) return s;
+    if (s & kSummaryBit) exact_samples += 1ull << 44;  // summary-certified (counter in the high bits)
+    if (!(s & kUnsure)) return s & ~kSummaryBit;
     ++exact_samples;
     Ray r = er;
     double v = 0.0;
@@ -567,7 +568,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
         warp_count_add(&stats[TF_STAT_RAY_SAMPLES], samples);
         warp_count_add(&stats[TF_STAT_RAY_HITS], hits);
         warp_count_add(&stats[TF_STAT_EXACT_SAMPLES], exact_samples & ((1ull << 40) - 1));
-        warp_count_add(&stats[TF_STAT_CERT_FAILURES], exact_samples >> 40);
+        warp_count_add(&stats[TF_STAT_CERT_FAILURES], (exact_samples >> 40) & 15ull);
+        warp_count_add(&stats[TF_STAT_SUMMARY_SAMPLES], exact_samples >> 44);
     }
 }
 
