@@ -45,19 +45,20 @@ enum {
 
 /* One TSDF subvolume resident on the device (tsdf.py:41-107).
  *
- * brick_bad_dev (optional, may be NULL): uint32 per 8^3 brick (x fastest,
- * ceil(n/8)^3 entries) counting the brick's voxels that are NOT "observed and
- * >= summary_threshold".  Built by tf_brick_summary for a truncation tau
- * (summary_threshold = tf_good_threshold(tau)) and kept exact by
- * tf_integrate; tf_raycast uses it to certify free-space samples without
- * gathering voxels.  Ignored (not used, not maintained) when NULL or when
- * summary_threshold does not match the call's tau. */
+ * brick_state_dev (optional, may be NULL): uint32 per 8^3 brick (x fastest,
+ * ceil(n/8)^3 entries): low 16 bits = voxels that are NOT "observed and
+ * >= summary_threshold", high 16 bits = observed voxels (weight > 0).  Built
+ * by tf_brick_summary for a truncation tau (summary_threshold =
+ * tf_good_threshold(tau)) and kept exact by tf_integrate; tf_raycast uses it
+ * to certify free-space and never-observed samples without gathering voxels.
+ * Ignored (not used, not maintained) when NULL or when summary_threshold
+ * does not match the call's tau. */
 typedef struct TfVolume {
     void *voxels_dev;    /* float2[n][n][n]: (tsdf, weight), x fastest */
     int64_t n;           /* voxels_per_side */
     int64_t origin[3];   /* origin_voxel: global voxel of local (0,0,0) */
     double voxel_size;   /* side_length / voxels_per_side (tsdf.py:80-82) */
-    uint32_t *brick_bad_dev;
+    uint32_t *brick_state_dev;
     float summary_threshold;
     int32_t reserved;
 } TfVolume;

@@ -28,7 +28,7 @@ _c_sz = ctypes.c_size_t
 
 class TfVolume(ctypes.Structure):
     _fields_ = [("voxels_dev", _c_p), ("n", _c_i64), ("origin", _c_i64 * 3),
-                ("voxel_size", _c_d), ("brick_bad_dev", _c_p), ("summary_threshold", ctypes.c_float),
+                ("voxel_size", _c_d), ("brick_state_dev", _c_p), ("summary_threshold", ctypes.c_float),
                 ("reserved", ctypes.c_int32)]
 
 

@@ -69,13 +69,13 @@ struct FrameGeom {
 
 // brick summary maintained by this call for volume `vol`?
 __device__ __forceinline__ bool keeps_summary(const TfVolume &vol, const FrameGeom &f) {
-    return vol.brick_bad_dev != nullptr && vol.summary_threshold == f.good_t;
+    return vol.brick_state_dev != nullptr && vol.summary_threshold == f.good_t;
 }
 
-__device__ __forceinline__ void summary_add(const TfVolume &vol, int64_t lin, int delta) {
+__device__ __forceinline__ void summary_add(const TfVolume &vol, int64_t lin, unsigned delta) {
     const int64_t n = vol.n, nb = (n + 7) / 8;
     const int64_t x = lin % n, y = (lin / n) % n, z = lin / (n * n);
-    atomicAdd(&vol.brick_bad_dev[((z >> 3) * nb + (y >> 3)) * nb + (x >> 3)], (unsigned)delta);
+    atomicAdd(&vol.brick_state_dev[((z >> 3) * nb + (y >> 3)) * nb + (x >> 3)], delta);
 }
 
 static MipDesc make_mip(int64_t width, int64_t height) {
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(256) brick_cull_kernel(
 __device__ __forceinline__ int update_voxel(float2 *__restrict__ vox, int64_t lin, double gx,
                                             double gy, double gz,
                                             const double2 *__restrict__ table,
-                                            const FrameGeom &f, int *dbad = nullptr) {
+                                            const FrameGeom &f, unsigned *dbad = nullptr) {
     const double *R = f.r_cw.m;
     const double pcx = dot3_plus(R[0], gx, R[1], gy, R[2], gz, f.t_cw.v[0]);  // :104
     const double pcy = dot3_plus(R[3], gx, R[4], gy, R[5], gz, f.t_cw.v[1]);  // :105
@@ -332,7 +332,7 @@ __device__ __forceinline__ int update_voxel(float2 *__restrict__ vox, int64_t li
     const double w_new = f.max_w < w_sum ? f.max_w : w_sum;                     // :133
     const float2 nv = make_float2(__double2float_rn(t_new), __double2float_rn(w_new));
     vox[lin] = nv;
-    if (dbad) *dbad = voxel_bad(nv, f.good_t) - voxel_bad(old, f.good_t);
+    if (dbad) *dbad = voxel_state(nv, f.good_t) - voxel_state(old, f.good_t);
     return 1;
 }
 
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(256) brick_update_exact_kernel(
                 if (x < n && y < n && z < n) {
                     const double gz = dmul((double)(z + vol.origin[2]), vs);    // :99
                     swept += 1;
-                    int db = 0;
+                    unsigned db = 0;
                     const int64_t lin = vox_index(n, z, y, x);
                     updates += update_voxel(vox, lin, gx, gy, gz, table, f, &db);
                     if (db && keeps_summary(vol, f)) summary_add(vol, lin, db);
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(256) brick_update_exact_kernel(
 __device__ __noinline__ int update_voxel_slow(float2 *__restrict__ vox, int64_t lin, double gx,
                                               double gy, double gz,
                                               const double2 *__restrict__ table,
-                                              const FrameGeom &f, int *dbad) {
+                                              const FrameGeom &f, unsigned *dbad) {
     return update_voxel(vox, lin, gx, gy, gz, table, f, dbad);
 }
 
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         const double gz0 = dmul((double)((int64_t)z0 + vol.origin[2]), vs);
         const float szx = f.r32[2] * vs32, szy = f.r32[5] * vs32, szz = f.r32[8] * vs32;
         const bool keep = keeps_summary(vol, f);
-        int dbad = 0;  // change of this brick's bad-voxel count (summary)
+        unsigned dbad = 0;  // change of this brick's packed state (summary)
 #pragma unroll 1
         for (int hy = 0; hy < 2; ++hy) {
             const unsigned y = y_base + 4 * hy;
@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                         } else {
                             const float2 nv = free_update(old[j], f);
                             vox[lin] = nv;
-                            dbad += voxel_bad(nv, f.good_t) - voxel_bad(old[j], f.good_t);
+                            dbad += voxel_state(nv, f.good_t) - voxel_state(old[j], f.good_t);
                         }
                     }
                     const bool ex = cls[j] == kExact;
@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                 for (int j = 0; overflow && j < kZBatch; ++j) {
                     if (!((overflow >> j) & 1u)) continue;
                     const double gz = dmul((double)((int64_t)(z0 + zb + j) + vol.origin[2]), vs);
-                    int db = 0;
+                    unsigned db = 0;
                     updates += update_voxel(vox, (int64_t)row + (int64_t)j * n * n, gx, gy, gz, table, f, &db);
                     dbad += db;
                 }
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         if (keep) {  // one atomic per brick and warp
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
-            if (lane == 0 && dbad) atomicAdd(&vol.brick_bad_dev[local], (unsigned)dbad);
+            if (lane == 0 && dbad) atomicAdd(&vol.brick_state_dev[local], dbad);
         }
     }
     if (stats) {
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
         const int64_t n = vol.n;
         const int64_t x = lin % n, y = (lin / n) % n, z = lin / (n * n);
         const double vs = vol.voxel_size;
-        int db = 0;
+        unsigned db = 0;
         updates += update_voxel((float2 *)vol.voxels_dev, lin, dmul((double)(x + vol.origin[0]), vs),
                                 dmul((double)(y + vol.origin[1]), vs),
                                 dmul((double)(z + vol.origin[2]), vs), table, f, &db);
@@ -664,11 +664,11 @@ __global__ void __launch_bounds__(256) brick_summary_kernel(const TfVolume vol) 
         for (int hy = 0; hy < 2; ++hy)
             for (int k = 0; k < 8; ++k) {
                 const int64_t y = y0 + 4 * hy, z = z0 + k;
-                if (x < n && y < n && z < n) bad += voxel_bad(vox[vox_index(n, z, y, x)], vol.summary_threshold);
+                if (x < n && y < n && z < n) bad += voxel_state(vox[vox_index(n, z, y, x)], vol.summary_threshold);
             }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
-        if (lane == 0) vol.brick_bad_dev[b] = bad;
+        if (lane == 0) vol.brick_state_dev[b] = bad;
     }
 }
 
@@ -871,7 +871,7 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
 extern "C" float tf_good_threshold(double tau) { return good_threshold(tau); }
 
 extern "C" int tf_brick_summary(const TfVolume *vol, void *stream_) {
-    if (!vol || !vol->voxels_dev || !vol->brick_bad_dev || vol->n < 2)
+    if (!vol || !vol->voxels_dev || !vol->brick_state_dev || vol->n < 2)
         return tf_set_error(TF_EINVAL, "tf_brick_summary: bad argument");
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

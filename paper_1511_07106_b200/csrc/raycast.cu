@@ -345,11 +345,24 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k) {
     if (!(cx && cy && cz)) return kUnsure;
     const unsigned hi = (unsigned)(r.n - 2);
     if (ix > hi || iy > hi || iz > hi) return 0u;                     // invalid (:38)
-    // a cell inside one brick whose voxels are all observed and >= T is
-    // certainly valid, positive and not near the surface
-    if (r.bad && (ix & 7u) != 7u && (iy & 7u) != 7u && (iz & 7u) != 7u &&
-        __ldg(&r.bad[((iz >> 3) * r.nb + (iy >> 3)) * r.nb + (ix >> 3)]) == 0u)
-        return kValidBit | kPosBit | kSummaryBit;
+    if (r.bad) {
+        // min corner in a never-observed brick: certainly invalid (:40-50);
+        // every corner in bricks whose voxels are all observed and >= T:
+        // certainly valid, positive and not near the surface
+        const unsigned bx = ix >> 3, by = iy >> 3, bz = iz >> 3;
+        const unsigned st = __ldg(&r.bad[(bz * r.nb + by) * r.nb + bx]);
+        if ((st >> 16) == 0u) return kSummaryBit;
+        if ((st & 0xFFFFu) == 0u) {
+            const unsigned ex = ((ix & 7u) == 7u), ey = ((iy & 7u) == 7u), ez = ((iz & 7u) == 7u);
+            bool good = true;
+            for (unsigned c = 1; c < 8 && good; ++c) {
+                if (((c & 1u) && !ex) || ((c & 2u) && !ey) || ((c & 4u) && !ez)) continue;
+                const unsigned nbx = bx + (c & 1u), nby = by + ((c >> 1) & 1u), nbz = bz + (c >> 2);
+                good = (__ldg(&r.bad[(nbz * r.nb + nby) * r.nb + nbx]) & 0xFFFFu) == 0u;
+            }
+            if (good) return kValidBit | kPosBit | kSummaryBit;
+        }
+    }
     const unsigned n = (unsigned)r.n;
     const float2 *b = r.vox + ((size_t)(iz * n + iy) * n + ix);
     const float2 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + n), c110 = __ldg(b + n + 1);
@@ -541,10 +554,10 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
             const double mag = fabs(q0x) + fabs(q0y) + fabs(q0z) + fabs(r.htx) + fabs(r.hty) +
                                fabs(r.htz) + (double)jhi[pick];
             if (!g.exact_only && vol.n <= 4000 && mag < 1e6 && jhi[pick] < (1 << 30) && g.coarse < (1 << 20)) {
-                const bool summ = vol.brick_bad_dev != nullptr && vol.summary_threshold == g.good_t;
+                const bool summ = vol.brick_state_dev != nullptr && vol.summary_threshold == g.good_t;
                 FastRay fr{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
                            (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh,
-                           summ ? vol.brick_bad_dev : nullptr, (unsigned)((vol.n + 7) / 8)};
+                           summ ? vol.brick_state_dev : nullptr, (unsigned)((vol.n + 7) / 8)};
                 changed |= march_fast(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
                                       exact_samples);
             } else {  // forced, or coordinates too large to certify: the exact reference march

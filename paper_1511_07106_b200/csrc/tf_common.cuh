@@ -62,6 +62,12 @@ __host__ __device__ inline float good_threshold(double tau) {
 
 __device__ __forceinline__ int voxel_bad(float2 v, float t) { return !(v.y > 0.0f && v.x >= t); }
 
+// packed brick-state contribution of one voxel: not-good (low 16 bits) and
+// observed (high 16 bits); deltas of packed values add up exactly mod 2^32
+__device__ __forceinline__ unsigned voxel_state(float2 v, float t) {
+    return (unsigned)voxel_bad(v, t) | ((v.y > 0.0f ? 1u : 0u) << 16);
+}
+
 // Warp-aggregated 64-bit counter add (integer: order-independent, exact).
 __device__ __forceinline__ void warp_count_add(unsigned long long *dst, unsigned long long v) {
 #pragma unroll

@@ -127,7 +127,7 @@ class TsdfSubvolume:
             pair = np.stack([t.astype(np.float32, copy=False), w.astype(np.float32, copy=False)], -1)
             self.voxels = torch.from_numpy(np.ascontiguousarray(pair)).to(nat.device())
         self._mirror = _Mirror(self._download, self._upload)
-        # free-space brick summary (TfVolume.brick_bad_dev): built lazily for a
+        # free-space brick summary (TfVolume.brick_state_dev): built lazily for a
         # truncation, kept exact by tf_integrate, dropped when the voxels are
         # replaced from the host
         self.brick_bad: torch.Tensor | None = None
