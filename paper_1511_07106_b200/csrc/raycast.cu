@@ -324,45 +324,55 @@ struct FastRay {
     unsigned nb;
 };
 
-__device__ __forceinline__ bool fixed_cell(double q, unsigned &i, float &fr) {
+// floor(q) from a 20-bit fixed point: lo = round(q 2^20) mod 2^32 (q in
+// (-2^11, 4096)).  The reference's q differs from fma(k, d, q0) by < 1e-9, so
+// floor is certain unless q is within 1.5 * 2^-20 of an integer, i.e. unless
+// the fraction field is 0, 1 or 2^20 - 1; then floor is i - 1 or i (fq <= 1)
+// or i or i + 1 (fq = 2^20 - 1): returned as the candidate range [lo, hi].
+__device__ __forceinline__ void fixed_cell(double q, unsigned &lo, unsigned &hi, float &fr) {
     const double t = dadd(q, 6442450944.0);  // 1.5 * 2^32: ulp(t) = 2^-20
-    const unsigned lo = (unsigned)__double2loint(t);
-    const unsigned fq = lo & 0xFFFFFu;
-    i = lo >> 20;
+    const unsigned bits = (unsigned)__double2loint(t);
+    const unsigned fq = bits & 0xFFFFFu;
+    const unsigned i = bits >> 20;
     fr = (float)fq * 9.5367431640625e-07f;  // 2^-20
-    return fq - 4u <= (1u << 20) - 9u;       // 4 <= fq <= 2^20 - 5: floor is certain
+    lo = fq <= 1u ? i - 1u : i;
+    hi = fq == 0xFFFFFu ? i + 1u : i;
 }
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 
 __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k) {
     const double kd = (double)k;
-    unsigned ix, iy, iz;
+    unsigned lx, hx, ly, hy, lz, hz;
     float fx, fy, fz;
-    const bool cx = fixed_cell(dfma(kd, r.dx, r.q0x), ix, fx);
-    const bool cy = fixed_cell(dfma(kd, r.dy, r.q0y), iy, fy);
-    const bool cz = fixed_cell(dfma(kd, r.dz, r.q0z), iz, fz);
-    if (!(cx && cy && cz)) return kUnsure;
-    const unsigned hi = (unsigned)(r.n - 2);
-    if (ix > hi || iy > hi || iz > hi) return 0u;                     // invalid (:38)
+    fixed_cell(dfma(kd, r.dx, r.q0x), lx, hx, fx);
+    fixed_cell(dfma(kd, r.dy, r.q0y), ly, hy, fy);
+    fixed_cell(dfma(kd, r.dz, r.q0z), lz, hz, fz);
+    const unsigned top = (unsigned)(r.n - 2);
+    // candidate cells all outside [0, n-2]: certainly invalid (:38); some outside: unsure
+    if (!((lx <= top || hx <= top) && (ly <= top || hy <= top) && (lz <= top || hz <= top))) return 0u;
+    if (!(lx <= top && hx <= top && ly <= top && hy <= top && lz <= top && hz <= top)) return kUnsure;
     if (r.bad) {
-        // min corner in a never-observed brick: certainly invalid (:40-50);
-        // every corner in bricks whose voxels are all observed and >= T:
-        // certainly valid, positive and not near the surface
-        const unsigned bx = ix >> 3, by = iy >> 3, bz = iz >> 3;
-        const unsigned st = __ldg(&r.bad[(bz * r.nb + by) * r.nb + bx]);
-        if ((st >> 16) == 0u) return kSummaryBit;
-        if ((st & 0xFFFFu) == 0u) {
-            const unsigned ex = ((ix & 7u) == 7u), ey = ((iy & 7u) == 7u), ez = ((iz & 7u) == 7u);
-            bool good = true;
-            for (unsigned c = 1; c < 8 && good; ++c) {
-                if (((c & 1u) && !ex) || ((c & 2u) && !ey) || ((c & 4u) && !ez)) continue;
-                const unsigned nbx = bx + (c & 1u), nby = by + ((c >> 1) & 1u), nbz = bz + (c >> 2);
-                good = (__ldg(&r.bad[(nbz * r.nb + nby) * r.nb + nbx]) & 0xFFFFu) == 0u;
-            }
-            if (good) return kValidBit | kPosBit | kSummaryBit;
-        }
+        // min corners all in never-observed bricks: certainly invalid (:40-50);
+        // every corner of every candidate cell in bricks whose voxels are all
+        // observed and >= T: certainly valid, positive and not near the surface
+        const unsigned bx0 = lx >> 3, bx1 = hx >> 3, by0 = ly >> 3, by1 = hy >> 3, bz0 = lz >> 3, bz1 = hz >> 3;
+        bool unseen = true;
+        for (unsigned bz = bz0; bz <= bz1 && unseen; ++bz)
+            for (unsigned by = by0; by <= by1 && unseen; ++by)
+                for (unsigned bx = bx0; bx <= bx1 && unseen; ++bx)
+                    unseen = (__ldg(&r.bad[(bz * r.nb + by) * r.nb + bx]) >> 16) == 0u;
+        if (unseen) return kSummaryBit;
+        const unsigned ex1 = (hx + 1u) >> 3, ey1 = (hy + 1u) >> 3, ez1 = (hz + 1u) >> 3;
+        bool good = true;
+        for (unsigned bz = bz0; bz <= ez1 && good; ++bz)
+            for (unsigned by = by0; by <= ey1 && good; ++by)
+                for (unsigned bx = bx0; bx <= ex1 && good; ++bx)
+                    good = (__ldg(&r.bad[(bz * r.nb + by) * r.nb + bx]) & 0xFFFFu) == 0u;
+        if (good) return kValidBit | kPosBit | kSummaryBit;
     }
+    if (lx != hx || ly != hy || lz != hz) return kUnsure;
+    const unsigned ix = lx, iy = ly, iz = lz;
     const unsigned n = (unsigned)r.n;
     const float2 *b = r.vox + ((size_t)(iz * n + iy) * n + ix);
     const float2 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + n), c110 = __ldg(b + n + 1);
