@@ -322,6 +322,7 @@ struct FastRay {
     double near_thresh;
     const unsigned *bad;  // brick summary (NULL: not usable for this tau)
     unsigned nb;
+    double idx, idy, idz;  // 1 / d (approximate; only used with margins)
 };
 
 // floor(q) from a 20-bit fixed point: lo = round(q 2^20) mod 2^32 (q in
@@ -348,31 +349,29 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k) {
     fixed_cell(dfma(kd, r.dx, r.q0x), lx, hx, fx);
     fixed_cell(dfma(kd, r.dy, r.q0y), ly, hy, fy);
     fixed_cell(dfma(kd, r.dz, r.q0z), lz, hz, fz);
-    const unsigned top = (unsigned)(r.n - 2);
-    // candidate cells all outside [0, n-2]: certainly invalid (:38); some outside: unsure
-    if (!((lx <= top || hx <= top) && (ly <= top || hy <= top) && (lz <= top || hz <= top))) return 0u;
-    if (!(lx <= top && hx <= top && ly <= top && hy <= top && lz <= top && hz <= top)) return kUnsure;
-    if (r.bad) {
-        // min corners all in never-observed bricks: certainly invalid (:40-50);
-        // every corner of every candidate cell in bricks whose voxels are all
-        // observed and >= T: certainly valid, positive and not near the surface
-        const unsigned bx0 = lx >> 3, bx1 = hx >> 3, by0 = ly >> 3, by1 = hy >> 3, bz0 = lz >> 3, bz1 = hz >> 3;
-        bool unseen = true;
-        for (unsigned bz = bz0; bz <= bz1 && unseen; ++bz)
-            for (unsigned by = by0; by <= by1 && unseen; ++by)
-                for (unsigned bx = bx0; bx <= bx1 && unseen; ++bx)
-                    unseen = (__ldg(&r.bad[(bz * r.nb + by) * r.nb + bx]) >> 16) == 0u;
-        if (unseen) return kSummaryBit;
-        const unsigned ex1 = (hx + 1u) >> 3, ey1 = (hy + 1u) >> 3, ez1 = (hz + 1u) >> 3;
-        bool good = true;
-        for (unsigned bz = bz0; bz <= ez1 && good; ++bz)
-            for (unsigned by = by0; by <= ey1 && good; ++by)
-                for (unsigned bx = bx0; bx <= ex1 && good; ++bx)
-                    good = (__ldg(&r.bad[(bz * r.nb + by) * r.nb + bx]) & 0xFFFFu) == 0u;
-        if (good) return kValidBit | kPosBit | kSummaryBit;
-    }
     if (lx != hx || ly != hy || lz != hz) return kUnsure;
     const unsigned ix = lx, iy = ly, iz = lz;
+    const unsigned top = (unsigned)(r.n - 2);
+    if (ix > top || iy > top || iz > top) return 0u;                  // invalid (:38)
+    if (r.bad) {
+        // min corner in a never-observed brick: certainly invalid (:40-50);
+        // every corner in bricks whose voxels are all observed and >= T:
+        // certainly valid, positive and not near the surface
+        const unsigned bx = ix >> 3, by = iy >> 3, bz = iz >> 3;
+        const unsigned st = __ldg(&r.bad[(bz * r.nb + by) * r.nb + bx]);
+        if ((st >> 16) == 0u) return kSummaryBit;
+        if ((st & 0xFFFFu) == 0u) {
+            const unsigned ex = ((ix & 7u) == 7u), ey = ((iy & 7u) == 7u), ez = ((iz & 7u) == 7u);
+            bool good = true;
+#pragma unroll
+            for (unsigned c = 1; c < 8; ++c) {
+                if (((c & 1u) && !ex) || ((c & 2u) && !ey) || ((c & 4u) && !ez)) continue;
+                const unsigned nbx = bx + (c & 1u), nby = by + ((c >> 1) & 1u), nbz = bz + (c >> 2);
+                good = good && (__ldg(&r.bad[(nbz * r.nb + nby) * r.nb + nbx]) & 0xFFFFu) == 0u;
+            }
+            if (good) return kValidBit | kPosBit | kSummaryBit;
+        }
+    }
     const unsigned n = (unsigned)r.n;
     const float2 *b = r.vox + ((size_t)(iz * n + iy) * n + ix);
     const float2 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + n), c110 = __ldg(b + n + 1);
@@ -389,6 +388,62 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k) {
     const float av = fabsf(v);
     if (av <= ev || fabsf(av - r.near) <= ev + r.near_tol) return kUnsure;
     return kValidBit | (v > 0.f ? kPosBit : 0u) | (av < r.near ? kNearBit : 0u);
+}
+
+// Summary run starting at march point j: if the cell of j certainly has its
+// min corner in brick b and b is never-observed (kind 2) or b and its +1
+// neighbours are all-good (kind 1), returns the kind and the last fine index
+// k_last >= j whose min corner certainly stays in b (and, for kind 1, below
+// n - 1, so the cell stays inside the volume).  0 = no run.
+__device__ __forceinline__ int summary_run(const FastRay &r, int j, int j_end, int &k_last) {
+    const double kd = (double)j;
+    const double q[3] = {dfma(kd, r.dx, r.q0x), dfma(kd, r.dy, r.q0y), dfma(kd, r.dz, r.q0z)};
+    unsigned lo[3], hi[3];
+    float fdummy;
+    fixed_cell(q[0], lo[0], hi[0], fdummy);
+    fixed_cell(q[1], lo[1], hi[1], fdummy);
+    fixed_cell(q[2], lo[2], hi[2], fdummy);
+    const unsigned top = (unsigned)(r.n - 2);
+    if (lo[0] != hi[0] || lo[1] != hi[1] || lo[2] != hi[2]) return 0;
+    if (lo[0] > top || lo[1] > top || lo[2] > top) return 0;
+    const unsigned bx = lo[0] >> 3, by = lo[1] >> 3, bz = lo[2] >> 3;
+    const unsigned st = __ldg(&r.bad[(bz * r.nb + by) * r.nb + bx]);
+    int kind = 0;
+    if ((st >> 16) == 0u) {
+        kind = 2;
+    } else if ((st & 0xFFFFu) == 0u) {
+        bool good = true;
+#pragma unroll
+        for (unsigned c = 1; c < 8; ++c) {
+            const unsigned nbx = bx + (c & 1u), nby = by + ((c >> 1) & 1u), nbz = bz + (c >> 2);
+            if (nbx >= r.nb || nby >= r.nb || nbz >= r.nb) continue;  // the cell stays in b there
+            good = good && (__ldg(&r.bad[(nbz * r.nb + nby) * r.nb + nbx]) & 0xFFFFu) == 0u;
+        }
+        if (good) kind = 1;
+    }
+    if (!kind) return 0;
+    // last k with the min corner certainly inside [8b, 8b + 8) (and < n - 1 for
+    // kind 1) on every axis; margin 1e-6 voxel >> the 1e-9 bound on q's error
+    const unsigned b3[3] = {bx, by, bz};
+    const double d3[3] = {r.dx, r.dy, r.dz}, id3[3] = {r.idx, r.idy, r.idz};
+    double klim = (double)j_end;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double up = (double)(8u * b3[a] + 8u);
+        if (kind == 1 && up > (double)(r.n - 1)) up = (double)(r.n - 1);
+        const double dn = (double)(8u * b3[a]);
+        double ka = klim;
+        if (d3[a] > 1e-12)
+            ka = floor((up - 1e-6 - q[a]) * id3[a]) + kd;
+        else if (d3[a] < -1e-12)
+            ka = floor((dn + 1e-6 - q[a]) * id3[a]) + kd;
+        else if (q[a] >= up - 1e-6 || q[a] < dn + 1e-6)
+            ka = kd - 1.0;
+        klim = fmin(klim, ka);
+    }
+    if (klim < kd) return 0;
+    k_last = (int)klim;
+    return kind;
 }
 
 // certified decisions of lattice point k (exact fallback when unsure)
@@ -440,7 +495,46 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
     bool prev_has = false;
     int prev_j = -1, last_j = j - 1, swept_j = j - 1;
     int phase = j % coarse;  // j mod coarse, tracked so no division runs per step
+    // fine points in (unseen_from, unseen_until] are certified invalid by a
+    // never-observed brick; unseen_from itself is processed normally (its scan
+    // may reach back before the run)
+    int unseen_from = 0x7fffffff, unseen_until = -1;
     while (j <= j_end) {
+        if (j > unseen_from && j <= unseen_until) {
+            // invalid sample; any scan covers (max(prev_j, swept_j), j], which
+            // lies inside the run (all invalid): nothing found (:362-405)
+            const bool scan = (prev_has && (prev & kPosBit)) || (swept_j < j - 1 && coarse > 2);
+            if (scan) swept_j = j;
+            last_j = j;
+            ++samples;
+            exact_samples += 1ull << 44;
+            j += coarse - phase;
+            phase = 0;
+            continue;
+        }
+        if (fr.bad) {
+            int k_last = 0;
+            const int kind = summary_run(fr, j, j_end, k_last);
+            if (kind == 1) {
+                // every march point in [j, k_last] is valid, positive, not near:
+                // coarse steps, no scans (:362-416)
+                while (j <= k_last) {
+                    ++samples;
+                    exact_samples += 1ull << 44;
+                    last_j = j;
+                    prev_j = j;
+                    j += coarse - phase;
+                    phase = 0;
+                }
+                prev_has = true;
+                prev = kValidBit | kPosBit;
+                continue;
+            }
+            if (kind == 2) {
+                unseen_from = j;
+                unseen_until = k_last;
+            }
+        }
         const unsigned s = cert_sample(fr, er, j, samples, exact_samples);
         const bool valid = s & kValidBit;
         bool do_scan = false;
@@ -567,7 +661,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
                 const bool summ = vol.brick_state_dev != nullptr && vol.summary_threshold == g.good_t;
                 FastRay fr{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
                            (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh,
-                           summ ? vol.brick_state_dev : nullptr, (unsigned)((vol.n + 7) / 8)};
+                           summ ? vol.brick_state_dev : nullptr, (unsigned)((vol.n + 7) / 8),
+                           1.0 / d[0], 1.0 / d[1], 1.0 / d[2]};
                 changed |= march_fast(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
                                       exact_samples);
             } else {  // forced, or coordinates too large to certify: the exact reference march
