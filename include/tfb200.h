@@ -47,7 +47,8 @@ enum {
  *
  * brick_state_dev (optional, may be NULL): uint32 per 8^3 brick (x fastest,
  * ceil(n/8)^3 entries): low 16 bits = voxels that are NOT "observed and
- * >= summary_threshold", high 16 bits = observed voxels (weight > 0).  Built
+ * >= summary_threshold", high 16 bits = observed voxels (weight > 0), and a
+ * derived flag byte per brick (brick_flags_dev, same indexing).  Built
  * by tf_brick_summary for a truncation tau (summary_threshold =
  * tf_good_threshold(tau)) and kept exact by tf_integrate; tf_raycast uses it
  * to certify free-space and never-observed samples without gathering voxels.
@@ -59,6 +60,9 @@ typedef struct TfVolume {
     int64_t origin[3];   /* origin_voxel: global voxel of local (0,0,0) */
     double voxel_size;   /* side_length / voxels_per_side (tsdf.py:80-82) */
     uint32_t *brick_state_dev;
+    uint8_t *brick_flags_dev;  /* per brick: bit0 never observed, bit1 the brick
+                                  and its +1 neighbours are all-good (cells with
+                                  a min corner in it are free space) */
     float summary_threshold;
     int32_t reserved;
 } TfVolume;

@@ -28,7 +28,8 @@ _c_sz = ctypes.c_size_t
 
 class TfVolume(ctypes.Structure):
     _fields_ = [("voxels_dev", _c_p), ("n", _c_i64), ("origin", _c_i64 * 3),
-                ("voxel_size", _c_d), ("brick_state_dev", _c_p), ("summary_threshold", ctypes.c_float),
+                ("voxel_size", _c_d), ("brick_state_dev", _c_p), ("brick_flags_dev", _c_p),
+                ("summary_threshold", ctypes.c_float),
                 ("reserved", ctypes.c_int32)]
 
 
@@ -168,11 +169,12 @@ def camera(intr) -> TfCamera:
 
 
 def volume_struct(voxels: torch.Tensor, n: int, origin, voxel_size: float,
-                  brick_bad: torch.Tensor | None = None, threshold: float = 0.0) -> TfVolume:
+                  brick_state: torch.Tensor | None = None, brick_flags: torch.Tensor | None = None,
+                  threshold: float = 0.0) -> TfVolume:
     o = np.asarray(origin, dtype=np.int64)
     return TfVolume(ptr(voxels), int(n), (_c_i64 * 3)(int(o[0]), int(o[1]), int(o[2])),
-                    float(voxel_size), ptr(brick_bad) if brick_bad is not None else None,
-                    float(threshold), 0)
+                    float(voxel_size), ptr(brick_state) if brick_state is not None else None,
+                    ptr(brick_flags) if brick_flags is not None else None, float(threshold), 0)
 
 
 class _Workspace:

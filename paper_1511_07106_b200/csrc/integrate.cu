@@ -651,6 +651,50 @@ __global__ void brick_stats_kernel(const unsigned int *__restrict__ active_count
     }
 }
 
+// Flag byte of brick (bx, by, bz) from the packed states: bit0 = never
+// observed, bit1 = it and its existing +1 neighbours contain only good voxels
+// (every cell whose min corner lies in it has only good corners).
+__device__ __forceinline__ unsigned char brick_flag(const unsigned *st, int64_t nb, int64_t bx,
+                                                    int64_t by, int64_t bz) {
+    const unsigned s0 = st[(bz * nb + by) * nb + bx];
+    unsigned char fl = (s0 >> 16) == 0u ? 1 : 0;
+    bool good = (s0 & 0xFFFFu) == 0u;
+    for (int c = 1; c < 8 && good; ++c) {
+        const int64_t x = bx + (c & 1), y = by + ((c >> 1) & 1), z = bz + (c >> 2);
+        if (x < nb && y < nb && z < nb) good = (st[(z * nb + y) * nb + x] & 0xFFFFu) == 0u;
+    }
+    return fl | (good ? 2 : 0);
+}
+
+// flags of every brick (after a full summary build)
+__global__ void __launch_bounds__(256) brick_flags_all_kernel(const TfVolume vol) {
+    const int64_t nb = (vol.n + 7) / 8, total = nb * nb * nb;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < total;
+         b += (int64_t)gridDim.x * blockDim.x)
+        vol.brick_flags_dev[b] = brick_flag(vol.brick_state_dev, nb, b % nb, (b / nb) % nb, b / (nb * nb));
+}
+
+// flags of the bricks whose 9^3 region contains an active brick (the only
+// ones whose flags can have changed this frame); duplicate writes agree
+__global__ void __launch_bounds__(256) brick_flags_active_kernel(
+    const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
+    const __grid_constant__ FrameGeom f, const uint32_t *__restrict__ active,
+    const unsigned int *__restrict__ active_count) {
+    const unsigned count = *active_count;
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < count * 8u; t += gridDim.x * blockDim.x) {
+        const unsigned g = active[t >> 3];
+        const int vi = find_volume(bt, g);
+        const TfVolume &vol = vt.vol[vi];
+        if (!keeps_summary(vol, f) || !vol.brick_flags_dev) continue;
+        const int64_t nb = bt.nb[vi], local = g - bt.offset[vi];
+        const int c = t & 7;
+        const int64_t bx = local % nb - (c & 1), by = (local / nb) % nb - ((c >> 1) & 1),
+                      bz = local / (nb * nb) - (c >> 2);
+        if (bx < 0 || by < 0 || bz < 0) continue;
+        vol.brick_flags_dev[(bz * nb + by) * nb + bx] = brick_flag(vol.brick_state_dev, nb, bx, by, bz);
+    }
+}
+
 // bad-voxel count of every brick from scratch (one warp per brick)
 __global__ void __launch_bounds__(256) brick_summary_kernel(const TfVolume vol) {
     const int64_t n = vol.n, nb = (n + 7) / 8, total = nb * nb * nb;
@@ -858,6 +902,14 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
         }
         tf_profile_end(prof, stream);
         if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
+        bool any_summary = false;
+        for (int v = 0; v < cnt; ++v)
+            any_summary |= vt.vol[v].brick_flags_dev && vt.vol[v].brick_state_dev &&
+                           vt.vol[v].summary_threshold == f.good_t;
+        if (any_summary) {
+            brick_flags_active_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, bt, f, active, count);
+            if ((rc = tf_check_launch("brick_flags_active_kernel"))) return rc;
+        }
         if (stats) {
             brick_stats_kernel<<<1, 32, 0, stream>>>(count, (unsigned long long)off,
                                                      (unsigned long long *)stats);
@@ -877,5 +929,8 @@ extern "C" int tf_brick_summary(const TfVolume *vol, void *stream_) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     brick_summary_kernel<<<(unsigned)sms * 8, 256, 0, (cudaStream_t)stream_>>>(*vol);
-    return tf_check_launch("brick_summary_kernel");
+    int rc = tf_check_launch("brick_summary_kernel");
+    if (rc || !vol->brick_flags_dev) return rc;
+    brick_flags_all_kernel<<<(unsigned)sms * 8, 256, 0, (cudaStream_t)stream_>>>(*vol);
+    return tf_check_launch("brick_flags_all_kernel");
 }

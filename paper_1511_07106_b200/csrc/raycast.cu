@@ -323,6 +323,7 @@ struct FastRay {
     const unsigned *bad;  // brick summary (NULL: not usable for this tau)
     unsigned nb;
     double idx, idy, idz;  // 1 / d (approximate; only used with margins)
+    const unsigned char *flags;  // per-brick flags (bit0 never observed, bit1 free)
 };
 
 // floor(q) from a 20-bit fixed point: lo = round(q 2^20) mod 2^32 (q in
@@ -390,60 +391,39 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k) {
     return kValidBit | (v > 0.f ? kPosBit : 0u) | (av < r.near ? kNearBit : 0u);
 }
 
-// Summary run starting at march point j: if the cell of j certainly has its
-// min corner in brick b and b is never-observed (kind 2) or b and its +1
-// neighbours are all-good (kind 1), returns the kind and the last fine index
-// k_last >= j whose min corner certainly stays in b (and, for kind 1, below
-// n - 1, so the cell stays inside the volume).  0 = no run.
-__device__ __forceinline__ int summary_run(const FastRay &r, int j, int j_end, int &k_last) {
+// Brick region of lattice point j: when the cell of j certainly has its min
+// corner in brick b, returns b's flag byte and sets `exit` to the largest k
+// (as a double; k <= exit) for which the min corner certainly stays in b —
+// and, for free-space bricks, at most n - 2 so the cell stays in the volume.
+// Margins: 1e-6 voxel against a < 1e-9 error of q.  Returns -1 if undecided.
+__device__ __forceinline__ int region_at(const FastRay &r, int j, double &exit) {
     const double kd = (double)j;
     const double q[3] = {dfma(kd, r.dx, r.q0x), dfma(kd, r.dy, r.q0y), dfma(kd, r.dz, r.q0z)};
     unsigned lo[3], hi[3];
     float fdummy;
-    fixed_cell(q[0], lo[0], hi[0], fdummy);
-    fixed_cell(q[1], lo[1], hi[1], fdummy);
-    fixed_cell(q[2], lo[2], hi[2], fdummy);
-    const unsigned top = (unsigned)(r.n - 2);
-    if (lo[0] != hi[0] || lo[1] != hi[1] || lo[2] != hi[2]) return 0;
-    if (lo[0] > top || lo[1] > top || lo[2] > top) return 0;
-    const unsigned bx = lo[0] >> 3, by = lo[1] >> 3, bz = lo[2] >> 3;
-    const unsigned st = __ldg(&r.bad[(bz * r.nb + by) * r.nb + bx]);
-    int kind = 0;
-    if ((st >> 16) == 0u) {
-        kind = 2;
-    } else if ((st & 0xFFFFu) == 0u) {
-        bool good = true;
 #pragma unroll
-        for (unsigned c = 1; c < 8; ++c) {
-            const unsigned nbx = bx + (c & 1u), nby = by + ((c >> 1) & 1u), nbz = bz + (c >> 2);
-            if (nbx >= r.nb || nby >= r.nb || nbz >= r.nb) continue;  // the cell stays in b there
-            good = good && (__ldg(&r.bad[(nbz * r.nb + nby) * r.nb + nbx]) & 0xFFFFu) == 0u;
-        }
-        if (good) kind = 1;
-    }
-    if (!kind) return 0;
-    // last k with the min corner certainly inside [8b, 8b + 8) (and < n - 1 for
-    // kind 1) on every axis; margin 1e-6 voxel >> the 1e-9 bound on q's error
-    const unsigned b3[3] = {bx, by, bz};
+    for (int a = 0; a < 3; ++a) fixed_cell(q[a], lo[a], hi[a], fdummy);
+    const unsigned top = (unsigned)(r.n - 2);
+    if (lo[0] != hi[0] || lo[1] != hi[1] || lo[2] != hi[2]) return -1;
+    if (lo[0] > top || lo[1] > top || lo[2] > top) return -1;
+    const unsigned b3[3] = {lo[0] >> 3, lo[1] >> 3, lo[2] >> 3};
+    const int fl = __ldg(&r.flags[(b3[2] * r.nb + b3[1]) * r.nb + b3[0]]);
     const double d3[3] = {r.dx, r.dy, r.dz}, id3[3] = {r.idx, r.idy, r.idz};
-    double klim = (double)j_end;
+    double e = 3.0e9;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         double up = (double)(8u * b3[a] + 8u);
-        if (kind == 1 && up > (double)(r.n - 1)) up = (double)(r.n - 1);
+        if ((fl & 2) && up > (double)(r.n - 1)) up = (double)(r.n - 1);
         const double dn = (double)(8u * b3[a]);
-        double ka = klim;
         if (d3[a] > 1e-12)
-            ka = floor((up - 1e-6 - q[a]) * id3[a]) + kd;
+            e = fmin(e, dfma(up - 1e-6 - q[a], id3[a], kd));
         else if (d3[a] < -1e-12)
-            ka = floor((dn + 1e-6 - q[a]) * id3[a]) + kd;
+            e = fmin(e, dfma(dn + 1e-6 - q[a], id3[a], kd));
         else if (q[a] >= up - 1e-6 || q[a] < dn + 1e-6)
-            ka = kd - 1.0;
-        klim = fmin(klim, ka);
+            e = -1.0;
     }
-    if (klim < kd) return 0;
-    k_last = (int)klim;
-    return kind;
+    exit = e;
+    return fl;
 }
 
 // certified decisions of lattice point k (exact fallback when unsure)
@@ -495,45 +475,53 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
     bool prev_has = false;
     int prev_j = -1, last_j = j - 1, swept_j = j - 1;
     int phase = j % coarse;  // j mod coarse, tracked so no division runs per step
-    // fine points in (unseen_from, unseen_until] are certified invalid by a
-    // never-observed brick; unseen_from itself is processed normally (its scan
-    // may reach back before the run)
-    int unseen_from = 0x7fffffff, unseen_until = -1;
+    // current brick region (DDA over 8^3 bricks): fine points j <= region_end
+    // have their min corner in one brick of kind region_kind (bit0 never
+    // observed, bit1 free space, 0 = ordinary)
+    int region_end = -1, region_kind = 0, region_start = 0;
     while (j <= j_end) {
-        if (j > unseen_from && j <= unseen_until) {
-            // invalid sample; any scan covers (max(prev_j, swept_j), j], which
-            // lies inside the run (all invalid): nothing found (:362-405)
-            const bool scan = (prev_has && (prev & kPosBit)) || (swept_j < j - 1 && coarse > 2);
-            if (scan) swept_j = j;
-            last_j = j;
-            ++samples;
-            exact_samples += 1ull << 44;
-            j += coarse - phase;
+        if (fr.flags && j > region_end) {
+            double ex = -1.0;
+            const int fl = region_at(fr, j, ex);
+            region_start = j;
+            if (fl < 0 || ex < (double)j) {
+                region_end = j;  // undecided: this point normally, retry at the next
+                region_kind = 0;
+            } else {
+                region_end = ex >= (double)j_end ? j_end : (int)ex;
+                region_kind = fl & 3;
+            }
+        }
+        if (region_kind & 2) {
+            // free space: every march point in [j, region_end] is valid, positive
+            // and not near -> coarse steps, no scans (:362-416)
+            const int m = region_end - region_end % coarse;  // last multiple of coarse
+            const int p_last = m > j ? m : j;
+            const int cnt = 1 + (m > j ? (m - (j + coarse - phase)) / coarse + 1 : 0);
+            samples += cnt;
+            exact_samples += (unsigned long long)cnt << 44;
+            prev_has = true;
+            prev = kValidBit | kPosBit;
+            prev_j = last_j = p_last;
+            if (p_last != j) phase = 0;
+            j = p_last + (coarse - phase);
             phase = 0;
             continue;
         }
-        if (fr.bad) {
-            int k_last = 0;
-            const int kind = summary_run(fr, j, j_end, k_last);
-            if (kind == 1) {
-                // every march point in [j, k_last] is valid, positive, not near:
-                // coarse steps, no scans (:362-416)
-                while (j <= k_last) {
-                    ++samples;
-                    exact_samples += 1ull << 44;
-                    last_j = j;
-                    prev_j = j;
-                    j += coarse - phase;
-                    phase = 0;
-                }
-                prev_has = true;
-                prev = kValidBit | kPosBit;
-                continue;
-            }
-            if (kind == 2) {
-                unseen_from = j;
-                unseen_until = k_last;
-            }
+        if ((region_kind & 1) && j > region_start) {
+            // never observed: the march points in [j, region_end] are invalid and any
+            // scan covers (max(prev_j, swept_j), p] inside the region: nothing found
+            // (:362-405); j is a multiple of coarse here (invalid -> coarse step)
+            const int cnt = (region_end - j) / coarse + 1;
+            const int p_last = j + (cnt - 1) * coarse;
+            const bool A = prev_has && (prev & kPosBit);
+            if (A || (coarse > 2 && (cnt >= 2 || swept_j < j - 1))) swept_j = p_last;
+            last_j = p_last;
+            samples += cnt;
+            exact_samples += (unsigned long long)cnt << 44;
+            j = p_last + coarse;
+            phase = 0;
+            continue;
         }
         const unsigned s = cert_sample(fr, er, j, samples, exact_samples);
         const bool valid = s & kValidBit;
@@ -662,7 +650,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
                 FastRay fr{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
                            (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh,
                            summ ? vol.brick_state_dev : nullptr, (unsigned)((vol.n + 7) / 8),
-                           1.0 / d[0], 1.0 / d[1], 1.0 / d[2]};
+                           1.0 / d[0], 1.0 / d[1], 1.0 / d[2],
+                           summ ? vol.brick_flags_dev : nullptr};
                 changed |= march_fast(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
                                       exact_samples);
             } else {  // forced, or coordinates too large to certify: the exact reference march

@@ -130,7 +130,8 @@ class TsdfSubvolume:
         # free-space brick summary (TfVolume.brick_state_dev): built lazily for a
         # truncation, kept exact by tf_integrate, dropped when the voxels are
         # replaced from the host
-        self.brick_bad: torch.Tensor | None = None
+        self.brick_bad: torch.Tensor | None = None    # packed per-brick state
+        self.brick_flags: torch.Tensor | None = None  # derived per-brick flags
         self._summary_t: float | None = None
 
     def invalidate_summary(self) -> None:
@@ -170,8 +171,9 @@ class TsdfSubvolume:
             nb = (self.voxels_per_side + 7) // 8
             if self.brick_bad is None:
                 self.brick_bad = torch.empty(nb ** 3, dtype=torch.int32, device=self.voxels.device)
+                self.brick_flags = torch.empty(nb ** 3, dtype=torch.uint8, device=self.voxels.device)
             vol = nat.volume_struct(self.voxels, self.voxels_per_side, self.origin_voxel,
-                                    self.voxel_size, self.brick_bad, thr)
+                                    self.voxel_size, self.brick_bad, self.brick_flags, thr)
             nat.check(L.tf_brick_summary(vol, nat.stream_handle()), "tf_brick_summary")
             self._summary_t = thr
         return self.brick_bad, thr
@@ -216,7 +218,7 @@ class TsdfSubvolume:
                                      self.voxel_size)
         bad, thr = self._summary_for(tau)
         return nat.volume_struct(self.voxels, self.voxels_per_side, self.origin_voxel,
-                                 self.voxel_size, bad, thr)
+                                 self.voxel_size, bad, self.brick_flags, thr)
 
     def __repr__(self) -> str:
         return (f"TsdfSubvolume(origin_voxel={self.origin_voxel!r}, "

@@ -367,9 +367,11 @@ def test_brick_summary_stays_exact_under_integration():
     lib = nat.load_library()
     for t in tiles:
         maintained = t.brick_bad.clone()
+        flags = t.brick_flags.clone()
         t.invalidate_summary()
         t._summary_for(params.truncation)
         assert torch.equal(maintained, t.brick_bad)
+        assert torch.equal(flags, t.brick_flags)
     good = sum(int(((t.brick_bad & 0xFFFF) == 0).sum().item()) for t in tiles)
     unseen = sum(int(((t.brick_bad >> 16) == 0).sum().item()) for t in tiles)
     assert good > 1000 and unseen > 1000  # both kinds of skippable bricks exist
