@@ -62,7 +62,9 @@ typedef struct TfVolume {
     uint32_t *brick_state_dev;
     uint8_t *brick_flags_dev;  /* per brick: bit0 never observed, bit1 the brick
                                   and its +1 neighbours are all-good (cells with
-                                  a min corner in it are free space) */
+                                  a min corner in it are free space); followed
+                                  by ceil(nb/8)^3 superbrick (64^3) bytes, the
+                                  AND of their bricks' flags */
     float summary_threshold;
     int32_t reserved;
 } TfVolume;

@@ -695,6 +695,32 @@ __global__ void __launch_bounds__(256) brick_flags_active_kernel(
     }
 }
 
+// superbrick (8^3 bricks) flags: AND of the member bricks' flags; one warp
+// per superbrick, after the brick flags are final
+__global__ void __launch_bounds__(256) super_flags_kernel(const __grid_constant__ VolumeTable vt,
+                                                          const __grid_constant__ FrameGeom f,
+                                                          int check_threshold) {
+    const int lane = threadIdx.x & 31;
+    for (int v = 0; v < vt.count; ++v) {
+        const TfVolume &vol = vt.vol[v];
+        if (!vol.brick_flags_dev || (check_threshold && !keeps_summary(vol, f))) continue;
+        const int64_t nb = (vol.n + 7) / 8, ns = (nb + 7) / 8, total = ns * ns * ns;
+        const unsigned char *bf = vol.brick_flags_dev;
+        unsigned char *sf = vol.brick_flags_dev + nb * nb * nb;
+        for (int64_t sb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sb < total;
+             sb += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+            const int64_t sx = sb % ns, sy = (sb / ns) % ns, sz = sb / (ns * ns);
+            unsigned acc = 3u;
+            for (int k = lane; k < 512; k += 32) {
+                const int64_t bx = sx * 8 + (k & 7), by = sy * 8 + ((k >> 3) & 7), bz = sz * 8 + (k >> 6);
+                if (bx < nb && by < nb && bz < nb) acc &= bf[(bz * nb + by) * nb + bx];
+            }
+            acc = __reduce_and_sync(0xffffffffu, acc);
+            if (lane == 0) sf[sb] = (unsigned char)acc;
+        }
+    }
+}
+
 // bad-voxel count of every brick from scratch (one warp per brick)
 __global__ void __launch_bounds__(256) brick_summary_kernel(const TfVolume vol) {
     const int64_t n = vol.n, nb = (n + 7) / 8, total = nb * nb * nb;
@@ -909,6 +935,8 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
         if (any_summary) {
             brick_flags_active_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, bt, f, active, count);
             if ((rc = tf_check_launch("brick_flags_active_kernel"))) return rc;
+            super_flags_kernel<<<(unsigned)sms * 2, 256, 0, stream>>>(vt, f, 1);
+            if ((rc = tf_check_launch("super_flags_kernel"))) return rc;
         }
         if (stats) {
             brick_stats_kernel<<<1, 32, 0, stream>>>(count, (unsigned long long)off,
@@ -932,5 +960,11 @@ extern "C" int tf_brick_summary(const TfVolume *vol, void *stream_) {
     int rc = tf_check_launch("brick_summary_kernel");
     if (rc || !vol->brick_flags_dev) return rc;
     brick_flags_all_kernel<<<(unsigned)sms * 8, 256, 0, (cudaStream_t)stream_>>>(*vol);
-    return tf_check_launch("brick_flags_all_kernel");
+    if ((rc = tf_check_launch("brick_flags_all_kernel"))) return rc;
+    VolumeTable vt{};
+    vt.count = 1;
+    vt.vol[0] = *vol;
+    FrameGeom f{};
+    super_flags_kernel<<<(unsigned)sms * 2, 256, 0, (cudaStream_t)stream_>>>(vt, f, 0);
+    return tf_check_launch("super_flags_kernel");
 }

@@ -391,11 +391,14 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k) {
     return kValidBit | (v > 0.f ? kPosBit : 0u) | (av < r.near ? kNearBit : 0u);
 }
 
-// Brick region of lattice point j: when the cell of j certainly has its min
-// corner in brick b, returns b's flag byte and sets `exit` to the largest k
-// (as a double; k <= exit) for which the min corner certainly stays in b —
-// and, for free-space bricks, at most n - 2 so the cell stays in the volume.
-// Margins: 1e-6 voxel against a < 1e-9 error of q.  Returns -1 if undecided.
+// Region of lattice point j for the brick DDA: when the cell of j certainly
+// has its min corner in a never-observed or free-space superbrick (64^3) or
+// brick (8^3), returns its flags (bit0 never observed, bit1 free space) and
+// sets `exit` to the largest k (as a double; k <= exit) for which the min
+// corner certainly stays in that box — for free space also at most n - 2, so
+// the cell stays in the volume.  Margins: 1e-6 voxel against a < 1e-9 error of
+// q, and q is >= 1.4e-6 inside its cell when the floor is certain.  Returns 0
+// for an ordinary brick (exit = its box) and -1 if undecided.
 __device__ __forceinline__ int region_at(const FastRay &r, int j, double &exit) {
     const double kd = (double)j;
     const double q[3] = {dfma(kd, r.dx, r.q0x), dfma(kd, r.dy, r.q0y), dfma(kd, r.dz, r.q0z)};
@@ -406,21 +409,22 @@ __device__ __forceinline__ int region_at(const FastRay &r, int j, double &exit) 
     const unsigned top = (unsigned)(r.n - 2);
     if (lo[0] != hi[0] || lo[1] != hi[1] || lo[2] != hi[2]) return -1;
     if (lo[0] > top || lo[1] > top || lo[2] > top) return -1;
-    const unsigned b3[3] = {lo[0] >> 3, lo[1] >> 3, lo[2] >> 3};
-    const int fl = __ldg(&r.flags[(b3[2] * r.nb + b3[1]) * r.nb + b3[0]]);
-    const double d3[3] = {r.dx, r.dy, r.dz}, id3[3] = {r.idx, r.idy, r.idz};
+    const unsigned ns = (r.nb + 7u) >> 3;
+    const unsigned char *sflags = r.flags + (size_t)r.nb * r.nb * r.nb;
+    int fl = __ldg(&sflags[((lo[2] >> 6) * ns + (lo[1] >> 6)) * ns + (lo[0] >> 6)]) & 3;
+    unsigned shift = 6;
+    if (!fl) {
+        fl = __ldg(&r.flags[((lo[2] >> 3) * r.nb + (lo[1] >> 3)) * r.nb + (lo[0] >> 3)]) & 3;
+        shift = 3;
+    }
+    const double cap = (fl & 2) ? (double)(r.n - 1) : 1.0e30;
+    const double id3[3] = {r.idx, r.idy, r.idz};
     double e = 3.0e9;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        double up = (double)(8u * b3[a] + 8u);
-        if ((fl & 2) && up > (double)(r.n - 1)) up = (double)(r.n - 1);
-        const double dn = (double)(8u * b3[a]);
-        if (d3[a] > 1e-12)
-            e = fmin(e, dfma(up - 1e-6 - q[a], id3[a], kd));
-        else if (d3[a] < -1e-12)
-            e = fmin(e, dfma(dn + 1e-6 - q[a], id3[a], kd));
-        else if (q[a] >= up - 1e-6 || q[a] < dn + 1e-6)
-            e = -1.0;
+        const double base = (double)((lo[a] >> shift) << shift);
+        const double bound = id3[a] > 0.0 ? fmin(base + (double)(1u << shift), cap) - 1e-6 : base + 1e-6;
+        e = fmin(e, dfma(bound - q[a], id3[a], kd));
     }
     exit = e;
     return fl;
@@ -495,9 +499,10 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
         if (region_kind & 2) {
             // free space: every march point in [j, region_end] is valid, positive
             // and not near -> coarse steps, no scans (:362-416)
-            const int m = region_end - region_end % coarse;  // last multiple of coarse
+            const int m = coarse == 2 ? (region_end & ~1) : region_end - region_end % coarse;
             const int p_last = m > j ? m : j;
-            const int cnt = 1 + (m > j ? (m - (j + coarse - phase)) / coarse + 1 : 0);
+            const int first = j + (coarse - phase);
+            const int cnt = 1 + (m > j ? (coarse == 2 ? (m - first) >> 1 : (m - first) / coarse) + 1 : 0);
             samples += cnt;
             exact_samples += (unsigned long long)cnt << 44;
             prev_has = true;
@@ -512,7 +517,7 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
             // never observed: the march points in [j, region_end] are invalid and any
             // scan covers (max(prev_j, swept_j), p] inside the region: nothing found
             // (:362-405); j is a multiple of coarse here (invalid -> coarse step)
-            const int cnt = (region_end - j) / coarse + 1;
+            const int cnt = (coarse == 2 ? (region_end - j) >> 1 : (region_end - j) / coarse) + 1;
             const int p_last = j + (cnt - 1) * coarse;
             const bool A = prev_has && (prev & kPosBit);
             if (A || (coarse > 2 && (cnt >= 2 || swept_j < j - 1))) swept_j = p_last;
@@ -650,7 +655,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
                 FastRay fr{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
                            (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh,
                            summ ? vol.brick_state_dev : nullptr, (unsigned)((vol.n + 7) / 8),
-                           1.0 / d[0], 1.0 / d[1], 1.0 / d[2],
+                           1.0 / (d[0] == 0.0 ? 1e-300 : d[0]), 1.0 / (d[1] == 0.0 ? 1e-300 : d[1]),
+                           1.0 / (d[2] == 0.0 ? 1e-300 : d[2]),
                            summ ? vol.brick_flags_dev : nullptr};
                 changed |= march_fast(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
                                       exact_samples);

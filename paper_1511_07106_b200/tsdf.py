@@ -171,7 +171,9 @@ class TsdfSubvolume:
             nb = (self.voxels_per_side + 7) // 8
             if self.brick_bad is None:
                 self.brick_bad = torch.empty(nb ** 3, dtype=torch.int32, device=self.voxels.device)
-                self.brick_flags = torch.empty(nb ** 3, dtype=torch.uint8, device=self.voxels.device)
+                ns = (nb + 7) // 8  # superbrick flags follow the brick flags
+                self.brick_flags = torch.empty(nb ** 3 + ns ** 3, dtype=torch.uint8,
+                                               device=self.voxels.device)
             vol = nat.volume_struct(self.voxels, self.voxels_per_side, self.origin_voxel,
                                     self.voxel_size, self.brick_bad, self.brick_flags, thr)
             nat.check(L.tf_brick_summary(vol, nat.stream_handle()), "tf_brick_summary")
