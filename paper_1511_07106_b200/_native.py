@@ -69,6 +69,7 @@ _SIGNATURES = {
     "tf_set_debug_flags": (None, [ctypes.c_uint32]),
     "tf_debug_flags": (ctypes.c_uint32, []),
     "tf_launch_count": (ctypes.c_uint64, []),
+    "tf_debug_ray_clock_buffer": (None, [_c_p]),
     "tf_profile_enable": (None, [_c_int]),
     "tf_profile_read": (_c_int, [_c_p, _c_p, _c_int]),
     "tf_integrate_workspace_size": (_c_sz, [_VOL, _c_int, _CAM]),

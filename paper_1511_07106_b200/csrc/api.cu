@@ -57,6 +57,10 @@ void tf_count_launch(unsigned n) { g_launches += n; }
 
 extern "C" uint64_t tf_launch_count(void) { return g_launches.load(); }
 
+static int64_t *g_ray_clock = nullptr;
+extern "C" void tf_debug_ray_clock_buffer(int64_t *buf) { g_ray_clock = buf; }
+int64_t *tf_ray_clock_buffer() { return g_ray_clock; }
+
 extern "C" void tf_profile_enable(int on) { g_profile_on = on; }
 
 void *tf_profile_begin(int kind, cudaStream_t stream) {

@@ -585,7 +585,8 @@ template <int kMinBlocks>
 __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ RayGeom g,
     double *__restrict__ out_dist, double *__restrict__ out_vert, double *__restrict__ out_norm,
-    unsigned long long *__restrict__ stats) {
+    unsigned long long *__restrict__ stats, int64_t *__restrict__ clocks) {
+    const long long t_start = clock64();
     // warp w of the block covers rows 4w..4w+3 of the 8x16 block tile
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t px = (int64_t)blockIdx.x * kRayBlockX + (lane & 7);
@@ -677,6 +678,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
             out_norm[3 * p + 2] = best.nz;
         }
     }
+    if (clocks && px < g.width && py < g.height) clocks[py * g.width + px] = clock64() - t_start;
     if (stats) {
         warp_count_add(&stats[TF_STAT_RAY_SAMPLES], samples);
         warp_count_add(&stats[TF_STAT_RAY_HITS], hits);
@@ -762,11 +764,11 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
             return e ? atoi(e) : 4;
         }();
         if (minb == 4)
-            raycast_kernel<4><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats);
+            raycast_kernel<4><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats, tf_ray_clock_buffer());
         else if (minb == 6)
-            raycast_kernel<6><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats);
+            raycast_kernel<6><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats, tf_ray_clock_buffer());
         else
-            raycast_kernel<5><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats);
+            raycast_kernel<5><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats, tf_ray_clock_buffer());
         tf_profile_end(prof, stream);
         int rc = tf_check_launch("raycast_kernel");
         if (rc) return rc;

@@ -81,5 +81,6 @@ __device__ __forceinline__ void warp_count_add(unsigned long long *dst, unsigned
 int tf_set_error(int code, const char *fmt, ...);
 int tf_check_launch(const char *what);
 void tf_count_launch(unsigned n);
+int64_t *tf_ray_clock_buffer();
 void *tf_profile_begin(int kind, cudaStream_t stream);
 void tf_profile_end(void *token, cudaStream_t stream);

@@ -1,0 +1,38 @@
+"""Debug: per-pixel raycast cycle map on the bench workload (config 3)."""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_1511_07106_b200 as tf  # noqa: E402
+from paper_1511_07106_b200 import _native as nat  # noqa: E402
+from paper_1511_07106_b200.synth import demo_scene  # noqa: E402
+
+intr = tf.RunConfig().intrinsics()
+spec = tf.init_grid(4.08, 1020, 510)
+params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+tiles = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in spec.keys]
+scene = demo_scene()
+poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)
+for p in poses[:40]:
+    tf.integrate_volumes(tiles, scene.render_depth(p, intr), p, intr, params)
+lib = nat.load_library()
+clk = torch.zeros(intr.height * intr.width, dtype=torch.int64, device="cuda")
+lib.tf_debug_ray_clock_buffer(clk.data_ptr())
+rm = tf.RayMap.empty(intr)
+st = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
+tf.raycast_volumes(tiles, poses[41], intr, rm, params, st)
+torch.cuda.synchronize()
+lib.tf_debug_ray_clock_buffer(None)
+c = clk.cpu().numpy().reshape(intr.height, intr.width).astype(np.float64)
+hit = np.isfinite(rm.distance)
+print("cycles/pixel: mean %.0f median %.0f p90 %.0f max %.0f" % (c.mean(), np.median(c), np.percentile(c, 90), c.max()))
+print("hit pixels mean %.0f, miss pixels mean %.0f, hit frac %.2f" % (c[hit].mean(), c[~hit].mean(), hit.mean()))
+w = c.reshape(intr.height // 4, 4, intr.width // 8, 8).max(axis=(1, 3))
+print("warp max mean %.0f; sum of warp max %.3g vs sum of pixel %.3g" % (w.mean(), w.sum() * 32, c.sum()))
+rows = c.reshape(12, 40, 640).mean(axis=(1, 2))
+print("row-band means:", " ".join("%.0f" % r for r in rows))
+print("stats: samples %d exact %d summary %d" % (st[nat.STAT_RAY_SAMPLES], st[nat.STAT_EXACT_SAMPLES], st[nat.STAT_SUMMARY_SAMPLES]))
+np.save("gpurun_out/ray_clocks.npy", c)
