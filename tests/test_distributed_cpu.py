@@ -1,0 +1,103 @@
+"""Multi-GPU host schedule on CPU: world size 2 over gloo (127.0.0.1).
+
+Covers the parts of distributed.py that are backend-agnostic: volume
+ownership, the rank-0 frame broadcast, the all-gather of partial ray maps
+and their rank-order _hit_wins merge.  The merge operator here is a numpy
+restatement of _hit_wins (_kernels.py:246-263); on GPUs the same schedule
+calls tf_raymap_merge.  The merged map must equal a single-process merge of
+all partials in any order (the reference's order-free invariant).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1511_07106_b200.distributed import (broadcast_frame, gather_partials,
+                                               merge_in_rank_order, owned_keys, owner_of)
+
+
+def hit_wins_merge(acc, other):
+    """_hit_wins applied per pixel: acc = (dist, vert, norm) tensors, in place."""
+    d0, v0, n0 = acc
+    d1, v1, n1 = other
+    better = d1 < d0
+    tie = d1 == d0
+    for a in range(3):
+        neq = n1[..., a] != n0[..., a]
+        better = better | (tie & neq & (n1[..., a] > n0[..., a]))
+        tie = tie & ~neq
+    d0[better] = d1[better]
+    v0[better] = v1[better]
+    n0[better] = n1[better]
+
+
+def partial_map(seed, h=12, w=16):
+    """A physically consistent partial map: the hit vertex is distance x the
+    pixel's ray; distances are coarse so exact ties (broken by normals) occur."""
+    g = torch.Generator().manual_seed(seed)
+    d = torch.where(torch.rand(h, w, generator=g) < 0.5, torch.full((h, w), float("inf")),
+                    torch.round(torch.rand(h, w, generator=g) * 8) / 8 + 1.0).double()
+    hit = torch.isfinite(d)
+    ray = torch.stack(torch.meshgrid(torch.arange(h), torch.arange(w), indexing="ij") +
+                      (torch.ones(h, w, dtype=torch.long),), -1).double()
+    v = torch.where(hit[..., None], d[..., None] * ray, torch.zeros(()).double())
+    n = torch.round(torch.rand(h, w, 3, generator=g) * 4).double() / 4  # ties happen
+    n = torch.where(hit[..., None], n, torch.zeros(()).double())
+    return [d, v, n]
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        depth = torch.full((4, 5), float(rank + 1), dtype=torch.float64)
+        broadcast_frame(depth, src=0)
+        parts = partial_map(100 + rank)
+        gathered = gather_partials(parts)
+        merged = merge_in_rank_order(gathered, hit_wins_merge)
+        out[rank] = {"depth": depth.clone(), "merged": [t.clone() for t in merged],
+                     "keys": owned_keys(list(range(8)), rank, world)}
+    finally:
+        dist.destroy_process_group()
+
+
+def test_owner_partition_covers_every_volume_once():
+    keys = [(i, 0, 0) for i in range(11)]
+    for world in (1, 2, 4, 8):
+        owned = [owned_keys(keys, r, world) for r in range(world)]
+        flat = [k for o in owned for k in o]
+        assert sorted(flat) == sorted(keys)
+        assert max(map(len, owned)) - min(map(len, owned)) <= 1
+        assert all(owner_of(i, world) == i % world for i in range(11))
+
+
+def test_gloo_world2_broadcast_gather_merge():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    # every rank received rank 0's frame
+    for r in range(world):
+        assert torch.equal(out[r]["depth"], torch.full((4, 5), 1.0, dtype=torch.float64))
+    # every rank holds the same merged map ...
+    assert all(torch.equal(a, b) for a, b in zip(out[0]["merged"], out[1]["merged"]))
+    # ... equal to a single-process merge of all partials, in either order
+    for order in ([0, 1], [1, 0]):
+        acc = [t.clone() for t in partial_map(100 + order[0])]
+        for r in order[1:]:
+            hit_wins_merge(acc, partial_map(100 + r))
+        assert all(torch.equal(a, b) for a, b in zip(acc, out[0]["merged"]))
+    # volume ownership is disjoint and complete
+    assert sorted(out[0]["keys"] + out[1]["keys"]) == list(range(8))
