@@ -265,8 +265,6 @@ def run_ours(args) -> None:
                                   "raycast": ray_ms / args.steps},
         "integrate": {"noop_updates_per_frame": sum_over_ranks(int(st[nat.STAT_NOOP_UPDATES])) / args.steps, "swept_voxels_per_frame": sum_over_ranks(int(st[nat.STAT_SWEPT_VOXELS])) / args.steps,
                       "exact_path_voxels_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_VOXELS])) / args.steps,
-                      "exact_reasons_per_frame": {k: sum_over_ranks(int(st[s])) / args.steps for k, s in
-                                                  (("pixel_rounding", nat.STAT_EXACT_PROJ), ("camera_plane", nat.STAT_EXACT_PLANE), ("sdf_band", nat.STAT_EXACT_SDF))},
                       "active_bricks_per_frame": sum_over_ranks(int(st[nat.STAT_ACTIVE_BRICKS])) / args.steps,
                       "total_bricks": sum_over_ranks(int(st[nat.STAT_TOTAL_BRICKS])) // max(args.steps, 1)},
         "raycast": {"exact_samples_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_SAMPLES])) / args.steps,

@@ -434,8 +434,10 @@ __device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f) {
 constexpr int kZBatch = 4;  // voxels in flight per thread
 
 // Lane layout per warp and brick: x = lane & 7, y = lane >> 3 (+4 for the
-// second half); each lane walks z in batches of kZBatch, so a warp
-// instruction touches four 64-byte rows.  Bricks come from the cull's list.
+// second half); each lane walks its (x, y) column's 8 z voxels in two
+// batches, so a warp instruction touches four 64-byte rows.  Column-level
+// work (float64 base, error bounds, whole-column rejection) is amortised over
+// the column; per voxel the screen is ~25 float32 instructions.
 __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const double2 *__restrict__ table,
@@ -450,7 +452,10 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const int lx = lane & 7, ly = lane >> 3;
     const float tau_ea = f.tau32 + 2.4e-7f * (f.tau32 + 16.f);  // d < 16 m rounding allowance
     const float2 fixed = make_float2(f.tau32, (float)f.max_w);
-    unsigned long long updates = 0, swept = 0, nop = 0, ex_proj = 0, ex_plane = 0, ex_sdf = 0;
+    const float hw = 0.5f * f.w32, hh = 0.5f * f.h32;
+    const float k3u = 9.6e-7f * f.fx32, k3v = 9.6e-7f * f.fy32;
+    const float k2u = 9.6e-7f * (fabsf(f.cx32) + 2.f), k2v = 9.6e-7f * (fabsf(f.cy32) + 2.f);
+    unsigned updates = 0, swept = 0, nop = 0;
     for (unsigned i = warp; i < count; i += nwarps) {
         const unsigned g = active[i];
         const int vi = find_volume(bt, g);
@@ -461,6 +466,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         const unsigned x = (bxy % nb) * kBrick + lx;
         const unsigned z0 = (local / (nb * nb)) * kBrick;
         const unsigned y_base = (bxy / nb) * kBrick + ly;
+        const unsigned nz = min(n - z0, (unsigned)kBrick);
         float2 *vox = (float2 *)vol.voxels_dev;
         const double vs = vol.voxel_size;
         const float vs32 = (float)vs;
@@ -468,11 +474,13 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         const double gx = dmul((double)((int64_t)x + vol.origin[0]), vs);
         const double gz0 = dmul((double)((int64_t)z0 + vol.origin[2]), vs);
         const float szx = f.r32[2] * vs32, szy = f.r32[5] * vs32, szz = f.r32[8] * vs32;
+        const float zspan = (float)(nz - 1);
         const bool keep = keeps_summary(vol, f);
         unsigned dbad = 0;  // change of this brick's packed state (summary)
 #pragma unroll 1
         for (int hy = 0; hy < 2; ++hy) {
             const unsigned y = y_base + 4 * hy;
+            const bool row_in = x < n && y < n;
             const double gy = dmul((double)((int64_t)y + vol.origin[1]), vs);
             // float32 column bases at z0 (plain float64, then rounded)
             const float pbx = (float)(R[0] * gx + R[1] * gy + R[2] * gz0 + f.t_cw.v[0]);
@@ -486,38 +494,67 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
             const float epd = 9.5367432e-7f * (fabsf(dbx) + fabsf(dby) + fabsf(dbz) + walk) + 1e-30f;
             const float mabs = 8.f * epd * (fabsf(dbx) + fabsf(dby) + fabsf(dbz) + 8.f * vs32 + epd);
             const float k1u = f.fx32 * epc * 1.05f, k1v = f.fy32 * epc * 1.05f;
-            const float k3u = 9.6e-7f * f.fx32, k3v = 9.6e-7f * f.fy32;
-            const float k2u = 9.6e-7f * (fabsf(f.cx32) + 2.f), k2v = 9.6e-7f * (fabsf(f.cy32) + 2.f);
-            const bool row_in = x < n && y < n;
-            const float hw = 0.5f * f.w32, hh = 0.5f * f.h32;
+            // column bound: all voxels in front by > 64 epc -> one (du, dv) for the
+            // column from its smallest pcz and largest |pcx|, |pcy| (linear in z)
+            const float pz1 = fmaf(zspan, szz, pbz);
+            const float zlo = fminf(pbz, pz1) - epc;
+            const bool front = zlo > 64.f * epc;
+            float du = 0.f, dv = 0.f;
+            bool col_live = row_in;
+            if (front) {
+                const float rzm = 1.0f / zlo;
+                const float px1 = fmaf(zspan, szx, pbx), py1 = fmaf(zspan, szy, pby);
+                const float xnm = (fmaxf(fabsf(pbx), fabsf(px1)) + epc) * rzm;
+                const float ynm = (fmaxf(fabsf(pby), fabsf(py1)) + epc) * rzm;
+                du = fmaf(k1u, rzm * (1.f + xnm), fmaf(k3u, xnm, k2u));
+                dv = fmaf(k1v, rzm * (1.f + ynm), fmaf(k3v, ynm, k2v));
+                // the column's projections lie between its end projections
+                const float a0 = fmaf(f.fx32, pbx / pbz, f.cx32 + 0.5f), a1 = fmaf(f.fx32, px1 / pz1, f.cx32 + 0.5f);
+                const float b0 = fmaf(f.fy32, pby / pbz, f.cy32 + 0.5f), b1 = fmaf(f.fy32, py1 / pz1, f.cy32 + 0.5f);
+                if (fmaxf(a0, a1) + du < 0.f || fminf(a0, a1) - du >= f.w32 ||
+                    fmaxf(b0, b1) + dv < 0.f || fminf(b0, b1) - dv >= f.h32)
+                    col_live = false;  // whole column clearly outside the image (:113)
+            } else if (fmaxf(pbz, pz1) + epc < 0.f) {
+                col_live = false;      // whole column behind the camera (:107)
+            }
+            if (row_in) swept += nz;
+            const float hu = 0.5f - du, hv = 0.5f - dv;
+            const bool fast = front && hu > 0.f && hv > 0.f;
+            unsigned exact_mask = 0;
 #pragma unroll 1
             for (int zb = 0; zb < kBrick; zb += kZBatch) {
                 int cls[kZBatch];
                 unsigned pix[kZBatch];
-                float2 px[kZBatch];
-                // A: pixel of every voxel of the batch.  |u+0.5 error| <= du with
-                // du = fx epc 1.05 rz (1 + |xn|) + 2^-20 (fx |xn| + |cx| + 2)
-                // (propagated column error + float32 rounding of inputs and ops)
+                // A: pixel of every voxel of the batch
 #pragma unroll
                 for (int j = 0; j < kZBatch; ++j) {
                     const float kz = (float)(zb + j);
                     const float pcx = fmaf(kz, szx, pbx), pcy = fmaf(kz, szy, pby), pcz = fmaf(kz, szz, pbz);
                     int c = kSkip;
                     pix[j] = 0;
-                    if (row_in && z0 + zb + j < n) {
-                        if (pcz > 64.f * epc) {
+                    if (col_live && (unsigned)(zb + j) < nz) {
+                        float ddu = du, ddv = dv;
+                        bool ok = fast;
+                        if (!fast) {  // rare: per-voxel bound (near the camera plane)
+                            ok = pcz > 64.f * epc;
+                            if (ok) {
+                                const float rz = rcp_approx(pcz);
+                                const float xn = fabsf(pcx * rz), yn = fabsf(pcy * rz);
+                                ddu = fmaf(k1u, rz * (1.f + xn), fmaf(k3u, xn, k2u));
+                                ddv = fmaf(k1v, rz * (1.f + yn), fmaf(k3v, yn, k2v));
+                            } else {
+                                c = (pcz + epc < 0.f) ? kSkip : kExact;  // behind (:107) / on the plane
+                            }
+                        }
+                        if (ok) {
                             const float rz = rcp_approx(pcz);
-                            const float xn = pcx * rz, yn = pcy * rz;
-                            const float a = fmaf(f.fx32, xn, f.cx32 + 0.5f);
-                            const float b = fmaf(f.fy32, yn, f.cy32 + 0.5f);
-                            const float du = fmaf(k1u, rz * (1.f + fabsf(xn)), fmaf(k3u, fabsf(xn), k2u));
-                            const float dv = fmaf(k1v, rz * (1.f + fabsf(yn)), fmaf(k3v, fabsf(yn), k2v));
+                            const float a = fmaf(f.fx32, pcx * rz, f.cx32 + 0.5f);
+                            const float b = fmaf(f.fy32, pcy * rz, f.cy32 + 0.5f);
                             const float fa = floorf(a), fb = floorf(b);
-                            if (fabsf(a - hw) >= hw + du || fabsf(b - hh) >= hh + dv) {
+                            if (fabsf(a - hw) >= hw + ddu || fabsf(b - hh) >= hh + ddv) {
                                 c = kSkip;  // clearly outside the image (:113)
-                            } else if (fabsf(a - fa - 0.5f) >= 0.5f - du || fabsf(b - fb - 0.5f) >= 0.5f - dv) {
-                                c = kExact;                             // within du of a rounding edge
-                                ++ex_proj;
+                            } else if (fabsf(a - fa - 0.5f) >= 0.5f - ddu || fabsf(b - fb - 0.5f) >= 0.5f - ddv) {
+                                c = kExact;  // within the bound of a rounding edge
                             } else {
                                 const int ui = (int)fa, vi2 = (int)fb;  // saturating conversion
                                 if ((unsigned)ui < (unsigned)f.width && (unsigned)vi2 < (unsigned)f.height) {
@@ -525,15 +562,12 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                                     pix[j] = (unsigned)vi2 * (unsigned)f.width + (unsigned)ui;
                                 }
                             }
-                        } else {
-                            c = (pcz + epc < 0.f) ? kSkip : kExact;  // behind (:107) / on the plane
-                            ex_plane += c == kExact;
                         }
-                        swept += 1;
                     }
                     cls[j] = c;
                 }
                 // B: screening depth / ray scale of the decided pixels
+                float2 px[kZBatch];
 #pragma unroll
                 for (int j = 0; j < kZBatch; ++j)
                     px[j] = cls[j] == kFree ? __ldg(&table32[pix[j]]) : make_float2(0.f, 0.f);
@@ -549,7 +583,6 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                     if (!(d > 0.f)) c = kSkip;  // d32 > 0 exactly when d > 0
                     else if (A > 0.f && fmaf(dist2, 1.00001f, mabs) <= A * A * 0.99999f) c = kFree;
                     else if (fmaf(dist2, 0.99999f, -mabs) > B * B * 1.00001f) c = kSkip;
-                    ex_sdf += c == kExact;
                     cls[j] = c;
                 }
                 // D: load the voxels with a free-space update
@@ -558,42 +591,38 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
 #pragma unroll
                 for (int j = 0; j < kZBatch; ++j)
                     old[j] = cls[j] == kFree ? vox[(size_t)row + (size_t)j * n * n] : make_float2(0.f, 0.f);
-                // E: free-space updates; exact voxels are queued
-                unsigned overflow = 0;
+                // E: free-space updates
 #pragma unroll
                 for (int j = 0; j < kZBatch; ++j) {
-                    const size_t lin = (size_t)row + (size_t)j * n * n;
                     if (cls[j] == kFree) {
                         ++updates;
                         if (fixed_point && old[j].x == fixed.x && old[j].y == fixed.y) {
                             ++nop;  // (tau32, max_w) is a host-verified fixed point
                         } else {
                             const float2 nv = free_update(old[j], f);
-                            vox[lin] = nv;
+                            vox[(size_t)row + (size_t)j * n * n] = nv;
                             dbad += voxel_state(nv, f.good_t) - voxel_state(old[j], f.good_t);
                         }
                     }
-                    const bool ex = cls[j] == kExact;
-                    const unsigned m = __ballot_sync(0xffffffffu, ex);
-                    if (m) {
-                        unsigned long long base = 0;
-                        if (lane == 0) base = atomicAdd(queue_count, (unsigned long long)__popc(m));
-                        base = __shfl_sync(0xffffffffu, base, 0) + __popc(m & ((1u << lane) - 1u));
-                        if (ex) {
-                            if (base < queue_cap)
-                                queue[base] = ((unsigned long long)vi << 40) | (unsigned long long)lin;
-                            else
-                                overflow |= 1u << j;  // queue full: exact update in place below
-                        }
-                    }
+                    if (cls[j] == kExact) exact_mask |= 1u << (zb + j);
                 }
-#pragma unroll 1
-                for (int j = 0; overflow && j < kZBatch; ++j) {
-                    if (!((overflow >> j) & 1u)) continue;
-                    const double gz = dmul((double)((int64_t)(z0 + zb + j) + vol.origin[2]), vs);
-                    unsigned db = 0;
-                    updates += update_voxel(vox, (int64_t)row + (int64_t)j * n * n, gx, gy, gz, table, f, &db);
-                    dbad += db;
+            }
+            // undecided voxels of the column go to the exact kernel
+            if (__any_sync(0xffffffffu, exact_mask != 0u) && exact_mask) {
+                const unsigned c = __popc(exact_mask);
+                const unsigned long long base = atomicAdd(queue_count, (unsigned long long)c);
+                unsigned k = 0;
+                for (unsigned m = exact_mask; m; m &= m - 1, ++k) {
+                    const unsigned zz = __ffs(m) - 1;
+                    const unsigned long long lin = (unsigned long long)(z0 + zz) * n * n + (unsigned long long)y * n + x;
+                    if (base + k < queue_cap) {
+                        queue[base + k] = ((unsigned long long)vi << 40) | lin;
+                    } else {  // queue full: exact update in place (still exact)
+                        const double gz = dmul((double)((int64_t)(z0 + zz) + vol.origin[2]), vs);
+                        unsigned db = 0;
+                        updates += update_voxel_slow(vox, (int64_t)lin, gx, gy, gz, table, f, &db);
+                        dbad += db;
+                    }
                 }
             }
         }
@@ -607,9 +636,6 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
         warp_count_add(&stats[TF_STAT_SWEPT_VOXELS], swept);
         warp_count_add(&stats[TF_STAT_NOOP_UPDATES], nop);
-        warp_count_add(&stats[TF_STAT_EXACT_PROJ], ex_proj);
-        warp_count_add(&stats[TF_STAT_EXACT_PLANE], ex_plane);
-        warp_count_add(&stats[TF_STAT_EXACT_SDF], ex_sdf);
     }
 }
 

@@ -28,8 +28,8 @@ def main(path, top=40):
         if cur is None or not r[ei].strip().isdigit():
             continue
         agg[cur][0] += int(r[ei])
-        agg[cur][1] += int(r[ti] or 0)
-        agg[cur][2] += int(r[wi] or 0)
+        agg[cur][1] += int(r[ti]) if r[ti].strip().isdigit() else 0
+        agg[cur][2] += int(r[wi]) if r[wi].strip().isdigit() else 0
     tot = sum(v[0] for v in agg.values())
     tots = sum(v[2] for v in agg.values())
     print(f"warp instructions {tot}, stall samples {tots}")
