@@ -265,6 +265,8 @@ def run_ours(args) -> None:
                                   "raycast": ray_ms / args.steps},
         "integrate": {"noop_updates_per_frame": sum_over_ranks(int(st[nat.STAT_NOOP_UPDATES])) / args.steps, "swept_voxels_per_frame": sum_over_ranks(int(st[nat.STAT_SWEPT_VOXELS])) / args.steps,
                       "exact_path_voxels_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_VOXELS])) / args.steps,
+                      "column_rejected_per_frame": sum_over_ranks(int(st[nat.STAT_COL_SKIPPED])) / args.steps,
+                      "depth_rejected_per_frame": sum_over_ranks(int(st[nat.STAT_DEPTH_SKIPPED])) / args.steps,
                       "active_bricks_per_frame": sum_over_ranks(int(st[nat.STAT_ACTIVE_BRICKS])) / args.steps,
                       "total_bricks": sum_over_ranks(int(st[nat.STAT_TOTAL_BRICKS])) // max(args.steps, 1)},
         "raycast": {"exact_samples_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_SAMPLES])) / args.steps,

@@ -85,9 +85,8 @@ enum {
     TF_STAT_RAY_HITS = 5,      /* hits merged by this raycast call */
     TF_STAT_EXACT_VOXELS = 6,  /* voxels the float32 screen deferred to the exact path */
     TF_STAT_NOOP_UPDATES = 7,  /* updates proven to leave the voxel unchanged (store skipped) */
-    TF_STAT_EXACT_PROJ = 8,    /* ... deferred: pixel rounding too close to call */
-    TF_STAT_EXACT_PLANE = 9,   /* ... deferred: on the camera plane */
-    TF_STAT_EXACT_SDF = 10,    /* ... deferred: sdf within the +-tau band */
+    TF_STAT_COL_SKIPPED = 8,   /* swept voxels rejected as whole columns */
+    TF_STAT_DEPTH_SKIPPED = 9, /* swept voxels rejected by the depth test (d <= 0 / sdf < -tau) */
     TF_STAT_EXACT_SAMPLES = 11, /* ray samples evaluated with the exact arithmetic */
     TF_STAT_CERT_FAILURES = 12, /* certified decisions contradicted by exact ones (must be 0) */
     TF_STAT_SUMMARY_SAMPLES = 13, /* ray samples certified by the brick summary alone */

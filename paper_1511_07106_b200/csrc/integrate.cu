@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const float hw = 0.5f * f.w32, hh = 0.5f * f.h32;
     const float k3u = 9.6e-7f * f.fx32, k3v = 9.6e-7f * f.fy32;
     const float k2u = 9.6e-7f * (fabsf(f.cx32) + 2.f), k2v = 9.6e-7f * (fabsf(f.cy32) + 2.f);
-    unsigned updates = 0, swept = 0, nop = 0;
+    unsigned updates = 0, swept = 0, nop = 0, col_skipped = 0, depth_skipped = 0;
     for (unsigned i = warp; i < count; i += nwarps) {
         const unsigned g = active[i];
         const int vi = find_volume(bt, g);
@@ -518,6 +518,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                 col_live = false;      // whole column behind the camera (:107)
             }
             if (row_in) swept += nz;
+            if (row_in && !col_live) col_skipped += nz;
             const float hu = 0.5f - du, hv = 0.5f - dv;
             const bool fast = front && hu > 0.f && hv > 0.f;
             unsigned exact_mask = 0;
@@ -583,6 +584,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                     if (!(d > 0.f)) c = kSkip;  // d32 > 0 exactly when d > 0
                     else if (A > 0.f && fmaf(dist2, 1.00001f, mabs) <= A * A * 0.99999f) c = kFree;
                     else if (fmaf(dist2, 0.99999f, -mabs) > B * B * 1.00001f) c = kSkip;
+                    depth_skipped += c == kSkip;
                     cls[j] = c;
                 }
                 // D: load the voxels with a free-space update
@@ -636,6 +638,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
         warp_count_add(&stats[TF_STAT_SWEPT_VOXELS], swept);
         warp_count_add(&stats[TF_STAT_NOOP_UPDATES], nop);
+        warp_count_add(&stats[TF_STAT_COL_SKIPPED], col_skipped);
+        warp_count_add(&stats[TF_STAT_DEPTH_SKIPPED], depth_skipped);
     }
 }
 
