@@ -87,6 +87,7 @@ enum {
     TF_STAT_NOOP_UPDATES = 7,  /* updates proven to leave the voxel unchanged (store skipped) */
     TF_STAT_COL_SKIPPED = 8,   /* swept voxels rejected as whole columns */
     TF_STAT_DEPTH_SKIPPED = 9, /* swept voxels rejected by the depth test (d <= 0 / sdf < -tau) */
+    TF_STAT_FREE_BRICKS = 10,  /* active bricks certified all free space (streaming kernel) */
     TF_STAT_EXACT_SAMPLES = 11, /* ray samples evaluated with the exact arithmetic */
     TF_STAT_CERT_FAILURES = 12, /* certified decisions contradicted by exact ones (must be 0) */
     TF_STAT_SUMMARY_SAMPLES = 13, /* ray samples certified by the brick summary alone */

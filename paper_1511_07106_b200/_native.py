@@ -55,7 +55,7 @@ def profile_read() -> dict:
 # TF_STAT_* slots (tfb200.h)
 STAT_VOXEL_UPDATES, STAT_SWEPT_VOXELS, STAT_ACTIVE_BRICKS, STAT_TOTAL_BRICKS = 0, 1, 2, 3
 STAT_RAY_SAMPLES, STAT_RAY_HITS, STAT_EXACT_VOXELS, STAT_NOOP_UPDATES = 4, 5, 6, 7
-STAT_COL_SKIPPED, STAT_DEPTH_SKIPPED, STAT_EXACT_SAMPLES = 8, 9, 11
+STAT_COL_SKIPPED, STAT_DEPTH_SKIPPED, STAT_FREE_BRICKS, STAT_EXACT_SAMPLES = 8, 9, 10, 11
 STAT_CERT_FAILURES = 12
 STAT_SUMMARY_SAMPLES = 13
 STAT_COUNT = 16

@@ -105,14 +105,27 @@ static MipDesc make_mip(int64_t width, int64_t height) {
 // One 16x16 block per finest tile.  Depths are >= 0, so their IEEE bit
 // patterns order like the values and the coarser levels use atomicMax on the
 // bits (exact; order-independent).
+// order-preserving float <-> uint32 keys (for atomicMin over signed floats)
+__device__ __forceinline__ unsigned fkey(float f) {
+    const unsigned b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_dec(unsigned k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
 __global__ void __launch_bounds__(256) frame_prep_kernel(
     const double *__restrict__ depth, double2 *__restrict__ table, float2 *__restrict__ table32,
-    unsigned long long *__restrict__ mip, const MipDesc m, const double fx,
+    unsigned long long *__restrict__ mip, unsigned *__restrict__ qmip, const double tau,
+    const MipDesc m, const double fx,
     const double fy, const double cx, const double cy, const int64_t width,
     const int64_t height) {
     const int64_t ui = (int64_t)blockIdx.x * kTile + threadIdx.x;
     const int64_t vi = (int64_t)blockIdx.y * kTile + threadIdx.y;
     double d = 0.0;
+    // free-space key: q = (d - tau) * ray_scale rounded down, -inf without depth;
+    // a voxel at distance dist seen through this pixel has sdf >= tau iff dist <= q
+    unsigned qk = 0xffffffffu;
     if (ui < width && vi < height) {
         d = depth[vi * width + ui];
         // _kernels.py:118-120
@@ -123,18 +136,32 @@ __global__ void __launch_bounds__(256) frame_prep_kernel(
         // screening copy: d32 > 0 exactly when d > 0 (tiny depths clamp up)
         const float d32 = d > 0.0 ? fmaxf(__double2float_rn(d), 1.17549435e-38f) : 0.0f;
         table32[vi * width + ui] = make_float2(d32, __double2float_rn(rs));
+        qk = fkey(d > 0.0 ? __double2float_rd((d - tau) * rs) : -INFINITY);
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qk = min(qk, __shfl_xor_sync(0xffffffffu, qk, o));
     // block max of the (non-negative) depths
     double v = d > 0.0 ? d : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     __shared__ double wmax[8];
+    __shared__ unsigned wq[8];
     const int t = threadIdx.y * kTile + threadIdx.x;
-    if ((t & 31) == 0) wmax[t >> 5] = v;
+    if ((t & 31) == 0) {
+        wmax[t >> 5] = v;
+        wq[t >> 5] = qk;
+    }
     __syncthreads();
     if (t == 0) {
         double b = wmax[0];
-        for (int i = 1; i < 8; ++i) b = fmax(b, wmax[i]);
+        unsigned qb = wq[0];
+        for (int i = 1; i < 8; ++i) {
+            b = fmax(b, wmax[i]);
+            qb = min(qb, wq[i]);
+        }
+        qmip[m.offset[0] + (int64_t)blockIdx.y * m.tiles_x[0] + blockIdx.x] = qb;
+        for (int l = 1; l < m.levels; ++l)
+            atomicMin(&qmip[m.offset[l] + ((int64_t)blockIdx.y >> l) * m.tiles_x[l] + ((int64_t)blockIdx.x >> l)], qb);
         const unsigned long long bits = (unsigned long long)__double_as_longlong(b);
         mip[m.offset[0] + (int64_t)blockIdx.y * m.tiles_x[0] + blockIdx.x] = bits;
         for (int l = 1; l < m.levels; ++l) {
@@ -164,6 +191,21 @@ __device__ double rect_max_depth(const unsigned long long *__restrict__ mip, con
     return __longlong_as_double((long long)best);
 }
 
+// Min of the free-space key over the pixel rectangle (same level choice as
+// rect_max_depth; cells cover a superset, so the min is a lower bound).
+__device__ float rect_min_q(const unsigned *__restrict__ qmip, const MipDesc &m, int64_t u0,
+                            int64_t u1, int64_t v0, int64_t v1) {
+    int l = 0;
+    while (l + 1 < m.levels &&
+           (((u1 >> (4 + l)) - (u0 >> (4 + l)) + 1) > 4 || ((v1 >> (4 + l)) - (v0 >> (4 + l)) + 1) > 4))
+        ++l;
+    unsigned best = 0xffffffffu;
+    for (int64_t ty = v0 >> (4 + l); ty <= (v1 >> (4 + l)); ++ty)
+        for (int64_t tx = u0 >> (4 + l); tx <= (u1 >> (4 + l)); ++tx)
+            best = min(best, __ldg(&qmip[m.offset[l] + ty * m.tiles_x[l] + tx]));
+    return fkey_dec(best);
+}
+
 // ---------------------------------------------------------------------------
 // 2. conservative brick culling
 // ---------------------------------------------------------------------------
@@ -178,9 +220,13 @@ __device__ __forceinline__ int find_volume(const BrickTable &bt, int64_t g) {
 // _kernels.py:107-127.  Evaluated in float32 around a float64 brick origin;
 // every comparison carries an explicit bound on the float32 error plus a wide
 // safety factor, so a brick is dropped only if no voxel can be updated.
-__device__ bool brick_may_update(const TfVolume &vol, int64_t bx, int64_t by, int64_t bz,
-                                 const FrameGeom &f, const unsigned long long *__restrict__ mip,
-                                 const MipDesc &m) {
+// Returns 0 (no voxel can update), 1 (some may) or 2 (every voxel certainly is
+// a free-space update: in front of the camera, projecting inside the image
+// onto pixels with depth, and closer than (d - tau) * ray_scale for every pixel
+// its projection box covers -> sdf >= tau, clamped value exactly tau).
+__device__ int brick_may_update(const TfVolume &vol, int64_t bx, int64_t by, int64_t bz,
+                                const FrameGeom &f, const unsigned long long *__restrict__ mip,
+                                const unsigned *__restrict__ qmip, const MipDesc &m, bool allow_free) {
     const int64_t n = vol.n;
     const int64_t i0[3] = {bx * kBrick, by * kBrick, bz * kBrick};
     double g0[3];
@@ -219,9 +265,10 @@ __device__ bool brick_may_update(const TfVolume &vol, int64_t bx, int64_t by, in
         xabs = fmaxf(xabs, fabsf(pcs[c][0]));
         yabs = fmaxf(yabs, fabsf(pcs[c][1]));
     }
-    if (zmax < -2.f * err) return false;  // every voxel has pcz <= 0 (:107)
+    if (zmax < -2.f * err) return 0;  // every voxel has pcz <= 0 (:107)
 
     int64_t u0 = 0, u1 = f.width - 1, v0 = 0, v1 = f.height - 1;
+    bool box_inside = false;  // projection box certainly inside the image
     if (zmin > 0.01f + 2.f * err) {
         // in front of the camera: all voxel projections lie inside the
         // projected corners' bounding box (convexity), up to rounding
@@ -244,14 +291,15 @@ __device__ bool brick_may_update(const TfVolume &vol, int64_t bx, int64_t by, in
         const float fu0 = floorf(umin - mu + 0.5f), fu1 = floorf(umax + mu + 0.5f);
         const float fv0 = floorf(vmin - mv + 0.5f), fv1 = floorf(vmax + mv + 0.5f);
         if (fu1 < 0.f || fv1 < 0.f || fu0 > f.w32 - 1.f || fv0 > f.h32 - 1.f)
-            return false;  // outside the image (:113)
+            return 0;  // outside the image (:113)
+        box_inside = fu0 >= 0.f && fv0 >= 0.f && fu1 <= f.w32 - 1.f && fv1 <= f.h32 - 1.f;
         u0 = fu0 < 0.f ? 0 : (int64_t)fu0;
         v0 = fv0 < 0.f ? 0 : (int64_t)fv0;
         u1 = fu1 > f.w32 - 1.f ? f.width - 1 : (int64_t)fu1;
         v1 = fv1 > f.h32 - 1.f ? f.height - 1 : (int64_t)fv1;
     }
     const float dmax = __double2float_ru(rect_max_depth(mip, m, u0, u1, v0, v1));
-    if (!(dmax > 0.f)) return false;  // no valid depth reachable (:116)
+    if (!(dmax > 0.f)) return 0;  // no valid depth reachable (:116)
 
     // sdf = d - dist / ray_scale < -tau for every voxel (:125-127)?
     float dd2 = 0.f, cabs = 0.f;
@@ -267,32 +315,129 @@ __device__ bool brick_may_update(const TfVolume &vol, int64_t bx, int64_t by, in
     const float rs_ub = sqrtf(ax * ax + ay * ay + 1.f) * (1.f + 1e-5f);
     const float q_lb = dist_lb / rs_ub;
     const float margin = 1e-5f * (dmax + fabsf(q_lb) + f.tau32) + 1e-6f;
-    if (dmax - q_lb < -f.tau32 - margin) return false;
-    return true;
+    if (dmax - q_lb < -f.tau32 - margin) return 0;
+    if (allow_free && box_inside) {
+        // farthest voxel (distance is convex: a corner) vs the smallest
+        // (d - tau) * ray_scale over the box, with float32 margins
+        float dd2max = 0.f;
+        for (int c = 0; c < 8; ++c) {
+            float q2 = 0.f;
+            for (int a = 0; a < 3; ++a) {
+                const float e = (((c >> a) & 1) ? gmax[a] : gmin[a]) - (float)f.cam.v[a];
+                q2 += e * e;
+            }
+            dd2max = fmaxf(dd2max, q2);
+        }
+        const float dist_ub = sqrtf(dd2max) * 1.00002f + 3.8e-6f * (gabs + cabs) + 1e-6f;
+        const float qmin = rect_min_q(qmip, m, u0, u1, v0, v1);
+        if (qmin > 0.f && dist_ub <= qmin * 0.99998f) return 2;
+    }
+    return 1;
 }
 
 __global__ void __launch_bounds__(256) brick_cull_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const __grid_constant__ MipDesc m,
-    const unsigned long long *__restrict__ mip, uint32_t *__restrict__ active,
-    unsigned int *__restrict__ active_count, const int no_cull) {
+    const unsigned long long *__restrict__ mip, const unsigned *__restrict__ qmip,
+    uint32_t *__restrict__ active, unsigned int *__restrict__ active_count,
+    uint32_t *__restrict__ active_free, unsigned int *__restrict__ free_count, const int no_cull,
+    const int allow_free) {
     const int64_t total = bt.offset[bt.count];
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool keep = false;
+    int kind = 0;
     if (g < total) {
         const int v = find_volume(bt, g);
         const int64_t local = g - bt.offset[v], nb = bt.nb[v];
-        keep = no_cull || brick_may_update(vt.vol[v], local % nb, (local / nb) % nb,
-                                           local / (nb * nb), f, mip, m);
+        kind = brick_may_update(vt.vol[v], local % nb, (local / nb) % nb, local / (nb * nb), f, mip,
+                                qmip, m, allow_free != 0);
+        if (no_cull && kind == 0) kind = 1;
     }
-    // warp-aggregated append (list order is irrelevant: voxels are independent)
-    const unsigned mask = __ballot_sync(0xffffffffu, keep);
-    if (mask) {
-        const int lane = threadIdx.x & 31;
+    // warp-aggregated appends (list order is irrelevant: voxels are independent)
+    const int lane = threadIdx.x & 31;
+    const unsigned mg = __ballot_sync(0xffffffffu, kind == 1), mf = __ballot_sync(0xffffffffu, kind == 2);
+    if (mg) {
         unsigned base = 0;
-        if (lane == 0) base = atomicAdd(active_count, (unsigned)__popc(mask));
+        if (lane == 0) base = atomicAdd(active_count, (unsigned)__popc(mg));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (keep) active[base + __popc(mask & ((1u << lane) - 1u))] = (uint32_t)g;
+        if (kind == 1) active[base + __popc(mg & ((1u << lane) - 1u))] = (uint32_t)g;
+    }
+    if (mf) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(free_count, (unsigned)__popc(mf));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (kind == 2) active_free[base + __popc(mf & ((1u << lane) - 1u))] = (uint32_t)g;
+    }
+}
+
+__device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f);
+
+// Certified free-space bricks: every voxel gets the clamped-to-tau running
+// mean (_kernels.py:128-133 with clamped == tau).  Pure streaming: 16-byte
+// voxel pairs, four lanes per 64-byte row, eight rows per warp instruction.
+__global__ void __launch_bounds__(256) brick_free_kernel(
+    const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
+    const __grid_constant__ FrameGeom f, const uint32_t *__restrict__ list,
+    const unsigned int *__restrict__ list_count, const int fixed_point,
+    unsigned long long *__restrict__ stats) {
+    const unsigned count = *list_count;
+    const int lane = threadIdx.x & 31;
+    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+    const float2 fixed = make_float2(f.tau32, (float)f.max_w);
+    unsigned updates = 0, nop = 0;
+    for (unsigned i = warp; i < count; i += nwarps) {
+        const unsigned g = list[i];
+        const int vi = find_volume(bt, g);
+        const TfVolume &vol = vt.vol[vi];
+        const unsigned n = (unsigned)vol.n, nb = (unsigned)bt.nb[vi];
+        const unsigned local = g - (unsigned)bt.offset[vi];
+        const unsigned x = (local % nb) * kBrick + 2 * (lane & 3);
+        const unsigned y0 = ((local / nb) % nb) * kBrick, z0 = (local / (nb * nb)) * kBrick;
+        float2 *vox = (float2 *)vol.voxels_dev;
+        const bool pair = (n & 1u) == 0u;
+        unsigned dbad = 0;
+#pragma unroll 2
+        for (int it = 0; it < 8; ++it) {
+            const unsigned r = (unsigned)(lane >> 2) + 8u * it;  // row = y + 8 z
+            const unsigned y = y0 + (r & 7u), z = z0 + (r >> 3);
+            if (y >= n || z >= n || x >= n) continue;
+            const size_t lin = ((size_t)z * n + y) * n + x;
+            const bool two = x + 1 < n;
+            float4 o;
+            if (pair) {
+                o = *reinterpret_cast<const float4 *>(vox + lin);
+            } else {
+                const float2 a = vox[lin];
+                const float2 b = two ? vox[lin + 1] : make_float2(0.f, 0.f);
+                o = make_float4(a.x, a.y, b.x, b.y);
+            }
+            const float2 a = make_float2(o.x, o.y), b = make_float2(o.z, o.w);
+            const bool na = fixed_point && a.x == fixed.x && a.y == fixed.y;
+            const bool nbp = !two || (fixed_point && b.x == fixed.x && b.y == fixed.y);
+            updates += 1u + (two ? 1u : 0u);
+            nop += (na ? 1u : 0u) + (two && nbp ? 1u : 0u);
+            if (na && nbp) continue;  // provably unchanged (host-verified fixed point)
+            const float2 ua = na ? a : free_update(a, f);
+            const float2 ub = nbp ? b : free_update(b, f);
+            dbad += voxel_state(ua, f.good_t) - voxel_state(a, f.good_t);
+            if (two) dbad += voxel_state(ub, f.good_t) - voxel_state(b, f.good_t);
+            if (pair) {
+                *reinterpret_cast<float4 *>(vox + lin) = make_float4(ua.x, ua.y, ub.x, ub.y);
+            } else {
+                vox[lin] = ua;
+                if (two) vox[lin + 1] = ub;
+            }
+        }
+        if (keeps_summary(vol, f)) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
+            if (lane == 0 && dbad) atomicAdd(&vol.brick_state_dev[local], dbad);
+        }
+    }
+    if (stats) {
+        warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
+        warp_count_add(&stats[TF_STAT_SWEPT_VOXELS], updates);
+        warp_count_add(&stats[TF_STAT_NOOP_UPDATES], nop);
     }
 }
 
@@ -674,9 +819,11 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
 }
 
 __global__ void brick_stats_kernel(const unsigned int *__restrict__ active_count,
+                                   const unsigned int *__restrict__ free_count,
                                    unsigned long long total, unsigned long long *stats) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
-        stats[TF_STAT_ACTIVE_BRICKS] += *active_count;
+        stats[TF_STAT_ACTIVE_BRICKS] += *active_count + *free_count;
+        stats[TF_STAT_FREE_BRICKS] += *free_count;
         stats[TF_STAT_TOTAL_BRICKS] += total;
     }
 }
@@ -777,7 +924,7 @@ __global__ void __launch_bounds__(256) brick_summary_kernel(const TfVolume vol) 
 // ---------------------------------------------------------------------------
 
 struct IntegrateLayout {
-    size_t table_off, table32_off, mip_off, count_off, active_off, queue_off, total;
+    size_t table_off, table32_off, mip_off, qmip_off, count_off, active_off, free_off, queue_off, total;
     unsigned long long queue_cap;
 };
 
@@ -796,9 +943,13 @@ static IntegrateLayout layout_for(int64_t total_bricks_max, const TfCamera *cam)
     off = align_up(off + (size_t)(cam->width * cam->height) * sizeof(float2), 256);
     L.mip_off = off;
     off = align_up(off + (size_t)m.total * sizeof(unsigned long long), 256);
+    L.qmip_off = off;
+    off = align_up(off + (size_t)m.total * sizeof(unsigned), 256);
     L.count_off = off;
     off = align_up(off + 256, 256);
     L.active_off = off;
+    off = align_up(off + (size_t)total_bricks_max * sizeof(uint32_t), 256);
+    L.free_off = off;
     off = align_up(off + (size_t)total_bricks_max * sizeof(uint32_t), 256);
     L.queue_off = off;
     L.queue_cap = kQueueCap;
@@ -859,6 +1010,9 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
     double2 *table = (double2 *)(ws + L.table_off);
     float2 *table32 = (float2 *)(ws + L.table32_off);
     unsigned long long *mip = (unsigned long long *)(ws + L.mip_off);
+    unsigned *qmip = (unsigned *)(ws + L.qmip_off);
+    unsigned int *fcount = (unsigned int *)(ws + L.count_off + 8);
+    uint32_t *active_free = (uint32_t *)(ws + L.free_off);
     unsigned int *count = (unsigned int *)(ws + L.count_off);
     unsigned long long *qcount = (unsigned long long *)(ws + L.count_off + 64);
     unsigned long long *queue = (unsigned long long *)(ws + L.queue_off);
@@ -866,11 +1020,12 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
     const MipDesc m = make_mip(cam->width, cam->height);
 
     void *prof_all = tf_profile_begin(TF_PROF_INTEGRATE_ALL, stream);
-    if (cudaMemsetAsync(mip, 0, (size_t)m.total * sizeof(unsigned long long), stream) != cudaSuccess)
+    if (cudaMemsetAsync(mip, 0, (size_t)m.total * sizeof(unsigned long long), stream) != cudaSuccess ||
+        cudaMemsetAsync(qmip, 0xff, (size_t)m.total * sizeof(unsigned), stream) != cudaSuccess)
         return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
     dim3 pblock(kTile, kTile);
     dim3 pgrid((unsigned)m.tiles_x[0], (unsigned)m.tiles_y[0]);
-    frame_prep_kernel<<<pgrid, pblock, 0, stream>>>(depth, table, table32, mip, m, cam->fx,
+    frame_prep_kernel<<<pgrid, pblock, 0, stream>>>(depth, table, table32, mip, qmip, tau, m, cam->fx,
                                                     cam->fy, cam->cx, cam->cy, cam->width,
                                                     cam->height);
     int rc = tf_check_launch("frame_prep_kernel");
@@ -940,8 +1095,10 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
         if (cudaMemsetAsync(count, 0, 128, stream) != cudaSuccess)  // brick + queue counters
             return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
         const unsigned cull_blocks = (unsigned)((off + 255) / 256);
-        brick_cull_kernel<<<cull_blocks, 256, 0, stream>>>(vt, bt, f, m, mip, active, count,
-                                                           (tf_debug_flags() & TF_DEBUG_NO_CULL) ? 1 : 0);
+        const int exact_only = (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) ? 1 : 0;
+        brick_cull_kernel<<<cull_blocks, 256, 0, stream>>>(
+            vt, bt, f, m, mip, qmip, active, count, active_free, fcount,
+            (tf_debug_flags() & TF_DEBUG_NO_CULL) ? 1 : 0, exact_only ? 0 : 1);
         if ((rc = tf_check_launch("brick_cull_kernel"))) return rc;
         void *prof = tf_profile_begin(TF_PROF_INTEGRATE_UPDATE, stream);
         if (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) {
@@ -952,6 +1109,10 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
                 vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap,
                 fixed_point, (unsigned long long *)stats);
             if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
+            if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
+            brick_free_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(vt, bt, f, active_free, fcount,
+                                                                    fixed_point, (unsigned long long *)stats);
+            if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
             exact_queue_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, f, table, queue, qcount,
                                                                      L.queue_cap,
                                                                      (unsigned long long *)stats);
@@ -965,11 +1126,13 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
         if (any_summary) {
             brick_flags_active_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, bt, f, active, count);
             if ((rc = tf_check_launch("brick_flags_active_kernel"))) return rc;
+            brick_flags_active_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, bt, f, active_free, fcount);
+            if ((rc = tf_check_launch("brick_flags_active_kernel"))) return rc;
             super_flags_kernel<<<(unsigned)sms * 2, 256, 0, stream>>>(vt, f, 1);
             if ((rc = tf_check_launch("super_flags_kernel"))) return rc;
         }
         if (stats) {
-            brick_stats_kernel<<<1, 32, 0, stream>>>(count, (unsigned long long)off,
+            brick_stats_kernel<<<1, 32, 0, stream>>>(count, fcount, (unsigned long long)off,
                                                      (unsigned long long *)stats);
             if ((rc = tf_check_launch("brick_stats_kernel"))) return rc;
         }
