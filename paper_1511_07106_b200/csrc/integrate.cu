@@ -226,14 +226,16 @@ __device__ __forceinline__ int find_volume(const BrickTable &bt, int64_t g) {
 // its projection box covers -> sdf >= tau, clamped value exactly tau).
 __device__ int brick_may_update(const TfVolume &vol, int64_t bx, int64_t by, int64_t bz,
                                 const FrameGeom &f, const unsigned long long *__restrict__ mip,
-                                const unsigned *__restrict__ qmip, const MipDesc &m, bool allow_free) {
+                                const unsigned *__restrict__ qmip, const MipDesc &m, bool allow_free,
+                                int span = 1) {
+    // box of span^3 bricks starting at brick (bx, by, bz)
     const int64_t n = vol.n;
     const int64_t i0[3] = {bx * kBrick, by * kBrick, bz * kBrick};
     double g0[3];
     float ext[3], gmin[3], gmax[3];
     float gabs = 0.f;
     for (int a = 0; a < 3; ++a) {
-        const int64_t i1 = min(i0[a] + kBrick - 1, n - 1);
+        const int64_t i1 = min(i0[a] + (int64_t)kBrick * span - 1, n - 1);
         // the reference's voxel centres (i + ht) * vs are monotone in i
         g0[a] = (double)(i0[a] + vol.origin[a]) * vol.voxel_size;
         const double g1 = (double)(i1 + vol.origin[a]) * vol.voxel_size;
@@ -335,37 +337,111 @@ __device__ int brick_may_update(const TfVolume &vol, int64_t bx, int64_t by, int
     return 1;
 }
 
+constexpr int kMacro = 4;  // macro cull box: 4^3 bricks = 32^3 voxels
+
+// Stage 1: one thread per 32^3 macro box of every volume.  Culled macros
+// drop their 64 bricks; certified free-space macros put all their bricks on
+// the free list; the rest go to stage 2.
+__global__ void __launch_bounds__(256) macro_cull_kernel(
+    const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
+    const __grid_constant__ FrameGeom f, const __grid_constant__ MipDesc m,
+    const unsigned long long *__restrict__ mip, const unsigned *__restrict__ qmip,
+    uint32_t *__restrict__ macros, unsigned int *__restrict__ macro_count,
+    uint32_t *__restrict__ active_free, unsigned int *__restrict__ free_count, const int no_cull,
+    const int allow_free) {
+    // macro index space: volume v owns nm(v)^3 macros after mfirst(v)
+    int64_t mfirst[TFB200_MAX_VOLUMES_PER_LAUNCH + 1];
+    mfirst[0] = 0;
+    for (int v = 0; v < bt.count; ++v) {
+        const int64_t nm = (bt.nb[v] + kMacro - 1) / kMacro;
+        mfirst[v + 1] = mfirst[v] + nm * nm * nm;
+    }
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int kind = 0;
+    int v = 0;
+    int64_t mx = 0, my = 0, mz = 0, nm = 1;
+    if (g < mfirst[bt.count]) {
+        while (g >= mfirst[v + 1]) ++v;
+        nm = (bt.nb[v] + kMacro - 1) / kMacro;
+        const int64_t local = g - mfirst[v];
+        mx = local % nm;
+        my = (local / nm) % nm;
+        mz = local / (nm * nm);
+        kind = brick_may_update(vt.vol[v], mx * kMacro, my * kMacro, mz * kMacro, f, mip, qmip, m,
+                                allow_free != 0, kMacro);
+        if (no_cull && kind == 0) kind = 1;
+    }
+    if (kind == 2) {  // every brick of the macro is certified free space
+        const int64_t nb = bt.nb[v];
+        unsigned cnt = 0;
+        uint32_t ids[kMacro * kMacro * kMacro];
+        for (int k = 0; k < kMacro * kMacro * kMacro; ++k) {
+            const int64_t bx = mx * kMacro + (k & 3), by = my * kMacro + ((k >> 2) & 3),
+                          bz = mz * kMacro + (k >> 4);
+            if (bx < nb && by < nb && bz < nb) ids[cnt++] = (uint32_t)(bt.offset[v] + (bz * nb + by) * nb + bx);
+        }
+        const unsigned base = atomicAdd(free_count, cnt);
+        for (unsigned k = 0; k < cnt; ++k) active_free[base + k] = ids[k];
+    }
+    const int lane = threadIdx.x & 31;
+    const unsigned mg = __ballot_sync(0xffffffffu, kind == 1);
+    if (mg) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(macro_count, (unsigned)__popc(mg));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (kind == 1) macros[base + __popc(mg & ((1u << lane) - 1u))] = (uint32_t)g;
+    }
+}
+
+// Stage 2: one thread per brick of every surviving macro (grid-stride).
 __global__ void __launch_bounds__(256) brick_cull_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const __grid_constant__ MipDesc m,
     const unsigned long long *__restrict__ mip, const unsigned *__restrict__ qmip,
+    const uint32_t *__restrict__ macros, const unsigned int *__restrict__ macro_count,
     uint32_t *__restrict__ active, unsigned int *__restrict__ active_count,
     uint32_t *__restrict__ active_free, unsigned int *__restrict__ free_count, const int no_cull,
     const int allow_free) {
-    const int64_t total = bt.offset[bt.count];
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int kind = 0;
-    if (g < total) {
-        const int v = find_volume(bt, g);
-        const int64_t local = g - bt.offset[v], nb = bt.nb[v];
-        kind = brick_may_update(vt.vol[v], local % nb, (local / nb) % nb, local / (nb * nb), f, mip,
-                                qmip, m, allow_free != 0);
-        if (no_cull && kind == 0) kind = 1;
+    int64_t mfirst[TFB200_MAX_VOLUMES_PER_LAUNCH + 1];
+    mfirst[0] = 0;
+    for (int v = 0; v < bt.count; ++v) {
+        const int64_t nm = (bt.nb[v] + kMacro - 1) / kMacro;
+        mfirst[v + 1] = mfirst[v] + nm * nm * nm;
     }
-    // warp-aggregated appends (list order is irrelevant: voxels are independent)
+    const unsigned total = *macro_count * (kMacro * kMacro * kMacro);
     const int lane = threadIdx.x & 31;
-    const unsigned mg = __ballot_sync(0xffffffffu, kind == 1), mf = __ballot_sync(0xffffffffu, kind == 2);
-    if (mg) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(active_count, (unsigned)__popc(mg));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (kind == 1) active[base + __popc(mg & ((1u << lane) - 1u))] = (uint32_t)g;
-    }
-    if (mf) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(free_count, (unsigned)__popc(mf));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (kind == 2) active_free[base + __popc(mf & ((1u << lane) - 1u))] = (uint32_t)g;
+    for (unsigned t0 = blockIdx.x * blockDim.x; t0 < total; t0 += gridDim.x * blockDim.x) {
+        const unsigned t = t0 + threadIdx.x;
+        int kind = 0;
+        uint32_t gb = 0;
+        if (t < total) {
+            const int64_t gm = macros[t >> 6];
+            const int sub = t & 63;
+            int v = 0;
+            while (gm >= mfirst[v + 1]) ++v;
+            const int64_t nb = bt.nb[v], nm = (nb + kMacro - 1) / kMacro, local = gm - mfirst[v];
+            const int64_t bx = (local % nm) * kMacro + (sub & 3), by = ((local / nm) % nm) * kMacro + ((sub >> 2) & 3),
+                          bz = (local / (nm * nm)) * kMacro + (sub >> 4);
+            if (bx < nb && by < nb && bz < nb) {
+                gb = (uint32_t)(bt.offset[v] + (bz * nb + by) * nb + bx);
+                kind = brick_may_update(vt.vol[v], bx, by, bz, f, mip, qmip, m, allow_free != 0);
+                if (no_cull && kind == 0) kind = 1;
+            }
+        }
+        // warp-aggregated appends (list order is irrelevant: voxels are independent)
+        const unsigned mg = __ballot_sync(0xffffffffu, kind == 1), mf = __ballot_sync(0xffffffffu, kind == 2);
+        if (mg) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(active_count, (unsigned)__popc(mg));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (kind == 1) active[base + __popc(mg & ((1u << lane) - 1u))] = gb;
+        }
+        if (mf) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(free_count, (unsigned)__popc(mf));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (kind == 2) active_free[base + __popc(mf & ((1u << lane) - 1u))] = gb;
+        }
     }
 }
 
@@ -872,29 +948,38 @@ __global__ void __launch_bounds__(256) brick_flags_active_kernel(
     }
 }
 
-// superbrick (8^3 bricks) flags: AND of the member bricks' flags; one warp
-// per superbrick, after the brick flags are final
+// superbrick (8^3 bricks) flags: AND of the member bricks' flags.  One warp
+// per (volume, superbrick) over all volumes of the launch; each lane ANDs 16
+// flag bytes read as 4 x uint32 words of 4 consecutive x bricks.
 __global__ void __launch_bounds__(256) super_flags_kernel(const __grid_constant__ VolumeTable vt,
                                                           const __grid_constant__ FrameGeom f,
                                                           int check_threshold) {
     const int lane = threadIdx.x & 31;
+    int64_t first[TFB200_MAX_VOLUMES_PER_LAUNCH + 1];
+    first[0] = 0;
     for (int v = 0; v < vt.count; ++v) {
+        const int64_t nb = (vt.vol[v].n + 7) / 8, ns = (nb + 7) / 8;
+        first[v + 1] = first[v] + ns * ns * ns;
+    }
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < first[vt.count];
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int v = 0;
+        while (w >= first[v + 1]) ++v;
         const TfVolume &vol = vt.vol[v];
         if (!vol.brick_flags_dev || (check_threshold && !keeps_summary(vol, f))) continue;
-        const int64_t nb = (vol.n + 7) / 8, ns = (nb + 7) / 8, total = ns * ns * ns;
+        const int64_t nb = (vol.n + 7) / 8, ns = (nb + 7) / 8, sb = w - first[v];
+        const int64_t sx = sb % ns, sy = (sb / ns) % ns, sz = sb / (ns * ns);
         const unsigned char *bf = vol.brick_flags_dev;
-        unsigned char *sf = vol.brick_flags_dev + nb * nb * nb;
-        for (int64_t sb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sb < total;
-             sb += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-            const int64_t sx = sb % ns, sy = (sb / ns) % ns, sz = sb / (ns * ns);
-            unsigned acc = 3u;
-            for (int k = lane; k < 512; k += 32) {
-                const int64_t bx = sx * 8 + (k & 7), by = sy * 8 + ((k >> 3) & 7), bz = sz * 8 + (k >> 6);
-                if (bx < nb && by < nb && bz < nb) acc &= bf[(bz * nb + by) * nb + bx];
-            }
-            acc = __reduce_and_sync(0xffffffffu, acc);
-            if (lane == 0) sf[sb] = (unsigned char)acc;
+        unsigned acc = 3u;
+        // 64 (y, z) rows of 8 x bricks; lane handles rows lane and lane + 32
+        for (int r = lane; r < 64; r += 32) {
+            const int64_t by = sy * 8 + (r & 7), bz = sz * 8 + (r >> 3);
+            if (by >= nb || bz >= nb) continue;
+            const int64_t bx0 = sx * 8;
+            for (int k = 0; k < 8 && bx0 + k < nb; ++k) acc &= bf[(bz * nb + by) * nb + bx0 + k];
         }
+        acc = __reduce_and_sync(0xffffffffu, acc);
+        if (lane == 0) vol.brick_flags_dev[nb * nb * nb + sb] = (unsigned char)acc;
     }
 }
 
@@ -924,7 +1009,8 @@ __global__ void __launch_bounds__(256) brick_summary_kernel(const TfVolume vol) 
 // ---------------------------------------------------------------------------
 
 struct IntegrateLayout {
-    size_t table_off, table32_off, mip_off, qmip_off, count_off, active_off, free_off, queue_off, total;
+    size_t table_off, table32_off, mip_off, qmip_off, count_off, active_off, free_off, macro_off, queue_off,
+        total;
     unsigned long long queue_cap;
 };
 
@@ -950,6 +1036,8 @@ static IntegrateLayout layout_for(int64_t total_bricks_max, const TfCamera *cam)
     L.active_off = off;
     off = align_up(off + (size_t)total_bricks_max * sizeof(uint32_t), 256);
     L.free_off = off;
+    off = align_up(off + (size_t)total_bricks_max * sizeof(uint32_t), 256);
+    L.macro_off = off;
     off = align_up(off + (size_t)total_bricks_max * sizeof(uint32_t), 256);
     L.queue_off = off;
     L.queue_cap = kQueueCap;
@@ -1013,6 +1101,8 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
     unsigned *qmip = (unsigned *)(ws + L.qmip_off);
     unsigned int *fcount = (unsigned int *)(ws + L.count_off + 8);
     uint32_t *active_free = (uint32_t *)(ws + L.free_off);
+    uint32_t *macros = (uint32_t *)(ws + L.macro_off);
+    unsigned int *mcount = (unsigned int *)(ws + L.count_off + 16);
     unsigned int *count = (unsigned int *)(ws + L.count_off);
     unsigned long long *qcount = (unsigned long long *)(ws + L.count_off + 64);
     unsigned long long *queue = (unsigned long long *)(ws + L.queue_off);
@@ -1094,11 +1184,19 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
         bt.offset[cnt] = off;
         if (cudaMemsetAsync(count, 0, 128, stream) != cudaSuccess)  // brick + queue counters
             return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
-        const unsigned cull_blocks = (unsigned)((off + 255) / 256);
         const int exact_only = (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) ? 1 : 0;
-        brick_cull_kernel<<<cull_blocks, 256, 0, stream>>>(
-            vt, bt, f, m, mip, qmip, active, count, active_free, fcount,
-            (tf_debug_flags() & TF_DEBUG_NO_CULL) ? 1 : 0, exact_only ? 0 : 1);
+        const int no_cull = (tf_debug_flags() & TF_DEBUG_NO_CULL) ? 1 : 0;
+        int64_t macros_total = 0;
+        for (int v = 0; v < cnt; ++v) {
+            const int64_t nm = (bt.nb[v] + kMacro - 1) / kMacro;
+            macros_total += nm * nm * nm;
+        }
+        macro_cull_kernel<<<(unsigned)((macros_total + 255) / 256), 256, 0, stream>>>(
+            vt, bt, f, m, mip, qmip, macros, mcount, active_free, fcount, no_cull, exact_only ? 0 : 1);
+        if ((rc = tf_check_launch("macro_cull_kernel"))) return rc;
+        brick_cull_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(
+            vt, bt, f, m, mip, qmip, macros, mcount, active, count, active_free, fcount, no_cull,
+            exact_only ? 0 : 1);
         if ((rc = tf_check_launch("brick_cull_kernel"))) return rc;
         void *prof = tf_profile_begin(TF_PROF_INTEGRATE_UPDATE, stream);
         if (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) {
@@ -1128,7 +1226,7 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
             if ((rc = tf_check_launch("brick_flags_active_kernel"))) return rc;
             brick_flags_active_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, bt, f, active_free, fcount);
             if ((rc = tf_check_launch("brick_flags_active_kernel"))) return rc;
-            super_flags_kernel<<<(unsigned)sms * 2, 256, 0, stream>>>(vt, f, 1);
+            super_flags_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, f, 1);
             if ((rc = tf_check_launch("super_flags_kernel"))) return rc;
         }
         if (stats) {

@@ -343,7 +343,7 @@ __device__ __forceinline__ void fixed_cell(double q, unsigned &lo, unsigned &hi,
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 
-__device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k) {
+__device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k, bool use_summary) {
     const double kd = (double)k;
     unsigned lx, hx, ly, hy, lz, hz;
     float fx, fy, fz;
@@ -354,7 +354,7 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k) {
     const unsigned ix = lx, iy = ly, iz = lz;
     const unsigned top = (unsigned)(r.n - 2);
     if (ix > top || iy > top || iz > top) return 0u;                  // invalid (:38)
-    if (r.bad) {
+    if (use_summary) {
         // min corner in a never-observed brick: certainly invalid (:40-50);
         // every corner in bricks whose voxels are all observed and >= T:
         // certainly valid, positive and not near the surface
@@ -383,8 +383,9 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k) {
     if (wmin <= 0.0f) return 0u;                                      // invalid (:40-50)
     const float v = lerpf(lerpf(lerpf(c000.x, c100.x, fx), lerpf(c010.x, c110.x, fx), fy),
                           lerpf(lerpf(c001.x, c101.x, fx), lerpf(c011.x, c111.x, fx), fy), fz);
-    const float cmax = fmaxf(fmaxf(fmaxf(fabsf(c000.x), fabsf(c100.x)), fmaxf(fabsf(c010.x), fabsf(c110.x))),
-                             fmaxf(fmaxf(fabsf(c001.x), fabsf(c101.x)), fmaxf(fabsf(c011.x), fabsf(c111.x))));
+    const float cmax = fmaxf(fmaxf(fmaxf(fabsf(c000.x), fabsf(c100.x)), fabsf(c010.x)),
+                             fmaxf(fmaxf(fabsf(c110.x), fabsf(c001.x)),
+                                   fmaxf(fmaxf(fabsf(c101.x), fabsf(c011.x)), fabsf(c111.x))));
     const float ev = 2e-5f * cmax + 1e-30f;
     const float av = fabsf(v);
     if (av <= ev || fabsf(av - r.near) <= ev + r.near_tol) return kUnsure;
@@ -433,9 +434,10 @@ __device__ __forceinline__ int region_at(const FastRay &r, int j, double &exit) 
 // certified decisions of lattice point k (exact fallback when unsure)
 __device__ __forceinline__ unsigned cert_sample(const FastRay &fr, const Ray &er, int k,
                                                 unsigned long long &samples,
-                                                unsigned long long &exact_samples) {
+                                                unsigned long long &exact_samples,
+                                                bool use_summary = true) {
     ++samples;
-    const unsigned s = fast_sample(fr, k);
+    const unsigned s = fast_sample(fr, k, use_summary && fr.bad != nullptr);
     if (s & kSummaryBit) exact_samples += 1ull << 44;  // summary-certified (counter in the high bits)
     if (!(s & kUnsure)) return s & ~kSummaryBit;
     ++exact_samples;
@@ -528,7 +530,8 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
             phase = 0;
             continue;
         }
-        const unsigned s = cert_sample(fr, er, j, samples, exact_samples);
+        // inside a known ordinary brick region the per-sample summary cannot help
+        const unsigned s = cert_sample(fr, er, j, samples, exact_samples, region_end < j || region_kind != 0);
         const bool valid = s & kValidBit;
         bool do_scan = false;
         if (!valid || !(s & kPosBit)) {                                 // :362-369
