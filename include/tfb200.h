@@ -91,6 +91,7 @@ enum {
     TF_STAT_EXACT_SAMPLES = 11, /* ray samples evaluated with the exact arithmetic */
     TF_STAT_CERT_FAILURES = 12, /* certified decisions contradicted by exact ones (must be 0) */
     TF_STAT_SUMMARY_SAMPLES = 13, /* ray samples certified by the brick summary alone */
+    TF_STAT_GENERAL_ALL_FREE = 14, /* general-path bricks whose voxels all turned out free space */
     TF_STAT_COUNT = 16
 };
 

@@ -58,6 +58,7 @@ STAT_RAY_SAMPLES, STAT_RAY_HITS, STAT_EXACT_VOXELS, STAT_NOOP_UPDATES = 4, 5, 6,
 STAT_COL_SKIPPED, STAT_DEPTH_SKIPPED, STAT_FREE_BRICKS, STAT_EXACT_SAMPLES = 8, 9, 10, 11
 STAT_CERT_FAILURES = 12
 STAT_SUMMARY_SAMPLES = 13
+STAT_GENERAL_ALL_FREE = 14
 STAT_COUNT = 16
 
 _VOL = ctypes.POINTER(TfVolume)

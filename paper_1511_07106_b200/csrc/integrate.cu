@@ -676,8 +676,9 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const float hw = 0.5f * f.w32, hh = 0.5f * f.h32;
     const float k3u = 9.6e-7f * f.fx32, k3v = 9.6e-7f * f.fy32;
     const float k2u = 9.6e-7f * (fabsf(f.cx32) + 2.f), k2v = 9.6e-7f * (fabsf(f.cy32) + 2.f);
-    unsigned updates = 0, swept = 0, nop = 0, col_skipped = 0, depth_skipped = 0;
+    unsigned updates = 0, swept = 0, nop = 0, col_skipped = 0, depth_skipped = 0, all_free_bricks = 0;
     for (unsigned i = warp; i < count; i += nwarps) {
+        unsigned not_free = 0;  // voxels of this brick that were not free-space updates
         const unsigned g = active[i];
         const int vi = find_volume(bt, g);
         const TfVolume &vol = vt.vol[vi];
@@ -828,6 +829,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                         }
                     }
                     if (cls[j] == kExact) exact_mask |= 1u << (zb + j);
+                    if (row_in && (unsigned)(zb + j) < nz && cls[j] != kFree) ++not_free;
                 }
             }
             // undecided voxels of the column go to the exact kernel
@@ -854,6 +856,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
             for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
             if (lane == 0 && dbad) atomicAdd(&vol.brick_state_dev[local], dbad);
         }
+        if (__all_sync(0xffffffffu, not_free == 0u) && lane == 0) ++all_free_bricks;
     }
     if (stats) {
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
@@ -861,6 +864,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         warp_count_add(&stats[TF_STAT_NOOP_UPDATES], nop);
         warp_count_add(&stats[TF_STAT_COL_SKIPPED], col_skipped);
         warp_count_add(&stats[TF_STAT_DEPTH_SKIPPED], depth_skipped);
+        warp_count_add(&stats[TF_STAT_GENERAL_ALL_FREE], all_free_bricks);
     }
 }
 
