@@ -269,7 +269,6 @@ def run_ours(args) -> None:
                       "depth_rejected_per_frame": sum_over_ranks(int(st[nat.STAT_DEPTH_SKIPPED])) / args.steps,
                       "active_bricks_per_frame": sum_over_ranks(int(st[nat.STAT_ACTIVE_BRICKS])) / args.steps,
                       "free_space_bricks_per_frame": sum_over_ranks(int(st[nat.STAT_FREE_BRICKS])) / args.steps,
-                      "general_bricks_all_free_per_frame": sum_over_ranks(int(st[nat.STAT_GENERAL_ALL_FREE])) / args.steps,
                       "total_bricks": sum_over_ranks(int(st[nat.STAT_TOTAL_BRICKS])) // max(args.steps, 1)},
         "raycast": {"exact_samples_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_SAMPLES])) / args.steps,
                     "certification_failures": sum_over_ranks(int(st[nat.STAT_CERT_FAILURES])),

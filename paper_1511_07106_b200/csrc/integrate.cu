@@ -446,10 +446,12 @@ __global__ void __launch_bounds__(256) brick_cull_kernel(
 }
 
 __device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f);
+__device__ __forceinline__ unsigned free_state_delta(float2 old, float2 nv, float t);
 
 // Certified free-space bricks: every voxel gets the clamped-to-tau running
 // mean (_kernels.py:128-133 with clamped == tau).  Pure streaming: 16-byte
-// voxel pairs, four lanes per 64-byte row, eight rows per warp instruction.
+// voxel pairs, four lanes per 64-byte row, eight rows per warp instruction,
+// four rows' loads in flight per lane.
 __global__ void __launch_bounds__(256) brick_free_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const uint32_t *__restrict__ list,
@@ -470,41 +472,57 @@ __global__ void __launch_bounds__(256) brick_free_kernel(
         const unsigned x = (local % nb) * kBrick + 2 * (lane & 3);
         const unsigned y0 = ((local / nb) % nb) * kBrick, z0 = (local / (nb * nb)) * kBrick;
         float2 *vox = (float2 *)vol.voxels_dev;
-        const bool pair = (n & 1u) == 0u;
+        const bool keep = keeps_summary(vol, f);
         unsigned dbad = 0;
-#pragma unroll 2
-        for (int it = 0; it < 8; ++it) {
-            const unsigned r = (unsigned)(lane >> 2) + 8u * it;  // row = y + 8 z
-            const unsigned y = y0 + (r & 7u), z = z0 + (r >> 3);
-            if (y >= n || z >= n || x >= n) continue;
-            const size_t lin = ((size_t)z * n + y) * n + x;
-            const bool two = x + 1 < n;
-            float4 o;
-            if (pair) {
-                o = *reinterpret_cast<const float4 *>(vox + lin);
-            } else {
-                const float2 a = vox[lin];
-                const float2 b = two ? vox[lin + 1] : make_float2(0.f, 0.f);
-                o = make_float4(a.x, a.y, b.x, b.y);
+        if ((n & 1u) == 0u && n - z0 >= (unsigned)kBrick && n - y0 >= (unsigned)kBrick &&
+            n - (x - 2 * (lane & 3)) >= (unsigned)kBrick) {
+            // interior brick, even n: 16-byte pairs, never split
+#pragma unroll 1
+            for (int h = 0; h < 8; h += 4) {
+                float4 o[4];
+                size_t lin[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const unsigned r = (unsigned)(lane >> 2) + 8u * (h + k);  // row = y + 8 z
+                    lin[k] = ((size_t)(z0 + (r >> 3)) * n + (y0 + (r & 7u))) * n + x;
+                    o[k] = *reinterpret_cast<const float4 *>(vox + lin[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float2 a = make_float2(o[k].x, o[k].y), b = make_float2(o[k].z, o[k].w);
+                    const bool na = fixed_point && a.x == fixed.x && a.y == fixed.y;
+                    const bool nbq = fixed_point && b.x == fixed.x && b.y == fixed.y;
+                    updates += 2;
+                    nop += (na ? 1u : 0u) + (nbq ? 1u : 0u);
+                    if (na && nbq) continue;  // provably unchanged (host-verified fixed point)
+                    const float2 ua = na ? a : free_update(a, f);
+                    const float2 ub = nbq ? b : free_update(b, f);
+                    if (keep) dbad += free_state_delta(a, ua, f.good_t) + free_state_delta(b, ub, f.good_t);
+                    *reinterpret_cast<float4 *>(vox + lin[k]) = make_float4(ua.x, ua.y, ub.x, ub.y);
+                }
             }
-            const float2 a = make_float2(o.x, o.y), b = make_float2(o.z, o.w);
-            const bool na = fixed_point && a.x == fixed.x && a.y == fixed.y;
-            const bool nbp = !two || (fixed_point && b.x == fixed.x && b.y == fixed.y);
-            updates += 1u + (two ? 1u : 0u);
-            nop += (na ? 1u : 0u) + (two && nbp ? 1u : 0u);
-            if (na && nbp) continue;  // provably unchanged (host-verified fixed point)
-            const float2 ua = na ? a : free_update(a, f);
-            const float2 ub = nbp ? b : free_update(b, f);
-            dbad += voxel_state(ua, f.good_t) - voxel_state(a, f.good_t);
-            if (two) dbad += voxel_state(ub, f.good_t) - voxel_state(b, f.good_t);
-            if (pair) {
-                *reinterpret_cast<float4 *>(vox + lin) = make_float4(ua.x, ua.y, ub.x, ub.y);
-            } else {
-                vox[lin] = ua;
-                if (two) vox[lin + 1] = ub;
+        } else {
+            // edge brick or odd n: per voxel
+#pragma unroll 1
+            for (int it = 0; it < 8; ++it) {
+                const unsigned r = (unsigned)(lane >> 2) + 8u * it;
+                const unsigned y = y0 + (r & 7u), z = z0 + (r >> 3);
+                if (y >= n || z >= n) continue;
+                for (unsigned xx = x; xx < x + 2 && xx < n; ++xx) {
+                    const size_t lin = ((size_t)z * n + y) * n + xx;
+                    const float2 a = vox[lin];
+                    ++updates;
+                    if (fixed_point && a.x == fixed.x && a.y == fixed.y) {
+                        ++nop;
+                        continue;
+                    }
+                    const float2 ua = free_update(a, f);
+                    if (keep) dbad += free_state_delta(a, ua, f.good_t);
+                    vox[lin] = ua;
+                }
             }
         }
-        if (keeps_summary(vol, f)) {
+        if (keep) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
             if (lane == 0 && dbad) atomicAdd(&vol.brick_state_dev[local], dbad);
@@ -643,6 +661,14 @@ struct ScreenConst {
     float cxh, cyh;   // cx + 0.5, cy + 0.5
 };
 
+// packed-state change of a free-space update old -> nv (nv.y > 0 always)
+__device__ __forceinline__ unsigned free_state_delta(float2 old, float2 nv, float t) {
+    const unsigned was_obs = old.y > 0.0f ? 1u : 0u;
+    const unsigned old_bad = (was_obs && old.x >= t) ? 0u : 1u;
+    const unsigned new_bad = nv.x >= t ? 0u : 1u;
+    return (new_bad - old_bad) + ((1u - was_obs) << 16);
+}
+
 // running weighted mean with clamped == tau (_kernels.py:129-133)
 __device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f) {
     const float wv = fmulr(old.y, old.x);
@@ -676,9 +702,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const float hw = 0.5f * f.w32, hh = 0.5f * f.h32;
     const float k3u = 9.6e-7f * f.fx32, k3v = 9.6e-7f * f.fy32;
     const float k2u = 9.6e-7f * (fabsf(f.cx32) + 2.f), k2v = 9.6e-7f * (fabsf(f.cy32) + 2.f);
-    unsigned updates = 0, swept = 0, nop = 0, col_skipped = 0, depth_skipped = 0, all_free_bricks = 0;
+    unsigned updates = 0, swept = 0, nop = 0, col_skipped = 0, depth_skipped = 0;
     for (unsigned i = warp; i < count; i += nwarps) {
-        unsigned not_free = 0;  // voxels of this brick that were not free-space updates
         const unsigned g = active[i];
         const int vi = find_volume(bt, g);
         const TfVolume &vol = vt.vol[vi];
@@ -825,11 +850,10 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                         } else {
                             const float2 nv = free_update(old[j], f);
                             vox[(size_t)row + (size_t)j * n * n] = nv;
-                            dbad += voxel_state(nv, f.good_t) - voxel_state(old[j], f.good_t);
+                            if (keep) dbad += free_state_delta(old[j], nv, f.good_t);
                         }
                     }
                     if (cls[j] == kExact) exact_mask |= 1u << (zb + j);
-                    if (row_in && (unsigned)(zb + j) < nz && cls[j] != kFree) ++not_free;
                 }
             }
             // undecided voxels of the column go to the exact kernel
@@ -856,7 +880,6 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
             for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
             if (lane == 0 && dbad) atomicAdd(&vol.brick_state_dev[local], dbad);
         }
-        if (__all_sync(0xffffffffu, not_free == 0u) && lane == 0) ++all_free_bricks;
     }
     if (stats) {
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
@@ -864,7 +887,6 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         warp_count_add(&stats[TF_STAT_NOOP_UPDATES], nop);
         warp_count_add(&stats[TF_STAT_COL_SKIPPED], col_skipped);
         warp_count_add(&stats[TF_STAT_DEPTH_SKIPPED], depth_skipped);
-        warp_count_add(&stats[TF_STAT_GENERAL_ALL_FREE], all_free_bricks);
     }
 }
 
