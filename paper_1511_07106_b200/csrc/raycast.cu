@@ -447,57 +447,139 @@ __device__ __forceinline__ unsigned cert_sample(const FastRay &fr, const Ray &er
     return kValidBit | (v > 0.0 ? kPosBit : 0u) | (fabs(v) < fr.near_thresh ? kNearBit : 0u);
 }
 
-// ---- the certified march as a per-lane state machine ------------------------
-//
-// One loop iteration = one step of the reference march for this lane: a
-// certified sample (march point, scan seed or scan point), a closed-form skip
-// of a summary region, or a switch to the next volume.  Every lane reaches the
-// single sample site each iteration, so the 32 rays of a warp stay converged
-// even though their marches are in different phases.  The decisions are the
-// reference's (_kernels.py:349-451): same march points, same scans and seeds,
-// same re-walk rules, same crossing acceptance (exact), same merge.
-
-enum : int { M_NEXTVOL = 0, M_MARCH = 1, M_SEED = 2, M_SCAN = 3, M_DONE = 4 };
-
-struct MarchState {
-    int j, j_end, phase, prev_j, last_j, swept_j;
-    int region_end, region_kind, region_start;
-    int k, scan_end;
-    unsigned prev, sp, s_march;
-    bool prev_has, exit_scan;
-};
-
-// march step after a march sample (:406-416)
-__device__ __forceinline__ void march_step(MarchState &m, unsigned s, int coarse) {
-    m.last_j = m.j;
-    const bool valid = s & kValidBit;
-    if (valid) {
-        m.prev_has = true;
-        m.prev = s;
-        m.prev_j = m.j;
+// _scan_crossing on certified decisions; the crossing itself is exact.
+// Returns whether a crossing was accepted (into `hit`).
+__device__ __forceinline__ bool scan_fast(const FastRay &fr, const Ray &er, int from, int end,
+                                          unsigned sp, Hit &hit, unsigned long long &samples,
+                                          unsigned long long &exact_samples) {
+    for (int k = from; k <= end; ++k) {
+        const unsigned s = cert_sample(fr, er, k, samples, exact_samples);
+        // sp_valid and sp_v > 0 and sv and s <= 0 (:169)
+        if ((sp & (kValidBit | kPosBit)) == (kValidBit | kPosBit) && (s & (kValidBit | kPosBit)) == kValidBit) {
+            Ray r = er;
+            double e0 = 0.0, e1 = 0.0;
+            const bool v0 = sample_at(r, k - 1, e0), v1 = sample_at(r, k, e1);
+            exact_samples += 2;
+            if (!v0 || !v1 || !(e0 > 0.0) || !(e1 <= 0.0)) {
+                // a certified decision disagreed with the exact arithmetic: never
+                // expected; counted (TF_STAT_CERT_FAILURES) so tests catch it
+                exact_samples += 1ull << 40;
+            } else if (accept_crossing(r, k, e0, e1, hit)) {
+                return true;
+            }
+        }
+        sp = s;
     }
-    if (valid && (s & kNearBit)) {
-        ++m.j;
-        m.phase = m.phase + 1 == coarse ? 0 : m.phase + 1;
-    } else {
-        m.j += coarse - m.phase;
-        m.phase = 0;
-    }
+    return false;
 }
 
-// start a scan over [scan_from, scan_end]; the seed is the last march sample
-// when it sits just before scan_from, else one more sample (:371-382, :420-432)
-__device__ __forceinline__ int start_scan(MarchState &m, int scan_from, int scan_end, bool exit_scan) {
-    const int k0 = scan_from - 1;
-    m.scan_end = scan_end;
-    m.exit_scan = exit_scan;
-    if (m.prev_has && k0 == m.prev_j) {
-        m.sp = m.prev;
-        m.k = scan_from;
-        return M_SCAN;
+// march_volume on certified decisions (_kernels.py:349-451); same control flow.
+// Returns whether `best` changed.
+__device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_end, const int coarse,
+                           Hit &best, unsigned long long &samples, unsigned long long &exact_samples) {
+    unsigned prev = 0u;  // decisions of the last valid march sample
+    bool prev_has = false;
+    int prev_j = -1, last_j = j - 1, swept_j = j - 1;
+    int phase = j % coarse;  // j mod coarse, tracked so no division runs per step
+    // current brick region (DDA over 8^3 bricks): fine points j <= region_end
+    // have their min corner in one brick of kind region_kind (bit0 never
+    // observed, bit1 free space, 0 = ordinary)
+    int region_end = -1, region_kind = 0, region_start = 0;
+    while (j <= j_end) {
+        if (fr.flags && j > region_end) {
+            double ex = -1.0;
+            const int fl = region_at(fr, j, ex);
+            region_start = j;
+            if (fl < 0 || ex < (double)j) {
+                region_end = j;  // undecided: this point normally, retry at the next
+                region_kind = 0;
+            } else {
+                region_end = ex >= (double)j_end ? j_end : (int)ex;
+                region_kind = fl & 3;
+            }
+        }
+        if (region_kind & 2) {
+            // free space: every march point in [j, region_end] is valid, positive
+            // and not near -> coarse steps, no scans (:362-416)
+            const int m = coarse == 2 ? (region_end & ~1) : region_end - region_end % coarse;
+            const int p_last = m > j ? m : j;
+            const int first = j + (coarse - phase);
+            const int cnt = 1 + (m > j ? (coarse == 2 ? (m - first) >> 1 : (m - first) / coarse) + 1 : 0);
+            samples += cnt;
+            exact_samples += (unsigned long long)cnt << 44;
+            prev_has = true;
+            prev = kValidBit | kPosBit;
+            prev_j = last_j = p_last;
+            if (p_last != j) phase = 0;
+            j = p_last + (coarse - phase);
+            phase = 0;
+            continue;
+        }
+        if ((region_kind & 1) && j > region_start) {
+            // never observed: the march points in [j, region_end] are invalid and any
+            // scan covers (max(prev_j, swept_j), p] inside the region: nothing found
+            // (:362-405); j is a multiple of coarse here (invalid -> coarse step)
+            const int cnt = (coarse == 2 ? (region_end - j) >> 1 : (region_end - j) / coarse) + 1;
+            const int p_last = j + (cnt - 1) * coarse;
+            const bool A = prev_has && (prev & kPosBit);
+            if (A || (coarse > 2 && (cnt >= 2 || swept_j < j - 1))) swept_j = p_last;
+            last_j = p_last;
+            samples += cnt;
+            exact_samples += (unsigned long long)cnt << 44;
+            j = p_last + coarse;
+            phase = 0;
+            continue;
+        }
+        // inside a known ordinary brick region the per-sample summary cannot help
+        const unsigned s = cert_sample(fr, er, j, samples, exact_samples, region_end < j || region_kind != 0);
+        const bool valid = s & kValidBit;
+        bool do_scan = false;
+        if (!valid || !(s & kPosBit)) {                                 // :362-369
+            if (prev_has && (prev & kPosBit))
+                do_scan = true;
+            else if (swept_j < j - 1 && (valid || coarse > 2))
+                do_scan = true;
+        }
+        if (do_scan) {
+            const int scan_from = (prev_j > swept_j ? prev_j : swept_j) + 1;
+            const int k0 = scan_from - 1;
+            const unsigned sp = (prev_has && k0 == prev_j) ? prev : cert_sample(fr, er, k0, samples, exact_samples);
+            Hit h;
+            const bool found = scan_fast(fr, er, scan_from, j, sp, h, samples, exact_samples);
+            swept_j = j;
+            if (found) {
+                if (hit_wins(h, best)) {
+                    best = h;
+                    return true;
+                }
+                return false;
+            }
+        }
+        last_j = j;
+        if (valid) {
+            prev_has = true;
+            prev = s;
+            prev_j = j;
+        }
+        if (valid && (s & kNearBit)) {  // fine step
+            ++j;
+            phase = phase + 1 == coarse ? 0 : phase + 1;
+        } else {                         // next multiple of coarse
+            j += coarse - phase;
+            phase = 0;
+        }
     }
-    m.k = k0;
-    return M_SEED;
+    const int scan_from = (last_j > swept_j ? last_j : swept_j) + 1;  // :417-451
+    if (scan_from <= j_end) {
+        const int k0 = scan_from - 1;
+        const unsigned sp = (prev_has && k0 == prev_j) ? prev : cert_sample(fr, er, k0, samples, exact_samples);
+        Hit h;
+        if (scan_fast(fr, er, scan_from, j_end, sp, h, samples, exact_samples) && hit_wins(h, best)) {
+            best = h;
+            return true;
+        }
+    }
+    return false;
 }
 
 constexpr int kRayBlockX = 8, kRayBlockY = 16;  // 128 threads; warp = 8x4 pixels
@@ -513,8 +595,6 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
     const int64_t px = (int64_t)blockIdx.x * kRayBlockX + (lane & 7);
     const int64_t py = (int64_t)blockIdx.y * kRayBlockY + w * 4 + (lane >> 3);
     unsigned long long samples = 0, hits = 0, exact_samples = 0;
-    // lanes with a pixel take part in the state machine's warp votes
-    const unsigned live = __ballot_sync(0xffffffffu, px < g.width && py < g.height);
     if (px < g.width && py < g.height) {
         const int64_t p = py * g.width + px;
         Hit best;
@@ -543,189 +623,51 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
         uint64_t pending = 0;  // bit v set = volume v still to march
         for (int v = 0; v < vt.count; ++v)
             if (ray_interval(vt.vol[v], o, d, jlo[v], jhi[v])) pending |= 1ull << v;
-        const double id[3] = {1.0 / (d[0] == 0.0 ? 1e-300 : d[0]), 1.0 / (d[1] == 0.0 ? 1e-300 : d[1]),
-                              1.0 / (d[2] == 0.0 ? 1e-300 : d[2])};
-        const int coarse = (int)g.coarse;
-        FastRay fr;
-        Ray er;
-        MarchState m;
-        int mode = M_NEXTVOL;
         bool changed = false;
-        for (;;) {
-            if (mode == M_NEXTVOL) {
-                // next volume by entry distance that can still beat the best hit
-                int pick = -1;
-                while (pending) {
-                    pick = -1;
-                    for (int v = 0; v < vt.count; ++v)
-                        if (((pending >> v) & 1ull) &&
-                            (pick < 0 || dmul((double)(jlo[v] - 1), vt.vol[v].voxel_size) <
-                                             dmul((double)(jlo[pick] - 1), vt.vol[pick].voxel_size)))
-                            pick = v;
-                    pending &= ~(1ull << pick);
-                    // no hit of this volume can have tstar below (j0 - 1) * delta
-                    if (!(dmul((double)(jlo[pick] - 1), vt.vol[pick].voxel_size) > best.t)) break;
-                    pick = -1;
-                }
-                if (pick < 0) {
-                    mode = M_DONE;
-                } else {
-                    const TfVolume &vol = vt.vol[pick];
-                    er.vox = (const float2 *)vol.voxels_dev;
-                    er.n = vol.n;
-                    er.htx = (double)vol.origin[0];
-                    er.hty = (double)vol.origin[1];
-                    er.htz = (double)vol.origin[2];
-                    er.vs = vol.voxel_size;
-                    er.ox = o[0];
-                    er.oy = o[1];
-                    er.oz = o[2];
-                    er.dx = d[0];
-                    er.dy = d[1];
-                    er.dz = d[2];
-                    er.samples = 0;
-                    const double q0x = dsub(ddiv(o[0], er.vs), er.htx);
-                    const double q0y = dsub(ddiv(o[1], er.vs), er.hty);
-                    const double q0z = dsub(ddiv(o[2], er.vs), er.htz);
-                    const double mag = fabs(q0x) + fabs(q0y) + fabs(q0z) + fabs(er.htx) + fabs(er.hty) +
-                                       fabs(er.htz) + (double)jhi[pick];
-                    if (g.exact_only || vol.n > 4000 || !(mag < 1e6) || jhi[pick] >= (1 << 30) ||
-                        g.coarse >= (1 << 20)) {
-                        // forced, or coordinates too large to certify: the exact reference march
-                        changed |= march_volume(er, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
-                        samples += er.samples;
-                        exact_samples += er.samples;
-                        continue;  // mode stays M_NEXTVOL
-                    }
-                    const bool summ = vol.brick_state_dev != nullptr && vol.summary_threshold == g.good_t;
-                    fr = FastRay{er.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
-                                 (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh,
-                                 summ ? vol.brick_state_dev : nullptr, (unsigned)((vol.n + 7) / 8),
-                                 id[0], id[1], id[2], summ ? vol.brick_flags_dev : nullptr};
-                    m.j = (int)jlo[pick];
-                    m.j_end = (int)jhi[pick];
-                    m.phase = m.j % coarse;
-                    m.prev_has = false;
-                    m.prev = 0u;
-                    m.prev_j = -1;
-                    m.last_j = m.swept_j = m.j - 1;
-                    m.region_end = -1;
-                    m.region_kind = 0;
-                    m.region_start = 0;
-                    mode = M_MARCH;
-                }
-            }
-            if (__all_sync(live, mode == M_DONE)) break;
-            if (mode == M_DONE) continue;
-
-            if (mode == M_MARCH) {
-                if (m.j > m.j_end) {  // march over: the exit re-walk (:417-451)
-                    const int scan_from = (m.last_j > m.swept_j ? m.last_j : m.swept_j) + 1;
-                    mode = scan_from <= m.j_end ? start_scan(m, scan_from, m.j_end, true) : M_NEXTVOL;
-                    continue;
-                }
-                if (fr.flags && m.j > m.region_end) {
-                    double ex = -1.0;
-                    const int fl = region_at(fr, m.j, ex);
-                    m.region_start = m.j;
-                    if (fl < 0 || ex < (double)m.j) {
-                        m.region_end = m.j;  // undecided: this point normally, retry at the next
-                        m.region_kind = 0;
-                    } else {
-                        m.region_end = ex >= (double)m.j_end ? m.j_end : (int)ex;
-                        m.region_kind = fl & 3;
-                    }
-                }
-                if (m.region_kind & 2) {
-                    // free space: every march point in [j, region_end] is valid, positive
-                    // and not near -> coarse steps, no scans (:362-416)
-                    const int re = m.region_end;
-                    const int mm = coarse == 2 ? (re & ~1) : re - re % coarse;
-                    const int p_last = mm > m.j ? mm : m.j;
-                    const int first = m.j + (coarse - m.phase);
-                    const int cnt = 1 + (mm > m.j ? (coarse == 2 ? (mm - first) >> 1 : (mm - first) / coarse) + 1 : 0);
-                    samples += cnt;
-                    exact_samples += (unsigned long long)cnt << 44;
-                    m.prev_has = true;
-                    m.prev = kValidBit | kPosBit;
-                    m.prev_j = m.last_j = p_last;
-                    if (p_last != m.j) m.phase = 0;
-                    m.j = p_last + (coarse - m.phase);
-                    m.phase = 0;
-                    continue;
-                }
-                if ((m.region_kind & 1) && m.j > m.region_start) {
-                    // never observed: the march points in [j, region_end] are invalid and
-                    // any scan covers (max(prev_j, swept_j), p] inside the region (all
-                    // invalid): nothing found (:362-405); j is a multiple of coarse here
-                    const int cnt = (coarse == 2 ? (m.region_end - m.j) >> 1 : (m.region_end - m.j) / coarse) + 1;
-                    const int p_last = m.j + (cnt - 1) * coarse;
-                    const bool A = m.prev_has && (m.prev & kPosBit);
-                    if (A || (coarse > 2 && (cnt >= 2 || m.swept_j < m.j - 1))) m.swept_j = p_last;
-                    m.last_j = p_last;
-                    samples += cnt;
-                    exact_samples += (unsigned long long)cnt << 44;
-                    m.j = p_last + coarse;
-                    m.phase = 0;
-                    continue;
-                }
-            }
-
-            // the one certified sample of this step
-            const int pos = mode == M_MARCH ? m.j : m.k;
-            const bool use_sum = mode != M_MARCH || m.region_end < m.j || m.region_kind != 0;
-            const unsigned sres = cert_sample(fr, er, pos, samples, exact_samples, use_sum);
-
-            if (mode == M_MARCH) {
-                const bool valid = sres & kValidBit;
-                bool do_scan = false;
-                if (!valid || !(sres & kPosBit)) {                               // :362-369
-                    if (m.prev_has && (m.prev & kPosBit))
-                        do_scan = true;
-                    else if (m.swept_j < m.j - 1 && (valid || coarse > 2))
-                        do_scan = true;
-                }
-                if (do_scan) {
-                    m.s_march = sres;
-                    mode = start_scan(m, (m.prev_j > m.swept_j ? m.prev_j : m.swept_j) + 1, m.j, false);
-                } else {
-                    march_step(m, sres, coarse);
-                }
-            } else if (mode == M_SEED) {
-                m.sp = sres;
-                ++m.k;
-                mode = M_SCAN;
-            } else {  // M_SCAN: sp_valid and sp_v > 0 and sv and s <= 0 (:169)
-                if ((m.sp & (kValidBit | kPosBit)) == (kValidBit | kPosBit) &&
-                    (sres & (kValidBit | kPosBit)) == kValidBit) {
-                    Ray r = er;
-                    double e0 = 0.0, e1 = 0.0;
-                    const bool v0 = sample_at(r, m.k - 1, e0), v1 = sample_at(r, m.k, e1);
-                    exact_samples += 2;
-                    Hit h;
-                    if (!v0 || !v1 || !(e0 > 0.0) || !(e1 <= 0.0)) {
-                        // a certified decision disagreed with the exact arithmetic: never
-                        // expected; counted (TF_STAT_CERT_FAILURES) so tests catch it
-                        exact_samples += 1ull << 40;
-                    } else if (accept_crossing(r, m.k, e0, e1, h)) {
-                        if (hit_wins(h, best)) {
-                            best = h;
-                            changed = true;
-                        }
-                        mode = M_NEXTVOL;  // the volume's march is finished (:389-405, :438)
-                        continue;
-                    }
-                }
-                m.sp = sres;
-                if (++m.k > m.scan_end) {
-                    if (m.exit_scan) {
-                        mode = M_NEXTVOL;
-                    } else {
-                        m.swept_j = m.j;
-                        march_step(m, m.s_march, coarse);
-                        mode = M_MARCH;
-                    }
-                }
+        while (pending) {
+            int pick = -1;
+            for (int v = 0; v < vt.count; ++v)
+                if (((pending >> v) & 1ull) &&
+                    (pick < 0 || dmul((double)(jlo[v] - 1), vt.vol[v].voxel_size) <
+                                     dmul((double)(jlo[pick] - 1), vt.vol[pick].voxel_size)))
+                    pick = v;
+            pending &= ~(1ull << pick);
+            const TfVolume &vol = vt.vol[pick];
+            // no hit of this volume can have tstar below (j0 - 1) * delta
+            if (dmul((double)(jlo[pick] - 1), vol.voxel_size) > best.t) continue;
+            Ray r;
+            r.vox = (const float2 *)vol.voxels_dev;
+            r.n = vol.n;
+            r.htx = (double)vol.origin[0];
+            r.hty = (double)vol.origin[1];
+            r.htz = (double)vol.origin[2];
+            r.vs = vol.voxel_size;
+            r.ox = o[0];
+            r.oy = o[1];
+            r.oz = o[2];
+            r.dx = d[0];
+            r.dy = d[1];
+            r.dz = d[2];
+            r.samples = 0;
+            const double q0x = dsub(ddiv(o[0], r.vs), r.htx);
+            const double q0y = dsub(ddiv(o[1], r.vs), r.hty);
+            const double q0z = dsub(ddiv(o[2], r.vs), r.htz);
+            const double mag = fabs(q0x) + fabs(q0y) + fabs(q0z) + fabs(r.htx) + fabs(r.hty) +
+                               fabs(r.htz) + (double)jhi[pick];
+            if (!g.exact_only && vol.n <= 4000 && mag < 1e6 && jhi[pick] < (1 << 30) && g.coarse < (1 << 20)) {
+                const bool summ = vol.brick_state_dev != nullptr && vol.summary_threshold == g.good_t;
+                FastRay fr{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
+                           (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh,
+                           summ ? vol.brick_state_dev : nullptr, (unsigned)((vol.n + 7) / 8),
+                           1.0 / (d[0] == 0.0 ? 1e-300 : d[0]), 1.0 / (d[1] == 0.0 ? 1e-300 : d[1]),
+                           1.0 / (d[2] == 0.0 ? 1e-300 : d[2]),
+                           summ ? vol.brick_flags_dev : nullptr};
+                changed |= march_fast(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
+                                      exact_samples);
+            } else {  // forced, or coordinates too large to certify: the exact reference march
+                changed |= march_volume(r, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
+                samples += r.samples;
+                exact_samples += r.samples;
             }
         }
         if (changed) {
