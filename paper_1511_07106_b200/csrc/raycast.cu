@@ -681,7 +681,13 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
             out_norm[3 * p + 2] = best.nz;
         }
     }
-    if (clocks && px < g.width && py < g.height) clocks[py * g.width + px] = clock64() - t_start;
+    if (clocks && px < g.width && py < g.height) {
+        const int64_t q = 4 * (py * g.width + px);
+        clocks[q] = clock64() - t_start;
+        clocks[q + 1] = (int64_t)samples;
+        clocks[q + 2] = (int64_t)(exact_samples & ((1ull << 40) - 1));
+        clocks[q + 3] = (int64_t)(exact_samples >> 44);
+    }
     if (stats) {
         warp_count_add(&stats[TF_STAT_RAY_SAMPLES], samples);
         warp_count_add(&stats[TF_STAT_RAY_HITS], hits);

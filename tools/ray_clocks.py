@@ -19,14 +19,22 @@ poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)
 for p in poses[:40]:
     tf.integrate_volumes(tiles, scene.render_depth(p, intr), p, intr, params)
 lib = nat.load_library()
-clk = torch.zeros(intr.height * intr.width, dtype=torch.int64, device="cuda")
+clk = torch.zeros(4 * intr.height * intr.width, dtype=torch.int64, device="cuda")
 lib.tf_debug_ray_clock_buffer(clk.data_ptr())
 rm = tf.RayMap.empty(intr)
 st = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
 tf.raycast_volumes(tiles, poses[41], intr, rm, params, st)
 torch.cuda.synchronize()
 lib.tf_debug_ray_clock_buffer(None)
-c = clk.cpu().numpy().reshape(intr.height, intr.width).astype(np.float64)
+allc = clk.cpu().numpy().reshape(intr.height, intr.width, 4).astype(np.float64)
+c = allc[..., 0]
+smp, ex, summ = allc[..., 1], allc[..., 2], allc[..., 3]
+ev = smp - summ
+print("per ray: samples %.0f evaluated %.0f exact %.1f summary %.0f" % (smp.mean(), ev.mean(), ex.mean(), summ.mean()))
+wmax = lambda a: a.reshape(intr.height // 4, 4, intr.width // 8, 8).max(axis=(1, 3))
+print("warp-max evaluated samples mean %.0f (lane mean %.0f); warp cycles / warp-max evaluated = %.0f" % (
+    wmax(ev).mean(), ev.mean(), (wmax(c) / np.maximum(wmax(ev), 1)).mean()))
+print("cycles per evaluated sample (pixel): median %.0f" % np.median(c / np.maximum(ev, 1)))
 hit = np.isfinite(rm.distance)
 print("cycles/pixel: mean %.0f median %.0f p90 %.0f max %.0f" % (c.mean(), np.median(c), np.percentile(c, 90), c.max()))
 print("hit pixels mean %.0f, miss pixels mean %.0f, hit frac %.2f" % (c[hit].mean(), c[~hit].mean(), hit.mean()))
