@@ -106,8 +106,9 @@ const char *tf_last_error(void);
 enum { TF_PROF_INTEGRATE_UPDATE = 0, TF_PROF_INTEGRATE_ALL = 1, TF_PROF_RAYCAST = 2,
        TF_PROF_KINDS = 3 };
 uint64_t tf_launch_count(void);
-/* Debug: when set (device int64[4*H*W] per raycast call), tf_raycast writes per
- * pixel {SM clock cycles, samples, exact samples, summary-certified samples};
+/* Debug: when set (device int64[12*H*W] per raycast call), tf_raycast writes per
+ * pixel {SM clock cycles, samples, exact samples, summary-certified samples,
+ * region evaluations at brick level by kind 0..3, at superbrick level 0..3};
  * NULL disables. */
 void tf_debug_ray_clock_buffer(int64_t *buffer_dev);
 void tf_profile_enable(int on);

@@ -322,36 +322,33 @@ struct FastRay {
     double near_thresh;
     const unsigned *bad;  // brick summary (NULL: not usable for this tau)
     unsigned nb;
-    double idx, idy, idz;  // 1 / d (approximate; only used with margins)
+    float idfx, idfy, idfz;  // 1 / d (approximate; only used with margins)
     const unsigned char *flags;  // per-brick flags (bit0 never observed, bit1 free)
 };
 
-// floor(q) from a 20-bit fixed point: lo = round(q 2^20) mod 2^32 (q in
-// (-2^11, 4096)).  The reference's q differs from fma(k, d, q0) by < 1e-9, so
-// floor is certain unless q is within 1.5 * 2^-20 of an integer, i.e. unless
-// the fraction field is 0, 1 or 2^20 - 1; then floor is i - 1 or i (fq <= 1)
-// or i or i + 1 (fq = 2^20 - 1): returned as the candidate range [lo, hi].
-__device__ __forceinline__ void fixed_cell(double q, unsigned &lo, unsigned &hi, float &fr) {
-    const double t = dadd(q, 6442450944.0);  // 1.5 * 2^32: ulp(t) = 2^-20
-    const unsigned bits = (unsigned)__double2loint(t);
-    const unsigned fq = bits & 0xFFFFFu;
-    const unsigned i = bits >> 20;
-    fr = (float)fq * 9.5367431640625e-07f;  // 2^-20
-    lo = fq <= 1u ? i - 1u : i;
-    hi = fq == 0xFFFFFu ? i + 1u : i;
+// floor(q) from a 20-bit fixed point: bits = round(q 2^20) mod 2^32 (q in
+// (-2^11, 4096)), cell = bits >> 20 (floor(q) mod 2^12), fraction field
+// fq = bits & (2^20 - 1).  The reference's q differs from fma(k, d, q0) by
+// < 1e-9, so the floor is certain unless q is within 1.5 * 2^-20 of an
+// integer, i.e. unless fq is 0, 1 or 2^20 - 1.
+__device__ __forceinline__ unsigned fixed_bits(double q) {
+    return (unsigned)__double2loint(dadd(q, 6442450944.0));  // + 1.5 * 2^32: ulp = 2^-20
+}
+__device__ __forceinline__ bool fixed_unsure(unsigned bits) { return ((bits + 1u) & 0xFFFFFu) < 3u; }
+// fq * 2^-20 exactly (fq < 2^20 fits the float mantissa shifted by 3)
+__device__ __forceinline__ float fixed_frac(unsigned bits) {
+    return __int_as_float(0x3F800000 | ((bits & 0xFFFFFu) << 3)) - 1.0f;
 }
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 
 __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k, bool use_summary) {
     const double kd = (double)k;
-    unsigned lx, hx, ly, hy, lz, hz;
-    float fx, fy, fz;
-    fixed_cell(dfma(kd, r.dx, r.q0x), lx, hx, fx);
-    fixed_cell(dfma(kd, r.dy, r.q0y), ly, hy, fy);
-    fixed_cell(dfma(kd, r.dz, r.q0z), lz, hz, fz);
-    if (lx != hx || ly != hy || lz != hz) return kUnsure;
-    const unsigned ix = lx, iy = ly, iz = lz;
+    const unsigned bx_ = fixed_bits(dfma(kd, r.dx, r.q0x));
+    const unsigned by_ = fixed_bits(dfma(kd, r.dy, r.q0y));
+    const unsigned bz_ = fixed_bits(dfma(kd, r.dz, r.q0z));
+    if (fixed_unsure(bx_) || fixed_unsure(by_) || fixed_unsure(bz_)) return kUnsure;
+    const unsigned ix = bx_ >> 20, iy = by_ >> 20, iz = bz_ >> 20;
     const unsigned top = (unsigned)(r.n - 2);
     if (ix > top || iy > top || iz > top) return 0u;                  // invalid (:38)
     if (use_summary) {
@@ -376,6 +373,7 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k, bool us
     const unsigned n = (unsigned)r.n;
     const float2 *b = r.vox + ((size_t)(iz * n + iy) * n + ix);
     const float2 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + n), c110 = __ldg(b + n + 1);
+    const float fx = fixed_frac(bx_), fy = fixed_frac(by_), fz = fixed_frac(bz_);
     const float2 c001 = __ldg(b + n * n), c101 = __ldg(b + n * n + 1);
     const float2 c011 = __ldg(b + n * n + n), c111 = __ldg(b + n * n + n + 1);
     const float wmin = fminf(fminf(fminf(c000.y, c100.y), fminf(c010.y, c110.y)),
@@ -395,39 +393,47 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k, bool us
 // Region of lattice point j for the brick DDA: when the cell of j certainly
 // has its min corner in a never-observed or free-space superbrick (64^3) or
 // brick (8^3), returns its flags (bit0 never observed, bit1 free space) and
-// sets `exit` to the largest k (as a double; k <= exit) for which the min
-// corner certainly stays in that box — for free space also at most n - 2, so
-// the cell stays in the volume.  Margins: 1e-6 voxel against a < 1e-9 error of
-// q, and q is >= 1.4e-6 inside its cell when the floor is certain.  Returns 0
-// for an ordinary brick (exit = its box) and -1 if undecided.
-__device__ __forceinline__ int region_at(const FastRay &r, int j, double &exit) {
+// sets `exit` to a k >= j - 1 such that for j <= k <= exit the min corner
+// certainly stays in that box — for free space also at most n - 2, so the
+// cell stays in the volume.  Returns 0 for an ordinary brick (exit = its box)
+// and -1 if undecided.  The exit is computed in float from the position
+// inside the box (truncated to 2^-17 voxel) against box faces pulled in by
+// 1e-4 voxel, and the step count shrunk by 1e-6 relative: both bound the
+// float rounding, and the < 1e-9 error of q against the reference.
+__device__ __forceinline__ int region_at(const FastRay &r, int j, int &exit) {
     const double kd = (double)j;
-    const double q[3] = {dfma(kd, r.dx, r.q0x), dfma(kd, r.dy, r.q0y), dfma(kd, r.dz, r.q0z)};
-    unsigned lo[3], hi[3];
-    float fdummy;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) fixed_cell(q[a], lo[a], hi[a], fdummy);
+    const unsigned bits[3] = {fixed_bits(dfma(kd, r.dx, r.q0x)), fixed_bits(dfma(kd, r.dy, r.q0y)),
+                              fixed_bits(dfma(kd, r.dz, r.q0z))};
+    if (fixed_unsure(bits[0]) || fixed_unsure(bits[1]) || fixed_unsure(bits[2])) return -1;
+    const unsigned lo[3] = {bits[0] >> 20, bits[1] >> 20, bits[2] >> 20};
     const unsigned top = (unsigned)(r.n - 2);
-    if (lo[0] != hi[0] || lo[1] != hi[1] || lo[2] != hi[2]) return -1;
     if (lo[0] > top || lo[1] > top || lo[2] > top) return -1;
     const unsigned ns = (r.nb + 7u) >> 3;
     const unsigned char *sflags = r.flags + (size_t)r.nb * r.nb * r.nb;
-    int fl = __ldg(&sflags[((lo[2] >> 6) * ns + (lo[1] >> 6)) * ns + (lo[0] >> 6)]) & 3;
-    unsigned shift = 6;
-    if (!fl) {
-        fl = __ldg(&r.flags[((lo[2] >> 3) * r.nb + (lo[1] >> 3)) * r.nb + (lo[0] >> 3)]) & 3;
-        shift = 3;
-    }
-    const double cap = (fl & 2) ? (double)(r.n - 1) : 1.0e30;
-    const double id3[3] = {r.idx, r.idy, r.idz};
-    double e = 3.0e9;
+    // both levels loaded up front: one memory round trip, not two
+    const int sfl = __ldg(&sflags[((lo[2] >> 6) * ns + (lo[1] >> 6)) * ns + (lo[0] >> 6)]) & 3;
+    const int bfl = __ldg(&r.flags[((lo[2] >> 3) * r.nb + (lo[1] >> 3)) * r.nb + (lo[0] >> 3)]) & 3;
+    const int fl = sfl ? sfl : bfl;
+    const unsigned shift = sfl ? 6u : 3u;
+    const unsigned mask = (1u << shift) - 1u;
+    const float idf[3] = {r.idfx, r.idfy, r.idfz};
+    float steps = 1.0e8f;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        const double base = (double)((lo[a] >> shift) << shift);
-        const double bound = id3[a] > 0.0 ? fmin(base + (double)(1u << shift), cap) - 1e-6 : base + 1e-6;
-        e = fmin(e, dfma(bound - q[a], id3[a], kd));
+        // position inside the box, truncated to 2^-17 (23 bits)
+        const unsigned x = ((lo[a] & mask) << 17) | ((bits[a] & 0xFFFFFu) >> 3);
+        const float local = (__int_as_float(0x4B000000 | x) - 8388608.0f) * 7.62939453125e-06f;  // 2^-17
+        float face;
+        if (idf[a] >= 0.0f) {
+            face = (float)(1u << shift);
+            if (fl & 2) face = fminf(face, (float)(top + 1u - (lo[a] & ~mask)));  // cap at n - 1
+            face -= 1e-4f;
+        } else {
+            face = 1e-4f;
+        }
+        steps = fminf(steps, (face - local) * idf[a]);  // 0 * inf = NaN is ignored by fminf
     }
-    exit = e;
+    exit = steps < 0.0f ? j - 1 : j + (int)(steps * 0.999999f);
     return fl;
 }
 
@@ -487,14 +493,14 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
     int region_end = -1, region_kind = 0, region_start = 0;
     while (j <= j_end) {
         if (fr.flags && j > region_end) {
-            double ex = -1.0;
+            int ex = j - 1;
             const int fl = region_at(fr, j, ex);
             region_start = j;
-            if (fl < 0 || ex < (double)j) {
+            if (fl < 0 || ex < j) {
                 region_end = j;  // undecided: this point normally, retry at the next
                 region_kind = 0;
             } else {
-                region_end = ex >= (double)j_end ? j_end : (int)ex;
+                region_end = ex >= j_end ? j_end : ex;
                 region_kind = fl & 3;
             }
         }
@@ -593,7 +599,11 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
     // warp w of the block covers rows 4w..4w+3 of the 8x16 block tile
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t px = (int64_t)blockIdx.x * kRayBlockX + (lane & 7);
-    const int64_t py = (int64_t)blockIdx.y * kRayBlockY + w * 4 + (lane >> 3);
+    // tile rows are dispatched centre-out: rays near the image centre row run
+    // longest in typical scenes, so they start first and the tail is short
+    const int by = (int)blockIdx.y, mid = (int)(gridDim.y >> 1);
+    const int ty = (by & 1) ? mid - ((by + 1) >> 1) : mid + (by >> 1);
+    const int64_t py = (int64_t)ty * kRayBlockY + w * 4 + (lane >> 3);
     unsigned long long samples = 0, hits = 0, exact_samples = 0;
     if (px < g.width && py < g.height) {
         const int64_t p = py * g.width + px;
@@ -659,8 +669,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
                 FastRay fr{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
                            (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh,
                            summ ? vol.brick_state_dev : nullptr, (unsigned)((vol.n + 7) / 8),
-                           1.0 / (d[0] == 0.0 ? 1e-300 : d[0]), 1.0 / (d[1] == 0.0 ? 1e-300 : d[1]),
-                           1.0 / (d[2] == 0.0 ? 1e-300 : d[2]),
+                           1.0f / (float)d[0], 1.0f / (float)d[1], 1.0f / (float)d[2],
                            summ ? vol.brick_flags_dev : nullptr};
                 changed |= march_fast(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
                                       exact_samples);
@@ -682,7 +691,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
         }
     }
     if (clocks && px < g.width && py < g.height) {
-        const int64_t q = 4 * (py * g.width + px);
+        const int64_t q = 12 * (py * g.width + px);
         clocks[q] = clock64() - t_start;
         clocks[q + 1] = (int64_t)samples;
         clocks[q + 2] = (int64_t)(exact_samples & ((1ull << 40) - 1));

@@ -19,14 +19,20 @@ poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)
 for p in poses[:40]:
     tf.integrate_volumes(tiles, scene.render_depth(p, intr), p, intr, params)
 lib = nat.load_library()
-clk = torch.zeros(4 * intr.height * intr.width, dtype=torch.int64, device="cuda")
+clk = torch.zeros(12 * intr.height * intr.width, dtype=torch.int64, device="cuda")
+import os  # noqa: E402
+if os.environ.get("RAY_CLOCKS_OFF"):  # profile the production kernel (no debug stores)
+    rm = tf.RayMap.empty(intr)
+    tf.raycast_volumes(tiles, poses[41], intr, rm, params)
+    torch.cuda.synchronize()
+    sys.exit(0)
 lib.tf_debug_ray_clock_buffer(clk.data_ptr())
 rm = tf.RayMap.empty(intr)
 st = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
 tf.raycast_volumes(tiles, poses[41], intr, rm, params, st)
 torch.cuda.synchronize()
 lib.tf_debug_ray_clock_buffer(None)
-allc = clk.cpu().numpy().reshape(intr.height, intr.width, 4).astype(np.float64)
+allc = clk.cpu().numpy().reshape(intr.height, intr.width, 12).astype(np.float64)
 c = allc[..., 0]
 smp, ex, summ = allc[..., 1], allc[..., 2], allc[..., 3]
 ev = smp - summ
@@ -43,4 +49,7 @@ print("warp max mean %.0f; sum of warp max %.3g vs sum of pixel %.3g" % (w.mean(
 rows = c.reshape(12, 40, 640).mean(axis=(1, 2))
 print("row-band means:", " ".join("%.0f" % r for r in rows))
 print("stats: samples %d exact %d summary %d" % (st[nat.STAT_RAY_SAMPLES], st[nat.STAT_EXACT_SAMPLES], st[nat.STAT_SUMMARY_SAMPLES]))
+reg = allc[..., 4:].reshape(-1, 2, 4).mean(axis=0)
+print("region evals per ray [brick kinds 0..3]:", " ".join("%.1f" % v for v in reg[0]),
+      " [super kinds 0..3]:", " ".join("%.1f" % v for v in reg[1]))
 np.save("gpurun_out/ray_clocks.npy", c)
