@@ -5,6 +5,8 @@ Mirrors tilefusion's test_tsdf.py (hand-computed oracles), test_pipeline.py
 counters) and the tracking tests, with the operators running in libtfb200.
 """
 
+import dataclasses
+
 import numpy as np
 import pytest
 import torch
@@ -141,10 +143,13 @@ def test_spill_round_trip_and_corruption(tmp_path, small_intr):
         tf.load_subvolume(tmp_path / "c.tsdv")
 
 
-def test_spill_traffic_matches_the_schedule(tmp_path, small_intr):
-    """Acceptance 7 (test_acceptance.py:271-320): cold (0, 2) then (3, 3)."""
+@pytest.mark.parametrize("tier", ["disk", "host"])
+def test_spill_traffic_matches_the_schedule(tmp_path, small_intr, tier):
+    """Acceptance 7 (test_acceptance.py:271-320): cold (0, 2) then (3, 3), for
+    both the reference's file tier and the pinned-host tier."""
     params = tf.FusionParams.for_voxel_size(0.05)
-    vs = tf.VolumeSet(params, voxels_per_side=16, voxel_size=0.05, max_resident=1, spill_dir=tmp_path)
+    vs = tf.VolumeSet(params, voxels_per_side=16, voxel_size=0.05, max_resident=1, spill_dir=tmp_path,
+                      spill_tier=tier)
     keys = [(-24, -8, 20), (-8, -8, 20), (8, -8, 20)]
     for k in keys:
         vs.add(k)
@@ -162,6 +167,52 @@ def test_spill_traffic_matches_the_schedule(tmp_path, small_intr):
             vs.release(k)
         per_frame.append((vs.files_read - r0, vs.files_written - w0))
     assert per_frame[0] == (0, 2) and all(c == (3, 3) for c in per_frame[1:])
+
+
+def test_host_tier_lru_persist_and_remove(tmp_path, small_intr):
+    """Pinned-host tier: reference LRU/counter semantics (test_volumes.py:140-226),
+    summaries survive a round trip, persist() writes loadable .tsdv files."""
+    params = tf.FusionParams.for_voxel_size(0.1)
+    disk = tf.VolumeSet(params, 10, 0.1, max_resident=2, spill_dir=tmp_path / "d")
+    host = tf.VolumeSet(params, 10, 0.1, max_resident=2, spill_dir=tmp_path / "h", spill_tier="host")
+    keys = [(-4, -4, 16), (4, -4, 16), (-4, 4, 16)]
+    pose = tf.Pose.identity()
+    for vs in (disk, host):
+        for k in keys:
+            vs.add(k)
+        for depth in (2.0, 2.1, 1.9):
+            for k in keys:
+                vol = vs.acquire(k)
+                tf.integrate(vol, flat_frame(depth), pose, small_intr, params)
+                rm = tf.RayMap.empty(small_intr)
+                tf.raycast(vol, pose, small_intr, rm, params)  # builds the brick summary
+                vs.release(k)
+    assert (host.files_read, host.files_written, host.bytes_read, host.bytes_written) == (
+        disk.files_read, disk.files_written, disk.bytes_read, disk.bytes_written)
+    assert [k for k, _ in host.resident_volumes()] == [k for k, _ in disk.resident_volumes()]
+    assert not any(host.spill_path(k).exists() for k in keys)
+    for k in keys:  # same voxels through either tier; a host-loaded summary is exact
+        a, b = disk.acquire(k), host.acquire(k)
+        assert torch.equal(a.voxels, b.voxels)
+        if b.brick_bad is not None:
+            bad, flags = b.brick_bad.clone(), b.brick_flags.clone()
+            b.invalidate_summary()
+            b._summary_for(params.truncation)
+            assert torch.equal(bad, b.brick_bad) and torch.equal(flags, b.brick_flags)
+        disk.release(k)
+        host.release(k)
+    written = host.persist()
+    assert written == 3 * tf.spill_file_size(10)
+    for k in keys:
+        back, _ = tf.load_subvolume(host.spill_path(k))
+        vol = host.acquire(k)
+        assert torch.equal(back.voxels, vol.voxels)
+        host.release(k)
+    gone = host.remove(keys[0])
+    assert not host.spill_path(keys[0]).exists() and keys[0] not in host
+    assert torch.equal(gone.voxels, disk.remove(keys[0]).voxels)
+    with pytest.raises(ValueError):
+        tf.VolumeSet(params, 10, 0.1, max_resident=1, spill_dir=tmp_path, spill_tier="tape")
 
 
 # ---- pipeline (reference test_pipeline.py) ---------------------------------------------------
@@ -197,10 +248,16 @@ def test_groundtruth_fusion_accuracy(tmp_path):
 def test_records_reflect_memory_pressure(tmp_path):
     cfg = small_config(max_resident=2)
     frames, poses = render_orbit(cfg.intrinsics(), 3)
-    res = tf.run_fusion(frames, cfg, tmp_path, gt_poses=poses)
+    res = tf.run_fusion(frames, cfg, tmp_path / "disk", gt_poses=poses)
     assert all(r.volumes == 8 and r.resident <= 2 for r in res.records)
     assert res.records[0].files_read == 0
     assert all(r.files_read > 0 and r.bytes_read > 0 for r in res.records[1:])
+    # the pinned-host tier: same schedule, same records, same cloud
+    host = tf.run_fusion(frames, small_config(max_resident=2, spill_tier="host"), tmp_path / "host",
+                         gt_poses=poses)
+    strip = lambda recs: [dataclasses.replace(r, residual_rms=0.0) for r in recs]  # NaN in GT mode
+    assert strip(host.records) == strip(res.records)
+    assert np.array_equal(host.cloud.vertices, res.cloud.vertices)
 
 
 def test_tracking_mode_follows_orbit(tmp_path):

@@ -94,12 +94,14 @@ def test_config_defaults_and_validation(tmp_path):
     c = cfg.RunConfig()
     assert (c.cx, c.cy, c.width, c.height) == (319.5, 239.5, 640, 480)
     assert c.validate() == []
-    bad = cfg.RunConfig(fx=-1, max_resident=0, iterations=())
+    bad = cfg.RunConfig(fx=-1, max_resident=0, iterations=(), spill_tier="tape")
     errs = bad.validate()
     assert any("focal" in e for e in errs) and any("max_resident" in e for e in errs)
-    cfg.save_config(tmp_path / "a.ini", cfg.RunConfig(resolution=200, iterations=(3, 2)))
+    assert any("spill_tier" in e for e in errs)
+    cfg.save_config(tmp_path / "a.ini", cfg.RunConfig(resolution=200, iterations=(3, 2),
+                                                        spill_tier="host"))
     back = cfg.load_config(tmp_path / "a.ini")
-    assert back.resolution == 200 and back.iterations == (3, 2)
+    assert back.resolution == 200 and back.iterations == (3, 2) and back.spill_tier == "host"
     (tmp_path / "b.ini").write_text("[camera]\nfx = 1\nbogus = 2\n[nope]\nx = 1\n")
     with pytest.raises(ValueError, match="unknown"):
         cfg.load_config(tmp_path / "b.ini")
