@@ -588,22 +588,22 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
     return false;
 }
 
-constexpr int kRayBlockX = 8, kRayBlockY = 16;  // 128 threads; warp = 8x4 pixels
+// a warp traces 8x4 pixels; a block of kBX x kBY pixels (kBX/8 x kBY/4 warps)
 
-template <int kMinBlocks>
-__global__ void __launch_bounds__(128, kMinBlocks) raycast_kernel(
+template <int kBX, int kBY, int kMinBlocks>
+__global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ RayGeom g,
     double *__restrict__ out_dist, double *__restrict__ out_vert, double *__restrict__ out_norm,
     unsigned long long *__restrict__ stats, int64_t *__restrict__ clocks) {
     const long long t_start = clock64();
-    // warp w of the block covers rows 4w..4w+3 of the 8x16 block tile
+    // warps tile the block's pixels in 8x4 units, row-major
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t px = (int64_t)blockIdx.x * kRayBlockX + (lane & 7);
+    const int64_t px = (int64_t)blockIdx.x * kBX + (w % (kBX / 8)) * 8 + (lane & 7);
     // tile rows are dispatched centre-out: rays near the image centre row run
     // longest in typical scenes, so they start first and the tail is short
     const int by = (int)blockIdx.y, mid = (int)(gridDim.y >> 1);
     const int ty = (by & 1) ? mid - ((by + 1) >> 1) : mid + (by >> 1);
-    const int64_t py = (int64_t)ty * kRayBlockY + w * 4 + (lane >> 3);
+    const int64_t py = (int64_t)ty * kBY + (w / (kBX / 8)) * 4 + (lane >> 3);
     unsigned long long samples = 0, hits = 0, exact_samples = 0;
     if (px < g.width && py < g.height) {
         const int64_t p = py * g.width + px;
@@ -765,8 +765,6 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
     g.coarse = coarse_step;
     g.exact_only = (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) ? 1 : 0;
     g.good_t = good_threshold(tau);
-    dim3 grid((unsigned)((cam->width + kRayBlockX - 1) / kRayBlockX),
-              (unsigned)((cam->height + kRayBlockY - 1) / kRayBlockY));
     for (int first = 0; first < nvol; first += TFB200_MAX_VOLUMES_PER_LAUNCH) {
         VolumeTable vt{};
         vt.count = nvol - first < TFB200_MAX_VOLUMES_PER_LAUNCH ? nvol - first
@@ -777,16 +775,23 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
                 return tf_set_error(TF_EINVAL, "tf_raycast: bad volume %d", first + v);
         }
         void *prof = tf_profile_begin(TF_PROF_RAYCAST, stream);
-        static const int minb = [] {
-            const char *e = getenv("TFB200_RAY_MINBLOCKS");  // tuning knob
-            return e ? atoi(e) : 4;
+        static const int shape = [] {
+            const char *e = getenv("TFB200_RAY_SHAPE");  // tuning knob: block shape variant
+            return e ? atoi(e) : 0;
         }();
-        if (minb == 4)
-            raycast_kernel<4><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats, tf_ray_clock_buffer());
-        else if (minb == 6)
-            raycast_kernel<6><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats, tf_ray_clock_buffer());
-        else
-            raycast_kernel<5><<<grid, 128, 0, stream>>>(vt, g, dist, vert, norm, (unsigned long long *)stats, tf_ray_clock_buffer());
+        unsigned long long *st = (unsigned long long *)stats;
+        int64_t *clk = tf_ray_clock_buffer();
+        auto launch = [&](auto kern, int bx, int by) {
+            dim3 grid((unsigned)((cam->width + bx - 1) / bx), (unsigned)((cam->height + by - 1) / by));
+            kern<<<grid, bx * by, 0, stream>>>(vt, g, dist, vert, norm, st, clk);
+        };
+        // 32x16-pixel blocks (16 warps, one block per SM): the warps of an SM
+        // trace neighbouring rays and share L1 lines
+        switch (shape) {
+        case 1: launch(raycast_kernel<16, 16, 2>, 16, 16); break;
+        case 2: launch(raycast_kernel<8, 16, 4>, 8, 16); break;
+        default: launch(raycast_kernel<32, 16, 1>, 32, 16); break;
+        }
         tf_profile_end(prof, stream);
         int rc = tf_check_launch("raycast_kernel");
         if (rc) return rc;

@@ -52,4 +52,11 @@ print("stats: samples %d exact %d summary %d" % (st[nat.STAT_RAY_SAMPLES], st[na
 reg = allc[..., 4:].reshape(-1, 2, 4).mean(axis=0)
 print("region evals per ray [brick kinds 0..3]:", " ".join("%.1f" % v for v in reg[0]),
       " [super kinds 0..3]:", " ".join("%.1f" % v for v in reg[1]))
-np.save("gpurun_out/ray_clocks.npy", c)
+np.save("gpurun_out/ray_clocks.npy", allc)
+w = np.unravel_index(np.argmax(c), c.shape)
+wy, wx = (w[0] // 4) * 4, (w[1] // 8) * 8
+print("slowest warp at rows %d-%d cols %d-%d: %.0f cycles; per lane (samples, exact, summary):" % (
+    wy, wy + 3, wx, wx + 7, c[w]))
+for yy in range(wy, wy + 4):
+    print("  ", " ".join("(%d,%d,%d)" % tuple(allc[yy, xx, 1:4]) for xx in range(wx, wx + 8)))
+print("  distances:", rm.distance[wy:wy + 4, wx:wx + 8].round(3).tolist())
