@@ -120,7 +120,8 @@ int tf_profile_read(double *ms_by_kind, int64_t *launches_by_kind, int nkinds);
  * every voxel / ray instead of the float32-screened / certified fast paths; TF_DEBUG_NO_FIXEDPOINT
  * stores every free-space update even when it provably leaves the voxel
  * unchanged. */
-enum { TF_DEBUG_NO_CULL = 1u, TF_DEBUG_EXACT_ONLY = 2u, TF_DEBUG_NO_FIXEDPOINT = 4u };
+enum { TF_DEBUG_NO_CULL = 1u, TF_DEBUG_EXACT_ONLY = 2u, TF_DEBUG_NO_FIXEDPOINT = 4u,
+       TF_DEBUG_LANE0_ONLY = 8u /* tf_raycast traces only lane 0 of each warp (timing) */ };
 void tf_set_debug_flags(uint32_t flags);
 uint32_t tf_debug_flags(void);
 

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libtfb200.so"
+LIB_PATH = Path(os.environ["TFB200_LIB"]) if os.environ.get("TFB200_LIB") else _PKG / "libtfb200.so"  # override: A/B runs only
 ABI_VERSION = 1
 
 _c_d = ctypes.c_double
@@ -41,6 +41,7 @@ class TfCamera(ctypes.Structure):
 DEBUG_NO_CULL = 1
 DEBUG_EXACT_ONLY = 2
 DEBUG_NO_FIXEDPOINT = 4
+DEBUG_LANE0_ONLY = 8
 PROF_INTEGRATE_UPDATE, PROF_INTEGRATE_ALL, PROF_RAYCAST, PROF_KINDS = 0, 1, 2, 3
 
 

@@ -51,7 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     log = []
     for s in SOURCES:
         obj = build_dir / (Path(s).stem + ".o")
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, f"-I{INCLUDE}", "-c", str(CSRC / s), "-o", str(obj)]
+        extra = os.environ.get("TFB200_NVCC_EXTRA", "").split()  # diagnostics builds only
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, f"-I{INCLUDE}", "-c", str(CSRC / s), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:

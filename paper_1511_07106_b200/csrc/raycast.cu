@@ -30,6 +30,7 @@ struct RayGeom {
     double near_thresh;  // NEAR_SURFACE_FRACTION * tau (_kernels.py:25, :298)
     int64_t coarse;
     int exact_only;      // TF_DEBUG_EXACT_ONLY: plain reference march for every ray
+    int lane0_only;      // TF_DEBUG_LANE0_ONLY: only lane 0 of each warp traces (timing studies)
     float good_t;        // brick-summary threshold for this tau
 };
 
@@ -455,11 +456,20 @@ __device__ __forceinline__ unsigned cert_sample(const FastRay &fr, const Ray &er
 
 // _scan_crossing on certified decisions; the crossing itself is exact.
 // Returns whether a crossing was accepted (into `hit`).
+// `end_s` = the decisions of point `end` when the march just sampled it
+// (kNoDecision otherwise): the reference samples it again; the result is the same.
+constexpr unsigned kNoDecision = 0x80000000u;
 __device__ __forceinline__ bool scan_fast(const FastRay &fr, const Ray &er, int from, int end,
                                           unsigned sp, Hit &hit, unsigned long long &samples,
-                                          unsigned long long &exact_samples) {
+                                          unsigned long long &exact_samples, unsigned end_s = kNoDecision) {
     for (int k = from; k <= end; ++k) {
-        const unsigned s = cert_sample(fr, er, k, samples, exact_samples);
+        unsigned s;
+        if (k == end && end_s != kNoDecision) {
+            ++samples;
+            s = end_s;
+        } else {
+            s = cert_sample(fr, er, k, samples, exact_samples);
+        }
         // sp_valid and sp_v > 0 and sv and s <= 0 (:169)
         if ((sp & (kValidBit | kPosBit)) == (kValidBit | kPosBit) && (s & (kValidBit | kPosBit)) == kValidBit) {
             Ray r = er;
@@ -481,8 +491,21 @@ __device__ __forceinline__ bool scan_fast(const FastRay &fr, const Ray &er, int 
 
 // march_volume on certified decisions (_kernels.py:349-451); same control flow.
 // Returns whether `best` changed.
+#ifdef TF_RAY_DIAG
+// diagnostics build (TFB200_NVCC_EXTRA=-DTF_RAY_DIAG): cycles / calls per
+// phase of march_fast into the debug ray buffer slots 4..11 of the pixel
+#define DIAG_T0 const long long _t0 = clock64();
+#define DIAG_ACC(i) diag[i] += clock64() - _t0; diag[(i) + 4] += 1;
+#define DIAG_PARAM , int64_t *diag
+#define DIAG_ARG , diag
+#else
+#define DIAG_T0
+#define DIAG_ACC(i)
+#define DIAG_PARAM
+#define DIAG_ARG
+#endif
 __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_end, const int coarse,
-                           Hit &best, unsigned long long &samples, unsigned long long &exact_samples) {
+                           Hit &best, unsigned long long &samples, unsigned long long &exact_samples DIAG_PARAM) {
     unsigned prev = 0u;  // decisions of the last valid march sample
     bool prev_has = false;
     int prev_j = -1, last_j = j - 1, swept_j = j - 1;
@@ -494,7 +517,9 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
     while (j <= j_end) {
         if (fr.flags && j > region_end) {
             int ex = j - 1;
+            DIAG_T0
             const int fl = region_at(fr, j, ex);
+            DIAG_ACC(0)
             region_start = j;
             if (fl < 0 || ex < j) {
                 region_end = j;  // undecided: this point normally, retry at the next
@@ -537,7 +562,9 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
             continue;
         }
         // inside a known ordinary brick region the per-sample summary cannot help
+        DIAG_T0
         const unsigned s = cert_sample(fr, er, j, samples, exact_samples, region_end < j || region_kind != 0);
+        DIAG_ACC(1)
         const bool valid = s & kValidBit;
         bool do_scan = false;
         if (!valid || !(s & kPosBit)) {                                 // :362-369
@@ -547,11 +574,13 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
                 do_scan = true;
         }
         if (do_scan) {
+            DIAG_T0
             const int scan_from = (prev_j > swept_j ? prev_j : swept_j) + 1;
             const int k0 = scan_from - 1;
             const unsigned sp = (prev_has && k0 == prev_j) ? prev : cert_sample(fr, er, k0, samples, exact_samples);
             Hit h;
-            const bool found = scan_fast(fr, er, scan_from, j, sp, h, samples, exact_samples);
+            const bool found = scan_fast(fr, er, scan_from, j, sp, h, samples, exact_samples, s);
+            DIAG_ACC(2)
             swept_j = j;
             if (found) {
                 if (hit_wins(h, best)) {
@@ -605,7 +634,7 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
     const int ty = (by & 1) ? mid - ((by + 1) >> 1) : mid + (by >> 1);
     const int64_t py = (int64_t)ty * kBY + (w / (kBX / 8)) * 4 + (lane >> 3);
     unsigned long long samples = 0, hits = 0, exact_samples = 0;
-    if (px < g.width && py < g.height) {
+    if (px < g.width && py < g.height && !(g.lane0_only && lane != 0)) {
         const int64_t p = py * g.width + px;
         Hit best;
         best.t = out_dist[p];
@@ -671,8 +700,14 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
                            summ ? vol.brick_state_dev : nullptr, (unsigned)((vol.n + 7) / 8),
                            1.0f / (float)d[0], 1.0f / (float)d[1], 1.0f / (float)d[2],
                            summ ? vol.brick_flags_dev : nullptr};
+#ifdef TF_RAY_DIAG
+                int64_t *diag = clocks ? clocks + 12 * p + 4 : nullptr;
+                if (!diag) __trap();
+#endif
+                DIAG_T0
                 changed |= march_fast(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
-                                      exact_samples);
+                                      exact_samples DIAG_ARG);
+                DIAG_ACC(3)
             } else {  // forced, or coordinates too large to certify: the exact reference march
                 changed |= march_volume(r, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
                 samples += r.samples;
@@ -764,6 +799,7 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
     g.near_thresh = 0.99 * tau;
     g.coarse = coarse_step;
     g.exact_only = (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) ? 1 : 0;
+    g.lane0_only = (tf_debug_flags() & TF_DEBUG_LANE0_ONLY) ? 1 : 0;
     g.good_t = good_threshold(tau);
     for (int first = 0; first < nvol; first += TFB200_MAX_VOLUMES_PER_LAUNCH) {
         VolumeTable vt{};

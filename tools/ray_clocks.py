@@ -32,7 +32,9 @@ st = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
 tf.raycast_volumes(tiles, poses[41], intr, rm, params, st)
 torch.cuda.synchronize()
 lib.tf_debug_ray_clock_buffer(None)
-allc = clk.cpu().numpy().reshape(intr.height, intr.width, 12).astype(np.float64)
+stride = int(os.environ.get("RAY_CLOCKS_STRIDE", "12"))  # 4 for libraries before the diag slots
+allc = clk.cpu().numpy()[: stride * intr.height * intr.width].reshape(intr.height, intr.width, stride)
+allc = np.concatenate([allc, np.zeros(allc.shape[:2] + (12 - stride,), allc.dtype)], -1).astype(np.float64)
 c = allc[..., 0]
 smp, ex, summ = allc[..., 1], allc[..., 2], allc[..., 3]
 ev = smp - summ
@@ -49,9 +51,12 @@ print("warp max mean %.0f; sum of warp max %.3g vs sum of pixel %.3g" % (w.mean(
 rows = c.reshape(12, 40, 640).mean(axis=(1, 2))
 print("row-band means:", " ".join("%.0f" % r for r in rows))
 print("stats: samples %d exact %d summary %d" % (st[nat.STAT_RAY_SAMPLES], st[nat.STAT_EXACT_SAMPLES], st[nat.STAT_SUMMARY_SAMPLES]))
-reg = allc[..., 4:].reshape(-1, 2, 4).mean(axis=0)
-print("region evals per ray [brick kinds 0..3]:", " ".join("%.1f" % v for v in reg[0]),
-      " [super kinds 0..3]:", " ".join("%.1f" % v for v in reg[1]))
+dg = allc[..., 4:]
+if dg.any():  # diagnostics build (-DTF_RAY_DIAG): cycles / calls per march phase
+    names = ["region_at", "cert_sample", "scan", "march_fast"]
+    for i, nm in enumerate(names):
+        print("  %-12s mean cycles %9.0f calls %7.1f -> %6.0f cycles/call" % (
+            nm, dg[..., i].mean(), dg[..., i + 4].mean(), dg[..., i].sum() / max(dg[..., i + 4].sum(), 1)))
 np.save("gpurun_out/ray_clocks.npy", allc)
 w = np.unravel_index(np.argmax(c), c.shape)
 wy, wx = (w[0] // 4) * 4, (w[1] // 8) * 8
@@ -59,4 +64,27 @@ print("slowest warp at rows %d-%d cols %d-%d: %.0f cycles; per lane (samples, ex
     wy, wy + 3, wx, wx + 7, c[w]))
 for yy in range(wy, wy + 4):
     print("  ", " ".join("(%d,%d,%d)" % tuple(allc[yy, xx, 1:4]) for xx in range(wx, wx + 8)))
+if dg.any():
+    for i, nm in enumerate(["region_at", "cert_sample", "scan", "march_fast"]):
+        blk = dg[wy:wy + 4, wx:wx + 8]
+        print("  slow warp %-12s cycles/lane %9.0f calls/lane %6.1f" % (nm, blk[..., i].mean(), blk[..., i + 4].mean()))
 print("  distances:", rm.distance[wy:wy + 4, wx:wx + 8].round(3).tolist())
+
+if os.environ.get("RAY_LANE0"):
+    # the same frame with only lane 0 of each warp tracing: lane 0's cycles
+    # alone vs. inside its full warp measure the cost of lane divergence
+    clk.zero_()
+    lib.tf_debug_ray_clock_buffer(clk.data_ptr())
+    lib.tf_set_debug_flags(nat.DEBUG_LANE0_ONLY)
+    rm2 = tf.RayMap.empty(intr)
+    tf.raycast_volumes(tiles, poses[41], intr, rm2, params)
+    torch.cuda.synchronize()
+    lib.tf_set_debug_flags(0)
+    lib.tf_debug_ray_clock_buffer(None)
+    solo = clk.cpu().numpy()[: stride * intr.height * intr.width].reshape(intr.height, intr.width, stride)
+    full0 = c[0::4, 0::8]
+    solo0 = solo[0::4, 0::8, 0].astype(np.float64)
+    print("lane 0: mean cycles in full warp %.0f, alone %.0f" % (full0.mean(), solo0.mean()))
+    order = np.argsort(full0.ravel())[::-1][:8]
+    print("slowest warps, lane-0 cycles full vs alone:",
+          " ".join("%.2fM/%.2fM" % (full0.ravel()[i] / 1e6, solo0.ravel()[i] / 1e6) for i in order))
