@@ -514,6 +514,7 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
     // have their min corner in one brick of kind region_kind (bit0 never
     // observed, bit1 free space, 0 = ordinary)
     int region_end = -1, region_kind = 0, region_start = 0;
+    unsigned last_s = kNoDecision;  // decisions of march point last_j
     while (j <= j_end) {
         if (fr.flags && j > region_end) {
             int ex = j - 1;
@@ -541,6 +542,7 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
             prev_has = true;
             prev = kValidBit | kPosBit;
             prev_j = last_j = p_last;
+            last_s = kValidBit | kPosBit;
             if (p_last != j) phase = 0;
             j = p_last + (coarse - phase);
             phase = 0;
@@ -555,6 +557,7 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
             const bool A = prev_has && (prev & kPosBit);
             if (A || (coarse > 2 && (cnt >= 2 || swept_j < j - 1))) swept_j = p_last;
             last_j = p_last;
+            last_s = 0u;  // invalid
             samples += cnt;
             exact_samples += (unsigned long long)cnt << 44;
             j = p_last + coarse;
@@ -563,7 +566,8 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
         }
         // inside a known ordinary brick region the per-sample summary cannot help
         DIAG_T0
-        const unsigned s = cert_sample(fr, er, j, samples, exact_samples, region_end < j || region_kind != 0);
+        const bool use_sum = region_end < j || region_kind != 0;
+        const unsigned s = cert_sample(fr, er, j, samples, exact_samples, use_sum);
         DIAG_ACC(1)
         const bool valid = s & kValidBit;
         bool do_scan = false;
@@ -577,7 +581,15 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
             DIAG_T0
             const int scan_from = (prev_j > swept_j ? prev_j : swept_j) + 1;
             const int k0 = scan_from - 1;
-            const unsigned sp = (prev_has && k0 == prev_j) ? prev : cert_sample(fr, er, k0, samples, exact_samples);
+            unsigned sp;
+            if (prev_has && k0 == prev_j) {
+                sp = prev;
+            } else if (k0 == last_j && last_s != kNoDecision) {
+                ++samples;  // the reference samples the seed again (:371-382)
+                sp = last_s;
+            } else {
+                sp = cert_sample(fr, er, k0, samples, exact_samples);
+            }
             Hit h;
             const bool found = scan_fast(fr, er, scan_from, j, sp, h, samples, exact_samples, s);
             DIAG_ACC(2)
@@ -591,6 +603,7 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
             }
         }
         last_j = j;
+        last_s = s;
         if (valid) {
             prev_has = true;
             prev = s;
@@ -607,7 +620,15 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
     const int scan_from = (last_j > swept_j ? last_j : swept_j) + 1;  // :417-451
     if (scan_from <= j_end) {
         const int k0 = scan_from - 1;
-        const unsigned sp = (prev_has && k0 == prev_j) ? prev : cert_sample(fr, er, k0, samples, exact_samples);
+        unsigned sp;
+        if (prev_has && k0 == prev_j) {
+            sp = prev;
+        } else if (k0 == last_j && last_s != kNoDecision) {
+            ++samples;
+            sp = last_s;
+        } else {
+            sp = cert_sample(fr, er, k0, samples, exact_samples);
+        }
         Hit h;
         if (scan_fast(fr, er, scan_from, j_end, sp, h, samples, exact_samples) && hit_wins(h, best)) {
             best = h;
