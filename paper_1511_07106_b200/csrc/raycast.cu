@@ -467,6 +467,13 @@ __device__ __forceinline__ bool scan_fast(const FastRay &fr, const Ray &er, int 
         if (k == end && end_s != kNoDecision) {
             ++samples;
             s = end_s;
+        } else if (k == end - 1 && end_s != kNoDecision &&
+                   (sp & (kValidBit | kPosBit)) != (kValidBit | kPosBit) &&
+                   (end_s & (kValidBit | kPosBit)) != kValidBit) {
+            // no crossing can involve point end - 1: one at end - 1 needs a
+            // valid positive seed, one at end a valid non-positive end point
+            ++samples;
+            s = 0u;
         } else {
             s = cert_sample(fr, er, k, samples, exact_samples);
         }
