@@ -854,6 +854,7 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
         switch (shape) {
         case 1: launch(raycast_kernel<16, 16, 2>, 16, 16); break;
         case 2: launch(raycast_kernel<8, 16, 4>, 8, 16); break;
+
         default: launch(raycast_kernel<32, 16, 1>, 32, 16); break;
         }
         tf_profile_end(prof, stream);
