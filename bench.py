@@ -290,6 +290,7 @@ def run_ours(args) -> None:
                     "certification_failures": sum_over_ranks(int(st[nat.STAT_CERT_FAILURES])),
                     "summary_certified_samples_per_frame": sum_over_ranks(int(st[nat.STAT_SUMMARY_SAMPLES])) / args.steps,
                     "samples_per_frame": samples / args.steps,
+                    "coop_rays_per_frame": sum_over_ranks(int(st[nat.STAT_COOP_RAYS])) / args.steps,
                     "samples_per_s": samples / (ms_total / 1e3)},
         "gpu_launches": int(launches),
     }

@@ -92,6 +92,7 @@ enum {
     TF_STAT_CERT_FAILURES = 12, /* certified decisions contradicted by exact ones (must be 0) */
     TF_STAT_SUMMARY_SAMPLES = 13, /* ray samples certified by the brick summary alone */
     TF_STAT_GENERAL_ALL_FREE = 14, /* general-path bricks whose voxels all turned out free space */
+    TF_STAT_COOP_RAYS = 15,   /* rays finished by the warp-cooperative raycast pass */
     TF_STAT_COUNT = 16
 };
 
@@ -121,7 +122,8 @@ int tf_profile_read(double *ms_by_kind, int64_t *launches_by_kind, int nkinds);
  * stores every free-space update even when it provably leaves the voxel
  * unchanged. */
 enum { TF_DEBUG_NO_CULL = 1u, TF_DEBUG_EXACT_ONLY = 2u, TF_DEBUG_NO_FIXEDPOINT = 4u,
-       TF_DEBUG_LANE0_ONLY = 8u /* tf_raycast traces only lane 0 of each warp (timing) */ };
+       TF_DEBUG_LANE0_ONLY = 8u /* tf_raycast traces only lane 0 of each warp (timing) */,
+       TF_DEBUG_COOP_ALL = 16u /* tf_raycast traces every ray with the warp-cooperative march */ };
 void tf_set_debug_flags(uint32_t flags);
 uint32_t tf_debug_flags(void);
 

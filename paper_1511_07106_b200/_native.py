@@ -42,6 +42,7 @@ DEBUG_NO_CULL = 1
 DEBUG_EXACT_ONLY = 2
 DEBUG_NO_FIXEDPOINT = 4
 DEBUG_LANE0_ONLY = 8
+DEBUG_COOP_ALL = 16
 PROF_INTEGRATE_UPDATE, PROF_INTEGRATE_ALL, PROF_RAYCAST, PROF_KINDS = 0, 1, 2, 3
 
 
@@ -60,6 +61,7 @@ STAT_COL_SKIPPED, STAT_DEPTH_SKIPPED, STAT_FREE_BRICKS, STAT_EXACT_SAMPLES = 8, 
 STAT_CERT_FAILURES = 12
 STAT_SUMMARY_SAMPLES = 13
 STAT_GENERAL_ALL_FREE = 14
+STAT_COOP_RAYS = 15
 STAT_COUNT = 16
 
 _VOL = ctypes.POINTER(TfVolume)

@@ -15,6 +15,7 @@
 // sample positions, the coarse/fine stepping, both re-walk rules, the
 // crossing interpolation and the analytic normal — is the reference's
 // arithmetic in the reference's order.
+#include <climits>
 #include <math.h>
 #include <stdlib.h>
 
@@ -512,7 +513,8 @@ __device__ __forceinline__ bool scan_fast(const FastRay &fr, const Ray &er, int 
 #define DIAG_ARG
 #endif
 __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_end, const int coarse,
-                           Hit &best, unsigned long long &samples, unsigned long long &exact_samples DIAG_PARAM) {
+                           Hit &best, unsigned long long &samples, unsigned long long &exact_samples,
+                           const long long deadline, bool &aborted DIAG_PARAM) {
     unsigned prev = 0u;  // decisions of the last valid march sample
     bool prev_has = false;
     int prev_j = -1, last_j = j - 1, swept_j = j - 1;
@@ -523,6 +525,11 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
     int region_end = -1, region_kind = 0, region_start = 0;
     unsigned last_s = kNoDecision;  // decisions of march point last_j
     while (j <= j_end) {
+        // the warp ran past its budget: hand the ray to the cooperative pass
+        if (clock64() > deadline) {
+            aborted = true;
+            return false;
+        }
         if (fr.flags && j > region_end) {
             int ex = j - 1;
             DIAG_T0
@@ -645,14 +652,63 @@ __device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_
     return false;
 }
 
+// unit ray direction of pixel (px, py) (_kernels.py:307-315)
+__device__ __forceinline__ void ray_direction(const RayGeom &g, int64_t px, int64_t py, double d[3]) {
+    const double *R = g.r_wc.m;
+    const double rx = ddiv(dsub((double)px, g.cx), g.fx);
+    const double ry = ddiv(dsub((double)py, g.cy), g.fy);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) d[a] = dadd(dadd(dmul(R[3 * a], rx), dmul(R[3 * a + 1], ry)), R[3 * a + 2]);
+    const double dn = dsqrt(dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2])));
+    d[0] = ddiv(d[0], dn);
+    d[1] = ddiv(d[1], dn);
+    d[2] = ddiv(d[2], dn);
+}
+
+// the exact (Ray) and certified (FastRay) views of a ray in one volume;
+// false when the certified march cannot be used (forced exact, or
+// coordinates too large to certify)
+__device__ __forceinline__ bool setup_volume(const RayGeom &g, const TfVolume &vol, const double o[3],
+                                             const double d[3], int64_t j_end, Ray &r, FastRay &fr) {
+    r.vox = (const float2 *)vol.voxels_dev;
+    r.n = vol.n;
+    r.htx = (double)vol.origin[0];
+    r.hty = (double)vol.origin[1];
+    r.htz = (double)vol.origin[2];
+    r.vs = vol.voxel_size;
+    r.ox = o[0];
+    r.oy = o[1];
+    r.oz = o[2];
+    r.dx = d[0];
+    r.dy = d[1];
+    r.dz = d[2];
+    r.samples = 0;
+    const double q0x = dsub(ddiv(o[0], r.vs), r.htx);
+    const double q0y = dsub(ddiv(o[1], r.vs), r.hty);
+    const double q0z = dsub(ddiv(o[2], r.vs), r.htz);
+    const double mag = fabs(q0x) + fabs(q0y) + fabs(q0z) + fabs(r.htx) + fabs(r.hty) + fabs(r.htz) +
+                       (double)j_end;
+    const bool summ = vol.brick_state_dev != nullptr && vol.summary_threshold == g.good_t;
+    fr = FastRay{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
+                 (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh,
+                 summ ? vol.brick_state_dev : nullptr, (unsigned)((vol.n + 7) / 8),
+                 1.0f / (float)d[0], 1.0f / (float)d[1], 1.0f / (float)d[2],
+                 summ ? vol.brick_flags_dev : nullptr};
+    return !g.exact_only && vol.n <= 4000 && mag < 1e6 && j_end < (1 << 30) && g.coarse < (1 << 20);
+}
+
 // a warp traces 8x4 pixels; a block of kBX x kBY pixels (kBX/8 x kBY/4 warps)
 
 template <int kBX, int kBY, int kMinBlocks>
 __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ RayGeom g,
     double *__restrict__ out_dist, double *__restrict__ out_vert, double *__restrict__ out_norm,
-    unsigned long long *__restrict__ stats, int64_t *__restrict__ clocks) {
+    unsigned long long *__restrict__ stats, int64_t *__restrict__ clocks, unsigned *__restrict__ rescue,
+    unsigned *__restrict__ rescue_count, long long budget) {
     const long long t_start = clock64();
+    const long long deadline = budget > 0 ? t_start + budget : LLONG_MAX;
+    long long t_start_ns = 0;
+    if (clocks) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start_ns));
     // warps tile the block's pixels in 8x4 units, row-major
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t px = (int64_t)blockIdx.x * kBX + (w % (kBX / 8)) * 8 + (lane & 7);
@@ -672,17 +728,8 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
         best.nx = out_norm[3 * p + 0];
         best.ny = out_norm[3 * p + 1];
         best.nz = out_norm[3 * p + 2];
-        // ray direction (_kernels.py:307-315)
-        const double *R = g.r_wc.m;
-        const double rx = ddiv(dsub((double)px, g.cx), g.fx);
-        const double ry = ddiv(dsub((double)py, g.cy), g.fy);
         double d[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) d[a] = dadd(dadd(dmul(R[3 * a], rx), dmul(R[3 * a + 1], ry)), R[3 * a + 2]);
-        const double dn = dsqrt(dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2])));
-        d[0] = ddiv(d[0], dn);
-        d[1] = ddiv(d[1], dn);
-        d[2] = ddiv(d[2], dn);
+        ray_direction(g, px, py, d);
         const double o[3] = {g.cam.v[0], g.cam.v[1], g.cam.v[2]};
 
         // entry intervals of every volume, visited nearest-entry first
@@ -690,7 +737,7 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
         uint64_t pending = 0;  // bit v set = volume v still to march
         for (int v = 0; v < vt.count; ++v)
             if (ray_interval(vt.vol[v], o, d, jlo[v], jhi[v])) pending |= 1ull << v;
-        bool changed = false;
+        bool changed = false, aborted = false;
         while (pending) {
             int pick = -1;
             for (int v = 0; v < vt.count; ++v)
@@ -703,46 +750,29 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
             // no hit of this volume can have tstar below (j0 - 1) * delta
             if (dmul((double)(jlo[pick] - 1), vol.voxel_size) > best.t) continue;
             Ray r;
-            r.vox = (const float2 *)vol.voxels_dev;
-            r.n = vol.n;
-            r.htx = (double)vol.origin[0];
-            r.hty = (double)vol.origin[1];
-            r.htz = (double)vol.origin[2];
-            r.vs = vol.voxel_size;
-            r.ox = o[0];
-            r.oy = o[1];
-            r.oz = o[2];
-            r.dx = d[0];
-            r.dy = d[1];
-            r.dz = d[2];
-            r.samples = 0;
-            const double q0x = dsub(ddiv(o[0], r.vs), r.htx);
-            const double q0y = dsub(ddiv(o[1], r.vs), r.hty);
-            const double q0z = dsub(ddiv(o[2], r.vs), r.htz);
-            const double mag = fabs(q0x) + fabs(q0y) + fabs(q0z) + fabs(r.htx) + fabs(r.hty) +
-                               fabs(r.htz) + (double)jhi[pick];
-            if (!g.exact_only && vol.n <= 4000 && mag < 1e6 && jhi[pick] < (1 << 30) && g.coarse < (1 << 20)) {
-                const bool summ = vol.brick_state_dev != nullptr && vol.summary_threshold == g.good_t;
-                FastRay fr{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
-                           (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh,
-                           summ ? vol.brick_state_dev : nullptr, (unsigned)((vol.n + 7) / 8),
-                           1.0f / (float)d[0], 1.0f / (float)d[1], 1.0f / (float)d[2],
-                           summ ? vol.brick_flags_dev : nullptr};
+            FastRay fr;
+            if (setup_volume(g, vol, o, d, jhi[pick], r, fr)) {
 #ifdef TF_RAY_DIAG
                 int64_t *diag = clocks ? clocks + 12 * p + 4 : nullptr;
                 if (!diag) __trap();
 #endif
                 DIAG_T0
                 changed |= march_fast(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
-                                      exact_samples DIAG_ARG);
+                                      exact_samples, deadline, aborted DIAG_ARG);
                 DIAG_ACC(3)
+                if (aborted) break;
             } else {  // forced, or coordinates too large to certify: the exact reference march
                 changed |= march_volume(r, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
                 samples += r.samples;
                 exact_samples += r.samples;
             }
         }
-        if (changed) {
+        if (aborted) {
+            // finished by raycast_coop_kernel (one warp per ray); nothing of
+            // this partial march is kept
+            samples = exact_samples = 0;
+            rescue[atomicAdd(rescue_count, 1u)] = (unsigned)p;
+        } else if (changed) {
             hits = 1;
             out_dist[p] = best.t;
             out_vert[3 * p + 0] = best.hx;
@@ -755,6 +785,14 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
     }
     if (clocks && px < g.width && py < g.height) {
         const int64_t q = 12 * (py * g.width + px);
+#ifndef TF_RAY_DIAG
+        // timeline: the pixel's start / end on the global nanosecond timer
+        clocks[q + 4] = t_start_ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(clocks[q + 5]));
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        clocks[q + 6] = smid;
+#endif
         clocks[q] = clock64() - t_start;
         clocks[q + 1] = (int64_t)samples;
         clocks[q + 2] = (int64_t)(exact_samples & ((1ull << 40) - 1));
@@ -766,6 +804,304 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
         warp_count_add(&stats[TF_STAT_EXACT_SAMPLES], exact_samples & ((1ull << 40) - 1));
         warp_count_add(&stats[TF_STAT_CERT_FAILURES], (exact_samples >> 40) & 15ull);
         warp_count_add(&stats[TF_STAT_SUMMARY_SAMPLES], exact_samples >> 44);
+    }
+}
+
+// ---- cooperative march: one warp per ray ---------------------------------
+//
+// Rays that graze partially observed space evaluate hundreds of samples and
+// keep a whole warp busy long after the rest of the frame is done (their
+// lanes diverge on every step).  raycast_kernel hands such rays over when
+// its warp exceeds a cycle budget; here the 32 lanes of a warp decide 32
+// consecutive fine lattice points of ONE ray at once (certified decisions,
+// as in the per-lane march) and then replay the reference's march over those
+// decisions warp-uniformly: the same march points, scans, seeds, crossings
+// and exit re-walk as march_volume (_kernels.py:349-451), so the result is
+// the same bits.
+
+// decisions of 64 consecutive fine points [base, base + 63] of one ray
+struct CoopWindow {
+    int base;
+    unsigned long long v, pos, nr;  // valid / value > 0 / |value| < 0.99 tau
+};
+
+// decisions of 32 consecutive points: bit i = point a + i
+struct Dec32 {
+    unsigned v, pos, nr;
+};
+
+// the 32 lanes decide points [b, b + 31] (only those in [lo, hi]; others read as invalid)
+__device__ __forceinline__ Dec32 coop_half(const FastRay &fr, const Ray &er, int b, int lo, int hi,
+                                           unsigned long long &exact_samples) {
+    const int lane = threadIdx.x & 31, k = b + lane;
+    unsigned s = 0u;
+    if (k >= lo && k <= hi) {
+        unsigned long long uncounted = 0;
+        s = cert_sample(fr, er, k, uncounted, exact_samples);
+    }
+    return Dec32{__ballot_sync(0xffffffffu, s & kValidBit), __ballot_sync(0xffffffffu, s & kPosBit),
+                 __ballot_sync(0xffffffffu, s & kNearBit)};
+}
+
+// decisions of [a, a + 31] (warp-uniform); slides the window forward as the
+// march advances, decides look-backs below it directly
+__device__ Dec32 coop_range(const FastRay &fr, const Ray &er, CoopWindow &w, int a, int lo, int hi,
+                            unsigned long long &exact_samples) {
+    if (a < w.base) return coop_half(fr, er, a, lo, hi, exact_samples);
+    if (a + 31 > w.base + 63) {
+        if (a + 31 <= w.base + 95) {  // slide by 32
+            w.base += 32;
+            const Dec32 h = coop_half(fr, er, w.base + 32, lo, hi, exact_samples);
+            w.v = (w.v >> 32) | ((unsigned long long)h.v << 32);
+            w.pos = (w.pos >> 32) | ((unsigned long long)h.pos << 32);
+            w.nr = (w.nr >> 32) | ((unsigned long long)h.nr << 32);
+        } else {  // jump, keeping 16 points of look-back below a
+            w.base = a - 16;
+            const Dec32 l = coop_half(fr, er, w.base, lo, hi, exact_samples);
+            const Dec32 h = coop_half(fr, er, w.base + 32, lo, hi, exact_samples);
+            w.v = l.v | ((unsigned long long)h.v << 32);
+            w.pos = l.pos | ((unsigned long long)h.pos << 32);
+            w.nr = l.nr | ((unsigned long long)h.nr << 32);
+        }
+    }
+    const int i = a - w.base;
+    return Dec32{(unsigned)(w.v >> i), (unsigned)(w.pos >> i), (unsigned)(w.nr >> i)};
+}
+
+__device__ __forceinline__ unsigned dec_bits(const Dec32 &d, int i) {
+    return ((d.v >> i) & 1u) * kValidBit | ((d.pos >> i) & 1u) * kPosBit | ((d.nr >> i) & 1u) * kNearBit;
+}
+
+// _scan_crossing over [from, end] with seed decisions sp (warp-uniform):
+// crossing candidates (previous valid > 0, this valid <= 0, :169) come from
+// the decision masks 32 points at a time; each is checked exactly in order
+__device__ bool coop_scan(const FastRay &fr, const Ray &er, CoopWindow &w, int lo, int hi, int from, int end,
+                          unsigned sp, Hit &hit, unsigned long long &samples,
+                          unsigned long long &exact_samples) {
+    samples += (unsigned long long)(end - from + 1);
+    for (int a = from; a <= end; a += 32) {
+        const Dec32 d = coop_range(fr, er, w, a, lo, hi, exact_samples);
+        const unsigned vp = d.v & d.pos;
+        const unsigned vp_prev = (vp << 1) | ((sp & (kValidBit | kPosBit)) == (kValidBit | kPosBit) ? 1u : 0u);
+        unsigned cand = vp_prev & d.v & ~d.pos;
+        const int len = end - a + 1;
+        if (len < 32) cand &= (1u << len) - 1u;
+        while (cand) {
+            const int k = a + __ffs(cand) - 1;
+            cand &= cand - 1;
+            Ray r = er;
+            double e0 = 0.0, e1 = 0.0;
+            const bool v0 = sample_at(r, k - 1, e0), v1 = sample_at(r, k, e1);
+            exact_samples += 2;
+            if (!v0 || !v1 || !(e0 > 0.0) || !(e1 <= 0.0)) {
+                exact_samples += 1ull << 40;  // certified decision disagreed: counted, never expected
+            } else if (accept_crossing(r, k, e0, e1, hit)) {
+                return true;
+            }
+        }
+        sp = ((vp >> 31) & 1u) ? (kValidBit | kPosBit) : 0u;  // only "valid and > 0" matters here
+    }
+    return false;
+}
+
+// march_volume (_kernels.py:349-451) replayed warp-uniformly over decision
+// masks.  With coarse == 2, runs of march points that change nothing but
+// counters are consumed in one step: invalid march points (each followed by
+// a scan when the last valid sample was positive: the scans tile one range,
+// searched once) and valid, positive, not-near march points (no scan).
+__device__ bool march_coop(const FastRay &fr, const Ray &er, int j, const int j_end, const int coarse,
+                           Hit &best, unsigned long long &samples, unsigned long long &exact_samples) {
+    const int lo = j - 1, hi = j_end;  // the only points the reference can sample
+    CoopWindow w;
+    w.base = INT_MIN / 2;
+    w.v = w.pos = w.nr = 0ull;
+    unsigned prev = 0u;
+    bool prev_has = false;
+    int prev_j = -1, last_j = j - 1, swept_j = j - 1;
+    while (j <= j_end) {
+        const Dec32 d = coop_range(fr, er, w, j, lo, hi, exact_samples);
+        const unsigned s = dec_bits(d, 0);
+        const bool valid = s & kValidBit;
+        if (coarse == 2 && !(j & 1)) {
+            // even march points j, j + 2, ... of this 32-point block (<= j_end)
+            const int span = min(j_end - j, 31);
+            const unsigned inblk = span >= 31 ? 0xffffffffu : ((2u << span) - 1u);
+            const unsigned even = 0x55555555u & inblk;
+            if (!valid) {
+                // run of invalid march points
+                const unsigned stop = d.v & even;
+                const int f = stop ? __ffs(stop) - 1 : (span >= 31 ? 32 : span + 1);
+                const int m = (f + 1) >> 1;  // march points j, ..., j + 2(m-1)
+                const int jl = j + 2 * (m - 1);
+                samples += m;
+                if (prev_has && (prev & kPosBit)) {  // every one of them scans (:362-369)
+                    const int scan_from = (prev_j > swept_j ? prev_j : swept_j) + 1;
+                    const int k0 = scan_from - 1;
+                    unsigned sp;
+                    if (k0 == prev_j) {
+                        sp = prev;
+                    } else {
+                        sp = dec_bits(coop_range(fr, er, w, k0, lo, hi, exact_samples), 0);
+                        ++samples;
+                    }
+                    samples += m - 1;  // the later scans' seeds
+                    Hit h;
+                    if (coop_scan(fr, er, w, lo, hi, scan_from, jl, sp, h, samples, exact_samples)) {
+                        if (hit_wins(h, best)) {
+                            best = h;
+                            return true;
+                        }
+                        return false;
+                    }
+                    swept_j = jl;
+                }
+                last_j = jl;
+                j = jl + 2;
+                continue;
+            }
+            if ((s & (kPosBit | kNearBit)) == kPosBit) {
+                // run of valid, positive, not-near march points: no scans
+                const unsigned stop = ~(d.v & d.pos & ~d.nr) & even;
+                const int f = stop ? __ffs(stop) - 1 : (span >= 31 ? 32 : span + 1);
+                const int m = (f + 1) >> 1;
+                const int jl = j + 2 * (m - 1);
+                samples += m;
+                prev_has = true;
+                prev = kValidBit | kPosBit;
+                prev_j = last_j = jl;
+                j = jl + 2;
+                continue;
+            }
+        }
+        // one march point (:356-416)
+        ++samples;
+        bool do_scan = false;
+        if (!valid || !(s & kPosBit)) {
+            if (prev_has && (prev & kPosBit))
+                do_scan = true;
+            else if (swept_j < j - 1 && (valid || coarse > 2))
+                do_scan = true;
+        }
+        if (do_scan) {
+            const int scan_from = (prev_j > swept_j ? prev_j : swept_j) + 1;
+            const int k0 = scan_from - 1;
+            unsigned sp;
+            if (prev_has && k0 == prev_j) {
+                sp = prev;
+            } else {
+                sp = dec_bits(coop_range(fr, er, w, k0, lo, hi, exact_samples), 0);
+                ++samples;
+            }
+            Hit h;
+            const bool found = coop_scan(fr, er, w, lo, hi, scan_from, j, sp, h, samples, exact_samples);
+            swept_j = j;
+            if (found) {
+                if (hit_wins(h, best)) {
+                    best = h;
+                    return true;
+                }
+                return false;
+            }
+        }
+        last_j = j;
+        if (valid) {
+            prev_has = true;
+            prev = s;
+            prev_j = j;
+        }
+        if (valid && (s & kNearBit))
+            j += 1;
+        else
+            j = (j / coarse + 1) * coarse;
+    }
+    const int scan_from = (last_j > swept_j ? last_j : swept_j) + 1;  // :417-451
+    if (scan_from <= j_end) {
+        const int k0 = scan_from - 1;
+        unsigned sp;
+        if (prev_has && k0 == prev_j) {
+            sp = prev;
+        } else {
+            sp = dec_bits(coop_range(fr, er, w, k0, lo, hi, exact_samples), 0);
+            ++samples;
+        }
+        Hit h;
+        if (coop_scan(fr, er, w, lo, hi, scan_from, j_end, sp, h, samples, exact_samples) && hit_wins(h, best)) {
+            best = h;
+            return true;
+        }
+    }
+    return false;
+}
+
+// the rays raycast_kernel handed over: one warp per ray, every lane holds the
+// same ray state; lane 0 writes
+__global__ void __launch_bounds__(128) raycast_coop_kernel(
+    const __grid_constant__ VolumeTable vt, const __grid_constant__ RayGeom g,
+    double *__restrict__ out_dist, double *__restrict__ out_vert, double *__restrict__ out_norm,
+    unsigned long long *__restrict__ stats, const unsigned *__restrict__ rescue,
+    const unsigned *__restrict__ rescue_count) {
+    const int lane = threadIdx.x & 31;
+    const unsigned count = *rescue_count;
+    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+    unsigned long long samples = 0, hits = 0, exact_samples = 0;
+    for (unsigned i = warp; i < count; i += nwarps) {
+        const int64_t p = rescue[i];
+        const int64_t py = p / g.width, px = p - py * g.width;
+        Hit best;
+        best.t = out_dist[p];
+        best.hx = out_vert[3 * p + 0];
+        best.hy = out_vert[3 * p + 1];
+        best.hz = out_vert[3 * p + 2];
+        best.nx = out_norm[3 * p + 0];
+        best.ny = out_norm[3 * p + 1];
+        best.nz = out_norm[3 * p + 2];
+        double d[3];
+        ray_direction(g, px, py, d);
+        const double o[3] = {g.cam.v[0], g.cam.v[1], g.cam.v[2]};
+        int64_t jlo[TFB200_MAX_VOLUMES_PER_LAUNCH], jhi[TFB200_MAX_VOLUMES_PER_LAUNCH];
+        uint64_t pending = 0;
+        for (int v = 0; v < vt.count; ++v)
+            if (ray_interval(vt.vol[v], o, d, jlo[v], jhi[v])) pending |= 1ull << v;
+        bool changed = false;
+        while (pending) {
+            int pick = -1;
+            for (int v = 0; v < vt.count; ++v)
+                if (((pending >> v) & 1ull) &&
+                    (pick < 0 || dmul((double)(jlo[v] - 1), vt.vol[v].voxel_size) <
+                                     dmul((double)(jlo[pick] - 1), vt.vol[pick].voxel_size)))
+                    pick = v;
+            pending &= ~(1ull << pick);
+            const TfVolume &vol = vt.vol[pick];
+            if (dmul((double)(jlo[pick] - 1), vol.voxel_size) > best.t) continue;
+            Ray r;
+            FastRay fr;
+            if (setup_volume(g, vol, o, d, jhi[pick], r, fr)) {
+                changed |= march_coop(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
+                                      exact_samples);
+            } else {
+                changed |= march_volume(r, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
+                samples += r.samples;
+                exact_samples += r.samples;
+            }
+        }
+        if (changed && lane == 0) {
+            ++hits;
+            out_dist[p] = best.t;
+            out_vert[3 * p + 0] = best.hx;
+            out_vert[3 * p + 1] = best.hy;
+            out_vert[3 * p + 2] = best.hz;
+            out_norm[3 * p + 0] = best.nx;
+            out_norm[3 * p + 1] = best.ny;
+            out_norm[3 * p + 2] = best.nz;
+        }
+    }
+    if (stats && threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&stats[TF_STAT_COOP_RAYS], (unsigned long long)count);
+    if (stats && lane == 0) {  // every lane counted the same ray: lane 0 reports
+        atomicAdd(&stats[TF_STAT_RAY_SAMPLES], samples);
+        atomicAdd(&stats[TF_STAT_RAY_HITS], hits);
+        atomicAdd(&stats[TF_STAT_EXACT_SAMPLES], exact_samples & ((1ull << 40) - 1));
+        atomicAdd(&stats[TF_STAT_CERT_FAILURES], (exact_samples >> 40) & 15ull);
     }
 }
 
@@ -843,23 +1179,44 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
             const char *e = getenv("TFB200_RAY_SHAPE");  // tuning knob: block shape variant
             return e ? atoi(e) : 0;
         }();
+        static const long long budget = [] {
+            // cycles a warp of the per-lane march may run before its unfinished
+            // rays move to the cooperative pass (0: never)
+            const char *e = getenv("TFB200_RAY_BUDGET");
+            return e ? atoll(e) : 1400000ll;
+        }();
+        const bool coop_all = (tf_debug_flags() & TF_DEBUG_COOP_ALL) != 0;
         unsigned long long *st = (unsigned long long *)stats;
         int64_t *clk = tf_ray_clock_buffer();
+        const int64_t npix = cam->width * cam->height;
+        unsigned *rescue = nullptr;  // [0] = count, then pixel indices
+        if (cudaMallocAsync((void **)&rescue, (size_t)(npix + 1) * sizeof(unsigned), stream) != cudaSuccess ||
+            cudaMemsetAsync(rescue, 0, sizeof(unsigned), stream) != cudaSuccess)
+            return tf_set_error(TF_ECUDA, "tf_raycast: cannot allocate the rescue list");
         auto launch = [&](auto kern, int bx, int by) {
             dim3 grid((unsigned)((cam->width + bx - 1) / bx), (unsigned)((cam->height + by - 1) / by));
-            kern<<<grid, bx * by, 0, stream>>>(vt, g, dist, vert, norm, st, clk);
+            kern<<<grid, bx * by, 0, stream>>>(vt, g, dist, vert, norm, st, clk, rescue + 1, rescue,
+                                               coop_all ? 1ll : budget);
         };
         // 32x16-pixel blocks (16 warps, one block per SM): the warps of an SM
         // trace neighbouring rays and share L1 lines
         switch (shape) {
         case 1: launch(raycast_kernel<16, 16, 2>, 16, 16); break;
         case 2: launch(raycast_kernel<8, 16, 4>, 8, 16); break;
-
         default: launch(raycast_kernel<32, 16, 1>, 32, 16); break;
         }
-        tf_profile_end(prof, stream);
         int rc = tf_check_launch("raycast_kernel");
         if (rc) return rc;
+        if (budget > 0 || coop_all) {
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            raycast_coop_kernel<<<(unsigned)sms * 4, 128, 0, stream>>>(vt, g, dist, vert, norm, st, rescue + 1,
+                                                                     rescue);
+            if ((rc = tf_check_launch("raycast_coop_kernel"))) return rc;
+        }
+        cudaFreeAsync(rescue, stream);
+        tf_profile_end(prof, stream);
     }
     return TF_OK;
 }

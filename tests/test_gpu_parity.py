@@ -354,6 +354,36 @@ def test_certified_raycast_equals_exact_march_full_size():
     assert stats[nat.STAT_CERT_FAILURES].item() == 0
 
 
+def test_cooperative_raycast_equals_exact_march_full_size():
+    """Every ray through the warp-cooperative march (TF_DEBUG_COOP_ALL) == exact march."""
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(4.08, 1020, 510)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    tiles = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length)
+             for k in spec.keys]
+    scene = demo_scene()
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)
+    for pose in poses[:10]:
+        tf.integrate_volumes(tiles, scene.render_depth(pose, intr), pose, intr, params)
+    lib = nat.load_library()
+    stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
+    try:
+        for pose in (poses[4], poses[11]):
+            coop = tf.RayMap.empty(intr)
+            lib.tf_set_debug_flags(nat.DEBUG_COOP_ALL)
+            tf.raycast_volumes(tiles, pose, intr, coop, params, stats)
+            exact = tf.RayMap.empty(intr)
+            lib.tf_set_debug_flags(nat.DEBUG_EXACT_ONLY)
+            tf.raycast_volumes(tiles, pose, intr, exact, params)
+            assert torch.isfinite(exact.distance_dev).sum().item() > 30000
+            assert torch.equal(coop.distance_dev, exact.distance_dev)
+            assert torch.equal(coop.vertices_dev, exact.vertices_dev)
+            assert torch.equal(coop.normals_dev, exact.normals_dev)
+    finally:
+        lib.tf_set_debug_flags(0)
+    assert stats[nat.STAT_CERT_FAILURES].item() == 0
+
+
 def test_brick_summary_stays_exact_under_integration():
     """The incrementally maintained free-space summary equals a rebuild."""
     intr = tf.RunConfig().intrinsics()

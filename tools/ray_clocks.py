@@ -88,3 +88,19 @@ if os.environ.get("RAY_LANE0"):
     order = np.argsort(full0.ravel())[::-1][:8]
     print("slowest warps, lane-0 cycles full vs alone:",
           " ".join("%.2fM/%.2fM" % (full0.ravel()[i] / 1e6, solo0.ravel()[i] / 1e6) for i in order))
+
+if not os.environ.get("RAY_LANE0") and allc[..., 5].any():
+    # timeline of warps (lane 0 of each 8x4 tile): start / end on the global timer
+    st0 = allc[0::4, 0::8, 4].ravel()
+    en0 = allc[0::4, 0::8, 5].ravel()
+    t0 = st0.min()
+    st0, en0 = (st0 - t0) / 1e3, (en0 - t0) / 1e3  # microseconds
+    T = en0.max()
+    grid = np.linspace(0, T, 400)
+    active = np.array([((st0 <= t) & (en0 > t)).sum() for t in grid])
+    print("kernel %.0f us; warps active (of 2368 slots): " % T +
+          " ".join("%d%%:%d" % (p, active[int(p / 100 * 399)]) for p in (10, 30, 50, 70, 80, 90, 95, 99)))
+    dur = en0 - st0
+    late = np.argsort(en0)[-5:]
+    print("last warps to finish: start/dur us", [(round(st0[i]), round(dur[i])) for i in late])
+    print("time with < 50%% of slots busy: %.0f us" % ((active < 1184).mean() * T))
