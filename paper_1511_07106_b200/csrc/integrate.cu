@@ -35,6 +35,8 @@
 
 #include "tf_common.cuh"
 
+#include <mutex>
+
 namespace tf {
 
 constexpr int kBrick = 8;         // brick edge in voxels
@@ -1098,6 +1100,31 @@ extern "C" size_t tf_integrate_workspace_size(const TfVolume *vols, int nvol, co
     return layout_for(chunk, cam).total;
 }
 
+// Per-device side stream (and fork / join events) for kernels that run next
+// to the caller's stream inside one call; joined back before the call returns.
+struct SideStream {
+    std::mutex mu;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+static SideStream *side_stream() {
+    constexpr int kMaxDev = 64;
+    static SideStream sides[kMaxDev];
+    static std::mutex init_mu;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+    std::lock_guard<std::mutex> lock(init_mu);
+    SideStream &s = sides[dev];
+    if (!s.stream) {
+        if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess)
+            return nullptr;
+    }
+    return &s;
+}
+
 extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
                             const TfCamera *cam, const double r_cw[9], const double t_cw[3],
                             const double cam_center[3], double tau, double max_weight,
@@ -1229,17 +1256,27 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
             brick_update_exact_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(
                 vt, bt, f, table, active, count, (unsigned long long *)stats);
         } else {
+            // the certified free-space bricks (bandwidth-bound) run on a side
+            // stream next to the general bricks (issue-bound): disjoint bricks
+            SideStream *side = side_stream();
+            if (!side) return tf_set_error(TF_ECUDA, "tf_integrate: cannot create the side stream");
+            std::unique_lock<std::mutex> side_lock(side->mu);
+            cudaEventRecord(side->fork, stream);
+            cudaStreamWaitEvent(side->stream, side->fork, 0);
+            brick_free_kernel<<<(unsigned)sms * 8, 256, 0, side->stream>>>(vt, bt, f, active_free, fcount,
+                                                                          fixed_point,
+                                                                          (unsigned long long *)stats);
+            if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
+            cudaEventRecord(side->join, side->stream);
             brick_update_kernel<<<(unsigned)sms * 6, 256, 0, stream>>>(
                 vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap,
                 fixed_point, (unsigned long long *)stats);
             if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
-            if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
-            brick_free_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(vt, bt, f, active_free, fcount,
-                                                                    fixed_point, (unsigned long long *)stats);
-            if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
             exact_queue_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, f, table, queue, qcount,
                                                                      L.queue_cap,
                                                                      (unsigned long long *)stats);
+            if ((rc = tf_check_launch("exact_queue_kernel"))) return rc;
+            cudaStreamWaitEvent(stream, side->join, 0);
         }
         tf_profile_end(prof, stream);
         if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
