@@ -165,6 +165,18 @@ int tf_raymap_merge(double *dst_dist_dev, double *dst_vert_dev, double *dst_norm
                     const double *src_dist_dev, const double *src_vert_dev,
                     const double *src_norm_dev, int64_t npixels, void *stream);
 
+/* Packed form for the cross-GPU row-block exchange: records of 4 doubles
+ * (t, nx, ny, nz), 32-byte aligned; dst[p] = src[p] where _hit_wins(src, dst). */
+int tf_raymap_merge_packed(double *dst_dev, const double *src_dev, int64_t npixels, void *stream);
+
+/* Vertices of rows [row0, row0 + nrows) rebuilt from their hit distances
+ * (dist_dev[i * dist_stride], row-major from row0): o + t d with the
+ * raycast's own arithmetic (bit-identical to what tf_raycast writes), 0 where
+ * t = +inf.  vert_dev: nrows * width * 3 doubles. */
+int tf_raymap_vertices(const double *dist_dev, int64_t dist_stride, double *vert_dev,
+                       const TfCamera *cam, const double r_wc[9], const double cam_center[3],
+                       int64_t row0, int64_t nrows, void *stream);
+
 /* ---- ICP source maps: geometry.depth_to_vertices + compute_normals
  * (geometry.py:261-302) of pyramid level `level` (stride 2^level subsampling of
  * the full-resolution depth, geometry.py:256-258), with that level's camera.

@@ -1137,6 +1137,39 @@ __global__ void trilinear_sample_kernel(const TfVolume vol, const double *__rest
     valid[i] = ok ? 1 : 0;
 }
 
+// _hit_wins over packed (t, nx, ny, nz) records: the cross-GPU row-block
+// reduction exchanges only these (vertices follow from t, tf_raymap_vertices)
+__global__ void raymap_merge_packed_kernel(double4 *__restrict__ dst, const double4 *__restrict__ src,
+                                           int64_t npix) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= npix) return;
+    const double4 a = src[p], b = dst[p];
+    const Hit h{a.x, 0, 0, 0, a.y, a.z, a.w};
+    const Hit cur{b.x, 0, 0, 0, b.y, b.z, b.w};
+    if (hit_wins(h, cur)) dst[p] = a;
+}
+
+// hit vertex = o + t d with the raycast's own arithmetic (accept_crossing:
+// dadd(o, dmul(tstar, d)), d from ray_direction), so a vertex rebuilt from t
+// is the one the raycast wrote; 0 where there is no hit (RayMap.empty)
+__global__ void raymap_vertices_kernel(const __grid_constant__ RayGeom g, const double *__restrict__ dist,
+                                       int64_t dist_stride, double *__restrict__ vert, int64_t row0,
+                                       int64_t nrows) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nrows * g.width) return;
+    const int64_t py = row0 + i / g.width, px = i % g.width;
+    const double t = dist[i * dist_stride];
+    double v[3] = {0.0, 0.0, 0.0};
+    if (t < INFINITY) {
+        double d[3];
+        ray_direction(g, px, py, d);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) v[a] = dadd(g.cam.v[a], dmul(t, d[a]));
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) vert[3 * i + a] = v[a];
+}
+
 }  // namespace tf
 
 using namespace tf;
@@ -1219,6 +1252,38 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
         tf_profile_end(prof, stream);
     }
     return TF_OK;
+}
+
+extern "C" int tf_raymap_merge_packed(double *dst_dev, const double *src_dev, int64_t npix, void *stream_) {
+    if (npix <= 0) return TF_OK;
+    if (!dst_dev || !src_dev) return tf_set_error(TF_EINVAL, "tf_raymap_merge_packed: null argument");
+    if (((uintptr_t)dst_dev | (uintptr_t)src_dev) & 31u)
+        return tf_set_error(TF_EINVAL, "tf_raymap_merge_packed: records must be 32-byte aligned");
+    raymap_merge_packed_kernel<<<(unsigned)((npix + 255) / 256), 256, 0, (cudaStream_t)stream_>>>(
+        (double4 *)dst_dev, (const double4 *)src_dev, npix);
+    return tf_check_launch("raymap_merge_packed_kernel");
+}
+
+extern "C" int tf_raymap_vertices(const double *dist_dev, int64_t dist_stride, double *vert_dev,
+                                  const TfCamera *cam, const double r_wc[9], const double cam_center[3],
+                                  int64_t row0, int64_t nrows, void *stream_) {
+    if (nrows <= 0) return TF_OK;
+    if (!dist_dev || !vert_dev || !cam || !r_wc || !cam_center || dist_stride < 1 || row0 < 0 ||
+        row0 + nrows > cam->height)
+        return tf_set_error(TF_EINVAL, "tf_raymap_vertices: bad argument");
+    RayGeom g{};
+    for (int i = 0; i < 9; ++i) g.r_wc.m[i] = r_wc[i];
+    for (int i = 0; i < 3; ++i) g.cam.v[i] = cam_center[i];
+    g.fx = cam->fx;
+    g.fy = cam->fy;
+    g.cx = cam->cx;
+    g.cy = cam->cy;
+    g.width = cam->width;
+    g.height = cam->height;
+    const int64_t n = nrows * cam->width;
+    raymap_vertices_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream_>>>(
+        g, dist_dev, dist_stride, vert_dev, row0, nrows);
+    return tf_check_launch("raymap_vertices_kernel");
 }
 
 extern "C" int tf_raymap_merge(double *dd, double *dv, double *dn, const double *sd,

@@ -9,11 +9,16 @@ The paper's CPU<->GPU volume swapping becomes ownership:
   rank integrates only its own volumes — integration has no data-path
   collective;
 * each rank raycasts its volumes into a partial ray map; the partial maps are
-  all-gathered and merged with the _hit_wins total order (tf_raymap_merge),
-  in rank order, so every rank holds the identical full model.  _hit_wins is
-  a strict total order, so the result equals the single-GPU raycast over all
-  volumes bit for bit (the reference's order-free invariant,
-  test_acceptance.py:349-361).
+  reduced by a row-block exchange: every rank packs its
+  partial as (t, nx, ny, nz) records, an all-to-all gives rank r every
+  rank's records of row block r, rank r folds them with the _hit_wins total
+  order in rank order (tf_raymap_merge_packed), and an all-gather of the
+  merged blocks gives every rank the full model; vertices are rebuilt from t
+  with the raycast's own arithmetic (tf_raymap_vertices), so they are the
+  bits the raycast wrote.  _hit_wins is a strict total order, so the result
+  equals the single-GPU raycast over all volumes bit for bit (the
+  reference's order-free invariant, test_acceptance.py:349-361).  Traffic
+  per rank and frame: 2 x 32 B x pixels x (world - 1) / world.
 
 ICP runs replicated on every rank over the merged model (no per-iteration
 collective).  The host-side schedule is backend-agnostic and is tested with
@@ -68,6 +73,44 @@ def merge_in_rank_order(gathered: list, merge: Callable) -> list:
     return acc
 
 
+def row_block(height: int, world: int) -> int:
+    """Rows per block of the row-block exchange (the last block is padded)."""
+    return -(-height // world)
+
+
+def rowblock_exchange(packed: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """All-to-all of packed partial records [world * B, W, 4] (rows padded to
+    world * B); returns [world, B, W, 4]: every rank's records of this rank's
+    row block, in rank order."""
+    if world == 1:
+        return packed.view(1, *packed.shape)
+    recv = torch.empty_like(packed)
+    dist.all_to_all_single(recv, packed.contiguous(), group=group)
+    return recv.view(world, packed.shape[0] // world, *packed.shape[1:])
+
+
+def merge_blocks(blocks: torch.Tensor, merge: Callable) -> torch.Tensor:
+    """Fold the ranks' records of one row block in rank order (merge(acc, other))."""
+    acc = blocks[0].clone()
+    for r in range(1, blocks.shape[0]):
+        merge(acc, blocks[r])
+    return acc
+
+
+def gather_blocks(block: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """All-gather of every rank's merged block -> [world * B, W, 4]."""
+    if world == 1:
+        return block
+    out = torch.empty((world,) + tuple(block.shape), dtype=block.dtype, device=block.device)
+    dist.all_gather(list(out.unbind(0)), block.contiguous(), group=group)
+    return out.view(world * block.shape[0], *block.shape[1:])
+
+
+def merge_packed_cuda(acc: torch.Tensor, other: torch.Tensor) -> None:
+    nat.check(nat.lib().tf_raymap_merge_packed(nat.ptr(acc), nat.ptr(other), acc.numel() // 4,
+                                               nat.stream_handle()), "tf_raymap_merge_packed")
+
+
 class ShardedFusion:
     """The per-rank slice of a static multi-volume map.
 
@@ -85,6 +128,12 @@ class ShardedFusion:
         self.partial = RayMap.empty(intr)
         self.model = RayMap.empty(intr)
         self.stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device=self.partial.distance_dev.device)
+        # row-block exchange buffer: (t, n) records, rows padded to world * B; the
+        # padding rows stay "no hit"
+        b = row_block(intr.height, world)
+        self._packed = torch.zeros((world * b, intr.width, 4), dtype=torch.float64,
+                                   device=self.partial.distance_dev.device)
+        self._packed[..., 0] = float("inf")
 
     def step(self, depth: torch.Tensor, pose: Pose) -> RayMap:
         integrate_volumes(self.tiles, depth, pose, self.intr, self.params, self.stats)
@@ -93,13 +142,17 @@ class ShardedFusion:
         if self.world == 1:
             self.model, self.partial = self.partial, self.model
             return self.model
-        parts = [self.partial.distance_dev, self.partial.vertices_dev, self.partial.normals_dev]
-        gathered = gather_partials(parts, self.group)
-
-        def merge(acc, other):
-            dst = RayMap(device_tensors=(acc[1], acc[2], acc[0]))
-            dst.merge_from(RayMap(device_tensors=(other[1], other[2], other[0])))
-
-        d, v, n = merge_in_rank_order(gathered, merge)
-        self.model = RayMap(device_tensors=(v, n, d))
+        h, w = self.intr.height, self.intr.width
+        packed = self._packed
+        packed[:h, :, 0] = self.partial.distance_dev
+        packed[:h, :, 1:] = self.partial.normals_dev
+        blocks = rowblock_exchange(packed, self.world, self.group)
+        merged = gather_blocks(merge_blocks(blocks, merge_packed_cuda), self.world, self.group)
+        self.model.distance_dev.copy_(merged[:h, :, 0])
+        self.model.normals_dev.copy_(merged[:h, :, 1:])
+        nat.check(nat.lib().tf_raymap_vertices(
+            nat.ptr(self.model.distance_dev), 1, nat.ptr(self.model.vertices_dev), nat.camera(self.intr),
+            nat.mat9(pose.rotation), nat.vec3(pose.translation), 0, h, nat.stream_handle()),
+            "tf_raymap_vertices")
+        self.model._device_written()
         return self.model

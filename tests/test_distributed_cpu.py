@@ -17,8 +17,9 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1511_07106_b200.distributed import (broadcast_frame, gather_partials,
-                                               merge_in_rank_order, owned_keys, owner_of)
+from paper_1511_07106_b200.distributed import (broadcast_frame, gather_blocks, gather_partials,
+                                               merge_blocks, merge_in_rank_order, owned_keys,
+                                               owner_of, row_block, rowblock_exchange)
 
 
 def hit_wins_merge(acc, other):
@@ -49,6 +50,59 @@ def partial_map(seed, h=12, w=16):
     n = torch.round(torch.rand(h, w, 3, generator=g) * 4).double() / 4  # ties happen
     n = torch.where(hit[..., None], n, torch.zeros(()).double())
     return [d, v, n]
+
+
+def hit_wins_packed(acc, other):
+    """_hit_wins on (t, nx, ny, nz) records, in place (tf_raymap_merge_packed)."""
+    better = other[..., 0] < acc[..., 0]
+    tie = other[..., 0] == acc[..., 0]
+    for a in range(1, 4):
+        neq = other[..., a] != acc[..., a]
+        better = better | (tie & neq & (other[..., a] > acc[..., a]))
+        tie = tie & ~neq
+    acc[better] = other[better]
+
+
+def packed_partial(seed, h, w, world):
+    d, _, n = partial_map(seed, h, w)
+    b = row_block(h, world)
+    out = torch.zeros((world * b, w, 4), dtype=torch.float64)
+    out[..., 0] = float("inf")
+    out[:h, :, 0] = d
+    out[:h, :, 1:] = n
+    return out
+
+
+def _rowblock_worker(rank, world, port, h, w, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        blocks = rowblock_exchange(packed_partial(200 + rank, h, w, world), world)
+        merged = gather_blocks(merge_blocks(blocks, hit_wins_packed), world)
+        out[rank] = merged[:h].clone()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,h", [(2, 12), (3, 7)])
+def test_gloo_rowblock_exchange_equals_single_merge(world, h):
+    """All-to-all of row blocks, rank-order _hit_wins fold, all-gather: every
+    rank ends with the single-process merge of all partials (ragged last block)."""
+    w = 5
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_rowblock_worker, args=(world, _free_port(), h, w, out), nprocs=world, join=True)
+    want = packed_partial(200, h, w, world)[:h].clone()
+    for r in range(1, world):
+        hit_wins_packed(want, packed_partial(200 + r, h, w, world)[:h])
+    for r in range(world):
+        assert torch.equal(out[r], want)
+    # order-free: folding in reverse rank order gives the same map
+    rev = packed_partial(200 + world - 1, h, w, world)[:h].clone()
+    for r in range(world - 2, -1, -1):
+        hit_wins_packed(rev, packed_partial(200 + r, h, w, world)[:h])
+    assert torch.equal(rev, want)
 
 
 def _free_port():

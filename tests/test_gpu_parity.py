@@ -247,6 +247,56 @@ def test_trilinear_sample_and_merge():
             assert got == val
 
 
+def test_rowblock_merge_kernels():
+    """tf_raymap_merge_packed == _hit_wins on packed records; tf_raymap_vertices
+    rebuilds exactly the vertices tf_raycast wrote (the cross-GPU exchange)."""
+    lib = nat.load_library()
+    rng = torch.Generator().manual_seed(3)
+    n = 4096
+    a = torch.zeros(n, 4, dtype=torch.float64)
+    b = torch.zeros(n, 4, dtype=torch.float64)
+    for x in (a, b):
+        x[:, 0] = torch.where(torch.rand(n, generator=rng) < 0.3, torch.full((n,), float("inf")),
+                              torch.round(torch.rand(n, generator=rng) * 4) / 4)
+        x[:, 1:] = torch.round(torch.rand(n, 3, generator=rng) * 2) / 2  # ties reach the normals
+    want = a.clone()
+    better = b[:, 0] < want[:, 0]
+    tie = b[:, 0] == want[:, 0]
+    for c in range(1, 4):
+        neq = b[:, c] != want[:, c]
+        better |= tie & neq & (b[:, c] > want[:, c])
+        tie &= ~neq
+    want[better] = b[better]
+    got, src = a.cuda(), b.cuda()
+    nat.check(lib.tf_raymap_merge_packed(nat.ptr(got), nat.ptr(src), n, nat.stream_handle()), "merge")
+    assert torch.equal(got.cpu(), want)
+
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(3.0, 254, 127)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    tiles = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length)
+             for k in spec.keys]
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 32)
+    for pose in poses[:4]:
+        tf.integrate_volumes(tiles, demo_scene().render_depth(pose, intr), pose, intr, params)
+    rm = tf.RayMap.empty(intr)
+    tf.raycast_volumes(tiles, poses[5], intr, rm, params)
+    assert torch.isfinite(rm.distance_dev).sum().item() > 10000
+    vert = torch.full_like(rm.vertices_dev, 7.0)
+    h = intr.height
+    nat.check(lib.tf_raymap_vertices(nat.ptr(rm.distance_dev), 1, nat.ptr(vert), nat.camera(intr),
+                                     nat.mat9(poses[5].rotation), nat.vec3(poses[5].translation), 0, h,
+                                     nat.stream_handle()), "vertices")
+    assert torch.equal(vert, rm.vertices_dev)
+    # a row block alone, from a strided (packed) distance view
+    packed = torch.cat([rm.distance_dev[..., None], rm.normals_dev], -1).contiguous()
+    blk = torch.zeros((100, intr.width, 3), dtype=torch.float64, device="cuda")
+    nat.check(lib.tf_raymap_vertices(nat.ptr(packed[200]), 4, nat.ptr(blk), nat.camera(intr),
+                                     nat.mat9(poses[5].rotation), nat.vec3(poses[5].translation), 200,
+                                     100, nat.stream_handle()), "vertices block")
+    assert torch.equal(blk, rm.vertices_dev[200:300])
+
+
 def test_fast_screen_equals_exact_path_full_size():
     """Config-3 volumes: the float32-screened kernel == reference-order float64 kernel."""
     intr = tf.RunConfig().intrinsics()
