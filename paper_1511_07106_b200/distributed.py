@@ -2,9 +2,9 @@
 
 The paper's CPU<->GPU volume swapping becomes ownership:
 
-* every active volume is owned by exactly one rank (``owner_of``: the i-th
-  allocated key goes to rank i mod world, deterministic and balanced by
-  count);
+* every active volume is owned by exactly one rank (``owned_keys``: contiguous
+  chunks of a checkerboard "spread" order of the keys, deterministic and
+  balanced by count, mixing busy and quiet regions of the map);
 * each frame's depth is broadcast from rank 0 (``broadcast_frame``) and each
   rank integrates only its own volumes — integration has no data-path
   collective;
@@ -39,12 +39,35 @@ from .tsdf import FusionParams, RayMap, TsdfSubvolume, integrate_volumes, raycas
 
 
 def owner_of(index: int, world: int) -> int:
-    """Rank owning the index-th allocated volume."""
+    """Rank owning the index-th allocated volume (round-robin)."""
     return index % world
 
 
+def spread_order(keys: Sequence) -> list:
+    """Keys reordered so that contiguous chunks mix the regions of the map.
+
+    Tiles of a scene are not equally busy (a floor, an object fill some of
+    them), and neighbours tend to be alike; chunking keys in checkerboard order
+    (parity of the tile's grid coordinates, then x, y, z) gives every rank a
+    spread of the map: with the 2x2x2 grid of config 3, 2 ranks each get one
+    tile of every (y, z) row and 4 ranks each get one tile per y and per z
+    layer, instead of whole layers.
+    """
+    keys = list(keys)
+    if not all(isinstance(k, tuple) and len(k) == 3 for k in keys):
+        return keys  # not grid keys: allocation order
+    axes = [sorted({k[a] for k in keys}) for a in range(3)]
+    grid = [tuple(axes[a].index(k[a]) for a in range(3)) for k in keys]
+    order = sorted(range(len(keys)), key=lambda i: (sum(grid[i]) % 2, grid[i]))
+    return [keys[i] for i in order]
+
+
 def owned_keys(keys: Sequence, rank: int, world: int) -> list:
-    return [k for i, k in enumerate(keys) if owner_of(i, world) == rank]
+    """This rank's keys: a contiguous chunk of the spread order, in allocation order."""
+    spread = spread_order(keys)
+    n = len(spread)
+    mine = {spread[i] for i in range(n) if i * world // n == rank} if n else set()
+    return [k for k in keys if k in mine]
 
 
 def broadcast_frame(depth: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:

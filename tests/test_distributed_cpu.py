@@ -129,12 +129,25 @@ def _worker(rank, world, port, out):
 
 def test_owner_partition_covers_every_volume_once():
     keys = [(i, 0, 0) for i in range(11)]
-    for world in (1, 2, 4, 8):
-        owned = [owned_keys(keys, r, world) for r in range(world)]
-        flat = [k for o in owned for k in o]
-        assert sorted(flat) == sorted(keys)
-        assert max(map(len, owned)) - min(map(len, owned)) <= 1
-        assert all(owner_of(i, world) == i % world for i in range(11))
+    grid = [(x, y, z) for x in (-511, -1) for y in (-511, -1) for z in (0, 510)]  # config 3
+    for ks in (keys, grid):
+        for world in (1, 2, 3, 4, 8):
+            owned = [owned_keys(ks, r, world) for r in range(world)]
+            flat = [k for o in owned for k in o]
+            assert sorted(flat) == sorted(ks)
+            assert max(map(len, owned)) - min(map(len, owned)) <= 1
+            for o in owned:  # allocation order kept within a rank
+                assert o == [k for k in ks if k in o]
+    assert all(owner_of(i, 4) == i % 4 for i in range(11))
+    # config 3 on 2 ranks: each rank gets one tile of every (y, z) row; on 4
+    # ranks one tile per y layer and per z layer
+    for world, axes in ((2, (1, 2)), (4, (1,))):
+        for r in range(world):
+            mine = owned_keys(grid, r, world)
+            for a in axes:
+                assert len({k[a] for k in mine}) == 2
+    for r in range(4):
+        assert len({k[2] for k in owned_keys(grid, r, 4)}) == 2
 
 
 def test_gloo_world2_broadcast_gather_merge():
