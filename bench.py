@@ -9,7 +9,7 @@ floor + box) along orbit_trajectory((0,0,1.5), 1.5, 64), ground-truth poses.
 One step = one frame through the hot path: fused integration of every
 volume + fused raycast of every volume (+ all-gather / _hit_wins merge of
 the partial ray maps across ranks when N > 1).  With N GPUs the 8 volumes
-are owned round-robin by the ranks (total work fixed -> "strong").
+are owned by the ranks in checkerboard-spread chunks (total work fixed -> "strong").
 
 value  = voxel updates per frame x frames/s, inputs resident in HBM, CUDA
          events on the launching stream, L2 flushed (256 MiB write) between
@@ -81,7 +81,7 @@ def config_desc(n_gpus: int) -> dict:
                         "510)), 640x480 demo-scene orbit frames, ground-truth poses; step = "
                         "integrate + raycast of every volume",
             "volumes": 8, "voxels_per_side": 512, "voxel_size_m": 0.004, "image": "640x480",
-            "ownership": f"round-robin over {n_gpus} rank(s)",
+            "ownership": f"checkerboard-spread chunks over {n_gpus} rank(s) (distributed.owned_keys)",
             "l2": "flushed between timed steps (256 MiB write); volumes 8.6 GB > L2"}
 
 
