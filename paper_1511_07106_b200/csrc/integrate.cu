@@ -906,7 +906,7 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
         const unsigned long long e = queue[i];
         const int v = (int)(e >> 40);
         const int64_t lin = (int64_t)(e & ((1ull << 40) - 1));
-        const TfVolume vol = vt.vol[v];
+        const TfVolume &vol = vt.vol[v];
         const int64_t n = vol.n;
         const int64_t x = lin % n, y = (lin / n) % n, z = lin / (n * n);
         const double vs = vol.voxel_size;
@@ -1272,7 +1272,7 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
                 vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap,
                 fixed_point, (unsigned long long *)stats);
             if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
-            exact_queue_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, f, table, queue, qcount,
+            exact_queue_kernel<<<(unsigned)sms * 16, 256, 0, stream>>>(vt, f, table, queue, qcount,
                                                                      L.queue_cap,
                                                                      (unsigned long long *)stats);
             if ((rc = tf_check_launch("exact_queue_kernel"))) return rc;
