@@ -21,6 +21,8 @@
 
 #include "tf_common.cuh"
 
+#include <mutex>
+
 namespace tf {
 
 struct RayGeom {
@@ -1174,6 +1176,45 @@ __global__ void raymap_vertices_kernel(const __grid_constant__ RayGeom g, const 
 
 using namespace tf;
 
+// Rescue list of the cooperative pass: one persistent buffer per (device,
+// stream), grown on demand — launches on one stream are ordered, launches on
+// different streams never share a buffer, and no allocation sits on the
+// per-frame path (a stream-ordered pool would hand memory back to the driver
+// at every host synchronisation).
+static unsigned *rescue_buffer(cudaStream_t stream, int64_t words) {
+    struct Buf {
+        int dev;
+        cudaStream_t stream;
+        unsigned *ptr;
+        int64_t words;
+    };
+    static std::mutex mu;
+    static Buf bufs[64];
+    static int nbufs = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    Buf *b = nullptr;
+    for (int i = 0; i < nbufs; ++i)
+        if (bufs[i].dev == dev && bufs[i].stream == stream) b = &bufs[i];
+    if (!b) {
+        if (nbufs == 64) return nullptr;
+        b = &bufs[nbufs++];
+        *b = Buf{dev, stream, nullptr, 0};
+    }
+    if (b->words < words) {
+        if (b->ptr) {
+            cudaStreamSynchronize(stream);  // the old buffer may still be in use on this stream
+            cudaFree(b->ptr);
+            b->ptr = nullptr;
+            b->words = 0;
+        }
+        if (cudaMalloc((void **)&b->ptr, (size_t)words * sizeof(unsigned)) != cudaSuccess) return nullptr;
+        b->words = words;
+    }
+    return b->ptr;
+}
+
 extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
                           int64_t coarse_step, const double r_wc[9], const double cam_center[3],
                           double *dist, double *vert, double *norm, uint64_t *stats,
@@ -1222,9 +1263,8 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
         unsigned long long *st = (unsigned long long *)stats;
         int64_t *clk = tf_ray_clock_buffer();
         const int64_t npix = cam->width * cam->height;
-        unsigned *rescue = nullptr;  // [0] = count, then pixel indices
-        if (cudaMallocAsync((void **)&rescue, (size_t)(npix + 1) * sizeof(unsigned), stream) != cudaSuccess ||
-            cudaMemsetAsync(rescue, 0, sizeof(unsigned), stream) != cudaSuccess)
+        unsigned *rescue = rescue_buffer(stream, npix + 1);  // [0] = count, then pixel indices
+        if (!rescue || cudaMemsetAsync(rescue, 0, sizeof(unsigned), stream) != cudaSuccess)
             return tf_set_error(TF_ECUDA, "tf_raycast: cannot allocate the rescue list");
         auto launch = [&](auto kern, int bx, int by) {
             dim3 grid((unsigned)((cam->width + bx - 1) / bx), (unsigned)((cam->height + by - 1) / by));
@@ -1248,7 +1288,6 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
                                                                      rescue);
             if ((rc = tf_check_launch("raycast_coop_kernel"))) return rc;
         }
-        cudaFreeAsync(rescue, stream);
         tf_profile_end(prof, stream);
     }
     return TF_OK;
