@@ -239,7 +239,10 @@ def device_depth(frame) -> torch.Tensor:
     upload once and pass the tensor.
     """
     if isinstance(frame, torch.Tensor):
-        t = frame.to(device=nat.device(), dtype=torch.float64)
+        # pinned host frames upload without blocking the host (stream-ordered;
+        # torch's pinned allocator keeps the buffer alive until the copy ran)
+        t = frame.to(device=nat.device(), dtype=torch.float64,
+                     non_blocking=frame.device.type == "cpu" and frame.is_pinned())
         return t.contiguous()
     data = frame.data if isinstance(frame, DepthFrame) else np.asarray(frame, dtype=np.float64)
     host = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64))
