@@ -257,6 +257,23 @@ def run_ours(args) -> None:
     ray_achieved = (64.0 * evaluated / max(ray_launches, 1)) / (ray_ms / max(ray_launches, 1) / 1e3) / 1e9 \
         if ray_ms > 0 else 0.0
 
+    # per-kernel sub-rooflines of the update bracket (16 B per update each)
+    def comp(kind, n_updates):
+        ms, n = prof[kind]
+        if ms <= 0:
+            return None
+        gbs = BYTES_PER_UPDATE * n_updates / (ms / 1e3) / 1e9
+        return {"ms_per_launch": ms / max(n, 1), "updates_per_launch": n_updates / max(n, 1),
+                "achieved_gbs": gbs, "frac": gbs / peak if peak else None}
+    free_upd = int(st[nat.STAT_FREE_KERNEL_UPDATES])
+    exact_upd = int(st[nat.STAT_EXACT_UPDATES])
+    components = {
+        "brick_free_kernel (certified free-space bricks, bandwidth-bound)": comp("integrate_free", free_upd),
+        "brick_update_kernel (general bricks: float32 screen + exact FP64 update)":
+            comp("integrate_general", updates_local - free_upd - exact_upd),
+        "exact_queue_kernel (near-surface band, reference arithmetic)": comp("integrate_exact", exact_upd),
+    }
+
     result = {
         "metric": METRIC, "value": value, "unit": "voxel-updates/s",
         "frames_per_s": fps, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -269,7 +286,8 @@ def run_ours(args) -> None:
                                "exact_queue_kernel, TF_PROF_INTEGRATE_UPDATE)", "peak_source": peak_src,
                      "bytes_per_update": BYTES_PER_UPDATE,
                      "launches": upd_launches, "kernel_ms_per_launch": upd_ms / max(upd_launches, 1),
-                     "updates_per_launch": updates_local / max(upd_launches, 1)},
+                     "updates_per_launch": updates_local / max(upd_launches, 1),
+                     "components": components},
         "roofline_raycast": {"bound": "latency (dependent gathers, divergence); not hbm",
                              "achieved": ray_achieved, "peak": peak, "unit": "GB/s",
                              "frac": ray_achieved / peak if peak else None, "traffic": ray_traffic,
@@ -285,12 +303,14 @@ def run_ours(args) -> None:
                       "depth_rejected_per_frame": sum_over_ranks(int(st[nat.STAT_DEPTH_SKIPPED])) / args.steps,
                       "active_bricks_per_frame": sum_over_ranks(int(st[nat.STAT_ACTIVE_BRICKS])) / args.steps,
                       "free_space_bricks_per_frame": sum_over_ranks(int(st[nat.STAT_FREE_BRICKS])) / args.steps,
+                      "general_bricks_all_free_per_frame": sum_over_ranks(int(st[nat.STAT_GENERAL_ALL_FREE])) / args.steps,
                       "total_bricks": sum_over_ranks(int(st[nat.STAT_TOTAL_BRICKS])) // max(args.steps, 1)},
         "raycast": {"exact_samples_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_SAMPLES])) / args.steps,
                     "certification_failures": sum_over_ranks(int(st[nat.STAT_CERT_FAILURES])),
                     "summary_certified_samples_per_frame": sum_over_ranks(int(st[nat.STAT_SUMMARY_SAMPLES])) / args.steps,
                     "samples_per_frame": samples / args.steps,
                     "coop_rays_per_frame": sum_over_ranks(int(st[nat.STAT_COOP_RAYS])) / args.steps,
+                    "coop_pass_ms_per_frame": prof["raycast_coop"][0] / args.steps,
                     "samples_per_s": samples / (ms_total / 1e3)},
         "gpu_launches": int(launches),
     }

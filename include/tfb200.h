@@ -93,7 +93,9 @@ enum {
     TF_STAT_SUMMARY_SAMPLES = 13, /* ray samples certified by the brick summary alone */
     TF_STAT_GENERAL_ALL_FREE = 14, /* general-path bricks whose voxels all turned out free space */
     TF_STAT_COOP_RAYS = 15,   /* rays finished by the warp-cooperative raycast pass */
-    TF_STAT_COUNT = 16
+    TF_STAT_FREE_KERNEL_UPDATES = 16, /* voxel updates by the certified free-space brick kernel */
+    TF_STAT_EXACT_UPDATES = 17,       /* voxel updates by the exact (reference arithmetic) queue */
+    TF_STAT_COUNT = 24
 };
 
 int tf_abi_version(void);
@@ -105,7 +107,8 @@ const char *tf_last_error(void);
  * them and returns summed milliseconds and launch counts per kind:
  * 0 = integration voxel-update kernel, 1 = whole tf_integrate, 2 = raycast. */
 enum { TF_PROF_INTEGRATE_UPDATE = 0, TF_PROF_INTEGRATE_ALL = 1, TF_PROF_RAYCAST = 2,
-       TF_PROF_KINDS = 3 };
+       TF_PROF_INTEGRATE_FREE = 3, TF_PROF_INTEGRATE_GENERAL = 4, TF_PROF_INTEGRATE_EXACT = 5,
+       TF_PROF_RAYCAST_COOP = 6, TF_PROF_KINDS = 7 };
 uint64_t tf_launch_count(void);
 /* Debug: when set (device int64[12*H*W] per raycast call), tf_raycast writes per
  * pixel {SM clock cycles, samples, exact samples, summary-certified samples,

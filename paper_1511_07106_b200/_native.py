@@ -43,7 +43,7 @@ DEBUG_EXACT_ONLY = 2
 DEBUG_NO_FIXEDPOINT = 4
 DEBUG_LANE0_ONLY = 8
 DEBUG_COOP_ALL = 16
-PROF_INTEGRATE_UPDATE, PROF_INTEGRATE_ALL, PROF_RAYCAST, PROF_KINDS = 0, 1, 2, 3
+PROF_INTEGRATE_UPDATE, PROF_INTEGRATE_ALL, PROF_RAYCAST, PROF_KINDS = 0, 1, 2, 7
 
 
 def profile_read() -> dict:
@@ -51,7 +51,8 @@ def profile_read() -> dict:
     ms = (ctypes.c_double * PROF_KINDS)()
     cnt = (ctypes.c_int64 * PROF_KINDS)()
     check(lib().tf_profile_read(ms, cnt, PROF_KINDS), "tf_profile_read")
-    names = ("integrate_update", "integrate_all", "raycast")
+    names = ("integrate_update", "integrate_all", "raycast", "integrate_free", "integrate_general",
+             "integrate_exact", "raycast_coop")
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(names)}
 
 # TF_STAT_* slots (tfb200.h)
@@ -62,7 +63,9 @@ STAT_CERT_FAILURES = 12
 STAT_SUMMARY_SAMPLES = 13
 STAT_GENERAL_ALL_FREE = 14
 STAT_COOP_RAYS = 15
-STAT_COUNT = 16
+STAT_FREE_KERNEL_UPDATES = 16
+STAT_EXACT_UPDATES = 17
+STAT_COUNT = 24
 
 _VOL = ctypes.POINTER(TfVolume)
 _CAM = ctypes.POINTER(TfCamera)

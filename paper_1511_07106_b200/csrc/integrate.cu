@@ -532,6 +532,7 @@ __global__ void __launch_bounds__(256) brick_free_kernel(
     }
     if (stats) {
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
+        warp_count_add(&stats[TF_STAT_FREE_KERNEL_UPDATES], updates);
         warp_count_add(&stats[TF_STAT_SWEPT_VOXELS], updates);
         warp_count_add(&stats[TF_STAT_NOOP_UPDATES], nop);
     }
@@ -704,7 +705,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const float hw = 0.5f * f.w32, hh = 0.5f * f.h32;
     const float k3u = 9.6e-7f * f.fx32, k3v = 9.6e-7f * f.fy32;
     const float k2u = 9.6e-7f * (fabsf(f.cx32) + 2.f), k2v = 9.6e-7f * (fabsf(f.cy32) + 2.f);
-    unsigned updates = 0, swept = 0, nop = 0, col_skipped = 0, depth_skipped = 0;
+    unsigned updates = 0, swept = 0, nop = 0, col_skipped = 0, depth_skipped = 0, all_free = 0;
     for (unsigned i = warp; i < count; i += nwarps) {
         const unsigned g = active[i];
         const int vi = find_volume(bt, g);
@@ -726,6 +727,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         const float zspan = (float)(nz - 1);
         const bool keep = keeps_summary(vol, f);
         unsigned dbad = 0;  // change of this brick's packed state (summary)
+        unsigned brick_free = 0, brick_vox = 0;  // free-space class / voxels of this brick (lane)
 #pragma unroll 1
         for (int hy = 0; hy < 2; ++hy) {
             const unsigned y = y_base + 4 * hy;
@@ -766,7 +768,10 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
             } else if (fmaxf(pbz, pz1) + epc < 0.f) {
                 col_live = false;      // whole column behind the camera (:107)
             }
-            if (row_in) swept += nz;
+            if (row_in) {
+                swept += nz;
+                brick_vox += nz;
+            }
             if (row_in && !col_live) col_skipped += nz;
             const float hu = 0.5f - du, hv = 0.5f - dv;
             const bool fast = front && hu > 0.f && hv > 0.f;
@@ -847,6 +852,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                 for (int j = 0; j < kZBatch; ++j) {
                     if (cls[j] == kFree) {
                         ++updates;
+                        ++brick_free;
                         if (fixed_point && old[j].x == fixed.x && old[j].y == fixed.y) {
                             ++nop;  // (tau32, max_w) is a host-verified fixed point
                         } else {
@@ -882,6 +888,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
             for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
             if (lane == 0 && dbad) atomicAdd(&vol.brick_state_dev[local], dbad);
         }
+        if (stats && __reduce_add_sync(0xffffffffu, brick_free) == __reduce_add_sync(0xffffffffu, brick_vox))
+            ++all_free;  // (counted on every lane; lane 0's count is reported)
     }
     if (stats) {
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
@@ -889,6 +897,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         warp_count_add(&stats[TF_STAT_NOOP_UPDATES], nop);
         warp_count_add(&stats[TF_STAT_COL_SKIPPED], col_skipped);
         warp_count_add(&stats[TF_STAT_DEPTH_SKIPPED], depth_skipped);
+        if (lane == 0 && all_free) atomicAdd(&stats[TF_STAT_GENERAL_ALL_FREE], (unsigned long long)all_free);
     }
 }
 
@@ -918,6 +927,7 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
     }
     if (stats) {
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
+        warp_count_add(&stats[TF_STAT_EXACT_UPDATES], updates);
         if (blockIdx.x == 0 && threadIdx.x == 0) stats[TF_STAT_EXACT_VOXELS] += *queue_count;
     }
 }
@@ -1263,18 +1273,24 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
             std::unique_lock<std::mutex> side_lock(side->mu);
             cudaEventRecord(side->fork, stream);
             cudaStreamWaitEvent(side->stream, side->fork, 0);
+            void *pf = tf_profile_begin(TF_PROF_INTEGRATE_FREE, side->stream);
             brick_free_kernel<<<(unsigned)sms * 8, 256, 0, side->stream>>>(vt, bt, f, active_free, fcount,
                                                                           fixed_point,
                                                                           (unsigned long long *)stats);
+            tf_profile_end(pf, side->stream);
             if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
             cudaEventRecord(side->join, side->stream);
+            void *pg = tf_profile_begin(TF_PROF_INTEGRATE_GENERAL, stream);
             brick_update_kernel<<<(unsigned)sms * 6, 256, 0, stream>>>(
                 vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap,
                 fixed_point, (unsigned long long *)stats);
+            tf_profile_end(pg, stream);
             if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
+            void *pe = tf_profile_begin(TF_PROF_INTEGRATE_EXACT, stream);
             exact_queue_kernel<<<(unsigned)sms * 16, 256, 0, stream>>>(vt, f, table, queue, qcount,
                                                                      L.queue_cap,
                                                                      (unsigned long long *)stats);
+            tf_profile_end(pe, stream);
             if ((rc = tf_check_launch("exact_queue_kernel"))) return rc;
             cudaStreamWaitEvent(stream, side->join, 0);
         }

@@ -1284,8 +1284,10 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
             int dev = 0, sms = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+void *pc = tf_profile_begin(TF_PROF_RAYCAST_COOP, stream);
             raycast_coop_kernel<<<(unsigned)sms * 4, 128, 0, stream>>>(vt, g, dist, vert, norm, st, rescue + 1,
                                                                      rescue);
+            tf_profile_end(pc, stream);
             if ((rc = tf_check_launch("raycast_coop_kernel"))) return rc;
         }
         tf_profile_end(prof, stream);
