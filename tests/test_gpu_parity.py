@@ -323,6 +323,57 @@ def test_fast_screen_equals_exact_path_full_size():
         assert torch.equal(x.voxels, y.voxels)
 
 
+def test_axis_aligned_rays_and_lattice_plane_cameras():
+    """Degenerate geometry: integer principal point (rays with exactly zero
+    components), axis-aligned camera rotations and camera centres on voxel
+    lattice planes.  Certified raycast == exact march and float32-screened
+    integration == exact integration, bit for bit."""
+    intr = CameraIntrinsics(100.0, 100.0, 80.0, 60.0, 160, 120)
+    spec = tf.init_grid(3.0, 124, 62)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    vs = spec.voxel_size
+    rot_y = lambda deg: tf.Pose(np.array([[np.cos(np.radians(deg)), 0, np.sin(np.radians(deg))],
+                                          [0, 1, 0],
+                                          [-np.sin(np.radians(deg)), 0, np.cos(np.radians(deg))]]),
+                                np.zeros(3)).rotation
+    poses = []
+    for deg, t in ((0, (0.0, 0.0, 0.0)), (90, (-1.5, 0.0, 1.5)), (180, (0.0, 0.0, 3.0)),
+                   (270, (1.5, 0.0, 1.5)), (0, (10 * vs, -5 * vs, 20 * vs))):
+        r = np.round(rot_y(deg), 12)  # exact 0 / +-1 entries
+        poses.append(tf.Pose(r, np.array(t)))
+    scene = demo_scene()
+    a = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in spec.keys]
+    b = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in spec.keys]
+    lib = nat.load_library()
+    stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
+    try:
+        for pose in poses:
+            frame = scene.render_depth(pose, intr)
+            lib.tf_set_debug_flags(0)
+            tf.integrate_volumes(a, frame, pose, intr, params)
+            lib.tf_set_debug_flags(nat.DEBUG_EXACT_ONLY)
+            tf.integrate_volumes(b, frame, pose, intr, params)
+        for x, y in zip(a, b):
+            assert torch.equal(x.voxels, y.voxels)
+        hits = 0
+        for pose in poses:
+            for flag in (0, nat.DEBUG_COOP_ALL):
+                fast = tf.RayMap.empty(intr)
+                lib.tf_set_debug_flags(flag)
+                tf.raycast_volumes(a, pose, intr, fast, params, stats)
+                exact = tf.RayMap.empty(intr)
+                lib.tf_set_debug_flags(nat.DEBUG_EXACT_ONLY)
+                tf.raycast_volumes(a, pose, intr, exact, params)
+                assert torch.equal(fast.distance_dev, exact.distance_dev)
+                assert torch.equal(fast.vertices_dev, exact.vertices_dev)
+                assert torch.equal(fast.normals_dev, exact.normals_dev)
+                hits += torch.isfinite(exact.distance_dev).sum().item()
+    finally:
+        lib.tf_set_debug_flags(0)
+    assert hits > 5000
+    assert stats[nat.STAT_CERT_FAILURES].item() == 0
+
+
 @pytest.mark.parametrize("n", [49, 50])
 def test_odd_and_even_sizes_vs_oracle(n):
     """Partial bricks and the unpaired (odd n) voxel path against the oracle."""
