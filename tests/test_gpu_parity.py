@@ -228,6 +228,35 @@ def test_fused_raycast_equals_per_volume_any_order():
     assert torch.equal(fused.normals_dev, single.normals_dev)
 
 
+def test_more_volumes_than_one_launch_holds():
+    """125 tiles (> TFB200_MAX_VOLUMES_PER_LAUNCH = 64): the chunked fused
+    integrate / raycast equal per-tile calls bit for bit."""
+    intr = CameraIntrinsics(131.25, 131.25, 79.5, 59.5, 160, 120)
+    spec = tf.init_grid(3.0, 100, 20)
+    assert len(spec.keys) == 125
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    fused = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in spec.keys]
+    single = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in spec.keys]
+    scene = demo_scene()
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 16)
+    for pose in poses[:3]:
+        frame = scene.render_depth(pose, intr)
+        tf.integrate_volumes(fused, frame, pose, intr, params)
+        for v in single:
+            tf.integrate(v, frame, pose, intr, params)
+    for x, y in zip(fused, single):
+        assert torch.equal(x.voxels, y.voxels)
+    a = tf.RayMap.empty(intr)
+    tf.raycast_volumes(fused, poses[1], intr, a, params)
+    b = tf.RayMap.empty(intr)
+    for v in single[::-1]:
+        tf.raycast(v, poses[1], intr, b, params)
+    assert np.isfinite(a.distance).sum() > 3000
+    assert torch.equal(a.distance_dev, b.distance_dev)
+    assert torch.equal(a.vertices_dev, b.vertices_dev)
+    assert torch.equal(a.normals_dev, b.normals_dev)
+
+
 def test_trilinear_sample_and_merge():
     g = load_golden("fusion_small.npz")
     n = int(g["n"])
