@@ -115,6 +115,11 @@ uint64_t tf_launch_count(void);
  * region evaluations at brick level by kind 0..3, at superbrick level 0..3};
  * NULL disables. */
 void tf_debug_ray_clock_buffer(int64_t *buffer_dev);
+
+/* Test hook (synchronous): n random (a, b) pairs, b an integer in [1, 256],
+ * through the table-driven correctly rounded division of the running-mean
+ * update vs. IEEE division; returns the number of mismatches (-1 on error). */
+int64_t tf_debug_weight_division_check(int64_t n, uint64_t seed);
 void tf_profile_enable(int on);
 int tf_profile_read(double *ms_by_kind, int64_t *launches_by_kind, int nkinds);
 

@@ -77,6 +77,7 @@ _SIGNATURES = {
     "tf_debug_flags": (ctypes.c_uint32, []),
     "tf_launch_count": (ctypes.c_uint64, []),
     "tf_debug_ray_clock_buffer": (None, [_c_p]),
+    "tf_debug_weight_division_check": (_c_i64, [_c_i64, ctypes.c_uint64]),
     "tf_profile_enable": (None, [_c_int]),
     "tf_profile_read": (_c_int, [_c_p, _c_p, _c_int]),
     "tf_integrate_workspace_size": (_c_sz, [_VOL, _c_int, _CAM]),

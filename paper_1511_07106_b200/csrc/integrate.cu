@@ -447,7 +447,8 @@ __global__ void __launch_bounds__(256) brick_cull_kernel(
     }
 }
 
-__device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f);
+__device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f, const double *rcp);
+__device__ __forceinline__ void fill_rcp(double *rcp);
 __device__ __forceinline__ unsigned free_state_delta(float2 old, float2 nv, float t);
 
 // Certified free-space bricks: every voxel gets the clamped-to-tau running
@@ -459,6 +460,8 @@ __global__ void __launch_bounds__(256) brick_free_kernel(
     const __grid_constant__ FrameGeom f, const uint32_t *__restrict__ list,
     const unsigned int *__restrict__ list_count, const int fixed_point,
     unsigned long long *__restrict__ stats) {
+    __shared__ double rcp[257];
+    fill_rcp(rcp);
     const unsigned count = *list_count;
     const int lane = threadIdx.x & 31;
     const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -497,8 +500,8 @@ __global__ void __launch_bounds__(256) brick_free_kernel(
                     updates += 2;
                     nop += (na ? 1u : 0u) + (nbq ? 1u : 0u);
                     if (na && nbq) continue;  // provably unchanged (host-verified fixed point)
-                    const float2 ua = na ? a : free_update(a, f);
-                    const float2 ub = nbq ? b : free_update(b, f);
+                    const float2 ua = na ? a : free_update(a, f, rcp);
+                    const float2 ub = nbq ? b : free_update(b, f, rcp);
                     if (keep) dbad += free_state_delta(a, ua, f.good_t) + free_state_delta(b, ub, f.good_t);
                     *reinterpret_cast<float4 *>(vox + lin[k]) = make_float4(ua.x, ua.y, ub.x, ub.y);
                 }
@@ -518,7 +521,7 @@ __global__ void __launch_bounds__(256) brick_free_kernel(
                         ++nop;
                         continue;
                     }
-                    const float2 ua = free_update(a, f);
+                    const float2 ua = free_update(a, f, rcp);
                     if (keep) dbad += free_state_delta(a, ua, f.good_t);
                     vox[lin] = ua;
                 }
@@ -672,13 +675,59 @@ __device__ __forceinline__ unsigned free_state_delta(float2 old, float2 nv, floa
     return (new_bad - old_bad) + ((1u - was_obs) << 16);
 }
 
+// a / b correctly rounded for the running-mean denominator b = w + sw.  When
+// b is an integer in [1, 256] (integral weights, the reference default), one
+// multiplication by RN(1/b) from a per-block table and one fused correction:
+// q = RN(a r), e = a - q b (exact with FMA), RN(q + e r) — Markstein's
+// theorem (r within 1/2 ulp of 1/b, q within 1 ulp of a/b) makes the result
+// RN(a / b), the IEEE quotient, as long as nothing underflows (|a| >= 2^-900
+// guards that).  Any other b takes the IEEE division.  Checked against
+// __ddiv_rn by tf_debug_weight_division_check (GPU test).
+__device__ __forceinline__ double div_weight(double a, double b, const double *__restrict__ rcp) {
+    const int bi = __double2int_rz(b);
+    if (bi >= 1 && bi <= 256 && (double)bi == b && fabs(a) >= 0x1p-900) {
+        const double r = rcp[bi];
+        const double q = dmul(a, r);
+        const double e = __fma_rn(-q, b, a);
+        return __fma_rn(e, r, q);
+    }
+    return ddiv(a, b);
+}
+
+// RN(1/b) for b = 0..256 into shared memory (entry 0 unused); every thread of
+// the block must call it
+__device__ __forceinline__ void fill_rcp(double *rcp) {
+    for (int b = threadIdx.x; b <= 256; b += blockDim.x) rcp[b] = b ? __drcp_rn((double)b) : 0.0;
+    __syncthreads();
+}
+
 // running weighted mean with clamped == tau (_kernels.py:129-133)
-__device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f) {
+__device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f, const double *rcp) {
     const float wv = fmulr(old.y, old.x);
     const double w_sum = dadd((double)old.y, f.sw);
-    const double t_new = ddiv(dadd((double)wv, f.sw_tau), w_sum);
+    const double t_new = div_weight(dadd((double)wv, f.sw_tau), w_sum, rcp);
     const double w_new = f.max_w < w_sum ? f.max_w : w_sum;
     return make_float2(__double2float_rn(t_new), __double2float_rn(w_new));
+}
+
+// test hook: random (a, b) pairs through div_weight vs __ddiv_rn
+__global__ void weight_division_check_kernel(int64_t n, unsigned long long seed, unsigned long long *mismatches) {
+    __shared__ double rcp[257];
+    fill_rcp(rcp);
+    unsigned long long bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long x = seed ^ (0x9E3779B97F4A7C15ull * (unsigned long long)(i + 1));
+        x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 27; x *= 0x94D049BB133111EBull; x ^= x >> 33;
+        const double b = (double)(1 + (x & 255u));
+        // a: random 52-bit mantissa, exponent in [-40, 12), random sign
+        const int ex = (int)((x >> 8) % 52u) - 40;
+        const unsigned long long m = (x >> 14) | 0x10000000000000ull;
+        double a = ldexp((double)(m & 0x1FFFFFFFFFFFFFull), ex - 52);
+        if (x & (1ull << 63)) a = -a;
+        const double got = div_weight(a, b, rcp), want = __ddiv_rn(a, b);
+        bad += __double_as_longlong(got) != __double_as_longlong(want);
+    }
+    if (bad) atomicAdd(mismatches, bad);
 }
 
 constexpr int kZBatch = 4;  // voxels in flight per thread
@@ -695,6 +744,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const unsigned int *__restrict__ active_count, unsigned long long *__restrict__ queue,
     unsigned long long *__restrict__ queue_count, const unsigned long long queue_cap,
     const int fixed_point, unsigned long long *__restrict__ stats) {
+    __shared__ double rcp[257];
+    fill_rcp(rcp);
     const unsigned count = *active_count;
     const int lane = threadIdx.x & 31;
     const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -856,7 +907,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                         if (fixed_point && old[j].x == fixed.x && old[j].y == fixed.y) {
                             ++nop;  // (tau32, max_w) is a host-verified fixed point
                         } else {
-                            const float2 nv = free_update(old[j], f);
+                            const float2 nv = free_update(old[j], f, rcp);
                             vox[(size_t)row + (size_t)j * n * n] = nv;
                             if (keep) dbad += free_state_delta(old[j], nv, f.good_t);
                         }
@@ -1337,4 +1388,15 @@ extern "C" int tf_brick_summary(const TfVolume *vol, void *stream_) {
     FrameGeom f{};
     super_flags_kernel<<<(unsigned)sms * 2, 256, 0, (cudaStream_t)stream_>>>(vt, f, 0);
     return tf_check_launch("super_flags_kernel");
+}
+
+extern "C" int64_t tf_debug_weight_division_check(int64_t n, uint64_t seed) {
+    unsigned long long *d = nullptr, h = 0;
+    if (n <= 0) return 0;
+    if (cudaMalloc(&d, sizeof(h)) != cudaSuccess) return -1;
+    cudaMemset(d, 0, sizeof(h));
+    weight_division_check_kernel<<<1184, 256>>>(n, seed, d);
+    const bool ok = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(d);
+    return ok ? (int64_t)h : -1;
 }

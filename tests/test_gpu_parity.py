@@ -228,6 +228,14 @@ def test_fused_raycast_equals_per_volume_any_order():
     assert torch.equal(fused.normals_dev, single.normals_dev)
 
 
+def test_table_division_is_ieee():
+    """The running-mean division by integral weights (table reciprocal + FMA
+    correction) equals IEEE division on 400 M random pairs."""
+    lib = nat.load_library()
+    for seed in (1, 2, 3, 4):
+        assert lib.tf_debug_weight_division_check(100_000_000, seed) == 0
+
+
 def test_more_volumes_than_one_launch_holds():
     """125 tiles (> TFB200_MAX_VOLUMES_PER_LAUNCH = 64): the chunked fused
     integrate / raycast equal per-tile calls bit for bit."""
