@@ -161,9 +161,17 @@ def run_ours(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TFB200_BENCH_FUNCTIONAL=1: every rank on cuda:0 over gloo — a functional
+    # check of the N > 1 path on a one-GPU box; its timings mean nothing
+    functional = os.environ.get("TFB200_BENCH_FUNCTIONAL") == "1"
+    if functional:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_1511_07106_b200 as tf
     from paper_1511_07106_b200 import _native as nat
