@@ -209,6 +209,26 @@ int tf_icp_reduce(const double *src_verts_dev, const double *src_norms_dev,
                   void *workspace_dev, size_t workspace_bytes, double *out29_dev,
                   void *stream);
 
+/* Device-resident track() (tracking.py:123-196): the whole pyramid, coarsest
+ * level first, iterations[l] steps per level, queued without host round trips.
+ * Per step: icp_terms (as tf_icp_reduce) and one single-warp kernel doing the
+ * host part of _solve_step (:100-120: pair minimum min_pairs[l], cond > 1e12
+ * gate, LU solve, finiteness) and the pose update (:178-183: Rodrigues,
+ * re-orthonormalisation, |delta| < step_eps ends the level).  state_dev
+ * (tf_icp_track_state_size() bytes) receives doubles {R[9] row-major, t[3],
+ * lost, count, rms, scratch}: the refined estimate, or lost = 1 (the caller
+ * then keeps its seed, :187-193); count / rms of the last successful step.
+ * Level l's source maps are src_*[l] (tf_vertex_normal_map at level l). */
+size_t tf_icp_track_state_size(void);
+int tf_icp_track(int nlevels, const double *const *src_verts_dev, const double *const *src_norms_dev,
+                 const uint8_t *const *src_valid_dev, const TfCamera *level_cams,
+                 const int *iterations, const int *min_pairs, const double *mdl_dist_dev,
+                 const double *mdl_vert_dev, const double *mdl_norm_dev, int64_t mdl_full_width,
+                 int64_t mdl_full_height, const double r_ref[9], const double t_ref[3],
+                 const double r_init[9], const double t_init[3], double max_dist_sq, double cos_min,
+                 double step_eps, void *workspace_dev, size_t workspace_bytes, double *state_dev,
+                 void *stream);
+
 /* ---- extraction: _kernels.extract_bound / extract_kernel
  * (_kernels.py:454-578), called by tsdf.extract_points (tsdf.py:261-280).
  * Two calls: tf_extract_count writes the vertex count (device int64) after an

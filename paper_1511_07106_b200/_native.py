@@ -77,6 +77,10 @@ _SIGNATURES = {
     "tf_debug_flags": (ctypes.c_uint32, []),
     "tf_launch_count": (ctypes.c_uint64, []),
     "tf_debug_ray_clock_buffer": (None, [_c_p]),
+    "tf_icp_track_state_size": (ctypes.c_size_t, []),
+    "tf_icp_track": (_c_int, [ctypes.c_int, _c_p, _c_p, _c_p, ctypes.POINTER(TfCamera), _c_p, _c_p,
+                              _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_d, _c_d,
+                              _c_d, _c_p, ctypes.c_size_t, _c_p, _c_p]),
     "tf_debug_weight_division_check": (_c_i64, [_c_i64, ctypes.c_uint64]),
     "tf_profile_enable": (None, [_c_int]),
     "tf_profile_read": (_c_int, [_c_p, _c_p, _c_int]),

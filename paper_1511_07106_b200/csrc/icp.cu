@@ -109,7 +109,13 @@ struct IcpParams {
     int64_t src_w, src_h, mdl_w, mdl_h;
     int stride;
     double max_d2, cos_min;
+    const double *state;  // device-resident tracking: estimate + flags (kSt*), else null
 };
+
+// device tracking state (doubles): estimate R (row-major) and t, flags, last
+// successful step's count and rms
+enum : int { kStR = 0, kStT = 9, kStLost = 12, kStCount = 13, kStRms = 14, kStLevelDone = 15,
+             kStSize = 16 };
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -124,13 +130,24 @@ __global__ void __launch_bounds__(kIcpThreads) icp_terms_kernel(
     const int64_t npix = P.src_w * P.src_h;
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double a[6] = {0, 0, 0, 0, 0, 0}, r = 0.0, cnt = 0.0;
+    double Re[9], te[3];
+    bool live = true;
+    if (P.state) {  // device-resident tracking: nothing to do once lost or converged
+        live = P.state[kStLost] == 0.0 && P.state[kStLevelDone] == 0.0;
+        for (int i = 0; i < 9; ++i) Re[i] = P.state[kStR + i];
+        for (int i = 0; i < 3; ++i) te[i] = P.state[kStT + i];
+    } else {
+        for (int i = 0; i < 9; ++i) Re[i] = P.r_est.m[i];
+        for (int i = 0; i < 3; ++i) te[i] = P.t_est.v[i];
+    }
+    if (!live) return;
     if (p < npix && sok[p]) {
         const double s[3] = {sv[3 * p], sv[3 * p + 1], sv[3 * p + 2]};
         const double snr[3] = {sn[3 * p], sn[3 * p + 1], sn[3 * p + 2]};
         double pw[3], nw[3], pr[3];
-        rot_apply(P.r_est.m, s, pw);                                  // :76
-        for (int i = 0; i < 3; ++i) pw[i] = dadd(pw[i], P.t_est.v[i]);
-        rot_apply(P.r_est.m, snr, nw);                                // :77
+        rot_apply(Re, s, pw);                                         // :76
+        for (int i = 0; i < 3; ++i) pw[i] = dadd(pw[i], te[i]);
+        rot_apply(Re, snr, nw);                                       // :77
         rot_apply(P.r_ref.m, pw, pr);                                 // :80
         for (int i = 0; i < 3; ++i) pr[i] = dadd(pr[i], P.t_ref.v[i]);
         const double z = pr[2];
@@ -206,6 +223,213 @@ __global__ void icp_finish_kernel(const double *__restrict__ partials, int64_t n
     if (lane == 0) out[k] = s;
 }
 
+
+// ---- device-resident tracking (track(), tracking.py:123-196) --------------
+//
+// One single-warp kernel per ICP iteration folds the block partials (same
+// fixed order as icp_finish_kernel) and does the host part of _solve_step
+// (tracking.py:100-120) and the pose update (:178-183) in FP64 on the device:
+// pair minimum, cond(A^T A) > 1e12 gate, LU solve with partial pivoting (as
+// LAPACK gesv), finiteness, Rodrigues, re-orthonormalisation to the polar
+// factor (the U V^T of the reference's SVD), convergence test.  No host round
+// trip per iteration: the whole pyramid is queued at once and later kernels
+// return immediately once the state says lost / level converged.  Deltas
+// agree with numpy to rounding (the parity bar for ICP is 1e-5 m / 1e-6 rad;
+// counts are exact).
+
+// 6x6 symmetric Jacobi eigenvalues (rare path: only when the cheap bound
+// cannot decide the conditioning gate)
+__device__ void sym6_eigenvalues(const double A[36], double ev[6]) {
+    double a[36];
+    for (int i = 0; i < 36; ++i) a[i] = A[i];
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        double off = 0.0;
+        for (int pp = 0; pp < 6; ++pp)
+            for (int q = pp + 1; q < 6; ++q) off += a[pp * 6 + q] * a[pp * 6 + q];
+        if (off == 0.0) break;
+        for (int pp = 0; pp < 6; ++pp)
+            for (int q = pp + 1; q < 6; ++q) {
+                const double apq = a[pp * 6 + q];
+                if (apq == 0.0) continue;
+                const double theta = (a[q * 6 + q] - a[pp * 6 + pp]) / (2.0 * apq);
+                const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+                for (int k = 0; k < 6; ++k) {  // columns p, q
+                    const double akp = a[k * 6 + pp], akq = a[k * 6 + q];
+                    a[k * 6 + pp] = c * akp - sn * akq;
+                    a[k * 6 + q] = sn * akp + c * akq;
+                }
+                for (int k = 0; k < 6; ++k) {  // rows p, q
+                    const double apk = a[pp * 6 + k], aqk = a[q * 6 + k];
+                    a[pp * 6 + k] = c * apk - sn * aqk;
+                    a[q * 6 + k] = sn * apk + c * aqk;
+                }
+            }
+    }
+    for (int i = 0; i < 6; ++i) ev[i] = a[i * 6 + i];
+}
+
+// LU with partial pivoting of A (in place) -> false if singular
+__device__ bool lu6(double A[36], int piv[6]) {
+    for (int k = 0; k < 6; ++k) {
+        int m = k;
+        for (int i = k + 1; i < 6; ++i)
+            if (fabs(A[i * 6 + k]) > fabs(A[m * 6 + k])) m = i;
+        piv[k] = m;
+        if (A[m * 6 + k] == 0.0) return false;
+        if (m != k)
+            for (int j = 0; j < 6; ++j) {
+                const double t = A[k * 6 + j];
+                A[k * 6 + j] = A[m * 6 + j];
+                A[m * 6 + j] = t;
+            }
+        const double inv = 1.0 / A[k * 6 + k];
+        for (int i = k + 1; i < 6; ++i) {
+            const double l = A[i * 6 + k] * inv;
+            A[i * 6 + k] = l;
+            for (int j = k + 1; j < 6; ++j) A[i * 6 + j] -= l * A[k * 6 + j];
+        }
+    }
+    return true;
+}
+
+__device__ void lu6_solve(const double LU[36], const int piv[6], double b[6]) {
+    for (int k = 0; k < 6; ++k)
+        if (piv[k] != k) {
+            const double t = b[k];
+            b[k] = b[piv[k]];
+            b[piv[k]] = t;
+        }
+    for (int i = 1; i < 6; ++i)
+        for (int j = 0; j < i; ++j) b[i] -= LU[i * 6 + j] * b[j];
+    for (int i = 5; i >= 0; --i) {
+        for (int j = i + 1; j < 6; ++j) b[i] -= LU[i * 6 + j] * b[j];
+        b[i] /= LU[i * 6 + i];
+    }
+}
+
+// np.linalg.cond(A) > 1e12 for symmetric positive semi-definite A; LU of A
+// given.  ||A||_F ||A^-1||_F >= cond_2 >= it / 6 decides almost every case;
+// the rest (and any doubt) takes the Jacobi eigenvalues.
+__device__ bool ill_conditioned(const double A[36], const double LU[36], const int piv[6]) {
+    double fa = 0.0, fi = 0.0;
+    for (int i = 0; i < 36; ++i) fa += A[i] * A[i];
+    for (int c = 0; c < 6; ++c) {
+        double e[6] = {0, 0, 0, 0, 0, 0};
+        e[c] = 1.0;
+        lu6_solve(LU, piv, e);
+        for (int i = 0; i < 6; ++i) fi += e[i] * e[i];
+    }
+    const double upper = sqrt(fa) * sqrt(fi);
+    if (isfinite(upper) && upper <= 1.0e12 * (1.0 - 1e-9)) return false;
+    if (isfinite(upper) && upper / 6.0 > 1.0e12 * (1.0 + 1e-9)) return true;
+    double ev[6];
+    sym6_eigenvalues(A, ev);
+    double lo = fabs(ev[0]), hi = fabs(ev[0]);
+    for (int i = 1; i < 6; ++i) {
+        lo = fmin(lo, fabs(ev[i]));
+        hi = fmax(hi, fabs(ev[i]));
+    }
+    return !(hi / lo <= 1.0e12);  // lo == 0 -> inf -> ill-conditioned
+}
+
+// 3x3 helpers (row-major)
+__device__ __forceinline__ void mat3_mul(const double A[9], const double B[9], double C[9]) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            C[i * 3 + j] = A[i * 3] * B[j] + A[i * 3 + 1] * B[3 + j] + A[i * 3 + 2] * B[6 + j];
+}
+
+// orthogonal polar factor of a near-rotation (= U V^T of its SVD): Newton
+// X <- (X + X^-T) / 2, quadratic from the first step
+__device__ void polar3(double X[9]) {
+    for (int it = 0; it < 8; ++it) {
+        const double c00 = X[4] * X[8] - X[5] * X[7], c01 = X[5] * X[6] - X[3] * X[8],
+                     c02 = X[3] * X[7] - X[4] * X[6];
+        const double c10 = X[2] * X[7] - X[1] * X[8], c11 = X[0] * X[8] - X[2] * X[6],
+                     c12 = X[1] * X[6] - X[0] * X[7];
+        const double c20 = X[1] * X[5] - X[2] * X[4], c21 = X[2] * X[3] - X[0] * X[5],
+                     c22 = X[0] * X[4] - X[1] * X[3];
+        const double det = X[0] * c00 + X[1] * c01 + X[2] * c02;
+        const double inv = 1.0 / det;  // X^-T = cofactor / det
+        const double cof[9] = {c00, c01, c02, c10, c11, c12, c20, c21, c22};
+        double change = 0.0;
+        for (int i = 0; i < 9; ++i) {
+            const double nx = 0.5 * (X[i] + cof[i] * inv);
+            change = fmax(change, fabs(nx - X[i]));
+            X[i] = nx;
+        }
+        if (change < 1e-17) break;
+    }
+}
+
+__global__ void __launch_bounds__(32 * kIcpTerms, 1) icp_step_kernel(const double *__restrict__ partials, int64_t nblocks, int min_pairs,
+                                double step_eps, double *__restrict__ st) {
+    const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
+    if (st[kStLost] != 0.0 || st[kStLevelDone] != 0.0) return;
+    __shared__ double sums[kIcpTerms];
+    if (k < kIcpTerms) {
+        double s = 0.0;
+        for (int64_t b = lane; b < nblocks; b += 32) s = dadd(s, partials[b * kIcpTerms + k]);
+        s = warp_sum(s);
+        if (lane == 0) sums[k] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const int count = (int)llrint(sums[28]);
+    if (count < min_pairs) {  // :101-102
+        st[kStLost] = 1.0;
+        return;
+    }
+    double A[36], LU[36], b[6];
+    int kk = 0;
+    for (int i = 0; i < 6; ++i)
+        for (int j = i; j < 6; ++j) {
+            A[i * 6 + j] = A[j * 6 + i] = sums[kk];
+            ++kk;
+        }
+    for (int i = 0; i < 36; ++i) LU[i] = A[i];
+    for (int i = 0; i < 6; ++i) b[i] = sums[21 + i];
+    int piv[6];
+    if (!lu6(LU, piv) || ill_conditioned(A, LU, piv)) {  // :111-112, LinAlgError
+        st[kStLost] = 1.0;
+        return;
+    }
+    lu6_solve(LU, piv, b);  // :114
+    bool finite = true;
+    for (int i = 0; i < 6; ++i) finite &= isfinite(b[i]);
+    if (!finite) {  // :117
+        st[kStLost] = 1.0;
+        return;
+    }
+    st[kStCount] = (double)count;
+    st[kStRms] = sqrt(sums[27] / (double)count);  // :119
+    // Rodrigues on delta[:3] (geometry.py:211-219), left-multiplied (:178-181)
+    const double ang = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+    double rot[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    if (ang != 0.0) {
+        const double x = b[0] / ang, y = b[1] / ang, z = b[2] / ang;
+        const double K[9] = {0.0, -z, y, z, 0.0, -x, -y, x, 0.0};
+        double K2[9];
+        mat3_mul(K, K, K2);
+        const double sa = sin(ang), ca = 1.0 - cos(ang);
+        for (int i = 0; i < 9; ++i) rot[i] += sa * K[i] + ca * K2[i];
+    }
+    double R[9], Rn[9], t[3];
+    for (int i = 0; i < 9; ++i) R[i] = st[kStR + i];
+    mat3_mul(rot, R, Rn);
+    for (int i = 0; i < 3; ++i)
+        t[i] = rot[i * 3] * st[kStT] + rot[i * 3 + 1] * st[kStT + 1] + rot[i * 3 + 2] * st[kStT + 2] + b[3 + i];
+    polar3(Rn);
+    for (int i = 0; i < 9; ++i) st[kStR + i] = Rn[i];
+    for (int i = 0; i < 3; ++i) st[kStT + i] = t[i];
+    double dn = 0.0;
+    for (int i = 0; i < 6; ++i) dn += b[i] * b[i];
+    if (sqrt(dn) < step_eps) st[kStLevelDone] = 1.0;  // :182-183
+}
+
+__global__ void icp_level_start_kernel(double *st) { st[kStLevelDone] = 0.0; }
+
 }  // namespace tf
 
 using namespace tf;
@@ -273,4 +497,58 @@ extern "C" int tf_icp_reduce(const double *sv, const double *sn, const uint8_t *
     if (rc) return rc;
     icp_finish_kernel<<<1, 32 * kIcpTerms, 0, stream>>>(partials, blocks, out29);
     return tf_check_launch("icp_finish_kernel");
+}
+
+extern "C" size_t tf_icp_track_state_size(void) { return kStSize * sizeof(double); }
+
+extern "C" int tf_icp_track(int nlevels, const double *const *src_verts, const double *const *src_norms,
+                            const uint8_t *const *src_valid, const TfCamera *level_cams,
+                            const int *iterations, const int *min_pairs, const double *md,
+                            const double *mv, const double *mn, int64_t mw, int64_t mh,
+                            const double r_ref[9], const double t_ref[3], const double r_init[9],
+                            const double t_init[3], double max_d2, double cos_min, double step_eps,
+                            void *workspace, size_t workspace_bytes, double *state, void *stream_) {
+    if (nlevels < 1 || nlevels > 20 || !src_verts || !src_norms || !src_valid || !level_cams ||
+        !iterations || !min_pairs || !md || !mv || !mn || !r_ref || !t_ref || !r_init || !t_init ||
+        !workspace || !state)
+        return tf_set_error(TF_EINVAL, "tf_icp_track: bad argument");
+    if (workspace_bytes < tf_icp_workspace_size(level_cams[0].width * level_cams[0].height))
+        return tf_set_error(TF_EINVAL, "tf_icp_track: workspace too small");
+    cudaStream_t stream = (cudaStream_t)stream_;
+    double init[kStSize] = {};
+    for (int i = 0; i < 9; ++i) init[kStR + i] = r_init[i];
+    for (int i = 0; i < 3; ++i) init[kStT + i] = t_init[i];
+    // pageable source: the call returns once the bytes are staged, so the
+    // stack array may go out of scope
+    if (cudaMemcpyAsync(state, init, sizeof(init), cudaMemcpyHostToDevice, stream) != cudaSuccess)
+        return tf_set_error(TF_ECUDA, "tf_icp_track: state upload failed");
+    double *partials = (double *)workspace;
+    int rc = TF_OK;
+    for (int level = nlevels - 1; level >= 0; --level) {  // coarsest first (:154)
+        const TfCamera &cam = level_cams[level];
+        IcpParams P{};
+        for (int i = 0; i < 9; ++i) P.r_ref.m[i] = r_ref[i];
+        for (int i = 0; i < 3; ++i) P.t_ref.v[i] = t_ref[i];
+        P.cam = LevelCam{cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height};
+        P.src_w = cam.width;
+        P.src_h = cam.height;
+        P.mdl_w = mw;
+        P.mdl_h = mh;
+        P.stride = 1 << level;
+        P.max_d2 = max_d2;
+        P.cos_min = cos_min;
+        P.state = state;
+        const int64_t blocks = (cam.width * cam.height + kIcpThreads - 1) / kIcpThreads;
+        icp_level_start_kernel<<<1, 1, 0, stream>>>(state);
+        if ((rc = tf_check_launch("icp_level_start_kernel"))) return rc;
+        for (int it = 0; it < iterations[level]; ++it) {
+            icp_terms_kernel<<<(unsigned)blocks, kIcpThreads, 0, stream>>>(
+                src_verts[level], src_norms[level], src_valid[level], md, mv, mn, P, partials);
+            if ((rc = tf_check_launch("icp_terms_kernel"))) return rc;
+            icp_step_kernel<<<1, 32 * kIcpTerms, 0, stream>>>(partials, blocks, min_pairs[level], step_eps,
+                                                              state);
+            if ((rc = tf_check_launch("icp_step_kernel"))) return rc;
+        }
+    }
+    return TF_OK;
 }

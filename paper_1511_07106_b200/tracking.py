@@ -19,6 +19,7 @@ conditioning gate and solve run in numpy exactly as in the reference
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -184,14 +185,7 @@ def apply_delta(estimate: Pose, delta: np.ndarray) -> Pose:
     return Pose(rot @ estimate.rotation, rot @ estimate.translation + delta[3:]).orthonormalized()
 
 
-def track(frame, intr: CameraIntrinsics, model: RayMap, ref_pose: Pose,
-          params: TrackingParams = TrackingParams(), init: Pose | None = None) -> TrackResult:
-    """Align a depth frame against a rendered model view (tracking.py:123-196).
-
-    ``frame`` is a DepthFrame (uploaded once) or a resident float64 depth
-    tensor.  Returns the refined camera-to-world pose, or the seed flagged
-    lost when too few pairs survive or the normal system is degenerate.
-    """
+def _pyramid(frame, intr: CameraIntrinsics, params: TrackingParams) -> list[SourceLevel]:
     depth = device_depth(frame)
     if tuple(depth.shape) != (intr.height, intr.width):
         raise ValueError(f"depth shape {tuple(depth.shape)} does not match intrinsics "
@@ -200,7 +194,76 @@ def track(frame, intr: CameraIntrinsics, model: RayMap, ref_pose: Pose,
     intrs = [intr]
     for _ in range(levels - 1):
         intrs.append(intrs[-1].scaled(0.5))
-    pyramid = [source_level(depth, intrs[l], l) for l in range(levels)]
+    return [source_level(depth, intrs[l], l) for l in range(levels)]
+
+
+class _TrackState:
+    """Device state of tf_icp_track and its pinned landing buffer."""
+
+    def __init__(self) -> None:
+        self._bufs: dict = {}
+
+    def buffers(self):
+        d = nat.device()
+        if d.index not in self._bufs:
+            n = int(nat.lib().tf_icp_track_state_size()) // 8
+            self._bufs[d.index] = (torch.zeros(n, dtype=torch.float64, device=d),
+                                   torch.zeros(n, dtype=torch.float64).pin_memory())
+        return self._bufs[d.index]
+
+
+_track_state = _TrackState()
+
+
+def track(frame, intr: CameraIntrinsics, model: RayMap, ref_pose: Pose,
+          params: TrackingParams = TrackingParams(), init: Pose | None = None) -> TrackResult:
+    """Align a depth frame against a rendered model view (tracking.py:123-196).
+
+    ``frame`` is a DepthFrame (uploaded once) or a resident float64 depth
+    tensor.  Returns the refined camera-to-world pose, or the seed flagged
+    lost when too few pairs survive or the normal system is degenerate.  The
+    whole pyramid runs on the device (tf_icp_track) with one read-back at the
+    end; ``track_host`` is the same loop with the 6x6 part in numpy.
+    """
+    pyramid = _pyramid(frame, intr, params)
+    model._device_read()
+    levels = len(pyramid)
+    L = nat.lib()
+    h0, w0 = pyramid[0].valid.shape
+    ws = nat.workspace.get(L.tf_icp_workspace_size(h0 * w0), slot="icp")
+    state, host = _track_state.buffers()
+    ptrs = lambda ts: (ctypes.c_void_p * levels)(*[t.data_ptr() for t in ts])
+    cams = (nat.TfCamera * levels)(*[nat.camera(p.intr) for p in pyramid])
+    its = (ctypes.c_int * levels)(*[int(i) for i in params.iterations])
+    mins = (ctypes.c_int * levels)(*[max(6, params.min_correspondences // 4 ** l) for l in range(levels)])
+    ref_inv = ref_pose.invert()
+    seed = init if init is not None else ref_pose
+    mh, mw = model.distance_dev.shape
+    nat.check(L.tf_icp_track(
+        levels, ptrs([p.verts for p in pyramid]), ptrs([p.norms for p in pyramid]),
+        ptrs([p.valid for p in pyramid]), cams, its, mins, nat.ptr(model.distance_dev),
+        nat.ptr(model.vertices_dev), nat.ptr(model.normals_dev), mw, mh,
+        nat.mat9(ref_inv.rotation), nat.vec3(ref_inv.translation), nat.mat9(seed.rotation),
+        nat.vec3(seed.translation), float(params.max_distance ** 2),
+        float(np.cos(np.deg2rad(params.max_angle_deg))), float(params.step_eps), nat.ptr(ws), ws.numel(),
+        nat.ptr(state), nat.stream_handle()), "tf_icp_track")
+    host.copy_(state, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    st = host.numpy()
+    count = int(st[13])
+    rms = float(st[14]) if count > 0 else float("inf")
+    if st[12] != 0.0:
+        return TrackResult(pose=seed, lost=True, correspondences=count, residual_rms=rms)
+    pose = Pose(st[0:9].reshape(3, 3).copy(), st[9:12].copy())
+    return TrackResult(pose=pose, lost=False, correspondences=count, residual_rms=rms)
+
+
+def track_host(frame, intr: CameraIntrinsics, model: RayMap, ref_pose: Pose,
+               params: TrackingParams = TrackingParams(), init: Pose | None = None) -> TrackResult:
+    """track() with one host round trip per step: the 6x6 gate / solve and
+    the pose update in numpy, operation for operation as tracking.py:100-183."""
+    pyramid = _pyramid(frame, intr, params)
+    levels = len(pyramid)
 
     ref_inv = ref_pose.invert()
     estimate = init if init is not None else ref_pose

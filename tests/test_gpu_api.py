@@ -6,6 +6,7 @@ counters) and the tracking tests, with the operators running in libtfb200.
 """
 
 import dataclasses
+import tempfile
 
 import numpy as np
 import pytest
@@ -327,6 +328,39 @@ def test_track_self_model_fixed_point_and_recovery(small_intr):
     res = tf.track(frame, small_intr, model, pose, params, init=pose.compose(bump))
     delta = pose.invert().compose(res.pose)
     assert np.degrees(rotation_angle(delta.rotation)) < 0.01 and np.linalg.norm(delta.translation) < 1e-4
+
+
+def test_device_track_matches_host_loop():
+    """tf_icp_track (whole pyramid on the device) vs the host-loop track_host
+    (numpy 6x6 gate / solve / pose update): same lost flags and counts, poses
+    equal to rounding, over an orbit with real motion between frames."""
+    from paper_1511_07106_b200.tracking import track_host
+    cfg = small_config(use_groundtruth=True)
+    intr = cfg.intrinsics()
+    frames, poses = render_orbit(intr, 8, step_deg=1.5)
+    pipe = tf.FusionPipeline(cfg, tempfile.mkdtemp())
+    params = tf.TrackingParams(min_correspondences=300)
+    checked = 0
+    for i, (f, p) in enumerate(zip(frames, poses)):
+        if i > 0:
+            model, model_pose = pipe._model, pipe._model_pose
+            for init in (None, poses[i - 1].compose(tf.Pose(rotation_from_axis_angle(
+                    np.array([0.3, 1.0, 0.0]), np.radians(0.7)), np.array([0.004, -0.002, 0.003])))):
+                a = tf.track(f, intr, model, model_pose, params, init=init)
+                b = track_host(f, intr, model, model_pose, params, init=init)
+                assert a.lost == b.lost and a.correspondences == b.correspondences
+                assert abs(a.residual_rms - b.residual_rms) <= 1e-12 + 1e-9 * b.residual_rms
+                # (acos of the trace amplifies 1e-16 to 1e-8 near identity: compare entries)
+                assert np.abs(a.pose.rotation - b.pose.rotation).max() < 1e-12
+                assert np.abs(a.pose.translation - b.pose.translation).max() < 1e-12
+                checked += 1
+        pipe.step(f, p)
+    assert checked == 14
+    # a lost case agrees too: far too few pairs required
+    strict = tf.TrackingParams(min_correspondences=10 ** 7)
+    a = tf.track(frames[1], intr, pipe._model, pipe._model_pose, strict)
+    b = track_host(frames[1], intr, pipe._model, pipe._model_pose, strict)
+    assert a.lost and b.lost and a.pose == b.pose
 
 
 def test_track_lost_cases(small_intr):
