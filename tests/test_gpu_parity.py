@@ -236,6 +236,40 @@ def test_table_division_is_ieee():
         assert lib.tf_debug_weight_division_check(100_000_000, seed) == 0
 
 
+@pytest.mark.parametrize("scale", [6.0, 8.0, 13.0])
+def test_coarse_strides_above_two(scale):
+    """Wider truncation -> coarse stride round(0.5 tau / vs) of 3, 4, 6: the
+    certified per-lane march and the cooperative march equal the exact
+    reference march (their coarse == 2 fast paths are not taken)."""
+    intr = CameraIntrinsics(131.25, 131.25, 79.5, 59.5, 160, 120)
+    spec = tf.init_grid(3.0, 124, 62)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size, truncation_scale=scale)
+    assert tf.tsdf.coarse_step(params, spec.voxel_size) == round(0.5 * scale)
+    tiles = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in spec.keys]
+    scene = demo_scene()
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 24)
+    for pose in poses[:5]:
+        tf.integrate_volumes(tiles, scene.render_depth(pose, intr), pose, intr, params)
+    lib = nat.load_library()
+    stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
+    try:
+        for pose in (poses[2], poses[7]):
+            exact = tf.RayMap.empty(intr)
+            lib.tf_set_debug_flags(nat.DEBUG_EXACT_ONLY)
+            tf.raycast_volumes(tiles, pose, intr, exact, params)
+            assert torch.isfinite(exact.distance_dev).sum().item() > 2000
+            for flag in (0, nat.DEBUG_COOP_ALL):
+                got = tf.RayMap.empty(intr)
+                lib.tf_set_debug_flags(flag)
+                tf.raycast_volumes(tiles, pose, intr, got, params, stats)
+                assert torch.equal(got.distance_dev, exact.distance_dev)
+                assert torch.equal(got.vertices_dev, exact.vertices_dev)
+                assert torch.equal(got.normals_dev, exact.normals_dev)
+    finally:
+        lib.tf_set_debug_flags(0)
+    assert stats[nat.STAT_CERT_FAILURES].item() == 0
+
+
 def test_more_volumes_than_one_launch_holds():
     """125 tiles (> TFB200_MAX_VOLUMES_PER_LAUNCH = 64): the chunked fused
     integrate / raycast equal per-tile calls bit for bit."""
