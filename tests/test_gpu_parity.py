@@ -236,6 +236,32 @@ def test_table_division_is_ieee():
         assert lib.tf_debug_weight_division_check(100_000_000, seed) == 0
 
 
+@pytest.mark.parametrize("sw,max_w", [(0.75, 128.0), (1.0, 5.0), (2.5, 10.0)])
+def test_fractional_and_capped_weights(sw, max_w):
+    """Non-integral running-mean denominators (the division falls back from
+    the reciprocal table), low caps (the fixed point and the weight cap):
+    float32-screened integration == exact integration, bit for bit."""
+    intr = CameraIntrinsics(131.25, 131.25, 79.5, 59.5, 160, 120)
+    spec = tf.init_grid(3.0, 124, 62)
+    params = tf.FusionParams(truncation=4 * spec.voxel_size, max_weight=max_w, sample_weight=sw)
+    a = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in spec.keys]
+    b = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in spec.keys]
+    scene = demo_scene()
+    lib = nat.load_library()
+    try:
+        for pose in tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 24)[:8]:
+            frame = scene.render_depth(pose, intr)
+            lib.tf_set_debug_flags(0)
+            tf.integrate_volumes(a, frame, pose, intr, params)
+            lib.tf_set_debug_flags(nat.DEBUG_EXACT_ONLY)
+            tf.integrate_volumes(b, frame, pose, intr, params)
+    finally:
+        lib.tf_set_debug_flags(0)
+    for x, y in zip(a, b):
+        assert torch.equal(x.voxels, y.voxels)
+    assert float(a[0].voxels[..., 1].max()) > 0
+
+
 @pytest.mark.parametrize("scale", [6.0, 8.0, 13.0])
 def test_coarse_strides_above_two(scale):
     """Wider truncation -> coarse stride round(0.5 tau / vs) of 3, 4, 6: the
