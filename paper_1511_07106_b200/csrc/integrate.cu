@@ -74,6 +74,20 @@ __device__ __forceinline__ bool keeps_summary(const TfVolume &vol, const FrameGe
     return vol.brick_state_dev != nullptr && vol.summary_threshold == f.good_t;
 }
 
+// Bricks whose packed state changed this call: each listed once (dirty
+// bitmap), so the flag pass visits only them and their lower neighbours.
+struct ChangedList {
+    uint32_t *list;
+    unsigned *count;
+    unsigned *dirty;
+};
+
+__device__ __forceinline__ void mark_changed(const ChangedList &c, unsigned g) {
+    if (!c.list) return;
+    const unsigned bit = 1u << (g & 31u);
+    if (!(atomicOr(&c.dirty[g >> 5], bit) & bit)) c.list[atomicAdd(c.count, 1u)] = g;
+}
+
 __device__ __forceinline__ void summary_add(const TfVolume &vol, int64_t lin, unsigned delta) {
     const int64_t n = vol.n, nb = (n + 7) / 8;
     const int64_t x = lin % n, y = (lin / n) % n, z = lin / (n * n);
@@ -459,7 +473,7 @@ __global__ void __launch_bounds__(256) brick_free_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const uint32_t *__restrict__ list,
     const unsigned int *__restrict__ list_count, const int fixed_point,
-    unsigned long long *__restrict__ stats) {
+    unsigned long long *__restrict__ stats, const ChangedList changed) {
     __shared__ double rcp[257];
     fill_rcp(rcp);
     const unsigned count = *list_count;
@@ -530,7 +544,10 @@ __global__ void __launch_bounds__(256) brick_free_kernel(
         if (keep) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
-            if (lane == 0 && dbad) atomicAdd(&vol.brick_state_dev[local], dbad);
+            if (lane == 0 && dbad) {
+                atomicAdd(&vol.brick_state_dev[local], dbad);
+                mark_changed(changed, g);
+            }
         }
     }
     if (stats) {
@@ -743,7 +760,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const float2 *__restrict__ table32, const uint32_t *__restrict__ active,
     const unsigned int *__restrict__ active_count, unsigned long long *__restrict__ queue,
     unsigned long long *__restrict__ queue_count, const unsigned long long queue_cap,
-    const int fixed_point, unsigned long long *__restrict__ stats) {
+    const int fixed_point, unsigned long long *__restrict__ stats, const ChangedList changed) {
     __shared__ double rcp[257];
     fill_rcp(rcp);
     const unsigned count = *active_count;
@@ -937,7 +954,10 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         if (keep) {  // one atomic per brick and warp
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
-            if (lane == 0 && dbad) atomicAdd(&vol.brick_state_dev[local], dbad);
+            if (lane == 0 && dbad) {
+                atomicAdd(&vol.brick_state_dev[local], dbad);
+                mark_changed(changed, g);
+            }
         }
         if (stats && __reduce_add_sync(0xffffffffu, brick_free) == __reduce_add_sync(0xffffffffu, brick_vox))
             ++all_free;  // (counted on every lane; lane 0's count is reported)
@@ -955,10 +975,11 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
 // The exact reference arithmetic for every queued (undecided) voxel; one
 // thread per voxel, so the float64 path runs without divergence.
 __global__ void __launch_bounds__(256) exact_queue_kernel(
-    const __grid_constant__ VolumeTable vt, const __grid_constant__ FrameGeom f,
+    const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
+    const __grid_constant__ FrameGeom f,
     const double2 *__restrict__ table, const unsigned long long *__restrict__ queue,
     const unsigned long long *__restrict__ queue_count, const unsigned long long queue_cap,
-    unsigned long long *__restrict__ stats) {
+    unsigned long long *__restrict__ stats, const ChangedList changed) {
     const unsigned long long total = min(*queue_count, queue_cap);
     unsigned long long updates = 0;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -974,7 +995,11 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
         updates += update_voxel((float2 *)vol.voxels_dev, lin, dmul((double)(x + vol.origin[0]), vs),
                                 dmul((double)(y + vol.origin[1]), vs),
                                 dmul((double)(z + vol.origin[2]), vs), table, f, &db);
-        if (db && keeps_summary(vol, f)) summary_add(vol, lin, db);
+        if (db && keeps_summary(vol, f)) {
+            summary_add(vol, lin, db);
+            const int64_t nb = bt.nb[v];
+            mark_changed(changed, (unsigned)(bt.offset[v] + ((z >> 3) * nb + (y >> 3)) * nb + (x >> 3)));
+        }
     }
     if (stats) {
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
@@ -1099,7 +1124,7 @@ __global__ void __launch_bounds__(256) brick_summary_kernel(const TfVolume vol) 
 
 struct IntegrateLayout {
     size_t table_off, table32_off, mip_off, qmip_off, count_off, active_off, free_off, macro_off, queue_off,
-        total;
+        changed_off, dirty_off, dirty_bytes, total;
     unsigned long long queue_cap;
 };
 
@@ -1131,6 +1156,11 @@ static IntegrateLayout layout_for(int64_t total_bricks_max, const TfCamera *cam)
     L.queue_off = off;
     L.queue_cap = kQueueCap;
     off = align_up(off + (size_t)L.queue_cap * sizeof(unsigned long long), 256);
+    L.changed_off = off;
+    off = align_up(off + (size_t)total_bricks_max * sizeof(uint32_t), 256);
+    L.dirty_off = off;
+    L.dirty_bytes = (size_t)((total_bricks_max + 31) / 32) * sizeof(uint32_t);
+    off = align_up(off + L.dirty_bytes, 256);
     L.total = off;
     return L;
 }
@@ -1296,8 +1326,11 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
             off += nb * nb * nb;
         }
         bt.offset[cnt] = off;
-        if (cudaMemsetAsync(count, 0, 128, stream) != cudaSuccess)  // brick + queue counters
+        if (cudaMemsetAsync(count, 0, 128, stream) != cudaSuccess ||  // brick + queue counters
+            cudaMemsetAsync(ws + L.dirty_off, 0, L.dirty_bytes, stream) != cudaSuccess)
             return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
+        const ChangedList changed{(uint32_t *)(ws + L.changed_off), (unsigned *)(ws + L.count_off + 24),
+                                  (unsigned *)(ws + L.dirty_off)};
         const int exact_only = (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) ? 1 : 0;
         const int no_cull = (tf_debug_flags() & TF_DEBUG_NO_CULL) ? 1 : 0;
         int64_t macros_total = 0;
@@ -1327,20 +1360,21 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
             void *pf = tf_profile_begin(TF_PROF_INTEGRATE_FREE, side->stream);
             brick_free_kernel<<<(unsigned)sms * 8, 256, 0, side->stream>>>(vt, bt, f, active_free, fcount,
                                                                           fixed_point,
-                                                                          (unsigned long long *)stats);
+                                                                          (unsigned long long *)stats,
+                                                                          changed);
             tf_profile_end(pf, side->stream);
             if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
             cudaEventRecord(side->join, side->stream);
             void *pg = tf_profile_begin(TF_PROF_INTEGRATE_GENERAL, stream);
             brick_update_kernel<<<(unsigned)sms * 6, 256, 0, stream>>>(
                 vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap,
-                fixed_point, (unsigned long long *)stats);
+                fixed_point, (unsigned long long *)stats, changed);
             tf_profile_end(pg, stream);
             if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
             void *pe = tf_profile_begin(TF_PROF_INTEGRATE_EXACT, stream);
-            exact_queue_kernel<<<(unsigned)sms * 16, 256, 0, stream>>>(vt, f, table, queue, qcount,
+            exact_queue_kernel<<<(unsigned)sms * 16, 256, 0, stream>>>(vt, bt, f, table, queue, qcount,
                                                                      L.queue_cap,
-                                                                     (unsigned long long *)stats);
+                                                                     (unsigned long long *)stats, changed);
             tf_profile_end(pe, stream);
             if ((rc = tf_check_launch("exact_queue_kernel"))) return rc;
             cudaStreamWaitEvent(stream, side->join, 0);
@@ -1351,11 +1385,19 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
         for (int v = 0; v < cnt; ++v)
             any_summary |= vt.vol[v].brick_flags_dev && vt.vol[v].brick_state_dev &&
                            vt.vol[v].summary_threshold == f.good_t;
-        if (any_summary) {
+        if (any_summary && exact_only) {  // the reference-order kernel does not list changes
             brick_flags_active_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, bt, f, active, count);
             if ((rc = tf_check_launch("brick_flags_active_kernel"))) return rc;
             brick_flags_active_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, bt, f, active_free, fcount);
             if ((rc = tf_check_launch("brick_flags_active_kernel"))) return rc;
+        } else if (any_summary) {
+            // flags depend on a brick's own and its +1 neighbours' states: the
+            // bricks whose state changed and their lower neighbours
+            brick_flags_active_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, bt, f, changed.list,
+                                                                          changed.count);
+            if ((rc = tf_check_launch("brick_flags_active_kernel"))) return rc;
+        }
+        if (any_summary) {
             super_flags_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, f, 1);
             if ((rc = tf_check_launch("super_flags_kernel"))) return rc;
         }
