@@ -1,0 +1,160 @@
+"""VolumeSet residency semantics and bin_endpoints known answers on the GPU
+package: the reference's test_volumes.py cases (volumes.py:156-331), run for
+both spill tiers — the reference's files ("disk") and pinned host memory
+("host", same LRU order and whole-image counters; files only on persist())."""
+
+import numpy as np
+import pytest
+
+import paper_1511_07106_b200 as tf
+from paper_1511_07106_b200.geometry import CameraIntrinsics, DepthFrame, Pose
+
+pytestmark = pytest.mark.gpu
+
+PARAMS = tf.FusionParams(truncation=0.2)
+TIERS = ["disk", "host"]
+
+
+def make_set(tmp_path, max_resident, tier, n=4):
+    return tf.VolumeSet(PARAMS, voxels_per_side=n, voxel_size=0.1, max_resident=max_resident,
+                        spill_dir=tmp_path, spill_tier=tier)
+
+
+@pytest.fixture
+def small_intr():
+    return CameraIntrinsics(fx=100.0, fy=100.0, cx=40.0, cy=30.0, width=80, height=60)
+
+
+@pytest.mark.parametrize("tier", TIERS)
+def test_volume_set_lifecycle(tmp_path, tier):
+    vs = make_set(tmp_path, 2, tier)
+    vs.add((0, 0, 0))
+    assert (0, 0, 0) in vs and len(vs) == 1
+    vol = vs.acquire((0, 0, 0))
+    vol.tsdf[0, 0, 0] = 0.25
+    with pytest.raises(RuntimeError):
+        vs.acquire((0, 0, 0))
+    vs.release((0, 0, 0))
+    with pytest.raises(RuntimeError):
+        vs.release((0, 0, 0))
+    with pytest.raises(KeyError):
+        vs.acquire((9, 9, 9))
+    assert vs.acquire((0, 0, 0)).tsdf[0, 0, 0] == np.float32(0.25)
+
+
+@pytest.mark.parametrize("tier", TIERS)
+def test_eviction_is_least_recently_used(tmp_path, tier):
+    vs = make_set(tmp_path, 2, tier)
+    a, b, c = (0, 0, 0), (4, 0, 0), (8, 0, 0)
+    for key in (a, b, c):
+        vs.add(key)
+    for key in (a, b, c):  # a is least recently used when c arrives: a is spilled
+        vs.acquire(key)
+        vs.release(key)
+    assert vs.files_written == 1
+    assert [k for k, _ in vs.resident_volumes()] == [b, c]
+    if tier == "disk":
+        assert vs.spill_path(a).exists() and not vs.spill_path(b).exists()
+    vs.acquire(a)
+    vs.release(a)
+    assert vs.files_read == 1 and vs.bytes_read == tf.spill_file_size(4)
+
+
+@pytest.mark.parametrize("tier", TIERS)
+def test_live_tiles_survive_pressure(tmp_path, tier):
+    vs = make_set(tmp_path, 1, tier)
+    vs.add((0, 0, 0))
+    vs.add((4, 0, 0))
+    vs.acquire((0, 0, 0))
+    vs.acquire((4, 0, 0))  # the budget is full of live tiles: overflow, not eviction
+    assert vs.resident_count == 2 and vs.files_written == 0
+    vs.release((0, 0, 0))
+    vs.release((4, 0, 0))
+
+
+@pytest.mark.parametrize("tier", TIERS)
+def test_round_robin_transfer_counts(tmp_path, tier):
+    vs = make_set(tmp_path, 1, tier)
+    keys = [(0, 0, 0), (4, 0, 0), (8, 0, 0)]
+    for key in keys:
+        vs.add(key)
+
+    def sweep():
+        for key in keys:
+            vs.acquire(key)
+            vs.release(key)
+
+    sweep()
+    assert (vs.files_read, vs.files_written) == (0, 2)
+    sweep()
+    assert (vs.files_read, vs.files_written) == (3, 5)
+    sweep()
+    assert (vs.files_read, vs.files_written) == (6, 8)
+    assert vs.bytes_written == 8 * tf.spill_file_size(4)
+
+
+@pytest.mark.parametrize("tier", TIERS)
+def test_remove_returns_archived_state(tmp_path, tier):
+    vs = make_set(tmp_path, 1, tier)
+    vs.add((0, 0, 0))
+    vs.add((4, 0, 0))
+    vol = vs.acquire((0, 0, 0))
+    vol.tsdf[1, 2, 3] = 0.125  # a host-mirror edit must survive the spill
+    vs.release((0, 0, 0))
+    vs.acquire((4, 0, 0))
+    vs.release((4, 0, 0))
+    archived = vs.remove((0, 0, 0))
+    assert archived.tsdf[1, 2, 3] == np.float32(0.125)
+    assert (0, 0, 0) not in vs and not vs.spill_path((0, 0, 0)).exists()
+
+
+@pytest.mark.parametrize("tier", TIERS)
+def test_flush_persists_without_evicting(tmp_path, tier):
+    vs = make_set(tmp_path, 4, tier)
+    for key in [(0, 0, 0), (4, 0, 0)]:
+        vs.add(key)
+        vs.acquire(key)
+        vs.release(key)
+    vs.flush()
+    assert vs.resident_count == 2 and vs.files_written == 2
+    if tier == "disk":
+        assert vs.spill_path((0, 0, 0)).exists() and vs.spill_path((4, 0, 0)).exists()
+    else:
+        assert vs.persist() == 2 * tf.spill_file_size(4)
+        back, _ = tf.load_subvolume(vs.spill_path((4, 0, 0)))
+        assert np.array_equal(back.tsdf, vs.acquire((4, 0, 0)).tsdf)
+
+
+@pytest.mark.parametrize("tier", TIERS)
+def test_volume_set_validation(tmp_path, tier):
+    with pytest.raises(ValueError):
+        make_set(tmp_path, 0, tier)
+    vs = make_set(tmp_path, 1, tier)
+    vs.add((0, 0, 0))
+    with pytest.raises(ValueError):
+        vs.add((0, 0, 0))
+
+
+# ---- bin_endpoints known answers (reference test_volumes.py:238-266) ----------------
+
+def test_bin_endpoints_single_pixel(small_intr):
+    depth = np.zeros((60, 80))
+    depth[30, 40] = 2.0  # optical axis: endpoint (0, 0, 2) in block (0, 0, 1) of 1.5 m
+    assert tf.bin_endpoints(DepthFrame(depth), small_intr, Pose.identity(), 30, 0.05) == {(0, 0, 30): 1}
+
+
+def test_bin_endpoints_uses_ray_length_along_unit_ray(small_intr):
+    depth = np.zeros((60, 80))
+    depth[30, 60] = 2.0  # 2 m along the unit ray (0.2, 0, 1) / |.|: x 0.392, z 1.961
+    assert tf.bin_endpoints(DepthFrame(depth), small_intr, Pose.identity(), 30, 0.05) == {(0, 0, 30): 1}
+
+
+def test_bin_endpoints_negative_cells(small_intr):
+    depth = np.zeros((60, 80))
+    depth[30, 40] = 2.0
+    behind = Pose(np.eye(3), np.array([-2.0, 0.0, 0.0]))
+    assert tf.bin_endpoints(DepthFrame(depth), small_intr, behind, 30, 0.05) == {(-60, 0, 30): 1}
+
+
+def test_bin_endpoints_empty_frame(small_intr):
+    assert tf.bin_endpoints(DepthFrame(np.zeros((60, 80))), small_intr, Pose.identity(), 30, 0.05) == {}
