@@ -330,6 +330,46 @@ def test_track_self_model_fixed_point_and_recovery(small_intr):
     assert np.degrees(rotation_angle(delta.rotation)) < 0.01 and np.linalg.norm(delta.translation) < 1e-4
 
 
+def test_params_volume_layout_and_validation():
+    """test_tsdf.py:38-63: params, empty layout, counters, validation."""
+    with pytest.raises(ValueError):
+        tf.FusionParams(truncation=0.0)
+    with pytest.raises(ValueError):
+        tf.FusionParams(truncation=0.1, max_weight=0.5, sample_weight=1.0)
+    assert tf.FusionParams.for_voxel_size(0.1).truncation == pytest.approx(0.4)
+    vol = tf.TsdfSubvolume.empty(np.array([-4, -4, 16]), 8, 0.8)
+    assert vol.voxel_size == pytest.approx(0.1)
+    assert np.allclose(vol.world_min, [-0.4, -0.4, 1.6]) and np.allclose(vol.world_max, [0.3, 0.3, 2.3])
+    assert vol.payload_bytes() == 8 * 8 ** 3 and vol.observed_count() == 0
+    with pytest.raises(ValueError):
+        tf.TsdfSubvolume.empty(np.array([0, 0]), 8, 0.8)
+    with pytest.raises(ValueError):
+        tf.TsdfSubvolume.empty(np.zeros(3), 1, 0.8)
+
+
+def test_raymap_downsampled_and_point_clouds(small_intr):
+    """test_tsdf.py:181-186, :201-210."""
+    rm = tf.RayMap.empty(small_intr)
+    rm.distance[0, 0] = 1.0  # a host-mirror edit reaches the device copy
+    half = rm.downsampled()
+    assert half.distance.shape == (30, 40) and half.valid[0, 0]
+    with pytest.raises(ValueError):
+        tf.PointCloud(np.zeros((3, 3)), np.zeros((2, 3)))
+    merged = tf.PointCloud.concatenate([tf.PointCloud(np.zeros((2, 3)), np.ones((2, 3))),
+                                        tf.PointCloud.empty()])
+    assert len(merged) == 2 and len(tf.PointCloud.concatenate([])) == 0
+
+
+def test_trilinear_outside_and_raycast_miss(wall_volume, small_intr):
+    """test_tsdf.py:129-134 (outside -> None) and :160-165 (a miss leaves +inf)."""
+    vol, params = wall_volume
+    assert tf.trilinear_sample(vol, np.array([10.0, 10.0, 10.0])) is None
+    rm = tf.RayMap.empty(small_intr)
+    away = tf.Pose(np.diag([1.0, -1.0, -1.0]), np.zeros(3))  # looking away from the wall
+    tf.raycast(vol, away, small_intr, rm, params)
+    assert np.isinf(rm.distance).all() and not rm.valid.any()
+
+
 def test_device_track_matches_host_loop():
     """tf_icp_track (whole pyramid on the device) vs the host-loop track_host
     (numpy 6x6 gate / solve / pose update): same lost flags and counts, poses

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import paper_1511_07106_b200 as tf
-from paper_1511_07106_b200.geometry import CameraIntrinsics, DepthFrame, Pose
+from paper_1511_07106_b200.geometry import DepthFrame, Pose
 
 pytestmark = pytest.mark.gpu
 
@@ -18,11 +18,6 @@ TIERS = ["disk", "host"]
 def make_set(tmp_path, max_resident, tier, n=4):
     return tf.VolumeSet(PARAMS, voxels_per_side=n, voxel_size=0.1, max_resident=max_resident,
                         spill_dir=tmp_path, spill_tier=tier)
-
-
-@pytest.fixture
-def small_intr():
-    return CameraIntrinsics(fx=100.0, fy=100.0, cx=40.0, cy=30.0, width=80, height=60)
 
 
 @pytest.mark.parametrize("tier", TIERS)
