@@ -403,6 +403,27 @@ def test_device_track_matches_host_loop():
     assert a.lost and b.lost and a.pose == b.pose
 
 
+def test_lone_sphere_is_degenerate_on_the_device(small_intr):
+    """test_tracking.py:132-152: exact sphere geometry leaves rotations about the
+    centre unobservable; the conditioning gate (now evaluated on the device)
+    must report lost, as the numpy host loop does."""
+    from paper_1511_07106_b200.synth import Scene, Sphere
+    from paper_1511_07106_b200.tracking import track_host
+    scene = Scene((Sphere(np.array([0.0, 0.0, 1.5]), 0.45),))
+    pose = tf.Pose.identity()
+    frame = scene.render_depth(pose, small_intr)
+    rays = small_intr.pixel_rays()
+    unit = rays / np.linalg.norm(rays, axis=-1, keepdims=True)
+    t = scene.primitives[0].intersect(np.zeros(3), unit.reshape(-1, 3)).reshape(unit.shape[:2])
+    hit = np.isfinite(t)
+    vertices = unit * np.where(hit, t, 0.0)[..., None]
+    normals = np.where(hit[..., None], (vertices - np.array([0.0, 0.0, 1.5])) / 0.45, 0.0)
+    model = tf.RayMap(vertices=vertices, normals=normals, distance=np.where(hit, t, np.inf))
+    params = tf.TrackingParams(min_correspondences=200)
+    assert tf.track(frame, small_intr, model, pose, params).lost
+    assert track_host(frame, small_intr, model, pose, params).lost
+
+
 def test_track_lost_cases(small_intr):
     scene = demo_scene()
     pose = tf.Pose.identity()
