@@ -323,12 +323,37 @@ struct FastRay {
     int n;
     double q0x, q0y, q0z, dx, dy, dz;
     float near, near_tol;
-    double near_thresh;
     const unsigned *bad;  // brick summary (NULL: not usable for this tau)
     unsigned nb;
     float idfx, idfy, idfz;  // 1 / d (approximate; only used with margins)
     const unsigned char *flags;  // per-brick flags (bit0 never observed, bit1 free)
 };
+
+// What the rare exact paths need beyond the FastRay, by reference into the
+// kernel's parameter space (two pointers instead of a dozen live doubles).
+struct RayRef {
+    const TfVolume *vol;
+    const RayGeom *g;
+};
+
+// the exact reference view of the ray (sample_at / accept_crossing)
+__device__ __forceinline__ Ray make_ray(const FastRay &fr, const RayRef &rr) {
+    Ray r;
+    r.vox = fr.vox;
+    r.n = rr.vol->n;
+    r.htx = (double)rr.vol->origin[0];
+    r.hty = (double)rr.vol->origin[1];
+    r.htz = (double)rr.vol->origin[2];
+    r.vs = rr.vol->voxel_size;
+    r.ox = rr.g->cam.v[0];
+    r.oy = rr.g->cam.v[1];
+    r.oz = rr.g->cam.v[2];
+    r.dx = fr.dx;
+    r.dy = fr.dy;
+    r.dz = fr.dz;
+    r.samples = 0;
+    return r;
+}
 
 // floor(q) from a 20-bit fixed point: bits = round(q 2^20) mod 2^32 (q in
 // (-2^11, 4096)), cell = bits >> 20 (floor(q) mod 2^12), fraction field
@@ -442,7 +467,7 @@ __device__ __forceinline__ int region_at(const FastRay &r, int j, int &exit) {
 }
 
 // certified decisions of lattice point k (exact fallback when unsure)
-__device__ __forceinline__ unsigned cert_sample(const FastRay &fr, const Ray &er, int k,
+__device__ __forceinline__ unsigned cert_sample(const FastRay &fr, const RayRef &er, int k,
                                                 unsigned long long &samples,
                                                 unsigned long long &exact_samples,
                                                 bool use_summary = true) {
@@ -451,10 +476,10 @@ __device__ __forceinline__ unsigned cert_sample(const FastRay &fr, const Ray &er
     if (s & kSummaryBit) exact_samples += 1ull << 44;  // summary-certified (counter in the high bits)
     if (!(s & kUnsure)) return s & ~kSummaryBit;
     ++exact_samples;
-    Ray r = er;
+    Ray r = make_ray(fr, er);
     double v = 0.0;
     if (!sample_at(r, k, v)) return 0u;
-    return kValidBit | (v > 0.0 ? kPosBit : 0u) | (fabs(v) < fr.near_thresh ? kNearBit : 0u);
+    return kValidBit | (v > 0.0 ? kPosBit : 0u) | (fabs(v) < er.g->near_thresh ? kNearBit : 0u);
 }
 
 // _scan_crossing on certified decisions; the crossing itself is exact.
@@ -462,7 +487,7 @@ __device__ __forceinline__ unsigned cert_sample(const FastRay &fr, const Ray &er
 // `end_s` = the decisions of point `end` when the march just sampled it
 // (kNoDecision otherwise): the reference samples it again; the result is the same.
 constexpr unsigned kNoDecision = 0x80000000u;
-__device__ __forceinline__ bool scan_fast(const FastRay &fr, const Ray &er, int from, int end,
+__device__ __forceinline__ bool scan_fast(const FastRay &fr, const RayRef &er, int from, int end,
                                           unsigned sp, Hit &hit, unsigned long long &samples,
                                           unsigned long long &exact_samples, unsigned end_s = kNoDecision) {
     for (int k = from; k <= end; ++k) {
@@ -482,7 +507,7 @@ __device__ __forceinline__ bool scan_fast(const FastRay &fr, const Ray &er, int 
         }
         // sp_valid and sp_v > 0 and sv and s <= 0 (:169)
         if ((sp & (kValidBit | kPosBit)) == (kValidBit | kPosBit) && (s & (kValidBit | kPosBit)) == kValidBit) {
-            Ray r = er;
+            Ray r = make_ray(fr, er);
             double e0 = 0.0, e1 = 0.0;
             const bool v0 = sample_at(r, k - 1, e0), v1 = sample_at(r, k, e1);
             exact_samples += 2;
@@ -514,7 +539,7 @@ __device__ __forceinline__ bool scan_fast(const FastRay &fr, const Ray &er, int 
 #define DIAG_PARAM
 #define DIAG_ARG
 #endif
-__device__ bool march_fast(const FastRay &fr, const Ray &er, int j, const int j_end, const int coarse,
+__device__ bool march_fast(const FastRay &fr, const RayRef &er, int j, const int j_end, const int coarse,
                            Hit &best, unsigned long long &samples, unsigned long long &exact_samples,
                            const long long deadline, bool &aborted DIAG_PARAM) {
     unsigned prev = 0u;  // decisions of the last valid march sample
@@ -692,7 +717,7 @@ __device__ __forceinline__ bool setup_volume(const RayGeom &g, const TfVolume &v
                        (double)j_end;
     const bool summ = vol.brick_state_dev != nullptr && vol.summary_threshold == g.good_t;
     fr = FastRay{r.vox, (int)vol.n, q0x, q0y, q0z, d[0], d[1], d[2],
-                 (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f, g.near_thresh,
+                 (float)g.near_thresh, (float)g.near_thresh * 2.4e-7f,
                  summ ? vol.brick_state_dev : nullptr, (unsigned)((vol.n + 7) / 8),
                  1.0f / (float)d[0], 1.0f / (float)d[1], 1.0f / (float)d[2],
                  summ ? vol.brick_flags_dev : nullptr};
@@ -759,8 +784,8 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
                 if (!diag) __trap();
 #endif
                 DIAG_T0
-                changed |= march_fast(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
-                                      exact_samples, deadline, aborted DIAG_ARG);
+                changed |= march_fast(fr, RayRef{&vol, &g}, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best,
+                                      samples, exact_samples, deadline, aborted DIAG_ARG);
                 DIAG_ACC(3)
                 if (aborted) break;
             } else {  // forced, or coordinates too large to certify: the exact reference march
@@ -833,7 +858,7 @@ struct Dec32 {
 };
 
 // the 32 lanes decide points [b, b + 31] (only those in [lo, hi]; others read as invalid)
-__device__ __forceinline__ Dec32 coop_half(const FastRay &fr, const Ray &er, int b, int lo, int hi,
+__device__ __forceinline__ Dec32 coop_half(const FastRay &fr, const RayRef &er, int b, int lo, int hi,
                                            unsigned long long &exact_samples) {
     const int lane = threadIdx.x & 31, k = b + lane;
     unsigned s = 0u;
@@ -847,7 +872,7 @@ __device__ __forceinline__ Dec32 coop_half(const FastRay &fr, const Ray &er, int
 
 // decisions of [a, a + 31] (warp-uniform); slides the window forward as the
 // march advances, decides look-backs below it directly
-__device__ Dec32 coop_range(const FastRay &fr, const Ray &er, CoopWindow &w, int a, int lo, int hi,
+__device__ Dec32 coop_range(const FastRay &fr, const RayRef &er, CoopWindow &w, int a, int lo, int hi,
                             unsigned long long &exact_samples) {
     if (a < w.base) return coop_half(fr, er, a, lo, hi, exact_samples);
     if (a + 31 > w.base + 63) {
@@ -877,7 +902,7 @@ __device__ __forceinline__ unsigned dec_bits(const Dec32 &d, int i) {
 // _scan_crossing over [from, end] with seed decisions sp (warp-uniform):
 // crossing candidates (previous valid > 0, this valid <= 0, :169) come from
 // the decision masks 32 points at a time; each is checked exactly in order
-__device__ bool coop_scan(const FastRay &fr, const Ray &er, CoopWindow &w, int lo, int hi, int from, int end,
+__device__ bool coop_scan(const FastRay &fr, const RayRef &er, CoopWindow &w, int lo, int hi, int from, int end,
                           unsigned sp, Hit &hit, unsigned long long &samples,
                           unsigned long long &exact_samples) {
     samples += (unsigned long long)(end - from + 1);
@@ -891,7 +916,7 @@ __device__ bool coop_scan(const FastRay &fr, const Ray &er, CoopWindow &w, int l
         while (cand) {
             const int k = a + __ffs(cand) - 1;
             cand &= cand - 1;
-            Ray r = er;
+            Ray r = make_ray(fr, er);
             double e0 = 0.0, e1 = 0.0;
             const bool v0 = sample_at(r, k - 1, e0), v1 = sample_at(r, k, e1);
             exact_samples += 2;
@@ -911,7 +936,7 @@ __device__ bool coop_scan(const FastRay &fr, const Ray &er, CoopWindow &w, int l
 // counters are consumed in one step: invalid march points (each followed by
 // a scan when the last valid sample was positive: the scans tile one range,
 // searched once) and valid, positive, not-near march points (no scan).
-__device__ bool march_coop(const FastRay &fr, const Ray &er, int j, const int j_end, const int coarse,
+__device__ bool march_coop(const FastRay &fr, const RayRef &er, int j, const int j_end, const int coarse,
                            Hit &best, unsigned long long &samples, unsigned long long &exact_samples) {
     const int lo = j - 1, hi = j_end;  // the only points the reference can sample
     CoopWindow w;
@@ -1079,8 +1104,8 @@ __global__ void __launch_bounds__(128) raycast_coop_kernel(
             Ray r;
             FastRay fr;
             if (setup_volume(g, vol, o, d, jhi[pick], r, fr)) {
-                changed |= march_coop(fr, r, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best, samples,
-                                      exact_samples);
+                changed |= march_coop(fr, RayRef{&vol, &g}, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best,
+                                      samples, exact_samples);
             } else {
                 changed |= march_volume(r, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
                 samples += r.samples;
