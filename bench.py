@@ -54,6 +54,7 @@ def parse_args():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-color", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-config2", action="store_true")
     p.add_argument("--frames", type=int, default=64, help="distinct frames cycled through")
@@ -325,6 +326,10 @@ def run_ours(args) -> None:
     cs = clocks.summary()
     result["clocks"] = cs
 
+    # ---- the same step with colour (north_star; the reference has no colour) ----
+    if not args.no_color and world == 1:
+        result["color"] = run_color(args, tf, torch, spec, params, intr, poses, scene, barrier)
+
     # ---- e2e through the public pipeline API, frames from pinned host memory ----
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, tf, nat, torch, dist, rank, world, intr, spec, params,
@@ -342,6 +347,39 @@ def run_ours(args) -> None:
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_color(args, tf, torch, spec, params, intr, poses, scene, barrier) -> dict:
+    """Config 3 with an RGB frame fused into a colour channel per volume (the
+    band voxels' running mean, tf_integrate_rgb) and the model colours
+    rendered (tf_raycast_colors) every step: device-resident inputs."""
+    from paper_1511_07106_b200.distributed import ShardedFusion
+    from paper_1511_07106_b200.synth import render_rgb
+
+    steps = min(args.steps, 50)
+    n = len(poses)
+    depth = [torch.from_numpy(scene.render_depth(p, intr).data).cuda() for p in poses]
+    rgb = [torch.from_numpy(render_rgb(scene, p, intr)).cuda() for p in poses]
+    shard = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length, params, intr,
+                          color=True)
+    for i in range(args.warmup):
+        shard.step(depth[i % n], poses[i % n], color=rgb[i % n])
+        tf.raycast_colors(shard.tiles, shard.model, poses[i % n], intr)
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for s in range(steps):
+        i = (args.warmup + s) % n
+        shard.step(depth[i], poses[i], color=rgb[i])
+        tf.raycast_colors(shard.tiles, shard.model, poses[i], intr)
+    b.record()
+    barrier()
+    ms = a.elapsed_time(b) / steps
+    del shard
+    torch.cuda.empty_cache()
+    return {"frames_per_s": 1000.0 / ms, "ms_per_step": ms, "steps": steps,
+            "path": "ShardedFusion.step(depth, pose, color=rgb) + raycast_colors, inputs resident",
+            "note": "colour is not in the reference; no L2 flush between steps"}
 
 
 def run_e2e(args, tf, nat, torch, dist, rank, world, intr, spec, params, poses, host_frames,

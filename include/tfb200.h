@@ -67,6 +67,11 @@ typedef struct TfVolume {
                                   AND of their bricks' flags */
     float summary_threshold;
     int32_t reserved;
+    uint8_t *color_dev;  /* optional (NULL = none): uchar4[n][n][n] = (r, g, b, w),
+                            the running mean of the RGB observations of the
+                            voxel while it lay in the truncation band, w their
+                            count (saturating at 255).  Not in the reference
+                            (SPEC.md:8): the rule is this library's own. */
 } TfVolume;
 
 /* Pinhole intrinsics of one pyramid level (geometry.py:27-57). */
@@ -147,6 +152,18 @@ int tf_integrate(const TfVolume *vols, int nvol, const double *depth_dev,
                  double sample_weight, void *workspace_dev, size_t workspace_bytes,
                  uint64_t *stats_dev, void *stream);
 
+/* tf_integrate with colour: rgb_dev (uint8 [H][W][3], NULL = none) is fused
+ * into the color_dev of every volume that has one.  A voxel's colour takes the
+ * observation of the pixel its TSDF update used, only when that update lies
+ * in the truncation band (sdf < tau, i.e. not clamped): c <- rint((w c + o) /
+ * (w + 1)) per channel in float32, w <- min(w + 1, 255).  TSDF and weights are
+ * exactly those of tf_integrate. */
+int tf_integrate_rgb(const TfVolume *vols, int nvol, const double *depth_dev,
+                     const uint8_t *rgb_dev, const TfCamera *cam, const double r_cw[9],
+                     const double t_cw[3], const double cam_center[3], double tau,
+                     double max_weight, double sample_weight, void *workspace_dev,
+                     size_t workspace_bytes, uint64_t *stats_dev, void *stream);
+
 /* ---- raycast: replaces _kernels.raycast_kernel (_kernels.py:266-451) with
  * its helpers _sample / _scan_crossing / _hit_wins, called by tsdf.raycast
  * (tsdf.py:193-225), fused over `nvol` volumes sharing one voxel size.
@@ -166,6 +183,15 @@ int tf_trilinear_sample(const TfVolume *vol, const double *points_dev, int64_t n
 /* ---- free-space brick summaries (see TfVolume.brick_bad_dev). */
 float tf_good_threshold(double tau);
 int tf_brick_summary(const TfVolume *vol, void *stream);
+
+/* Colours of a rendered ray map: for every pixel with a finite distance the
+ * hit point o + t d (the raycast's own arithmetic) is looked up in the first
+ * volume (in `vols` order) whose cell around it has all 8 corner colours
+ * observed (w > 0): trilinear RGB in float32 into colors_dev (float32
+ * [H][W][3]); 0 elsewhere.  Not in the reference. */
+int tf_raycast_colors(const TfVolume *vols, int nvol, const TfCamera *cam, const double r_wc[9],
+                      const double cam_center[3], const double *dist_dev, float *colors_dev,
+                      void *stream);
 
 /* ---- raymap merge: _hit_wins (_kernels.py:246-263) of a partial map into
  * `dst` (the cross-GPU reduction of DESIGN.md "Multi-GPU"). */

@@ -30,7 +30,7 @@ class TfVolume(ctypes.Structure):
     _fields_ = [("voxels_dev", _c_p), ("n", _c_i64), ("origin", _c_i64 * 3),
                 ("voxel_size", _c_d), ("brick_state_dev", _c_p), ("brick_flags_dev", _c_p),
                 ("summary_threshold", ctypes.c_float),
-                ("reserved", ctypes.c_int32)]
+                ("reserved", ctypes.c_int32), ("color_dev", _c_p)]
 
 
 class TfCamera(ctypes.Structure):
@@ -87,6 +87,9 @@ _SIGNATURES = {
     "tf_integrate_workspace_size": (_c_sz, [_VOL, _c_int, _CAM]),
     "tf_integrate": (_c_int, [_VOL, _c_int, _c_p, _CAM, _c_p, _c_p, _c_p, _c_d, _c_d, _c_d,
                               _c_p, _c_sz, _c_p, _c_p]),
+    "tf_integrate_rgb": (_c_int, [_VOL, _c_int, _c_p, _c_p, _CAM, _c_p, _c_p, _c_p, _c_d, _c_d, _c_d,
+                                  _c_p, _c_sz, _c_p, _c_p]),
+    "tf_raycast_colors": (_c_int, [_VOL, _c_int, _CAM, _c_p, _c_p, _c_p, _c_p, _c_p]),
     "tf_raycast": (_c_int, [_VOL, _c_int, _CAM, _c_d, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
                             _c_p, _c_p]),
     "tf_trilinear_sample": (_c_int, [_VOL, _c_p, _c_i64, _c_p, _c_p, _c_p]),
@@ -186,11 +189,12 @@ def camera(intr) -> TfCamera:
 
 def volume_struct(voxels: torch.Tensor, n: int, origin, voxel_size: float,
                   brick_state: torch.Tensor | None = None, brick_flags: torch.Tensor | None = None,
-                  threshold: float = 0.0) -> TfVolume:
+                  threshold: float = 0.0, color: torch.Tensor | None = None) -> TfVolume:
     o = np.asarray(origin, dtype=np.int64)
     return TfVolume(ptr(voxels), int(n), (_c_i64 * 3)(int(o[0]), int(o[1]), int(o[2])),
                     float(voxel_size), ptr(brick_state) if brick_state is not None else None,
-                    ptr(brick_flags) if brick_flags is not None else None, float(threshold), 0)
+                    ptr(brick_flags) if brick_flags is not None else None, float(threshold), 0,
+                    ptr(color) if color is not None else None)
 
 
 class _Workspace:

@@ -67,6 +67,7 @@ struct FrameGeom {
     float r32[9];
     float fx32, fy32, cx32, cy32, tau32, w32, h32;
     float good_t;  // free-space summary threshold for this tau
+    const uint8_t *rgb;  // colour frame (tf_integrate_rgb) or null
 };
 
 // brick summary maintained by this call for volume `vol`?
@@ -566,7 +567,8 @@ __global__ void __launch_bounds__(256) brick_free_kernel(
 __device__ __forceinline__ int update_voxel(float2 *__restrict__ vox, int64_t lin, double gx,
                                             double gy, double gz,
                                             const double2 *__restrict__ table,
-                                            const FrameGeom &f, unsigned *dbad = nullptr) {
+                                            const FrameGeom &f, unsigned *dbad = nullptr,
+                                            uint8_t *color = nullptr) {
     const double *R = f.r_cw.m;
     const double pcx = dot3_plus(R[0], gx, R[1], gy, R[2], gz, f.t_cw.v[0]);  // :104
     const double pcy = dot3_plus(R[3], gx, R[4], gy, R[5], gz, f.t_cw.v[1]);  // :105
@@ -595,6 +597,19 @@ __device__ __forceinline__ int update_voxel(float2 *__restrict__ vox, int64_t li
     const float2 nv = make_float2(__double2float_rn(t_new), __double2float_rn(w_new));
     vox[lin] = nv;
     if (dbad) *dbad = voxel_state(nv, f.good_t) - voxel_state(old, f.good_t);
+    if (color && f.rgb && sdf < f.tau) {
+        // colour running mean while in the truncation band (tfb200.h, tf_integrate_rgb)
+        uchar4 *cp = reinterpret_cast<uchar4 *>(color) + lin;
+        const uchar4 c = *cp;
+        const uint8_t *o = f.rgb + 3 * ((int64_t)vf * f.width + (int64_t)uf);
+        const float w = (float)c.w, w1 = w + 1.0f;
+        uchar4 nc;
+        nc.x = (unsigned char)rintf(__fdiv_rn(__fadd_rn(__fmul_rn(w, (float)c.x), (float)o[0]), w1));
+        nc.y = (unsigned char)rintf(__fdiv_rn(__fadd_rn(__fmul_rn(w, (float)c.y), (float)o[1]), w1));
+        nc.z = (unsigned char)rintf(__fdiv_rn(__fadd_rn(__fmul_rn(w, (float)c.z), (float)o[2]), w1));
+        nc.w = c.w == 255 ? 255 : (unsigned char)(c.w + 1);
+        *cp = nc;
+    }
     return 1;
 }
 
@@ -634,7 +649,7 @@ __global__ void __launch_bounds__(256) brick_update_exact_kernel(
                     swept += 1;
                     unsigned db = 0;
                     const int64_t lin = vox_index(n, z, y, x);
-                    updates += update_voxel(vox, lin, gx, gy, gz, table, f, &db);
+                    updates += update_voxel(vox, lin, gx, gy, gz, table, f, &db, vol.color_dev);
                     if (db && keeps_summary(vol, f)) summary_add(vol, lin, db);
                 }
             }
@@ -652,8 +667,8 @@ __global__ void __launch_bounds__(256) brick_update_exact_kernel(
 __device__ __noinline__ int update_voxel_slow(float2 *__restrict__ vox, int64_t lin, double gx,
                                               double gy, double gz,
                                               const double2 *__restrict__ table,
-                                              const FrameGeom &f, unsigned *dbad) {
-    return update_voxel(vox, lin, gx, gy, gz, table, f, dbad);
+                                              const FrameGeom &f, unsigned *dbad, uint8_t *color) {
+    return update_voxel(vox, lin, gx, gy, gz, table, f, dbad, color);
 }
 
 // ---- float32 screening ------------------------------------------------------
@@ -945,7 +960,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                     } else {  // queue full: exact update in place (still exact)
                         const double gz = dmul((double)((int64_t)(z0 + zz) + vol.origin[2]), vs);
                         unsigned db = 0;
-                        updates += update_voxel_slow(vox, (int64_t)lin, gx, gy, gz, table, f, &db);
+                        updates += update_voxel_slow(vox, (int64_t)lin, gx, gy, gz, table, f, &db,
+                                                     vol.color_dev);
                         dbad += db;
                     }
                 }
@@ -994,7 +1010,7 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
         unsigned db = 0;
         updates += update_voxel((float2 *)vol.voxels_dev, lin, dmul((double)(x + vol.origin[0]), vs),
                                 dmul((double)(y + vol.origin[1]), vs),
-                                dmul((double)(z + vol.origin[2]), vs), table, f, &db);
+                                dmul((double)(z + vol.origin[2]), vs), table, f, &db, vol.color_dev);
         if (db && keeps_summary(vol, f)) {
             summary_add(vol, lin, db);
             const int64_t nb = bt.nb[v];
@@ -1221,6 +1237,15 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
                             const double cam_center[3], double tau, double max_weight,
                             double sample_weight, void *workspace, size_t workspace_bytes,
                             uint64_t *stats, void *stream_) {
+    return tf_integrate_rgb(vols, nvol, depth, nullptr, cam, r_cw, t_cw, cam_center, tau, max_weight,
+                            sample_weight, workspace, workspace_bytes, stats, stream_);
+}
+
+extern "C" int tf_integrate_rgb(const TfVolume *vols, int nvol, const double *depth, const uint8_t *rgb,
+                                const TfCamera *cam, const double r_cw[9], const double t_cw[3],
+                                const double cam_center[3], double tau, double max_weight,
+                                double sample_weight, void *workspace, size_t workspace_bytes,
+                                uint64_t *stats, void *stream_) {
     cudaStream_t stream = (cudaStream_t)stream_;
     if (nvol == 0) return TF_OK;
     if (!vols || nvol < 0 || !depth || !cam || !r_cw || !t_cw || !cam_center || !workspace)
@@ -1281,6 +1306,7 @@ extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
     f.max_w = max_weight;
     f.sw = sample_weight;
     f.sw_tau = sample_weight * tau;  // IEEE double product, as the reference's sw * clamped
+    f.rgb = rgb;
     for (int i = 0; i < 9; ++i) f.r32[i] = (float)r_cw[i];
     f.fx32 = (float)cam->fx;
     f.fy32 = (float)cam->fy;

@@ -1197,6 +1197,57 @@ __global__ void raymap_vertices_kernel(const __grid_constant__ RayGeom g, const 
     for (int a = 0; a < 3; ++a) vert[3 * i + a] = v[a];
 }
 
+// colour at a rendered hit (tf_raycast_colors): the hit point from t with the
+// raycast's arithmetic, then the first volume whose cell around it has all
+// 8 corner colours observed, trilinear in float32
+__global__ void raycast_colors_kernel(const __grid_constant__ VolumeTable vt, const __grid_constant__ RayGeom g,
+                                      const double *__restrict__ dist, float *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.width * g.height) return;
+    const int64_t py = i / g.width, px = i - py * g.width;
+    const double t = dist[i];
+    float rgb[3] = {0.f, 0.f, 0.f};
+    if (t < INFINITY) {
+        double d[3];
+        ray_direction(g, px, py, d);
+        const double h[3] = {dadd(g.cam.v[0], dmul(t, d[0])), dadd(g.cam.v[1], dmul(t, d[1])),
+                             dadd(g.cam.v[2], dmul(t, d[2]))};
+        for (int v = 0; v < vt.count; ++v) {
+            const TfVolume &vol = vt.vol[v];
+            if (!vol.color_dev) continue;
+            double q[3], fl[3];
+            bool inside = true;
+            for (int a = 0; a < 3; ++a) {
+                q[a] = dsub(ddiv(h[a], vol.voxel_size), (double)vol.origin[a]);
+                fl[a] = floor(q[a]);
+                inside = inside && fl[a] >= 0.0 && fl[a] <= (double)(vol.n - 2);
+            }
+            if (!inside) continue;
+            const int64_t n = vol.n, x = (int64_t)fl[0], y = (int64_t)fl[1], z = (int64_t)fl[2];
+            const uchar4 *c = reinterpret_cast<const uchar4 *>(vol.color_dev) + (z * n + y) * n + x;
+            const uchar4 k[8] = {c[0], c[1], c[n], c[n + 1], c[n * n], c[n * n + 1], c[n * n + n],
+                                 c[n * n + n + 1]};
+            bool seen = true;
+            for (int j = 0; j < 8; ++j) seen = seen && k[j].w > 0;
+            if (!seen) continue;
+            const float fx = (float)(q[0] - fl[0]), fy = (float)(q[1] - fl[1]), fz = (float)(q[2] - fl[2]);
+            const float w8[8] = {(1 - fx) * (1 - fy) * (1 - fz), fx * (1 - fy) * (1 - fz),
+                                 (1 - fx) * fy * (1 - fz),       fx * fy * (1 - fz),
+                                 (1 - fx) * (1 - fy) * fz,       fx * (1 - fy) * fz,
+                                 (1 - fx) * fy * fz,             fx * fy * fz};
+            for (int j = 0; j < 8; ++j) {
+                rgb[0] += w8[j] * (float)k[j].x;
+                rgb[1] += w8[j] * (float)k[j].y;
+                rgb[2] += w8[j] * (float)k[j].z;
+            }
+            break;
+        }
+    }
+    out[3 * i + 0] = rgb[0];
+    out[3 * i + 1] = rgb[1];
+    out[3 * i + 2] = rgb[2];
+}
+
 }  // namespace tf
 
 using namespace tf;
@@ -1370,4 +1421,29 @@ extern "C" int tf_trilinear_sample(const TfVolume *vol, const double *pts, int64
     trilinear_sample_kernel<<<(unsigned)((npts + 127) / 128), 128, 0, (cudaStream_t)stream_>>>(
         *vol, pts, npts, values, valid);
     return tf_check_launch("trilinear_sample_kernel");
+}
+
+extern "C" int tf_raycast_colors(const TfVolume *vols, int nvol, const TfCamera *cam, const double r_wc[9],
+                                 const double cam_center[3], const double *dist, float *colors, void *stream_) {
+    if (!cam || !r_wc || !cam_center || !dist || !colors || nvol < 0 || (nvol > 0 && !vols))
+        return tf_set_error(TF_EINVAL, "tf_raycast_colors: bad argument");
+    RayGeom g{};
+    for (int i = 0; i < 9; ++i) g.r_wc.m[i] = r_wc[i];
+    for (int i = 0; i < 3; ++i) g.cam.v[i] = cam_center[i];
+    g.fx = cam->fx;
+    g.fy = cam->fy;
+    g.cx = cam->cx;
+    g.cy = cam->cy;
+    g.width = cam->width;
+    g.height = cam->height;
+    const int64_t npix = cam->width * cam->height;
+    if (npix <= 0) return TF_OK;
+    // the first volume in order with a coloured cell wins: all volumes go in one launch
+    if (nvol > TFB200_MAX_VOLUMES_PER_LAUNCH)
+        return tf_set_error(TF_EINVAL, "tf_raycast_colors: more than %d volumes", TFB200_MAX_VOLUMES_PER_LAUNCH);
+    VolumeTable vt{};
+    vt.count = nvol;
+    for (int v = 0; v < nvol; ++v) vt.vol[v] = vols[v];
+    raycast_colors_kernel<<<(unsigned)((npix + 255) / 256), 256, 0, (cudaStream_t)stream_>>>(vt, g, dist, colors);
+    return tf_check_launch("raycast_colors_kernel");
 }

@@ -143,11 +143,14 @@ class ShardedFusion:
 
     def __init__(self, keys: Sequence, voxels_per_side: int, side_length: float,
                  params: FusionParams, intr: CameraIntrinsics, rank: int = 0, world: int = 1,
-                 group=None) -> None:
+                 group=None, color: bool = False) -> None:
         self.rank, self.world, self.group = rank, world, group
         self.params, self.intr = params, intr
         self.keys = owned_keys(keys, rank, world)
         self.tiles = [TsdfSubvolume.empty(k, voxels_per_side, side_length) for k in self.keys]
+        if color:
+            for t in self.tiles:
+                t.enable_color()
         self.partial = RayMap.empty(intr)
         self.model = RayMap.empty(intr)
         self.stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device=self.partial.distance_dev.device)
@@ -158,8 +161,8 @@ class ShardedFusion:
                                    device=self.partial.distance_dev.device)
         self._packed[..., 0] = float("inf")
 
-    def step(self, depth: torch.Tensor, pose: Pose) -> RayMap:
-        integrate_volumes(self.tiles, depth, pose, self.intr, self.params, self.stats)
+    def step(self, depth: torch.Tensor, pose: Pose, color=None) -> RayMap:
+        integrate_volumes(self.tiles, depth, pose, self.intr, self.params, self.stats, color=color)
         self.partial.reset()
         raycast_volumes(self.tiles, pose, self.intr, self.partial, self.params, self.stats)
         if self.world == 1:

@@ -133,6 +133,15 @@ class TsdfSubvolume:
         self.brick_bad: torch.Tensor | None = None    # packed per-brick state
         self.brick_flags: torch.Tensor | None = None  # derived per-brick flags
         self._summary_t: float | None = None
+        # optional colour (not in the reference): uint8 [n, n, n, 4] = (r, g, b, count)
+        self.color: torch.Tensor | None = None
+
+    def enable_color(self) -> "TsdfSubvolume":
+        """Give the volume a colour channel (all unobserved); returns it."""
+        if self.color is None:
+            n = self.voxels_per_side
+            self.color = torch.zeros((n, n, n, 4), dtype=torch.uint8, device=self.voxels.device)
+        return self
 
     def invalidate_summary(self) -> None:
         """Call after writing ``voxels`` directly (outside the package's kernels)."""
@@ -217,10 +226,10 @@ class TsdfSubvolume:
         """ABI descriptor; with ``tau`` it carries the brick summary for that truncation."""
         if tau is None:
             return nat.volume_struct(self.voxels, self.voxels_per_side, self.origin_voxel,
-                                     self.voxel_size)
+                                     self.voxel_size, color=self.color)
         bad, thr = self._summary_for(tau)
         return nat.volume_struct(self.voxels, self.voxels_per_side, self.origin_voxel,
-                                 self.voxel_size, bad, self.brick_flags, thr)
+                                 self.voxel_size, bad, self.brick_flags, thr, color=self.color)
 
     def __repr__(self) -> str:
         return (f"TsdfSubvolume(origin_voxel={self.origin_voxel!r}, "
@@ -260,16 +269,30 @@ def _vol_array(vols: Sequence[TsdfSubvolume], tau: float | None = None):
 # integration (tsdf.py:110-144)
 # ---------------------------------------------------------------------------
 
+def device_rgb(color, intr: CameraIntrinsics) -> torch.Tensor:
+    """A colour frame (uint8 [H, W, 3], numpy or tensor) as a contiguous device tensor."""
+    t = color if isinstance(color, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(color))
+    if t.dtype != torch.uint8 or tuple(t.shape) != (intr.height, intr.width, 3):
+        raise ValueError(f"colour frame must be uint8 {(intr.height, intr.width, 3)}")
+    return t.to(nat.device()).contiguous()
+
+
 def integrate_volumes(volumes: Sequence[TsdfSubvolume], frame, pose: Pose,
                       intr: CameraIntrinsics, params: FusionParams,
-                      stats: torch.Tensor | None = None) -> None:
-    """Fuse one depth frame into every volume with one fused launch sequence."""
+                      stats: torch.Tensor | None = None, color=None) -> None:
+    """Fuse one depth frame into every volume with one fused launch sequence.
+
+    ``color`` (uint8 [H, W, 3]) is fused into the volumes that have a colour
+    channel (``enable_color``): a running mean of the observations while the
+    voxel lies in the truncation band (include/tfb200.h, tf_integrate_rgb).
+    """
     volumes = list(volumes)
     if not volumes:
         return
     depth = device_depth(frame)
     if tuple(depth.shape) != (intr.height, intr.width):
         raise ValueError("frame size does not match intrinsics")
+    rgb = device_rgb(color, intr) if color is not None else None
     for v in volumes:
         v._device_read()
     inverse = pose.invert()
@@ -278,24 +301,42 @@ def integrate_volumes(volumes: Sequence[TsdfSubvolume], frame, pose: Pose,
     L = nat.lib()
     need = L.tf_integrate_workspace_size(arr, len(volumes), cam)
     ws = nat.workspace.get(need)
-    nat.check(L.tf_integrate(arr, len(volumes), nat.ptr(depth), cam, nat.mat9(inverse.rotation),
-                             nat.vec3(inverse.translation), nat.vec3(pose.translation),
-                             float(params.truncation), float(params.max_weight),
-                             float(params.sample_weight), nat.ptr(ws), ws.numel(),
-                             nat.ptr(stats if stats is not None else nat.stats.buffer()),
-                             nat.stream_handle()), "tf_integrate")
+    nat.check(L.tf_integrate_rgb(arr, len(volumes), nat.ptr(depth), nat.ptr(rgb) if rgb is not None else None,
+                                 cam, nat.mat9(inverse.rotation),
+                                 nat.vec3(inverse.translation), nat.vec3(pose.translation),
+                                 float(params.truncation), float(params.max_weight),
+                                 float(params.sample_weight), nat.ptr(ws), ws.numel(),
+                                 nat.ptr(stats if stats is not None else nat.stats.buffer()),
+                                 nat.stream_handle()), "tf_integrate")
     for v in volumes:
         v._device_written()
 
 
 def integrate(subvolume: TsdfSubvolume, frame: DepthFrame, pose: Pose, intr: CameraIntrinsics,
-              params: FusionParams) -> TsdfSubvolume:
-    """Fuse one depth frame into the subvolume in place; returns it."""
+              params: FusionParams, color=None) -> TsdfSubvolume:
+    """Fuse one depth frame (and optionally its colour) into the subvolume in place; returns it."""
     data = frame.data if isinstance(frame, DepthFrame) else frame
     if tuple(data.shape) != (intr.height, intr.width):  # tsdf.py:124-125
         raise ValueError("frame size does not match intrinsics")
-    integrate_volumes([subvolume], frame, pose, intr, params)
+    integrate_volumes([subvolume], frame, pose, intr, params, color=color)
     return subvolume
+
+
+def raycast_colors(volumes: Sequence[TsdfSubvolume], raymap: "RayMap", pose: Pose,
+                   intr: CameraIntrinsics) -> torch.Tensor:
+    """Colours (float32 [H, W, 3], device) of a ray map rendered from ``pose``:
+    trilinear colour at each hit from the first listed volume with the hit
+    cell's 8 corners coloured; 0 without a hit or colour (tf_raycast_colors)."""
+    volumes = [v for v in volumes if v.color is not None]
+    out = torch.zeros((intr.height, intr.width, 3), dtype=torch.float32, device=nat.device())
+    if not volumes:
+        return out
+    raymap._device_read()
+    arr = _vol_array(volumes)
+    nat.check(nat.lib().tf_raycast_colors(arr, len(volumes), nat.camera(intr), nat.mat9(pose.rotation),
+                                          nat.vec3(pose.translation), nat.ptr(raymap.distance_dev),
+                                          nat.ptr(out), nat.stream_handle()), "tf_raycast_colors")
+    return out
 
 
 def trilinear_sample(subvolume: TsdfSubvolume, point: Array) -> float | None:
