@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .geometry import (CameraIntrinsics, DepthFrame, Pose, rotation_from_axis_angle)
+from .geometry import CameraIntrinsics, Pose, rotation_from_axis_angle
 from .tsdf import RayMap, device_depth
 
 

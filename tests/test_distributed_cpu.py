@@ -11,7 +11,6 @@ all partials in any order (the reference's order-free invariant).
 import os
 import socket
 
-import numpy as np
 import pytest
 import torch
 import torch.distributed as dist

@@ -5,7 +5,6 @@ import sys
 from pathlib import Path
 
 import numpy as np
-import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1511_07106_b200 as tf  # noqa: E402
