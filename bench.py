@@ -230,6 +230,8 @@ def run_ours(args) -> None:
         barrier()
     lib.tf_profile_enable(0)
     launches = lib.tf_launch_count() - launches0
+    if shard._peer is not None and shard._peer.error():
+        raise RuntimeError("peer-memory ray-map reduction: a flag wait timed out")
     ms_total = sum(a.elapsed_time(b) for a, b in zip(starts, stops))
     prof = nat.profile_read()
     st = shard.stats.cpu().numpy()
@@ -287,7 +289,11 @@ def run_ours(args) -> None:
         "metric": METRIC, "value": value, "unit": "voxel-updates/s",
         "frames_per_s": fps, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_desc(world),
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(config_desc(world), **({"raymap_exchange": {
+            "p2p": "peer-memory reduce kernel (csrc/comm.cu, CUDA IPC over NVLink)",
+            "collective": "NCCL row-block all-to-all + merge + all-gather"}[shard.exchange]}
+            if world > 1 else {})),
         "voxel_updates_per_frame": updates_per_frame,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,

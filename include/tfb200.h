@@ -273,6 +273,53 @@ int tf_endpoint_cells(const double *depth_dev, const TfCamera *cam, const double
                       const double t_wc[3], double block_side, int64_t *cells_dev,
                       void *stream);
 
+/* ---- multi-GPU ray-map reduction over peer memory (the
+ * survey's tf_comm_init / tf_exchange_* rows).  One process per GPU.  Each
+ * rank owns a "region" in its own HBM holding its partial ray map (what its
+ * tf_raycast over its own volumes writes) and its copy of the merged model;
+ * the regions are mapped into every peer with CUDA IPC (NVLink / NVSwitch).
+ * tf_comm_reduce_raymap is ONE kernel per rank: it signals "partial ready"
+ * to every peer, waits for theirs, folds the peers' (t, normal) records of
+ * its row block with the _hit_wins total order in rank order
+ * (_kernels.py:246-263; equal to the single-GPU raycast over all volumes,
+ * bit for bit), takes the winner's vertex, stores the merged rows straight
+ * into every rank's model (all-gather by stores), and its last block
+ * signals "done"; a one-warp kernel then waits for every peer's "done", after
+ * which the local model is complete and every peer has finished reading the
+ * local partial.  Replaces the NCCL all-to-all + merge + all-gather of the
+ * row-block exchange (distributed.rowblock_exchange).  Waits time out after
+ * TF_COMM_TIMEOUT_NS (error flag, tf_comm_error) instead of hanging.
+ *
+ * Region layout (offsets in bytes, TF_COMM_* indices): flags, partial
+ * distance [H][W] f64, partial vertices [H][W][3], partial normals
+ * [H][W][3], model distance, model vertices, model normals. */
+#define TF_COMM_HANDLE_BYTES 64
+#define TF_COMM_MAX_RANKS 64
+#define TF_COMM_TIMEOUT_NS 20000000000ull
+enum { TF_COMM_FLAGS = 0, TF_COMM_PART_DIST, TF_COMM_PART_VERT, TF_COMM_PART_NORM,
+       TF_COMM_MODEL_DIST, TF_COMM_MODEL_VERT, TF_COMM_MODEL_NORM, TF_COMM_NSECTIONS };
+enum { TF_COMM_NOWAIT = 1u /* no flags, no waits: emulated ranks on one device (tests) */ };
+typedef struct TfComm TfComm;
+
+/* Allocates (cudaMalloc on the current device) and initialises this rank's
+ * region: no-hit partial and model (+inf distance, zero vectors), zero flags. */
+int tf_comm_create(int rank, int world, int64_t width, int64_t height, TfComm **out);
+/* Region base and section offsets (TF_COMM_NSECTIONS entries). */
+int tf_comm_layout(const TfComm *comm, void **base, int64_t *offsets);
+/* IPC handle of this rank's region (TF_COMM_HANDLE_BYTES bytes). */
+int tf_comm_export(const TfComm *comm, void *handle);
+/* Maps every peer's region (handles: world x TF_COMM_HANDLE_BYTES, rank
+ * order; this rank's own entry is ignored). */
+int tf_comm_import(TfComm *comm, const void *handles);
+/* Test hook: the comms of `world` emulated ranks living in this process on
+ * one device see each other's regions directly (no IPC). */
+int tf_comm_link_local(TfComm *const *comms, int world);
+/* The reduction described above, asynchronous on `stream`. */
+int tf_comm_reduce_raymap(TfComm *comm, unsigned flags, void *stream);
+/* Synchronous read of the region's error flag (1 = a wait timed out). */
+int tf_comm_error(const TfComm *comm, int *error);
+int tf_comm_destroy(TfComm *comm);
+
 #ifdef __cplusplus
 }
 #endif

@@ -109,7 +109,22 @@ _SIGNATURES = {
     "tf_extract_count": (_c_int, [_VOL, _c_p, _c_sz, _c_p, _c_p]),
     "tf_extract_emit": (_c_int, [_VOL, _c_p, _c_sz, _c_p, _c_p, _c_p]),
     "tf_endpoint_cells": (_c_int, [_c_p, _CAM, _c_p, _c_p, _c_d, _c_p, _c_p]),
+    "tf_comm_create": (_c_int, [_c_int, _c_int, _c_i64, _c_i64, ctypes.POINTER(_c_p)]),
+    "tf_comm_layout": (_c_int, [_c_p, ctypes.POINTER(_c_p), _c_p]),
+    "tf_comm_export": (_c_int, [_c_p, _c_p]),
+    "tf_comm_import": (_c_int, [_c_p, _c_p]),
+    "tf_comm_link_local": (_c_int, [_c_p, _c_int]),
+    "tf_comm_reduce_raymap": (_c_int, [_c_p, ctypes.c_uint, _c_p]),
+    "tf_comm_error": (_c_int, [_c_p, ctypes.POINTER(_c_int)]),
+    "tf_comm_destroy": (_c_int, [_c_p]),
 }
+
+# peer-memory ray-map reduction (tfb200.h "multi-GPU ray-map reduction")
+COMM_HANDLE_BYTES = 64
+COMM_MAX_RANKS = 64
+(COMM_FLAGS, COMM_PART_DIST, COMM_PART_VERT, COMM_PART_NORM, COMM_MODEL_DIST, COMM_MODEL_VERT,
+ COMM_MODEL_NORM, COMM_NSECTIONS) = range(8)
+COMM_NOWAIT = 1
 
 EXPORTED = tuple(_SIGNATURES)
 

@@ -21,7 +21,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libtfb200.so"
-SOURCES = ["api.cu", "integrate.cu", "raycast.cu", "icp.cu", "extract.cu"]
+SOURCES = ["api.cu", "integrate.cu", "raycast.cu", "icp.cu", "extract.cu", "comm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler",
               "-fPIC,-ffp-contract=off", "-Xptxas", "-v"]

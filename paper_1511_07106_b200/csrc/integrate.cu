@@ -33,6 +33,8 @@
 // and the only HBM traffic per voxel update is its 8-byte read + 8-byte write.
 #include <math.h>
 
+#include <cmath>
+
 #include "tf_common.cuh"
 
 #include <mutex>
@@ -63,6 +65,8 @@ struct FrameGeom {
     int64_t width, height;
     double tau, max_w, sw;
     double sw_tau;  // RN(sample_weight * tau): the free-space numerator term (:132)
+    int unit_sw;    // sample_weight == 1 and max_weight finite: float32 weight path
+    float max_w32;  // RN32(max_weight)
     // float32 copies for the conservative screen
     float r32[9];
     float fx32, fy32, cx32, cy32, tau32, w32, h32;
@@ -462,8 +466,8 @@ __global__ void __launch_bounds__(256) brick_cull_kernel(
     }
 }
 
-__device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f, const double *rcp);
-__device__ __forceinline__ void fill_rcp(double *rcp);
+__device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f, const double2 *rcp);
+__device__ __forceinline__ void fill_rcp(double2 *rcp);
 __device__ __forceinline__ unsigned free_state_delta(float2 old, float2 nv, float t);
 
 // Certified free-space bricks: every voxel gets the clamped-to-tau running
@@ -475,7 +479,7 @@ __global__ void __launch_bounds__(256) brick_free_kernel(
     const __grid_constant__ FrameGeom f, const uint32_t *__restrict__ list,
     const unsigned int *__restrict__ list_count, const int fixed_point,
     unsigned long long *__restrict__ stats, const ChangedList changed) {
-    __shared__ double rcp[257];
+    __shared__ double2 rcp[257];
     fill_rcp(rcp);
     const unsigned count = *list_count;
     const int lane = threadIdx.x & 31;
@@ -483,8 +487,10 @@ __global__ void __launch_bounds__(256) brick_free_kernel(
     const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
     const float2 fixed = make_float2(f.tau32, (float)f.max_w);
     unsigned updates = 0, nop = 0;
+    unsigned g_next = warp < count ? list[warp] : 0u;  // next brick id, loaded one brick ahead
     for (unsigned i = warp; i < count; i += nwarps) {
-        const unsigned g = list[i];
+        const unsigned g = g_next;
+        if (i + nwarps < count) g_next = list[i + nwarps];
         const int vi = find_volume(bt, g);
         const TfVolume &vol = vt.vol[vi];
         const unsigned n = (unsigned)vol.n, nb = (unsigned)bt.nb[vi];
@@ -715,10 +721,10 @@ __device__ __forceinline__ unsigned free_state_delta(float2 old, float2 nv, floa
 // RN(a / b), the IEEE quotient, as long as nothing underflows (|a| >= 2^-900
 // guards that).  Any other b takes the IEEE division.  Checked against
 // __ddiv_rn by tf_debug_weight_division_check (GPU test).
-__device__ __forceinline__ double div_weight(double a, double b, const double *__restrict__ rcp) {
+__device__ __forceinline__ double div_weight(double a, double b, const double2 *__restrict__ rcp) {
     const int bi = __double2int_rz(b);
     if (bi >= 1 && bi <= 256 && (double)bi == b && fabs(a) >= 0x1p-900) {
-        const double r = rcp[bi];
+        const double r = rcp[bi].x;
         const double q = dmul(a, r);
         const double e = __fma_rn(-q, b, a);
         return __fma_rn(e, r, q);
@@ -726,16 +732,43 @@ __device__ __forceinline__ double div_weight(double a, double b, const double *_
     return ddiv(a, b);
 }
 
-// RN(1/b) for b = 0..256 into shared memory (entry 0 unused); every thread of
-// the block must call it
-__device__ __forceinline__ void fill_rcp(double *rcp) {
-    for (int b = threadIdx.x; b <= 256; b += blockDim.x) rcp[b] = b ? __drcp_rn((double)b) : 0.0;
+// RN(1/b) for b = 1..256, evaluated at compile time (IEEE division, correctly
+// rounded; entry 0 unused).  Computing it per block with __drcp_rn cost ~10 %
+// of the update kernel's stall samples (block start-up behind a barrier).
+struct RcpTable {
+    double v[257];
+    constexpr RcpTable() : v{} {
+        for (int b = 1; b <= 256; ++b) v[b] = 1.0 / (double)b;
+    }
+};
+__device__ const RcpTable g_rcp_table = RcpTable();
+
+// {RN(1/b), b} into shared memory; every thread of the block must call it
+__device__ __forceinline__ void fill_rcp(double2 *rcp) {
+    for (int b = threadIdx.x; b <= 256; b += blockDim.x) rcp[b] = make_double2(g_rcp_table.v[b], (double)b);
     __syncthreads();
 }
 
 // running weighted mean with clamped == tau (_kernels.py:129-133)
-__device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f, const double *rcp) {
+__device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f, const double2 *rcp) {
     const float wv = fmulr(old.y, old.x);
+    if (f.unit_sw) {
+        // sample_weight 1 and an integral weight w in [0, 255]: w + 1 is exact
+        // in float32, so the float64 weight sum, its integer test and
+        // RN32(min(max_w, w + 1)) = min(RN32(max_w), w + 1) need no float64
+        // conversions; the quotient is div_weight's (same operations).
+        // m = 2^23 + w for integral 0 <= w < 2^23: its low bits index the table.
+        const float m = __fadd_rn(old.y, 8388608.0f);
+        if (old.y >= 0.0f && old.y <= 255.0f && __fsub_rn(m, 8388608.0f) == old.y) {
+            const double2 rb = rcp[__float_as_uint(m) - 0x4AFFFFFFu];  // {RN(1/(w+1)), w+1}
+            const double a = dadd((double)wv, f.sw_tau);
+            if (fabs(a) >= 0x1p-900) {
+                const double q = dmul(a, rb.x);
+                const double t = __fma_rn(__fma_rn(-q, rb.y, a), rb.x, q);
+                return make_float2(__double2float_rn(t), fminf(__fadd_rn(old.y, 1.0f), f.max_w32));
+            }
+        }
+    }
     const double w_sum = dadd((double)old.y, f.sw);
     const double t_new = div_weight(dadd((double)wv, f.sw_tau), w_sum, rcp);
     const double w_new = f.max_w < w_sum ? f.max_w : w_sum;
@@ -744,7 +777,7 @@ __device__ __forceinline__ float2 free_update(float2 old, const FrameGeom &f, co
 
 // test hook: random (a, b) pairs through div_weight vs __ddiv_rn
 __global__ void weight_division_check_kernel(int64_t n, unsigned long long seed, unsigned long long *mismatches) {
-    __shared__ double rcp[257];
+    __shared__ double2 rcp[257];
     fill_rcp(rcp);
     unsigned long long bad = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -776,7 +809,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const unsigned int *__restrict__ active_count, unsigned long long *__restrict__ queue,
     unsigned long long *__restrict__ queue_count, const unsigned long long queue_cap,
     const int fixed_point, unsigned long long *__restrict__ stats, const ChangedList changed) {
-    __shared__ double rcp[257];
+    __shared__ double2 rcp[257];
     fill_rcp(rcp);
     const unsigned count = *active_count;
     const int lane = threadIdx.x & 31;
@@ -789,8 +822,10 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const float k3u = 9.6e-7f * f.fx32, k3v = 9.6e-7f * f.fy32;
     const float k2u = 9.6e-7f * (fabsf(f.cx32) + 2.f), k2v = 9.6e-7f * (fabsf(f.cy32) + 2.f);
     unsigned updates = 0, swept = 0, nop = 0, col_skipped = 0, depth_skipped = 0, all_free = 0;
+    unsigned g_next = warp < count ? active[warp] : 0u;  // next brick id, loaded one brick ahead
     for (unsigned i = warp; i < count; i += nwarps) {
-        const unsigned g = active[i];
+        const unsigned g = g_next;
+        if (i + nwarps < count) g_next = active[i + nwarps];
         const int vi = find_volume(bt, g);
         const TfVolume &vol = vt.vol[vi];
         const unsigned n = (unsigned)vol.n, nb = (unsigned)bt.nb[vi];
@@ -1306,6 +1341,8 @@ extern "C" int tf_integrate_rgb(const TfVolume *vols, int nvol, const double *de
     f.max_w = max_weight;
     f.sw = sample_weight;
     f.sw_tau = sample_weight * tau;  // IEEE double product, as the reference's sw * clamped
+    f.unit_sw = sample_weight == 1.0 && std::isfinite(max_weight);
+    f.max_w32 = (float)max_weight;
     f.rgb = rgb;
     for (int i = 0; i < 9; ++i) f.r32[i] = (float)r_cw[i];
     f.fx32 = (float)cam->fx;

@@ -43,11 +43,7 @@ struct Hit {
 
 // _hit_wins (_kernels.py:246-263)
 __device__ __forceinline__ bool hit_wins(const Hit &h, const Hit &cur) {
-    if (h.t < cur.t) return true;
-    if (h.t > cur.t) return false;
-    if (h.nx != cur.nx) return h.nx > cur.nx;
-    if (h.ny != cur.ny) return h.ny > cur.ny;
-    return h.nz > cur.nz;
+    return record_wins(h.t, h.nx, h.ny, h.nz, cur.t, cur.nx, cur.ny, cur.nz);
 }
 
 // 8 corners of the cell with minimum corner (ix, iy, iz): c[z][y][x] order

@@ -68,6 +68,18 @@ __device__ __forceinline__ unsigned voxel_state(float2 v, float t) {
     return (unsigned)voxel_bad(v, t) | ((v.y > 0.0f ? 1u : 0u) << 16);
 }
 
+// _hit_wins (_kernels.py:246-263) on (t, normal) records: the smaller t wins;
+// on an exact tie the larger nx, then ny, then nz.  A strict total order, so
+// folds over partial ray maps are order-free.
+__device__ __forceinline__ bool record_wins(double t, double nx, double ny, double nz, double ct,
+                                            double cnx, double cny, double cnz) {
+    if (t < ct) return true;
+    if (t > ct) return false;
+    if (nx != cnx) return nx > cnx;
+    if (ny != cny) return ny > cny;
+    return nz > cnz;
+}
+
 // Warp-aggregated 64-bit counter add (integer: order-independent, exact).
 __device__ __forceinline__ void warp_count_add(unsigned long long *dst, unsigned long long v) {
 #pragma unroll

@@ -20,6 +20,14 @@ The paper's CPU<->GPU volume swapping becomes ownership:
   reference's order-free invariant, test_acceptance.py:349-361).  Traffic
   per rank and frame: 2 x 32 B x pixels x (world - 1) / world.
 
+On GPUs that can map each other's memory (NVLink / NVSwitch) the exchange,
+the fold and the all-gather are one kernel per rank over peer memory
+(``PeerExchange``, csrc/comm.cu): each rank's raycast writes its partial into
+a region its peers have mapped, and the reduce kernel reads its row block of
+every partial and stores the merged rows into every rank's model; the NCCL
+row-block exchange above remains for ranks without peer access (and runs the
+same host schedule on gloo in the CPU tests).
+
 ICP runs replicated on every rank over the merged model (no per-iteration
 collective).  The host-side schedule is backend-agnostic and is tested with
 gloo on CPU (tests/test_distributed_cpu.py); the CUDA merge is tested on one
@@ -28,6 +36,8 @@ GPU.
 
 from __future__ import annotations
 
+import ctypes
+import weakref
 from typing import Callable, Sequence
 
 import torch
@@ -134,16 +144,118 @@ def merge_packed_cuda(acc: torch.Tensor, other: torch.Tensor) -> None:
                                                nat.stream_handle()), "tf_raymap_merge_packed")
 
 
+def exchange_handles(handle: bytes, world: int, group=None) -> list[bytes]:
+    """All-gather of every rank's IPC handle bytes, in rank order (host plumbing)."""
+    if world == 1:
+        return [handle]
+    out: list = [None] * world
+    dist.all_gather_object(out, handle, group=group)
+    return out
+
+
+def peer_exchange_supported(world: int, group=None) -> bool:
+    """True when every rank sits on its own CUDA device and every pair of
+    those devices can map each other's memory (one node, NVLink / NVSwitch)."""
+    if world == 1 or not torch.cuda.is_available():
+        return False
+    mine = torch.cuda.current_device()
+    devs: list = [None] * world
+    dist.all_gather_object(devs, mine, group=group)
+    ok = len(set(devs)) == world and all(
+        torch.cuda.can_device_access_peer(mine, d) for d in devs if d != mine)
+    oks: list = [None] * world
+    dist.all_gather_object(oks, bool(ok), group=group)
+    return all(oks)
+
+
+class _RegionView:
+    """CUDA array interface over a section of a comm region (float64); keeps
+    the owning PeerExchange alive while any tensor views it."""
+
+    def __init__(self, address: int, shape: tuple, owner) -> None:
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8",
+                                         "data": (address, False), "version": 2,
+                                         "strides": None}
+        self._owner = owner
+
+
+class PeerExchange:
+    """Peer-memory ray-map reduction across the ranks' GPUs (csrc/comm.cu).
+
+    ``partial`` is the RayMap this rank's raycast writes (in the region its
+    peers map); after ``reduce()`` every rank's ``model`` holds the merged map,
+    equal bit for bit to the single-GPU raycast over all volumes.
+    ``connect()`` maps the peers' regions (IPC handles all-gathered over the
+    process group).  ``link_local`` wires emulated ranks of one process on one
+    device instead (tests; their reductions run with ``nowait=True``).
+    """
+
+    def __init__(self, intr: CameraIntrinsics, rank: int, world: int) -> None:
+        lib = nat.lib()
+        h = ctypes.c_void_p()
+        nat.check(lib.tf_comm_create(rank, world, intr.width, intr.height, ctypes.byref(h)),
+                  "tf_comm_create")
+        self._h = h
+        weakref.finalize(self, lib.tf_comm_destroy, ctypes.c_void_p(h.value))
+        self.rank, self.world = rank, world
+        base = ctypes.c_void_p()
+        offs = (ctypes.c_int64 * nat.COMM_NSECTIONS)()
+        nat.check(lib.tf_comm_layout(h, ctypes.byref(base), offs), "tf_comm_layout")
+        dev = nat.device()
+        hh, ww = intr.height, intr.width
+
+        def view(sec: int, shape: tuple) -> torch.Tensor:
+            return torch.as_tensor(_RegionView(base.value + offs[sec], shape, self), device=dev)
+
+        self.partial = RayMap(device_tensors=(view(nat.COMM_PART_VERT, (hh, ww, 3)),
+                                              view(nat.COMM_PART_NORM, (hh, ww, 3)),
+                                              view(nat.COMM_PART_DIST, (hh, ww))))
+        self.model = RayMap(device_tensors=(view(nat.COMM_MODEL_VERT, (hh, ww, 3)),
+                                            view(nat.COMM_MODEL_NORM, (hh, ww, 3)),
+                                            view(nat.COMM_MODEL_DIST, (hh, ww))))
+
+    def export(self) -> bytes:
+        buf = ctypes.create_string_buffer(nat.COMM_HANDLE_BYTES)
+        nat.check(nat.lib().tf_comm_export(self._h, buf), "tf_comm_export")
+        return buf.raw
+
+    def connect(self, group=None) -> None:
+        handles = exchange_handles(self.export(), self.world, group)
+        nat.check(nat.lib().tf_comm_import(self._h, b"".join(handles)), "tf_comm_import")
+
+    @staticmethod
+    def link_local(exchanges: Sequence["PeerExchange"]) -> None:
+        arr = (ctypes.c_void_p * len(exchanges))(*[e._h.value for e in exchanges])
+        nat.check(nat.lib().tf_comm_link_local(arr, len(exchanges)), "tf_comm_link_local")
+
+    def reduce(self, nowait: bool = False) -> RayMap:
+        nat.check(nat.lib().tf_comm_reduce_raymap(self._h, nat.COMM_NOWAIT if nowait else 0,
+                                                  nat.stream_handle()), "tf_comm_reduce_raymap")
+        self.model._device_written()
+        return self.model
+
+    def error(self) -> int:
+        """1 when a flag wait timed out (synchronous read)."""
+        e = ctypes.c_int()
+        nat.check(nat.lib().tf_comm_error(self._h, ctypes.byref(e)), "tf_comm_error")
+        return e.value
+
+
 class ShardedFusion:
     """The per-rank slice of a static multi-volume map.
 
     ``step(depth, pose)`` integrates this rank's volumes, raycasts them into a
-    partial map and merges all ranks' partials into ``model`` on every rank.
+    partial map and merges all ranks' partials into ``model`` on every rank:
+    over peer memory (``exchange="p2p"``, one kernel, the default when every
+    pair of the ranks' GPUs can map each other) or with the NCCL row-block
+    exchange (``exchange="collective"``).
     """
 
     def __init__(self, keys: Sequence, voxels_per_side: int, side_length: float,
                  params: FusionParams, intr: CameraIntrinsics, rank: int = 0, world: int = 1,
-                 group=None, color: bool = False) -> None:
+                 group=None, color: bool = False, exchange: str = "auto") -> None:
+        if exchange not in ("auto", "p2p", "collective"):
+            raise ValueError(f"exchange must be 'auto', 'p2p' or 'collective', not {exchange!r}")
         self.rank, self.world, self.group = rank, world, group
         self.params, self.intr = params, intr
         self.keys = owned_keys(keys, rank, world)
@@ -160,6 +272,14 @@ class ShardedFusion:
         self._packed = torch.zeros((world * b, intr.width, 4), dtype=torch.float64,
                                    device=self.partial.distance_dev.device)
         self._packed[..., 0] = float("inf")
+        self.exchange = "none" if world == 1 else exchange
+        self._peer = None
+        if exchange == "auto" and world > 1:
+            self.exchange = "p2p" if peer_exchange_supported(world, group) else "collective"
+        if self.exchange == "p2p":
+            self._peer = PeerExchange(intr, rank, world)
+            self._peer.connect(group)
+            self.partial, self.model = self._peer.partial, self._peer.model
 
     def step(self, depth: torch.Tensor, pose: Pose, color=None) -> RayMap:
         integrate_volumes(self.tiles, depth, pose, self.intr, self.params, self.stats, color=color)
@@ -168,6 +288,8 @@ class ShardedFusion:
         if self.world == 1:
             self.model, self.partial = self.partial, self.model
             return self.model
+        if self._peer is not None:
+            return self._peer.reduce()
         h, w = self.intr.height, self.intr.width
         packed = self._packed
         packed[:h, :, 0] = self.partial.distance_dev

@@ -167,3 +167,29 @@ def test_gloo_world2_broadcast_gather_merge():
         assert all(torch.equal(a, b) for a, b in zip(acc, out[0]["merged"]))
     # volume ownership is disjoint and complete
     assert sorted(out[0]["keys"] + out[1]["keys"]) == list(range(8))
+
+
+def _handles_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1511_07106_b200.distributed import exchange_handles, peer_exchange_supported
+        out[rank] = (exchange_handles(bytes([rank + 1]) * 64, world),
+                     peer_exchange_supported(world))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_peer_handle_exchange(world):
+    """PeerExchange.connect's host plumbing: every rank gets every rank's IPC
+    handle in rank order; without distinct CUDA devices the peer-memory path
+    is not selected (the NCCL/gloo row-block exchange runs instead)."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_handles_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    want = [bytes([r + 1]) * 64 for r in range(world)]
+    for r in range(world):
+        assert out[r][0] == want
+        assert out[r][1] is False

@@ -69,3 +69,53 @@ def test_two_ranks_equal_one_process():
     for r in range(world):
         for got, ref in zip(out[r][:3], want):
             assert torch.equal(got, ref)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_exchange_emulated_ranks_equal_one_process(world):
+    """The peer-memory reduction (csrc/comm.cu) with `world` emulated ranks in
+    this process on the one GPU: each rank integrates and raycasts only the
+    volumes it owns into its region's partial, then each rank's reduce kernel
+    runs in turn without flag waits (TF_COMM_NOWAIT; ranks that wait on one
+    another never share a GPU).  Every rank's model equals the single-process
+    raycast over all volumes bit for bit, frame after frame."""
+    from paper_1511_07106_b200.distributed import PeerExchange, ShardedFusion, owned_keys
+    tf, intr, spec, params, poses, frames = _setup()
+    single = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length, params,
+                           intr, 0, 1)
+    peers = [PeerExchange(intr, r, world) for r in range(world)]
+    PeerExchange.link_local(peers)
+    tiles = [[tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length)
+              for k in owned_keys(spec.keys, r, world)] for r in range(world)]
+    assert sum(len(t) for t in tiles) == len(spec.keys)
+    for f, p in zip(frames, poses):
+        want = single.step(f, p)
+        for r in range(world):
+            tf.integrate_volumes(tiles[r], f, p, intr, params)
+            peers[r].partial.reset()
+            tf.raycast_volumes(tiles[r], p, intr, peers[r].partial, params)
+        for r in range(world):
+            peers[r].reduce(nowait=True)
+        torch.cuda.synchronize()
+        assert torch.isfinite(want.distance_dev).sum().item() > 3000
+        for r in range(world):
+            m = peers[r].model
+            assert torch.equal(m.distance_dev, want.distance_dev)
+            assert torch.equal(m.vertices_dev, want.vertices_dev)
+            assert torch.equal(m.normals_dev, want.normals_dev)
+    assert all(pe.error() == 0 for pe in peers)
+
+
+def test_peer_exchange_region_and_handle():
+    """A fresh region reads as the empty ray map; the IPC handle exports."""
+    from paper_1511_07106_b200.distributed import PeerExchange
+    tf, intr, *_ = _setup()
+    pe = PeerExchange(intr, 1, 2)
+    for m in (pe.partial, pe.model):
+        assert torch.equal(m.distance_dev, torch.full((intr.height, intr.width), float("inf"),
+                                                      dtype=torch.float64, device="cuda"))
+        assert not m.vertices_dev.any() and not m.normals_dev.any()
+    h = pe.export()
+    assert len(h) == 64 and any(h)
+    with pytest.raises(RuntimeError):
+        pe.reduce()  # rank 0's region is not mapped
