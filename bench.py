@@ -319,6 +319,8 @@ def run_ours(args) -> None:
                       "active_bricks_per_frame": sum_over_ranks(int(st[nat.STAT_ACTIVE_BRICKS])) / args.steps,
                       "free_space_bricks_per_frame": sum_over_ranks(int(st[nat.STAT_FREE_BRICKS])) / args.steps,
                       "general_bricks_all_free_per_frame": sum_over_ranks(int(st[nat.STAT_GENERAL_ALL_FREE])) / args.steps,
+                      "general_parts_all_free_per_frame": sum_over_ranks(int(st[nat.STAT_PART_ALL_FREE])) / args.steps,
+                      "general_parts_all_skip_per_frame": sum_over_ranks(int(st[nat.STAT_PART_ALL_SKIP])) / args.steps,
                       "total_bricks": sum_over_ranks(int(st[nat.STAT_TOTAL_BRICKS])) // max(args.steps, 1)},
         "raycast": {"exact_samples_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_SAMPLES])) / args.steps,
                     "certification_failures": sum_over_ranks(int(st[nat.STAT_CERT_FAILURES])),

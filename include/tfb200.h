@@ -100,6 +100,8 @@ enum {
     TF_STAT_COOP_RAYS = 15,   /* rays finished by the warp-cooperative raycast pass */
     TF_STAT_FREE_KERNEL_UPDATES = 16, /* voxel updates by the certified free-space brick kernel */
     TF_STAT_EXACT_UPDATES = 17,       /* voxel updates by the exact (reference arithmetic) queue */
+    TF_STAT_PART_ALL_FREE = 18,  /* 8x4x4 parts of general bricks whose voxels all were free-space updates */
+    TF_STAT_PART_ALL_SKIP = 19,  /* 8x4x4 parts of general bricks whose voxels all were rejected */
     TF_STAT_COUNT = 24
 };
 

@@ -65,6 +65,8 @@ STAT_GENERAL_ALL_FREE = 14
 STAT_COOP_RAYS = 15
 STAT_FREE_KERNEL_UPDATES = 16
 STAT_EXACT_UPDATES = 17
+STAT_PART_ALL_FREE = 18
+STAT_PART_ALL_SKIP = 19
 STAT_COUNT = 24
 
 _VOL = ctypes.POINTER(TfVolume)

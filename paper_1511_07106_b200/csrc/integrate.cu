@@ -42,7 +42,8 @@
 namespace tf {
 
 constexpr int kBrick = 8;         // brick edge in voxels
-constexpr int kTile = 16;         // finest depth-mip tile in pixels
+constexpr int kTile = 16;         // frame_prep block edge in pixels
+constexpr int kCellShift = 2;     // finest depth-mip cell: 4x4 pixels (level l: 4 << l)
 constexpr int kMaxMipLevels = 12;
 
 struct MipDesc {
@@ -104,7 +105,7 @@ static MipDesc make_mip(int64_t width, int64_t height) {
     int64_t off = 0;
     int l = 0;
     for (; l < kMaxMipLevels; ++l) {
-        int64_t cell = (int64_t)kTile << l;
+        int64_t cell = (int64_t)1 << (kCellShift + l);
         m.tiles_x[l] = (width + cell - 1) / cell;
         m.tiles_y[l] = (height + cell - 1) / cell;
         m.offset[l] = off;
@@ -159,35 +160,70 @@ __global__ void __launch_bounds__(256) frame_prep_kernel(
         table32[vi * width + ui] = make_float2(d32, __double2float_rn(rs));
         qk = fkey(d > 0.0 ? __double2float_rd((d - tau) * rs) : -INFINITY);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) qk = min(qk, __shfl_xor_sync(0xffffffffu, qk, o));
-    // block max of the (non-negative) depths
-    double v = d > 0.0 ? d : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    __shared__ double wmax[8];
-    __shared__ unsigned wq[8];
+    // max-depth (IEEE bits of non-negative doubles order like the values) and
+    // min free-space key mips: the cells of sizes 4, 8 and 16 px lie inside
+    // this block and are written directly; coarser ones take atomics
+    __shared__ unsigned long long sd[kTile * kTile];
+    __shared__ unsigned sq[kTile * kTile];
+    __shared__ unsigned long long cd[21];  // 16 + 4 + 1 in-block cells
+    __shared__ unsigned cq[21];
     const int t = threadIdx.y * kTile + threadIdx.x;
-    if ((t & 31) == 0) {
-        wmax[t >> 5] = v;
-        wq[t >> 5] = qk;
+    sd[t] = (unsigned long long)__double_as_longlong(d > 0.0 ? d : 0.0);
+    sq[t] = qk;
+    __syncthreads();
+    if (t < 16) {  // 4x4-pixel cells
+        const int ix = t & 3, iy = t >> 2;
+        unsigned long long b = 0;
+        unsigned q = 0xffffffffu;
+        for (int yy = 0; yy < 4; ++yy)
+            for (int xx = 0; xx < 4; ++xx) {
+                const int s2 = (iy * 4 + yy) * kTile + ix * 4 + xx;
+                b = sd[s2] > b ? sd[s2] : b;
+                q = min(q, sq[s2]);
+            }
+        cd[t] = b;
+        cq[t] = q;
     }
     __syncthreads();
-    if (t == 0) {
-        double b = wmax[0];
-        unsigned qb = wq[0];
-        for (int i = 1; i < 8; ++i) {
-            b = fmax(b, wmax[i]);
-            qb = min(qb, wq[i]);
+    if (t < 4) {  // 8x8
+        const int ix = t & 1, iy = t >> 1;
+        unsigned long long b = 0;
+        unsigned q = 0xffffffffu;
+        for (int k = 0; k < 4; ++k) {
+            const int c = (iy * 2 + (k >> 1)) * 4 + ix * 2 + (k & 1);
+            b = cd[c] > b ? cd[c] : b;
+            q = min(q, cq[c]);
         }
-        qmip[m.offset[0] + (int64_t)blockIdx.y * m.tiles_x[0] + blockIdx.x] = qb;
-        for (int l = 1; l < m.levels; ++l)
-            atomicMin(&qmip[m.offset[l] + ((int64_t)blockIdx.y >> l) * m.tiles_x[l] + ((int64_t)blockIdx.x >> l)], qb);
-        const unsigned long long bits = (unsigned long long)__double_as_longlong(b);
-        mip[m.offset[0] + (int64_t)blockIdx.y * m.tiles_x[0] + blockIdx.x] = bits;
-        for (int l = 1; l < m.levels; ++l) {
-            const int64_t tx = (int64_t)blockIdx.x >> l, ty = (int64_t)blockIdx.y >> l;
-            atomicMax(&mip[m.offset[l] + ty * m.tiles_x[l] + tx], bits);
+        cd[16 + t] = b;
+        cq[16 + t] = q;
+    }
+    __syncthreads();
+    if (t == 0) {  // 16x16
+        unsigned long long b = 0;
+        unsigned q = 0xffffffffu;
+        for (int k = 0; k < 4; ++k) {
+            b = cd[16 + k] > b ? cd[16 + k] : b;
+            q = min(q, cq[16 + k]);
+        }
+        cd[20] = b;
+        cq[20] = q;
+    }
+    __syncthreads();
+    if (t < 21) {
+        const int l = t < 16 ? 0 : (t < 20 ? 1 : 2);
+        const int per = 4 >> l, k = t - (l == 0 ? 0 : (l == 1 ? 16 : 20));
+        const int64_t gx = (int64_t)blockIdx.x * per + (k % per), gy = (int64_t)blockIdx.y * per + (k / per);
+        if (l < m.levels && gx < m.tiles_x[l] && gy < m.tiles_y[l]) {
+            mip[m.offset[l] + gy * m.tiles_x[l] + gx] = cd[t];
+            qmip[m.offset[l] + gy * m.tiles_x[l] + gx] = cq[t];
+        }
+    }
+    if (t == 0) {
+        for (int l = 3; l < m.levels; ++l) {
+            const int64_t tx = (int64_t)blockIdx.x >> (l - 2), ty = (int64_t)blockIdx.y >> (l - 2);
+            if (tx >= m.tiles_x[l] || ty >= m.tiles_y[l]) break;
+            atomicMax(&mip[m.offset[l] + ty * m.tiles_x[l] + tx], cd[20]);
+            atomicMin(&qmip[m.offset[l] + ty * m.tiles_x[l] + tx], cq[20]);
         }
     }
 }
@@ -199,11 +235,12 @@ __device__ double rect_max_depth(const unsigned long long *__restrict__ mip, con
                                  int64_t u0, int64_t u1, int64_t v0, int64_t v1) {
     int l = 0;
     while (l + 1 < m.levels &&
-           (((u1 >> (4 + l)) - (u0 >> (4 + l)) + 1) > 4 || ((v1 >> (4 + l)) - (v0 >> (4 + l)) + 1) > 4))
+           (((u1 >> (kCellShift + l)) - (u0 >> (kCellShift + l)) + 1) > 4 ||
+            ((v1 >> (kCellShift + l)) - (v0 >> (kCellShift + l)) + 1) > 4))
         ++l;
     unsigned long long best = 0;
-    const int64_t tx0 = u0 >> (4 + l), tx1 = u1 >> (4 + l);
-    const int64_t ty0 = v0 >> (4 + l), ty1 = v1 >> (4 + l);
+    const int64_t tx0 = u0 >> (kCellShift + l), tx1 = u1 >> (kCellShift + l);
+    const int64_t ty0 = v0 >> (kCellShift + l), ty1 = v1 >> (kCellShift + l);
     for (int64_t ty = ty0; ty <= ty1; ++ty)
         for (int64_t tx = tx0; tx <= tx1; ++tx) {
             const unsigned long long b = __ldg(&mip[m.offset[l] + ty * m.tiles_x[l] + tx]);
@@ -218,11 +255,12 @@ __device__ float rect_min_q(const unsigned *__restrict__ qmip, const MipDesc &m,
                             int64_t u1, int64_t v0, int64_t v1) {
     int l = 0;
     while (l + 1 < m.levels &&
-           (((u1 >> (4 + l)) - (u0 >> (4 + l)) + 1) > 4 || ((v1 >> (4 + l)) - (v0 >> (4 + l)) + 1) > 4))
+           (((u1 >> (kCellShift + l)) - (u0 >> (kCellShift + l)) + 1) > 4 ||
+            ((v1 >> (kCellShift + l)) - (v0 >> (kCellShift + l)) + 1) > 4))
         ++l;
     unsigned best = 0xffffffffu;
-    for (int64_t ty = v0 >> (4 + l); ty <= (v1 >> (4 + l)); ++ty)
-        for (int64_t tx = u0 >> (4 + l); tx <= (u1 >> (4 + l)); ++tx)
+    for (int64_t ty = v0 >> (kCellShift + l); ty <= (v1 >> (kCellShift + l)); ++ty)
+        for (int64_t tx = u0 >> (kCellShift + l); tx <= (u1 >> (kCellShift + l)); ++tx)
             best = min(best, __ldg(&qmip[m.offset[l] + ty * m.tiles_x[l] + tx]));
     return fkey_dec(best);
 }
@@ -822,6 +860,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const float k3u = 9.6e-7f * f.fx32, k3v = 9.6e-7f * f.fy32;
     const float k2u = 9.6e-7f * (fabsf(f.cx32) + 2.f), k2v = 9.6e-7f * (fabsf(f.cy32) + 2.f);
     unsigned updates = 0, swept = 0, nop = 0, col_skipped = 0, depth_skipped = 0, all_free = 0;
+    unsigned part_free = 0, part_skip = 0;
     unsigned g_next = warp < count ? active[warp] : 0u;  // next brick id, loaded one brick ahead
     for (unsigned i = warp; i < count; i += nwarps) {
         const unsigned g = g_next;
@@ -981,6 +1020,18 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                     }
                     if (cls[j] == kExact) exact_mask |= 1u << (zb + j);
                 }
+                if (stats) {  // the batch is one 8x4x4 part of the brick
+                    bool lf = true, ls = true;
+#pragma unroll
+                    for (int j = 0; j < kZBatch; ++j) {
+                        lf = lf && cls[j] == kFree;
+                        ls = ls && cls[j] == kSkip;
+                    }
+                    lf = __all_sync(0xffffffffu, lf);
+                    ls = __all_sync(0xffffffffu, ls);
+                    part_free += lf;
+                    part_skip += ls;
+                }
             }
             // undecided voxels of the column go to the exact kernel
             if (__any_sync(0xffffffffu, exact_mask != 0u) && exact_mask) {
@@ -1020,6 +1071,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         warp_count_add(&stats[TF_STAT_COL_SKIPPED], col_skipped);
         warp_count_add(&stats[TF_STAT_DEPTH_SKIPPED], depth_skipped);
         if (lane == 0 && all_free) atomicAdd(&stats[TF_STAT_GENERAL_ALL_FREE], (unsigned long long)all_free);
+        if (lane == 0 && part_free) atomicAdd(&stats[TF_STAT_PART_ALL_FREE], (unsigned long long)part_free);
+        if (lane == 0 && part_skip) atomicAdd(&stats[TF_STAT_PART_ALL_SKIP], (unsigned long long)part_skip);
     }
 }
 
@@ -1318,7 +1371,7 @@ extern "C" int tf_integrate_rgb(const TfVolume *vols, int nvol, const double *de
         cudaMemsetAsync(qmip, 0xff, (size_t)m.total * sizeof(unsigned), stream) != cudaSuccess)
         return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
     dim3 pblock(kTile, kTile);
-    dim3 pgrid((unsigned)m.tiles_x[0], (unsigned)m.tiles_y[0]);
+    dim3 pgrid((unsigned)((cam->width + kTile - 1) / kTile), (unsigned)((cam->height + kTile - 1) / kTile));
     frame_prep_kernel<<<pgrid, pblock, 0, stream>>>(depth, table, table32, mip, qmip, tau, m, cam->fx,
                                                     cam->fy, cam->cx, cam->cy, cam->width,
                                                     cam->height);
