@@ -364,7 +364,7 @@ def run_color(args, tf, torch, spec, params, intr, poses, scene, barrier) -> dic
     from paper_1511_07106_b200.distributed import ShardedFusion
     from paper_1511_07106_b200.synth import render_rgb
 
-    steps = min(args.steps, 50)
+    steps = args.steps  # the same frame mix as the device-timed loop (early frames are slower)
     n = len(poses)
     depth = [torch.from_numpy(scene.render_depth(p, intr).data).cuda() for p in poses]
     rgb = [torch.from_numpy(render_rgb(scene, p, intr)).cuda() for p in poses]
@@ -396,7 +396,7 @@ def run_e2e(args, tf, nat, torch, dist, rank, world, intr, spec, params, poses, 
 
     nframes = len(poses)
     pinned = [torch.from_numpy(f).pin_memory() for f in host_frames]
-    steps = min(args.steps, 50)
+    steps = args.steps  # the same frame mix as the device-timed loop (early frames are slower)
     if world == 1:
         cfg = tf.RunConfig(side_length=4.08, resolution=1020, resident_resolution=510,
                            use_groundtruth=True, max_resident=8)
