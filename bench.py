@@ -27,6 +27,7 @@ restatement in oracle/, all host threads) on the same workload and metric.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -457,15 +458,29 @@ def run_config2(args, tf, nat, torch, barrier, max_over_ranks) -> dict:
     scene = demo_scene()
     steps = min(args.steps, 63)
     frames = [torch.from_numpy(scene.render_depth(p, intr).data).cuda() for p in poses[:steps + 1]]
+    # an untimed pass over the same frames first (allocator growth, workspaces,
+    # first launches), then the timed pass with a fresh pipeline
+    warm = tf.FusionPipeline(cfg, tempfile.mkdtemp(prefix="tfb200_c2w_"))
+    warm.step(frames[0], poses[0])
+    for i in range(1, steps + 1):
+        warm.step(frames[i])
+    torch.cuda.synchronize()
+    del warm
     pipe = tf.FusionPipeline(cfg, tempfile.mkdtemp(prefix="tfb200_c2_"))
-    pipe.step(frames[0], poses[0])   # frame 0 defines the world frame (warm-up)
+    pipe.step(frames[0], poses[0])   # frame 0 defines the world frame
+    gc.collect()
     barrier()
     pipe.stats.zero_()
+    gc.disable()  # no collector pause inside the 60-80 ms timed pass
     t0 = time.perf_counter()
     for i in range(1, steps + 1):
         pipe.step(frames[i])
+        if os.environ.get("TFB200_C2_TRACE"):
+            torch.cuda.synchronize()
+            print(f"config2 frame {i}: {1e3 * (time.perf_counter() - t0):.2f} ms", file=sys.stderr)
     barrier()
     sec = max_over_ranks(time.perf_counter() - t0)
+    gc.enable()
     ks = pipe.kernel_stats()
     lost = sum(1 for r in pipe.records[1:] if not r.tracked)
     err = max(float(np.abs(p.translation - q.translation).max())
