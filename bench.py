@@ -212,6 +212,8 @@ def run_ours(args) -> None:
     for i in range(args.warmup):
         shard.step(dev_frames[i % nframes], poses[i % nframes])
     barrier()
+    if shard._peer is not None and shard._peer.error():
+        raise RuntimeError("peer-memory ray-map reduction: a flag wait timed out (warm-up)")
 
     # ---- timed region: resident inputs, per-step events, L2 flushed between ----
     shard.stats.zero_()

@@ -91,11 +91,13 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
-// spin until *flag >= epoch; after the timeout raise the error flag and go on
+// spin until *flag >= epoch; after the timeout raise the error flag and go
+// on.  Once the flag is raised every later wait returns at once, so a broken
+// exchange costs one timeout, not one per frame (the host reports the error).
 __device__ void wait_flag(const unsigned long long *flag, unsigned long long epoch, unsigned *error) {
     const unsigned long long t0 = globaltimer_ns();
     while (ld_acquire_sys(flag) < epoch) {
-        if (globaltimer_ns() - t0 > TF_COMM_TIMEOUT_NS) {
+        if (*(volatile unsigned *)error || globaltimer_ns() - t0 > TF_COMM_TIMEOUT_NS) {
             atomicOr(error, 1u);
             return;
         }

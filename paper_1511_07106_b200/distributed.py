@@ -241,6 +241,32 @@ class PeerExchange:
         return e.value
 
 
+def _connect_peers(intr: CameraIntrinsics, rank: int, world: int, group, required: bool):
+    """Every rank's PeerExchange, mapped to every peer — or None on every rank
+    when any rank could not create, export or map a region (the ranks agree
+    through two all-gathers, so none is left waiting in a collective)."""
+    pe, handle = None, None
+    try:
+        pe = PeerExchange(intr, rank, world)
+        handle = pe.export()
+    except RuntimeError:
+        pe = None
+    handles = exchange_handles(handle, world, group)
+    ok = pe is not None and all(h is not None for h in handles)
+    if ok:
+        try:
+            nat.check(nat.lib().tf_comm_import(pe._h, b"".join(handles)), "tf_comm_import")
+        except RuntimeError:
+            ok = False
+    oks: list = [None] * world
+    dist.all_gather_object(oks, ok, group=group)
+    if all(oks):
+        return pe
+    if required:
+        raise RuntimeError("peer-memory exchange requested but a rank could not map its peers")
+    return None
+
+
 class ShardedFusion:
     """The per-rank slice of a static multi-volume map.
 
@@ -277,9 +303,11 @@ class ShardedFusion:
         if exchange == "auto" and world > 1:
             self.exchange = "p2p" if peer_exchange_supported(world, group) else "collective"
         if self.exchange == "p2p":
-            self._peer = PeerExchange(intr, rank, world)
-            self._peer.connect(group)
-            self.partial, self.model = self._peer.partial, self._peer.model
+            self._peer = _connect_peers(intr, rank, world, group, required=exchange == "p2p")
+            if self._peer is None:
+                self.exchange = "collective"
+            else:
+                self.partial, self.model = self._peer.partial, self._peer.model
 
     def step(self, depth: torch.Tensor, pose: Pose, color=None) -> RayMap:
         integrate_volumes(self.tiles, depth, pose, self.intr, self.params, self.stats, color=color)

@@ -193,3 +193,33 @@ def test_gloo_peer_handle_exchange(world):
     for r in range(world):
         assert out[r][0] == want
         assert out[r][1] is False
+
+
+def _connect_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1511_07106_b200.distributed import _connect_peers
+        from paper_1511_07106_b200.geometry import CameraIntrinsics
+        intr = CameraIntrinsics(100.0, 100.0, 31.5, 23.5, 64, 48)
+        got = _connect_peers(intr, rank, world, None, required=False)
+        try:
+            _connect_peers(intr, rank, world, None, required=True)
+            raised = False
+        except RuntimeError:
+            raised = True
+        out[rank] = (got is None, raised)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_peer_connect_agreement():
+    """No rank can map peer memory here (no GPU): every rank agrees to fall
+    back (None) or, when the peer path was required, every rank raises —
+    none is left waiting in a collective."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_connect_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert out[0] == (True, True) and out[1] == (True, True)
