@@ -1062,13 +1062,13 @@ __global__ void __launch_bounds__(128) raycast_coop_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ RayGeom g,
     double *__restrict__ out_dist, double *__restrict__ out_vert, double *__restrict__ out_norm,
     unsigned long long *__restrict__ stats, const unsigned *__restrict__ rescue,
-    const unsigned *__restrict__ rescue_count) {
+    const unsigned *__restrict__ rescue_count, const unsigned first) {
     const int lane = threadIdx.x & 31;
     const unsigned count = *rescue_count;
     const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
     unsigned long long samples = 0, hits = 0, exact_samples = 0;
-    for (unsigned i = warp; i < count; i += nwarps) {
+    for (unsigned i = first + warp; i < count; i += nwarps) {
         const int64_t p = rescue[i];
         const int64_t py = p / g.width, px = p - py * g.width;
         Hit best;
@@ -1126,6 +1126,103 @@ __global__ void __launch_bounds__(128) raycast_coop_kernel(
         atomicAdd(&stats[TF_STAT_EXACT_SAMPLES], exact_samples & ((1ull << 40) - 1));
         atomicAdd(&stats[TF_STAT_CERT_FAILURES], (exact_samples >> 40) & 15ull);
     }
+}
+
+// The first `cap` handed-over rays, split into (ray, volume) items, one warp
+// each: a ray's marches through different volumes are independent (each
+// returns its first accepted crossing whatever the running best is; the
+// nearest-entry order only lets the per-lane pass skip volumes), so they run
+// in parallel and raycast_coop_merge_kernel folds the per-volume hits with
+// _hit_wins — the same result, with the pass bounded by the slowest
+// ray-volume march instead of the slowest ray.  slots: 8 doubles per item
+// (t, hit xyz, normal xyz; t = +inf: no hit).
+__global__ void __launch_bounds__(128) raycast_coop_items_kernel(
+    const __grid_constant__ VolumeTable vt, const __grid_constant__ RayGeom g,
+    unsigned long long *__restrict__ stats, const unsigned *__restrict__ rescue,
+    const unsigned *__restrict__ rescue_count, const unsigned cap, double *__restrict__ slots) {
+    const int lane = threadIdx.x & 31;
+    const unsigned count = min(*rescue_count, cap);
+    const unsigned nitems = count * (unsigned)vt.count;
+    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+    unsigned long long samples = 0, exact_samples = 0;
+    for (unsigned i = warp; i < nitems; i += nwarps) {
+        const unsigned ray = i / (unsigned)vt.count;
+        const int v = (int)(i - ray * (unsigned)vt.count);
+        const int64_t p = rescue[ray];
+        const int64_t py = p / g.width, px = p - py * g.width;
+        double d[3];
+        ray_direction(g, px, py, d);
+        const double o[3] = {g.cam.v[0], g.cam.v[1], g.cam.v[2]};
+        Hit best{INFINITY, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        bool found = false;
+        int64_t jlo = 0, jhi = 0;
+        const TfVolume &vol = vt.vol[v];
+        if (ray_interval(vol, o, d, jlo, jhi)) {
+            Ray r;
+            FastRay fr;
+            if (setup_volume(g, vol, o, d, jhi, r, fr)) {
+                found = march_coop(fr, RayRef{&vol, &g}, (int)jlo, (int)jhi, (int)g.coarse, best, samples,
+                                   exact_samples);
+            } else {
+                found = march_volume(r, jlo, jhi, g.coarse, g.near_thresh, best);
+                samples += r.samples;
+                exact_samples += r.samples;
+            }
+        }
+        if (lane == 0) {
+            double *sl = slots + 8 * (size_t)i;
+            sl[0] = found ? best.t : INFINITY;
+            sl[1] = best.hx;
+            sl[2] = best.hy;
+            sl[3] = best.hz;
+            sl[4] = best.nx;
+            sl[5] = best.ny;
+            sl[6] = best.nz;
+        }
+    }
+    if (stats && lane == 0) {  // every lane counted the same item: lane 0 reports
+        atomicAdd(&stats[TF_STAT_RAY_SAMPLES], samples);
+        atomicAdd(&stats[TF_STAT_EXACT_SAMPLES], exact_samples & ((1ull << 40) - 1));
+        atomicAdd(&stats[TF_STAT_CERT_FAILURES], (exact_samples >> 40) & 15ull);
+    }
+}
+
+// one thread per split ray: fold its volumes' hits into the map (_hit_wins)
+__global__ void raycast_coop_merge_kernel(const int nvol, const unsigned *__restrict__ rescue,
+                                          const unsigned *__restrict__ rescue_count, const unsigned cap,
+                                          const double *__restrict__ slots, double *__restrict__ out_dist,
+                                          double *__restrict__ out_vert, double *__restrict__ out_norm,
+                                          unsigned long long *__restrict__ stats) {
+    const unsigned j = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned count = min(*rescue_count, cap);
+    unsigned long long hits = 0;
+    if (j < count) {
+        const int64_t p = rescue[j];
+        Hit best{out_dist[p], out_vert[3 * p], out_vert[3 * p + 1], out_vert[3 * p + 2],
+                 out_norm[3 * p], out_norm[3 * p + 1], out_norm[3 * p + 2]};
+        bool changed = false;
+        for (int v = 0; v < nvol; ++v) {
+            const double *sl = slots + 8 * ((size_t)j * nvol + v);
+            if (!(sl[0] < INFINITY)) continue;
+            const Hit h{sl[0], sl[1], sl[2], sl[3], sl[4], sl[5], sl[6]};
+            if (hit_wins(h, best)) {
+                best = h;
+                changed = true;
+            }
+        }
+        if (changed) {
+            hits = 1;
+            out_dist[p] = best.t;
+            out_vert[3 * p + 0] = best.hx;
+            out_vert[3 * p + 1] = best.hy;
+            out_vert[3 * p + 2] = best.hz;
+            out_norm[3 * p + 0] = best.nx;
+            out_norm[3 * p + 1] = best.ny;
+            out_norm[3 * p + 2] = best.nz;
+        }
+    }
+    if (stats) warp_count_add(&stats[TF_STAT_RAY_HITS], hits);
 }
 
 __global__ void raymap_merge_kernel(double *__restrict__ dd, double *__restrict__ dv,
@@ -1335,7 +1432,11 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
         unsigned long long *st = (unsigned long long *)stats;
         int64_t *clk = tf_ray_clock_buffer();
         const int64_t npix = cam->width * cam->height;
-        unsigned *rescue = rescue_buffer(stream, npix + 1);  // [0] = count, then pixel indices
+        // [0] = count, then pixel indices; then the per-(ray, volume) hit slots
+        // of the first kCoopSplitRays handed-over rays (8 doubles each)
+        constexpr unsigned kCoopSplitRays = 16384;
+        const int64_t slot_off = (npix + 1 + 63) / 64 * 64;  // words, 256-byte aligned
+        unsigned *rescue = rescue_buffer(stream, slot_off + (int64_t)kCoopSplitRays * vt.count * 16);
         if (!rescue || cudaMemsetAsync(rescue, 0, sizeof(unsigned), stream) != cudaSuccess)
             return tf_set_error(TF_ECUDA, "tf_raycast: cannot allocate the rescue list");
         auto launch = [&](auto kern, int bx, int by) {
@@ -1356,9 +1457,17 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
             int dev = 0, sms = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-void *pc = tf_profile_begin(TF_PROF_RAYCAST_COOP, stream);
+            void *pc = tf_profile_begin(TF_PROF_RAYCAST_COOP, stream);
+            double *slots = (double *)(rescue + slot_off);
+            raycast_coop_items_kernel<<<(unsigned)sms * 4, 128, 0, stream>>>(vt, g, st, rescue + 1, rescue,
+                                                                           kCoopSplitRays, slots);
+            if ((rc = tf_check_launch("raycast_coop_items_kernel"))) return rc;
+            raycast_coop_merge_kernel<<<kCoopSplitRays / 128, 128, 0, stream>>>(
+                vt.count, rescue + 1, rescue, kCoopSplitRays, slots, dist, vert, norm, st);
+            if ((rc = tf_check_launch("raycast_coop_merge_kernel"))) return rc;
+            // rays beyond the split capacity: one warp per whole ray (usually none)
             raycast_coop_kernel<<<(unsigned)sms * 4, 128, 0, stream>>>(vt, g, dist, vert, norm, st, rescue + 1,
-                                                                     rescue);
+                                                                     rescue, kCoopSplitRays);
             tf_profile_end(pc, stream);
             if ((rc = tf_check_launch("raycast_coop_kernel"))) return rc;
         }
