@@ -1465,8 +1465,9 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
             raycast_coop_merge_kernel<<<kCoopSplitRays / 128, 128, 0, stream>>>(
                 vt.count, rescue + 1, rescue, kCoopSplitRays, slots, dist, vert, norm, st);
             if ((rc = tf_check_launch("raycast_coop_merge_kernel"))) return rc;
-            // rays beyond the split capacity: one warp per whole ray (usually none)
-            raycast_coop_kernel<<<(unsigned)sms * 4, 128, 0, stream>>>(vt, g, dist, vert, norm, st, rescue + 1,
+            // rays beyond the split capacity: one warp per whole ray (usually
+            // none, so a small grid: the launch is nearly free when empty)
+            raycast_coop_kernel<<<(unsigned)sms, 128, 0, stream>>>(vt, g, dist, vert, norm, st, rescue + 1,
                                                                      rescue, kCoopSplitRays);
             tf_profile_end(pc, stream);
             if ((rc = tf_check_launch("raycast_coop_kernel"))) return rc;
