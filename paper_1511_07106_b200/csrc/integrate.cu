@@ -612,7 +612,7 @@ __device__ __forceinline__ int update_voxel(float2 *__restrict__ vox, int64_t li
                                             double gy, double gz,
                                             const double2 *__restrict__ table,
                                             const FrameGeom &f, unsigned *dbad = nullptr,
-                                            uint8_t *color = nullptr) {
+                                            uint8_t *color = nullptr, const float2 *old_in = nullptr) {
     const double *R = f.r_cw.m;
     const double pcx = dot3_plus(R[0], gx, R[1], gy, R[2], gz, f.t_cw.v[0]);  // :104
     const double pcy = dot3_plus(R[3], gx, R[4], gy, R[5], gz, f.t_cw.v[1]);  // :105
@@ -632,7 +632,7 @@ __device__ __forceinline__ int update_voxel(float2 *__restrict__ vox, int64_t li
     const double sdf = dsub(d, ddiv(dist, px.y));                               // :125
     if (sdf < -f.tau) return 0;                                                 // :126
     const double clamped = sdf < f.tau ? sdf : f.tau;                           // :128
-    const float2 old = vox[lin];
+    const float2 old = old_in ? *old_in : vox[lin];
     // numba types float(f32) as float32: the product is a float32 op (:129-132)
     const float wv = fmulr(old.y, old.x);
     const double w_sum = dadd((double)old.y, f.sw);                             // :131
@@ -1092,13 +1092,16 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
         const int v = (int)(e >> 40);
         const int64_t lin = (int64_t)(e & ((1ull << 40) - 1));
         const TfVolume &vol = vt.vol[v];
+        // the voxel's old value is loaded before the float64 projection, so its
+        // HBM round trip overlaps the arithmetic instead of following it
+        const float2 old = ((const float2 *)vol.voxels_dev)[lin];
         const int64_t n = vol.n;
         const int64_t x = lin % n, y = (lin / n) % n, z = lin / (n * n);
         const double vs = vol.voxel_size;
         unsigned db = 0;
         updates += update_voxel((float2 *)vol.voxels_dev, lin, dmul((double)(x + vol.origin[0]), vs),
                                 dmul((double)(y + vol.origin[1]), vs),
-                                dmul((double)(z + vol.origin[2]), vs), table, f, &db, vol.color_dev);
+                                dmul((double)(z + vol.origin[2]), vs), table, f, &db, vol.color_dev, &old);
         if (db && keeps_summary(vol, f)) {
             summary_add(vol, lin, db);
             const int64_t nb = bt.nb[v];
