@@ -999,7 +999,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                     cls[j] = c;
                 }
                 // D: load the voxels with a free-space update
-                const unsigned row = (z0 + zb) * n * n + y * n + x;  // < 2^32 for n <= 1625
+                const size_t row = ((size_t)(z0 + zb) * n + y) * n + x;
                 float2 old[kZBatch];
 #pragma unroll
                 for (int j = 0; j < kZBatch; ++j)
@@ -1042,7 +1042,9 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                     const unsigned zz = __ffs(m) - 1;
                     const unsigned long long lin = (unsigned long long)(z0 + zz) * n * n + (unsigned long long)y * n + x;
                     if (base + k < queue_cap) {
-                        queue[base + k] = ((unsigned long long)vi << 40) | lin;
+                        // (volume, z, y, x) packed 6 / 16 / 16 / 16 bits (n <= 65535)
+                        queue[base + k] = ((unsigned long long)vi << 48) | ((unsigned long long)(z0 + zz) << 32) |
+                                          ((unsigned long long)y << 16) | x;
                     } else {  // queue full: exact update in place (still exact)
                         const double gz = dmul((double)((int64_t)(z0 + zz) + vol.origin[2]), vs);
                         unsigned db = 0;
@@ -1089,14 +1091,15 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (unsigned long long)gridDim.x * blockDim.x) {
         const unsigned long long e = queue[i];
-        const int v = (int)(e >> 40);
-        const int64_t lin = (int64_t)(e & ((1ull << 40) - 1));
+        const int v = (int)(e >> 48);
+        const int64_t z = (int64_t)((e >> 32) & 0xFFFFu), y = (int64_t)((e >> 16) & 0xFFFFu),
+                      x = (int64_t)(e & 0xFFFFu);
         const TfVolume &vol = vt.vol[v];
+        const int64_t n = vol.n;
+        const int64_t lin = (z * n + y) * n + x;
         // the voxel's old value is loaded before the float64 projection, so its
         // HBM round trip overlaps the arithmetic instead of following it
         const float2 old = ((const float2 *)vol.voxels_dev)[lin];
-        const int64_t n = vol.n;
-        const int64_t x = lin % n, y = (lin / n) % n, z = lin / (n * n);
         const double vs = vol.voxel_size;
         unsigned db = 0;
         updates += update_voxel((float2 *)vol.voxels_dev, lin, dmul((double)(x + vol.origin[0]), vs),
@@ -1343,9 +1346,12 @@ extern "C" int tf_integrate_rgb(const TfVolume *vols, int nvol, const double *de
         return tf_set_error(TF_EINVAL, "tf_integrate: null argument");
     if (cam->width <= 0 || cam->height <= 0)
         return tf_set_error(TF_EINVAL, "tf_integrate: bad image size");
-    for (int v = 0; v < nvol; ++v)
+    for (int v = 0; v < nvol; ++v) {
         if (!vols[v].voxels_dev || vols[v].n < 2 || !(vols[v].voxel_size > 0.0))
             return tf_set_error(TF_EINVAL, "tf_integrate: bad volume %d", v);
+        if (vols[v].n > 65535)  // 16-bit voxel coordinates in the exact queue
+            return tf_set_error(TF_EINVAL, "tf_integrate: volume %d: n = %lld > 65535", v, (long long)vols[v].n);
+    }
     int64_t chunk = 0;
     bricks_of(vols, nvol, &chunk);
     if (chunk > (int64_t)0xffffffffLL)

@@ -604,3 +604,38 @@ def test_brick_summary_stays_exact_under_integration():
     unseen = sum(int(((t.brick_bad >> 16) == 0).sum().item()) for t in tiles)
     assert good > 1000 and unseen > 1000  # both kinds of skippable bricks exist
     assert lib.tf_good_threshold(params.truncation) > 0.99 * params.truncation
+
+
+def test_volume_offsets_beyond_32_bits():
+    """n = 1640 (35 GB per volume): voxel offsets of slices z >= 1597 exceed
+    2^32.  A plane 0.52 m in front of a camera at z = 6.0 m puts the surface
+    at voxel z ~ 1630, so bricks there mix free-space and band voxels (the
+    general kernel's free-space path writes past 2^32); the float32-screened
+    integration equals the exact one, bit for bit, and so do the raycasts."""
+    n, vs = 1640, 0.004
+    intr = CameraIntrinsics(131.25, 131.25, 79.5, 59.5, 160, 120)
+    params = tf.FusionParams.for_voxel_size(vs)
+    pose = Pose(np.eye(3), np.array([0.0, 0.0, 6.0]))
+    depth = torch.full((120, 160), 0.52, dtype=torch.float64, device="cuda")
+    lib = nat.load_library()
+    a = tf.TsdfSubvolume.empty((-820, -820, 0), n, n * vs)
+    b = tf.TsdfSubvolume.empty((-820, -820, 0), n, n * vs)
+    try:
+        tf.integrate_volumes([a], depth, pose, intr, params)
+        lib.tf_set_debug_flags(nat.DEBUG_EXACT_ONLY)
+        tf.integrate_volumes([b], depth, pose, intr, params)
+        lib.tf_set_debug_flags(0)
+        assert (a.voxels[1620:, ..., 1] > 0).any()
+        assert torch.equal(a.voxels[1500:], b.voxels[1500:])
+        assert torch.equal(a.voxels, b.voxels)
+        got, want = tf.RayMap.empty(intr), tf.RayMap.empty(intr)
+        tf.raycast_volumes([a], pose, intr, got, params)
+        lib.tf_set_debug_flags(nat.DEBUG_EXACT_ONLY)
+        tf.raycast_volumes([a], pose, intr, want, params)
+        assert torch.isfinite(want.distance_dev).sum().item() > 10000
+        assert torch.equal(got.distance_dev, want.distance_dev)
+        assert torch.equal(got.normals_dev, want.normals_dev)
+    finally:
+        lib.tf_set_debug_flags(0)
+        del a, b
+        torch.cuda.empty_cache()
