@@ -97,3 +97,21 @@ def test_product_package_never_imports_the_oracle():
     for py in pkg.rglob("*.py"):
         text = py.read_text()
         assert "import oracle" not in text and "from oracle" not in text, py
+
+
+def test_peer_exchange_abi_rejects_bad_arguments_without_gpu():
+    """tf_comm_*: argument checks come before any CUDA call."""
+    lib = nat.load_library()
+    h = ctypes.c_void_p()
+    assert lib.tf_comm_create(2, 2, 640, 480, ctypes.byref(h)) == -1      # rank >= world
+    assert lib.tf_comm_create(0, 0, 640, 480, ctypes.byref(h)) == -1      # world < 1
+    assert lib.tf_comm_create(0, nat.COMM_MAX_RANKS + 1, 640, 480, ctypes.byref(h)) == -1
+    assert lib.tf_comm_create(0, 2, 0, 480, ctypes.byref(h)) == -1        # empty image
+    assert b"tf_comm_create" in lib.tf_last_error()
+    assert lib.tf_comm_reduce_raymap(None, 0, None) == -1
+    assert lib.tf_comm_import(None, None) == -1
+    assert lib.tf_comm_export(None, None) == -1
+    assert lib.tf_comm_link_local(None, 2) == -1
+    e = ctypes.c_int(7)
+    assert lib.tf_comm_error(None, ctypes.byref(e)) == -1
+    assert lib.tf_comm_destroy(None) == 0
