@@ -209,10 +209,43 @@ def endpoints_fixture():
     print("endpoints_small:", len(keys), "cells")
 
 
+def pipeline_fixture():
+    """run_fusion with ICP tracking on (pipeline.py:117-197, :208-230): one
+    128^3 tile, 160x120 frames of the 1.5-degree orbit (config 2's motion),
+    ground truth only for frame 0; per-frame poses and records, final cloud."""
+    import tempfile
+    cfg = tf.RunConfig(fx=131.25, fy=131.25, cx=79.5, cy=59.5, width=160, height=120,
+                       side_length=3.0, resolution=126, resident_resolution=126,
+                       use_groundtruth=False)
+    intr = cfg.intrinsics()
+    scene = anchored_scene()
+    poses = tf.orbit_trajectory(np.array([0.0, 0.0, 1.5]), 1.5, 240)[:10]
+    frames = [scene.render_depth(p, intr) for p in poses]
+    with tempfile.TemporaryDirectory() as tmp:
+        res = tf.run_fusion(frames, cfg, tmp, gt_poses=poses)
+    rec = res.records
+    np.savez_compressed(
+        OUT / "pipeline_small.npz",
+        intr=intr_arr(intr), gt_poses=pose_arr(poses), frames=np.stack([f.data for f in frames]),
+        poses=pose_arr(res.poses), tracked=np.array([r.tracked for r in rec]),
+        correspondences=np.array([r.correspondences for r in rec], np.int64),
+        residual_rms=np.array([r.residual_rms for r in rec], np.float64),
+        cloud_vertices=res.cloud.vertices, cloud_normals=res.cloud.normals,
+        lost_frames=np.int64(res.lost_frames),
+    )
+    print("pipeline_small:", len(rec), "frames,", len(res.cloud.vertices), "cloud points, lost",
+          res.lost_frames)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # regenerate only the named fixtures
+        for name in sys.argv[1:]:
+            globals()[name + "_fixture"]()
+        sys.exit(0)
     fusion_fixture()
     tiled_fixture()
     icp_fixture()
     endpoints_fixture()
+    pipeline_fixture()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size, "bytes")
