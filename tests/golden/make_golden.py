@@ -237,6 +237,51 @@ def pipeline_fixture():
           res.lost_frames)
 
 
+def dynamic_fixture():
+    """Dynamic placement down a corridor (config 4's kind, pipeline.py:126-127,
+    volumes.py:249-331): walls, floor and a box, depth beyond 4 m zeroed,
+    ground-truth poses, at most 4 tiles of 34^3 voxels, 3 resident (so tiles
+    spill to disk and come back); per frame the allocated keys in order and
+    the record counters, then the final cloud."""
+    import tempfile
+    cfg = tf.RunConfig(fx=65.625, fy=65.625, cx=39.5, cy=29.5, width=80, height=60,
+                       dynamic=True, block_voxels=34, block_side_length=0.64, max_volumes=4,
+                       max_resident=3, use_groundtruth=True)
+    intr = cfg.intrinsics()
+    scene = tf.Scene((
+        tf.Plane(np.array([0.9, 0.0, 0.0]), np.array([-1.0, 0.0, 0.0])),
+        tf.Plane(np.array([-0.9, 0.0, 0.0]), np.array([1.0, 0.0, 0.0])),
+        tf.Plane(np.array([0.0, 0.5, 0.0]), np.array([0.0, -1.0, 0.0])),
+        tf.Box(np.array([-0.5, 0.2, 2.0]), np.array([-0.2, 0.5, 2.4])),
+    ))
+    poses = tf.corridor_trajectory(3.0, 12)
+    frames = []
+    for p in poses:
+        d = scene.render_depth(p, intr).data.copy()
+        d[d > 4.0] = 0.0
+        frames.append(tf.DepthFrame(d))
+    keys, offsets, counters = [], [0], []
+    with tempfile.TemporaryDirectory() as tmp:
+        pipe = tf.FusionPipeline(cfg, tmp)
+        for f, p in zip(frames, poses):
+            r = pipe.step(f, p)
+            ks = pipe.volumes.keys()
+            keys.extend(ks)
+            offsets.append(len(keys))
+            counters.append([r.volumes, r.resident, r.files_read, r.files_written, r.bytes_read,
+                             r.bytes_written])
+        res = pipe.finish()
+    np.savez_compressed(
+        OUT / "dynamic_small.npz",
+        intr=intr_arr(intr), poses=pose_arr(poses), frames=np.stack([f.data for f in frames]),
+        keys=np.array(keys, np.int64).reshape(-1, 3), offsets=np.array(offsets, np.int64),
+        counters=np.array(counters, np.int64),
+        cloud_vertices=res.cloud.vertices, cloud_normals=res.cloud.normals,
+    )
+    print("dynamic_small:", len(frames), "frames,", len(set(keys)), "distinct keys,",
+          int(np.array(counters)[:, 3].sum()), "spill writes,", len(res.cloud.vertices), "cloud points")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:  # regenerate only the named fixtures
         for name in sys.argv[1:]:
@@ -247,5 +292,6 @@ if __name__ == "__main__":
     icp_fixture()
     endpoints_fixture()
     pipeline_fixture()
+    dynamic_fixture()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size, "bytes")

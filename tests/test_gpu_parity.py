@@ -666,3 +666,28 @@ def test_pipeline_with_tracking_matches_the_reference(tmp_path):
     assert np.allclose(rms[ok], g["residual_rms"][ok], rtol=1e-6, atol=1e-12)
     assert np.array_equal(res.cloud.vertices, g["cloud_vertices"])
     assert np.array_equal(res.cloud.normals, g["cloud_normals"])
+
+
+@pytest.mark.parametrize("tier", ["disk", "host"])
+def test_dynamic_placement_and_spill_match_the_reference(tmp_path, tier):
+    """Dynamic placement down a corridor with tiles spilling (at most 4 tiles,
+    3 resident), against the reference's own pipeline
+    (tests/golden/dynamic_small.npz, pipeline.py:117-197, volumes.py:249-331):
+    every frame's allocated keys in allocation order, the residency and spill
+    counters, and the final extracted cloud, bit for bit — with the reference's
+    disk tier and with the pinned-host tier."""
+    g = load_golden("dynamic_small.npz")
+    fx, fy, cx, cy, w, h = g["intr"]
+    cfg = tf.RunConfig(fx=fx, fy=fy, cx=cx, cy=cy, width=int(w), height=int(h), dynamic=True,
+                       block_voxels=34, block_side_length=0.64, max_volumes=4, max_resident=3,
+                       use_groundtruth=True, spill_tier=tier)
+    pipe = tf.FusionPipeline(cfg, tmp_path)
+    for i, (f, m) in enumerate(zip(g["frames"], g["poses"])):
+        r = pipe.step(tf.DepthFrame(f), Pose(m[:3, :3], m[:3, 3]))
+        want = [tuple(k) for k in g["keys"][g["offsets"][i]:g["offsets"][i + 1]].tolist()]
+        assert list(pipe.volumes.keys()) == want, f"frame {i}"
+        got = [r.volumes, r.resident, r.files_read, r.files_written, r.bytes_read, r.bytes_written]
+        assert got == g["counters"][i].tolist(), f"frame {i}"
+    res = pipe.finish()
+    assert np.array_equal(res.cloud.vertices, g["cloud_vertices"])
+    assert np.array_equal(res.cloud.normals, g["cloud_normals"])
