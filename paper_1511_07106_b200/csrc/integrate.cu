@@ -512,7 +512,7 @@ __device__ __forceinline__ unsigned free_state_delta(float2 old, float2 nv, floa
 // mean (_kernels.py:128-133 with clamped == tau).  Pure streaming: 16-byte
 // voxel pairs, four lanes per 64-byte row, eight rows per warp instruction,
 // four rows' loads in flight per lane.
-__global__ void __launch_bounds__(256) brick_free_kernel(
+__global__ void __launch_bounds__(256, 4) brick_free_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const uint32_t *__restrict__ list,
     const unsigned int *__restrict__ list_count, const int fixed_point,
