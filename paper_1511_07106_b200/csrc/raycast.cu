@@ -1444,16 +1444,17 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
             kern<<<grid, bx * by, 0, stream>>>(vt, g, dist, vert, norm, st, clk, rescue + 1, rescue,
                                                coop_all ? 1ll : budget);
         };
-        // 16x8-pixel blocks of 4 warps, 4 blocks per SM (128 registers): a
-        // block whose slowest warp runs to its budget holds a quarter of an
-        // SM, not all of it, while neighbouring warps still share L1 lines
-        // (32x16 blocks of 16 warps: 0.938 ms; 16x8: 0.859 ms)
+        // 16x8-pixel blocks of 4 warps, 5 blocks per SM (96 registers): a
+        // block whose slowest warp runs to its budget holds a fifth of an SM,
+        // not all of it, while neighbouring warps still share L1 lines; 20
+        // warps per SM hide more latency than the spills cost (32x16 blocks of
+        // 16 warps at 128 registers: 0.938 ms; 16x8 x4: 0.859; 16x8 x5: 0.839)
         switch (shape) {
         case 1: launch(raycast_kernel<32, 16, 1>, 32, 16); break;
-        case 2: launch(raycast_kernel<8, 16, 4>, 8, 16); break;
+        case 2: launch(raycast_kernel<16, 8, 4>, 16, 8); break;
         case 3: launch(raycast_kernel<32, 8, 2>, 32, 8); break;
-        case 4: launch(raycast_kernel<8, 8, 8>, 8, 8); break;
-        default: launch(raycast_kernel<16, 8, 4>, 16, 8); break;
+        case 4: launch(raycast_kernel<8, 16, 5>, 8, 16); break;
+        default: launch(raycast_kernel<16, 8, 5>, 16, 8); break;
         }
         int rc = tf_check_launch("raycast_kernel");
         if (rc) return rc;
