@@ -1464,7 +1464,7 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             void *pc = tf_profile_begin(TF_PROF_RAYCAST_COOP, stream);
             double *slots = (double *)(rescue + slot_off);
-            raycast_coop_items_kernel<<<(unsigned)sms * 4, 128, 0, stream>>>(vt, g, st, rescue + 1, rescue,
+            raycast_coop_items_kernel<<<(unsigned)sms * 8, 128, 0, stream>>>(vt, g, st, rescue + 1, rescue,
                                                                            kCoopSplitRays, slots);
             if ((rc = tf_check_launch("raycast_coop_items_kernel"))) return rc;
             raycast_coop_merge_kernel<<<kCoopSplitRays / 128, 128, 0, stream>>>(
