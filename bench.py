@@ -497,13 +497,14 @@ def run_config2(args, tf, nat, torch, barrier, max_over_ranks) -> dict:
 # CPU baseline (oracle restatement of the reference kernels, all host threads)
 # ---------------------------------------------------------------------------
 
-def cpu_frame_sample(intr, spec, params, poses, host_frames, volumes: int, threads: int) -> dict:
+def cpu_frame_sample(intr, spec, params, poses, host_frames, volumes: int, threads: int,
+                     first: int = 0) -> dict:
     import oracle
 
     n = spec.voxels_per_side
     vs = spec.voxel_size
     coarse = max(2, int(round(0.5 * params.truncation / vs)))
-    keys = spec.keys[:volumes]
+    keys = [spec.keys[(first + i) % len(spec.keys)] for i in range(volumes)]
     tiles = [(np.zeros((n, n, n), np.float32), np.zeros((n, n, n), np.float32)) for _ in keys]
     p0, p1 = poses[0], poses[1]
     for (t, w), k in zip(tiles, keys):
@@ -557,19 +558,25 @@ def run_reference(args) -> None:
     threads = oracle.default_threads()
     intr, spec, params, poses, scene = workload(2)
     host_frames = [scene.render_depth(p, intr).data for p in poses]
-    vols = 8 if threads >= 32 else (4 if threads >= 8 else 1)
-    steps, warmup = max(1, min(args.steps, 5)), min(args.warmup, 1)
-    for _ in range(warmup):
-        cpu_frame_sample(intr, spec, params, poses, host_frames, vols, threads)
+    # exactly --warmup untimed and --steps timed samples; each sample is
+    # bounded (volumes per sample shrink as K + W grow: ~120 volume-samples in
+    # all, ~0.5 s each) and the samples walk round-robin over the 8 volumes
+    steps, warmup = max(1, args.steps), max(0, args.warmup)
+    cap = 8 if threads >= 32 else (4 if threads >= 8 else 1)
+    vols = max(1, min(cap, 120 // (steps + warmup)))
+    for i in range(warmup):
+        cpu_frame_sample(intr, spec, params, poses, host_frames, vols, threads, first=i * vols)
     times, ups = [], []
-    for _ in range(steps):
-        s = cpu_frame_sample(intr, spec, params, poses, host_frames, vols, threads)
+    for i in range(steps):
+        s = cpu_frame_sample(intr, spec, params, poses, host_frames, vols, threads,
+                             first=(warmup + i) * vols)
         times.append((s["t_integrate"] + s["t_raycast"]) * 8 / vols)
         ups.append(s["updates"] * 8 / vols)
     frame_s = sum(times) / len(times)
     value = (sum(ups) / len(ups)) / frame_s
-    sample = (f"per step: frame 1 of the workload on {vols} of 8 volumes (integrate + raycast), "
-              f"C restatement of the reference kernels on {threads} host threads, scaled to 8")
+    sample = (f"per step: frame 1 of the workload on {vols} of the 8 volumes (round-robin over the "
+              f"steps; integrate + raycast), C restatement of the reference kernels on {threads} "
+              f"host threads, scaled to 8")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "voxel-updates/s",
         "frames_per_s": 1.0 / frame_s, "n_gpus": world, "steps": steps, "warmup": warmup,
