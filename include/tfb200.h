@@ -166,6 +166,27 @@ int tf_integrate_rgb(const TfVolume *vols, int nvol, const double *depth_dev,
                      double max_weight, double sample_weight, void *workspace_dev,
                      size_t workspace_bytes, uint64_t *stats_dev, void *stream);
 
+/* tf_integrate_rgb in two halves, so the first can run on another stream
+ * while the previous frame's raycast still occupies the GPU:
+ * tf_integrate_prepare builds the per-frame pixel tables, depth mips and the
+ * culled brick lists in the workspace (it reads the depth frame and the
+ * volumes' geometry, never their voxels or summaries); tf_integrate_finish
+ * then runs the voxel updates and the summary upkeep.  finish must follow a
+ * prepare with the same arguments on the same workspace (the caller orders
+ * the two streams), and no other integrate call may use that workspace in
+ * between.  With more volumes than one launch holds, prepare does nothing
+ * and finish does both. */
+int tf_integrate_prepare(const TfVolume *vols, int nvol, const double *depth_dev,
+                         const TfCamera *cam, const double r_cw[9], const double t_cw[3],
+                         const double cam_center[3], double tau, double max_weight,
+                         double sample_weight, void *workspace_dev, size_t workspace_bytes,
+                         void *stream);
+int tf_integrate_finish(const TfVolume *vols, int nvol, const double *depth_dev,
+                        const uint8_t *rgb_dev, const TfCamera *cam, const double r_cw[9],
+                        const double t_cw[3], const double cam_center[3], double tau,
+                        double max_weight, double sample_weight, void *workspace_dev,
+                        size_t workspace_bytes, uint64_t *stats_dev, void *stream);
+
 /* ---- raycast: replaces _kernels.raycast_kernel (_kernels.py:266-451) with
  * its helpers _sample / _scan_crossing / _hit_wins, called by tsdf.raycast
  * (tsdf.py:193-225), fused over `nvol` volumes sharing one voxel size.

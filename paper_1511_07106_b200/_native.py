@@ -18,6 +18,7 @@ import torch
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ["TFB200_LIB"]) if os.environ.get("TFB200_LIB") else _PKG / "libtfb200.so"  # override: A/B runs only
 ABI_VERSION = 1
+MAX_VOLUMES_PER_LAUNCH = 64  # TFB200_MAX_VOLUMES_PER_LAUNCH
 
 _c_d = ctypes.c_double
 _c_i64 = ctypes.c_int64
@@ -91,6 +92,10 @@ _SIGNATURES = {
                               _c_p, _c_sz, _c_p, _c_p]),
     "tf_integrate_rgb": (_c_int, [_VOL, _c_int, _c_p, _c_p, _CAM, _c_p, _c_p, _c_p, _c_d, _c_d, _c_d,
                                   _c_p, _c_sz, _c_p, _c_p]),
+    "tf_integrate_prepare": (_c_int, [_VOL, _c_int, _c_p, _CAM, _c_p, _c_p, _c_p, _c_d, _c_d, _c_d,
+                                      _c_p, _c_sz, _c_p]),
+    "tf_integrate_finish": (_c_int, [_VOL, _c_int, _c_p, _c_p, _CAM, _c_p, _c_p, _c_p, _c_d, _c_d, _c_d,
+                                     _c_p, _c_sz, _c_p, _c_p]),
     "tf_raycast_colors": (_c_int, [_VOL, _c_int, _CAM, _c_p, _c_p, _c_p, _c_p, _c_p]),
     "tf_raycast": (_c_int, [_VOL, _c_int, _CAM, _c_d, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
                             _c_p, _c_p]),

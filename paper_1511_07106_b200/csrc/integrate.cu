@@ -1326,20 +1326,15 @@ static SideStream *side_stream() {
     return &s;
 }
 
-extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
-                            const TfCamera *cam, const double r_cw[9], const double t_cw[3],
-                            const double cam_center[3], double tau, double max_weight,
-                            double sample_weight, void *workspace, size_t workspace_bytes,
-                            uint64_t *stats, void *stream_) {
-    return tf_integrate_rgb(vols, nvol, depth, nullptr, cam, r_cw, t_cw, cam_center, tau, max_weight,
-                            sample_weight, workspace, workspace_bytes, stats, stream_);
-}
-
-extern "C" int tf_integrate_rgb(const TfVolume *vols, int nvol, const double *depth, const uint8_t *rgb,
-                                const TfCamera *cam, const double r_cw[9], const double t_cw[3],
-                                const double cam_center[3], double tau, double max_weight,
-                                double sample_weight, void *workspace, size_t workspace_bytes,
-                                uint64_t *stats, void *stream_) {
+// phases: 1 = prepare (pixel tables, mips, culling into the workspace),
+// 2 = finish (the voxel updates and summary upkeep), 3 = both.  More volumes
+// than one launch holds reuse the workspace per chunk, so there prepare does
+// nothing and finish runs both phases.
+static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, const uint8_t *rgb,
+                          const TfCamera *cam, const double r_cw[9], const double t_cw[3],
+                          const double cam_center[3], double tau, double max_weight,
+                          double sample_weight, void *workspace, size_t workspace_bytes,
+                          uint64_t *stats, void *stream_, int phases) {
     cudaStream_t stream = (cudaStream_t)stream_;
     if (nvol == 0) return TF_OK;
     if (!vols || nvol < 0 || !depth || !cam || !r_cw || !t_cw || !cam_center || !workspace)
@@ -1374,18 +1369,27 @@ extern "C" int tf_integrate_rgb(const TfVolume *vols, int nvol, const double *de
     unsigned long long *queue = (unsigned long long *)(ws + L.queue_off);
     uint32_t *active = (uint32_t *)(ws + L.active_off);
     const MipDesc m = make_mip(cam->width, cam->height);
+    bool do_prep = (phases & 1) != 0;
+    const bool do_fin = (phases & 2) != 0;
+    if (nvol > TFB200_MAX_VOLUMES_PER_LAUNCH) {
+        if (!do_fin) return TF_OK;
+        do_prep = true;
+    }
 
-    void *prof_all = tf_profile_begin(TF_PROF_INTEGRATE_ALL, stream);
-    if (cudaMemsetAsync(mip, 0, (size_t)m.total * sizeof(unsigned long long), stream) != cudaSuccess ||
-        cudaMemsetAsync(qmip, 0xff, (size_t)m.total * sizeof(unsigned), stream) != cudaSuccess)
-        return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
-    dim3 pblock(kTile, kTile);
-    dim3 pgrid((unsigned)((cam->width + kTile - 1) / kTile), (unsigned)((cam->height + kTile - 1) / kTile));
-    frame_prep_kernel<<<pgrid, pblock, 0, stream>>>(depth, table, table32, mip, qmip, tau, m, cam->fx,
-                                                    cam->fy, cam->cx, cam->cy, cam->width,
-                                                    cam->height);
-    int rc = tf_check_launch("frame_prep_kernel");
-    if (rc) return rc;
+    void *prof_all = do_fin ? tf_profile_begin(TF_PROF_INTEGRATE_ALL, stream) : nullptr;
+    int rc = TF_OK;
+    if (do_prep) {
+        if (cudaMemsetAsync(mip, 0, (size_t)m.total * sizeof(unsigned long long), stream) != cudaSuccess ||
+            cudaMemsetAsync(qmip, 0xff, (size_t)m.total * sizeof(unsigned), stream) != cudaSuccess)
+            return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
+        dim3 pblock(kTile, kTile);
+        dim3 pgrid((unsigned)((cam->width + kTile - 1) / kTile), (unsigned)((cam->height + kTile - 1) / kTile));
+        frame_prep_kernel<<<pgrid, pblock, 0, stream>>>(depth, table, table32, mip, qmip, tau, m, cam->fx,
+                                                        cam->fy, cam->cx, cam->cy, cam->width,
+                                                        cam->height);
+        rc = tf_check_launch("frame_prep_kernel");
+        if (rc) return rc;
+    }
 
     FrameGeom f{};
     for (int i = 0; i < 9; ++i) f.r_cw.m[i] = r_cw[i];
@@ -1451,25 +1455,28 @@ extern "C" int tf_integrate_rgb(const TfVolume *vols, int nvol, const double *de
             off += nb * nb * nb;
         }
         bt.offset[cnt] = off;
-        if (cudaMemsetAsync(count, 0, 128, stream) != cudaSuccess ||  // brick + queue counters
-            cudaMemsetAsync(ws + L.dirty_off, 0, L.dirty_bytes, stream) != cudaSuccess)
-            return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
         const ChangedList changed{(uint32_t *)(ws + L.changed_off), (unsigned *)(ws + L.count_off + 24),
                                   (unsigned *)(ws + L.dirty_off)};
         const int exact_only = (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) ? 1 : 0;
         const int no_cull = (tf_debug_flags() & TF_DEBUG_NO_CULL) ? 1 : 0;
-        int64_t macros_total = 0;
-        for (int v = 0; v < cnt; ++v) {
-            const int64_t nm = (bt.nb[v] + kMacro - 1) / kMacro;
-            macros_total += nm * nm * nm;
+        if (do_prep) {
+            if (cudaMemsetAsync(count, 0, 128, stream) != cudaSuccess ||  // brick + queue counters
+                cudaMemsetAsync(ws + L.dirty_off, 0, L.dirty_bytes, stream) != cudaSuccess)
+                return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
+            int64_t macros_total = 0;
+            for (int v = 0; v < cnt; ++v) {
+                const int64_t nm = (bt.nb[v] + kMacro - 1) / kMacro;
+                macros_total += nm * nm * nm;
+            }
+            macro_cull_kernel<<<(unsigned)((macros_total + 255) / 256), 256, 0, stream>>>(
+                vt, bt, f, m, mip, qmip, macros, mcount, active_free, fcount, no_cull, exact_only ? 0 : 1);
+            if ((rc = tf_check_launch("macro_cull_kernel"))) return rc;
+            brick_cull_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(
+                vt, bt, f, m, mip, qmip, macros, mcount, active, count, active_free, fcount, no_cull,
+                exact_only ? 0 : 1);
+            if ((rc = tf_check_launch("brick_cull_kernel"))) return rc;
         }
-        macro_cull_kernel<<<(unsigned)((macros_total + 255) / 256), 256, 0, stream>>>(
-            vt, bt, f, m, mip, qmip, macros, mcount, active_free, fcount, no_cull, exact_only ? 0 : 1);
-        if ((rc = tf_check_launch("macro_cull_kernel"))) return rc;
-        brick_cull_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(
-            vt, bt, f, m, mip, qmip, macros, mcount, active, count, active_free, fcount, no_cull,
-            exact_only ? 0 : 1);
-        if ((rc = tf_check_launch("brick_cull_kernel"))) return rc;
+        if (!do_fin) continue;
         void *prof = tf_profile_begin(TF_PROF_INTEGRATE_UPDATE, stream);
         if (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) {
             brick_update_exact_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(
@@ -1532,8 +1539,43 @@ extern "C" int tf_integrate_rgb(const TfVolume *vols, int nvol, const double *de
             if ((rc = tf_check_launch("brick_stats_kernel"))) return rc;
         }
     }
-    tf_profile_end(prof_all, stream);
+    if (prof_all) tf_profile_end(prof_all, stream);
     return TF_OK;
+}
+
+extern "C" int tf_integrate_rgb(const TfVolume *vols, int nvol, const double *depth, const uint8_t *rgb,
+                                const TfCamera *cam, const double r_cw[9], const double t_cw[3],
+                                const double cam_center[3], double tau, double max_weight,
+                                double sample_weight, void *workspace, size_t workspace_bytes,
+                                uint64_t *stats, void *stream) {
+    return integrate_impl(vols, nvol, depth, rgb, cam, r_cw, t_cw, cam_center, tau, max_weight, sample_weight,
+                          workspace, workspace_bytes, stats, stream, 3);
+}
+
+extern "C" int tf_integrate(const TfVolume *vols, int nvol, const double *depth,
+                            const TfCamera *cam, const double r_cw[9], const double t_cw[3],
+                            const double cam_center[3], double tau, double max_weight,
+                            double sample_weight, void *workspace, size_t workspace_bytes,
+                            uint64_t *stats, void *stream) {
+    return integrate_impl(vols, nvol, depth, nullptr, cam, r_cw, t_cw, cam_center, tau, max_weight,
+                          sample_weight, workspace, workspace_bytes, stats, stream, 3);
+}
+
+extern "C" int tf_integrate_prepare(const TfVolume *vols, int nvol, const double *depth, const TfCamera *cam,
+                                    const double r_cw[9], const double t_cw[3], const double cam_center[3],
+                                    double tau, double max_weight, double sample_weight, void *workspace,
+                                    size_t workspace_bytes, void *stream) {
+    return integrate_impl(vols, nvol, depth, nullptr, cam, r_cw, t_cw, cam_center, tau, max_weight,
+                          sample_weight, workspace, workspace_bytes, nullptr, stream, 1);
+}
+
+extern "C" int tf_integrate_finish(const TfVolume *vols, int nvol, const double *depth, const uint8_t *rgb,
+                                   const TfCamera *cam, const double r_cw[9], const double t_cw[3],
+                                   const double cam_center[3], double tau, double max_weight,
+                                   double sample_weight, void *workspace, size_t workspace_bytes,
+                                   uint64_t *stats, void *stream) {
+    return integrate_impl(vols, nvol, depth, rgb, cam, r_cw, t_cw, cam_center, tau, max_weight, sample_weight,
+                          workspace, workspace_bytes, stats, stream, 2);
 }
 
 extern "C" float tf_good_threshold(double tau) { return good_threshold(tau); }

@@ -45,7 +45,8 @@ import torch.distributed as dist
 
 from . import _native as nat
 from .geometry import CameraIntrinsics, Pose
-from .tsdf import FusionParams, RayMap, TsdfSubvolume, integrate_volumes, raycast_volumes
+from .tsdf import (FusionParams, RayMap, SplitIntegrator, TsdfSubvolume, integrate_volumes,
+                   raycast_volumes)
 
 
 def owner_of(index: int, world: int) -> int:
@@ -298,6 +299,7 @@ class ShardedFusion:
         self._packed = torch.zeros((world * b, intr.width, 4), dtype=torch.float64,
                                    device=self.partial.distance_dev.device)
         self._packed[..., 0] = float("inf")
+        self._integrator = SplitIntegrator()
         self.exchange = "none" if world == 1 else exchange
         self._peer = None
         if exchange == "auto" and world > 1:
@@ -309,8 +311,12 @@ class ShardedFusion:
             else:
                 self.partial, self.model = self._peer.partial, self._peer.model
 
-    def step(self, depth: torch.Tensor, pose: Pose, color=None) -> RayMap:
-        integrate_volumes(self.tiles, depth, pose, self.intr, self.params, self.stats, color=color)
+    def step(self, depth: torch.Tensor, pose: Pose, color=None, depth_ready=None) -> RayMap:
+        """One frame.  ``depth_ready`` (see SplitIntegrator): an event after
+        which ``depth`` is valid, True for a frame with no pending producer,
+        or None (the integration's first half then waits for the stream)."""
+        self._integrator(self.tiles, depth, pose, self.intr, self.params, self.stats, color=color,
+                         depth_ready=depth_ready)
         self.partial.reset()
         raycast_volumes(self.tiles, pose, self.intr, self.partial, self.params, self.stats)
         if self.world == 1:

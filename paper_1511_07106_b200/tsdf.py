@@ -279,13 +279,20 @@ def device_rgb(color, intr: CameraIntrinsics) -> torch.Tensor:
 
 def integrate_volumes(volumes: Sequence[TsdfSubvolume], frame, pose: Pose,
                       intr: CameraIntrinsics, params: FusionParams,
-                      stats: torch.Tensor | None = None, color=None) -> None:
+                      stats: torch.Tensor | None = None, color=None, *, phase: str = "all",
+                      workspace_slot: str = "main") -> None:
     """Fuse one depth frame into every volume with one fused launch sequence.
 
     ``color`` (uint8 [H, W, 3]) is fused into the volumes that have a colour
     channel (``enable_color``): a running mean of the observations while the
     voxel lies in the truncation band (include/tfb200.h, tf_integrate_rgb).
+
+    ``phase`` "prepare" then "finish" (same arguments, same
+    ``workspace_slot``) split the call in two (tf_integrate_prepare /
+    tf_integrate_finish), so the first half can run on another stream.
     """
+    if phase not in ("all", "prepare", "finish"):
+        raise ValueError(f"phase must be 'all', 'prepare' or 'finish', not {phase!r}")
     volumes = list(volumes)
     if not volumes:
         return
@@ -300,16 +307,63 @@ def integrate_volumes(volumes: Sequence[TsdfSubvolume], frame, pose: Pose,
     cam = nat.camera(intr)
     L = nat.lib()
     need = L.tf_integrate_workspace_size(arr, len(volumes), cam)
-    ws = nat.workspace.get(need)
-    nat.check(L.tf_integrate_rgb(arr, len(volumes), nat.ptr(depth), nat.ptr(rgb) if rgb is not None else None,
-                                 cam, nat.mat9(inverse.rotation),
-                                 nat.vec3(inverse.translation), nat.vec3(pose.translation),
-                                 float(params.truncation), float(params.max_weight),
-                                 float(params.sample_weight), nat.ptr(ws), ws.numel(),
-                                 nat.ptr(stats if stats is not None else nat.stats.buffer()),
-                                 nat.stream_handle()), "tf_integrate")
+    ws = nat.workspace.get(need, workspace_slot)
+    geom = (cam, nat.mat9(inverse.rotation), nat.vec3(inverse.translation), nat.vec3(pose.translation),
+            float(params.truncation), float(params.max_weight), float(params.sample_weight),
+            nat.ptr(ws), ws.numel())
+    if phase == "prepare":
+        nat.check(L.tf_integrate_prepare(arr, len(volumes), nat.ptr(depth), *geom, nat.stream_handle()),
+                  "tf_integrate_prepare")
+        return
+    fn = L.tf_integrate_rgb if phase == "all" else L.tf_integrate_finish
+    nat.check(fn(arr, len(volumes), nat.ptr(depth), nat.ptr(rgb) if rgb is not None else None, *geom,
+                 nat.ptr(stats if stats is not None else nat.stats.buffer()), nat.stream_handle()),
+              "tf_integrate")
     for v in volumes:
         v._device_written()
+
+
+class SplitIntegrator:
+    """integrate_volumes with its first half (pixel tables, depth mips,
+    culling: tf_integrate_prepare) on a side stream, so it overlaps the tail
+    of the previous frame's raycast; the second half (the voxel updates) runs
+    on the current stream after it.  The side stream waits for the previous
+    call's updates to release this integrator's own workspace and for the
+    depth: ``depth_ready`` is an event after which the depth is valid, True
+    when it has no pending producer (a resident frame), or None — then the
+    whole call runs on the current stream (no overlap, no cross-stream
+    synchronisation).  Results are those of integrate_volumes."""
+
+    def __init__(self) -> None:
+        self._prep = self._ws_free = self._prepared = None
+        self._slot = f"split{id(self)}"
+
+    def __call__(self, volumes: Sequence[TsdfSubvolume], depth, pose: Pose, intr: CameraIntrinsics,
+                 params: FusionParams, stats: torch.Tensor | None = None, color=None,
+                 depth_ready=None) -> None:
+        volumes = list(volumes)
+        if (depth_ready is None or not volumes or len(volumes) > nat.MAX_VOLUMES_PER_LAUNCH
+                or not isinstance(depth, torch.Tensor) or not depth.is_cuda):
+            # nothing to overlap with: one call on the current stream
+            integrate_volumes(volumes, depth, pose, intr, params, stats, color=color)
+            return
+        main = torch.cuda.current_stream(depth.device)
+        if self._prep is None:
+            self._prep = torch.cuda.Stream(device=depth.device)
+            self._ws_free, self._prepared = torch.cuda.Event(), torch.cuda.Event()
+            self._ws_free.record(main)
+        prep = self._prep
+        if depth_ready is not True:
+            prep.wait_event(depth_ready)
+        prep.wait_event(self._ws_free)
+        with torch.cuda.stream(prep):
+            integrate_volumes(volumes, depth, pose, intr, params, phase="prepare", workspace_slot=self._slot)
+        self._prepared.record(prep)
+        main.wait_event(self._prepared)
+        integrate_volumes(volumes, depth, pose, intr, params, stats, color=color, phase="finish",
+                          workspace_slot=self._slot)
+        self._ws_free.record(main)
+        depth.record_stream(prep)
 
 
 def integrate(subvolume: TsdfSubvolume, frame: DepthFrame, pose: Pose, intr: CameraIntrinsics,

@@ -641,7 +641,8 @@ def test_volume_offsets_beyond_32_bits():
         torch.cuda.empty_cache()
 
 
-def test_pipeline_with_tracking_matches_the_reference(tmp_path):
+@pytest.mark.parametrize("pinned", [False, True])
+def test_pipeline_with_tracking_matches_the_reference(tmp_path, pinned):
     """run_fusion with ICP tracking on, against the reference's own
     run_fusion (tests/golden/pipeline_small.npz, pipeline.py:117-197): the
     same frames tracked, identical inlier counts per frame, poses equal to
@@ -653,7 +654,10 @@ def test_pipeline_with_tracking_matches_the_reference(tmp_path):
     cfg = tf.RunConfig(fx=fx, fy=fy, cx=cx, cy=cy, width=int(w), height=int(h), side_length=3.0,
                        resolution=126, resident_resolution=126, use_groundtruth=False)
     gt = [Pose(m[:3, :3], m[:3, 3]) for m in g["gt_poses"]]
-    frames = [tf.DepthFrame(f) for f in g["frames"]]
+    # pinned host frames take the double-buffered upload and the split
+    # integration (its first half overlapping the previous raycast)
+    frames = ([torch.from_numpy(np.ascontiguousarray(f)).pin_memory() for f in g["frames"]] if pinned
+              else [tf.DepthFrame(f) for f in g["frames"]])
     res = tf.run_fusion(frames, cfg, tmp_path, gt_poses=gt)
     assert res.lost_frames == int(g["lost_frames"]) == 0
     assert [r.tracked for r in res.records] == g["tracked"].tolist()
@@ -691,3 +695,31 @@ def test_dynamic_placement_and_spill_match_the_reference(tmp_path, tier):
     res = pipe.finish()
     assert np.array_equal(res.cloud.vertices, g["cloud_vertices"])
     assert np.array_equal(res.cloud.normals, g["cloud_normals"])
+
+
+def test_split_integration_equals_one_call():
+    """SplitIntegrator (tf_integrate_prepare on a side stream, then
+    tf_integrate_finish) == integrate_volumes, bit for bit, voxels and brick
+    summaries, frame after frame, with the frames' pipelining on."""
+    intr = CameraIntrinsics(131.25, 131.25, 79.5, 59.5, 160, 120)
+    spec = tf.init_grid(3.0, 124, 62)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    a = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in spec.keys]
+    b = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in spec.keys]
+    scene = demo_scene()
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 24)[:8]
+    frames = [torch.from_numpy(scene.render_depth(p, intr).data).cuda() for p in poses]
+    torch.cuda.synchronize()
+    split = tf.tsdf.SplitIntegrator()
+    for f, p in zip(frames, poses):
+        tf.integrate_volumes(a, f, p, intr, params)
+        split(b, f, p, intr, params, depth_ready=True)
+        rm = tf.RayMap.empty(intr)
+        tf.raycast_volumes(b, p, intr, rm, params)  # the raycast the next prepare overlaps
+    torch.cuda.synchronize()
+    for x, y in zip(a, b):
+        assert torch.equal(x.voxels, y.voxels)
+        if x.brick_bad is not None:
+            assert torch.equal(x.brick_bad, y.brick_bad)
+            assert torch.equal(x.brick_flags, y.brick_flags)
+    assert float(b[0].voxels[..., 1].max()) > 0
