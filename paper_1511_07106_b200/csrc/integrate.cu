@@ -1085,7 +1085,9 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
     const __grid_constant__ FrameGeom f,
     const double2 *__restrict__ table, const unsigned long long *__restrict__ queue,
     const unsigned long long *__restrict__ queue_count, const unsigned long long queue_cap,
-    unsigned long long *__restrict__ stats, const ChangedList changed) {
+    unsigned long long *__restrict__ stats, const ChangedList changed,
+    const unsigned *__restrict__ active_count, const unsigned *__restrict__ free_count,
+    const unsigned long long total_bricks) {
     const unsigned long long total = min(*queue_count, queue_cap);
     unsigned long long updates = 0;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -1114,7 +1116,12 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
     if (stats) {
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
         warp_count_add(&stats[TF_STAT_EXACT_UPDATES], updates);
-        if (blockIdx.x == 0 && threadIdx.x == 0) stats[TF_STAT_EXACT_VOXELS] += *queue_count;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {  // this call's brick counters (brick_stats_kernel)
+            stats[TF_STAT_EXACT_VOXELS] += *queue_count;
+            stats[TF_STAT_ACTIVE_BRICKS] += *active_count + *free_count;
+            stats[TF_STAT_FREE_BRICKS] += *free_count;
+            stats[TF_STAT_TOTAL_BRICKS] += total_bricks;
+        }
     }
 }
 
@@ -1506,7 +1513,8 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
             void *pe = tf_profile_begin(TF_PROF_INTEGRATE_EXACT, stream);
             exact_queue_kernel<<<(unsigned)sms * 16, 256, 0, stream>>>(vt, bt, f, table, queue, qcount,
                                                                      L.queue_cap,
-                                                                     (unsigned long long *)stats, changed);
+                                                                     (unsigned long long *)stats, changed,
+                                                                     count, fcount, (unsigned long long)off);
             tf_profile_end(pe, stream);
             if ((rc = tf_check_launch("exact_queue_kernel"))) return rc;
             cudaStreamWaitEvent(stream, side->join, 0);
@@ -1533,7 +1541,7 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
             super_flags_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(vt, f, 1);
             if ((rc = tf_check_launch("super_flags_kernel"))) return rc;
         }
-        if (stats) {
+        if (stats && exact_only) {  // otherwise exact_queue_kernel counted them
             brick_stats_kernel<<<1, 32, 0, stream>>>(count, fcount, (unsigned long long)off,
                                                      (unsigned long long *)stats);
             if ((rc = tf_check_launch("brick_stats_kernel"))) return rc;
