@@ -141,7 +141,17 @@ __global__ void __launch_bounds__(256) frame_prep_kernel(
     unsigned long long *__restrict__ mip, unsigned *__restrict__ qmip, const double tau,
     const MipDesc m, const double fx,
     const double fy, const double cx, const double cy, const int64_t width,
-    const int64_t height) {
+    const int64_t height, unsigned *__restrict__ zero_a, const int zero_a_words,
+    unsigned *__restrict__ zero_b, const int64_t zero_b_words) {
+    // the first chunk's brick / queue counters and dirty bitmap start at zero
+    // (instead of two memsets before the culling)
+    {
+        const int64_t tid = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * (kTile * kTile) +
+                            threadIdx.y * kTile + threadIdx.x;
+        const int64_t nthreads = (int64_t)gridDim.x * gridDim.y * (kTile * kTile);
+        if (tid < zero_a_words) zero_a[tid] = 0u;
+        for (int64_t i = tid; i < zero_b_words; i += nthreads) zero_b[i] = 0u;
+    }
     const int64_t ui = (int64_t)blockIdx.x * kTile + threadIdx.x;
     const int64_t vi = (int64_t)blockIdx.y * kTile + threadIdx.y;
     double d = 0.0;
@@ -1393,7 +1403,8 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
         dim3 pgrid((unsigned)((cam->width + kTile - 1) / kTile), (unsigned)((cam->height + kTile - 1) / kTile));
         frame_prep_kernel<<<pgrid, pblock, 0, stream>>>(depth, table, table32, mip, qmip, tau, m, cam->fx,
                                                         cam->fy, cam->cx, cam->cy, cam->width,
-                                                        cam->height);
+                                                        cam->height, count, 32, (unsigned *)(ws + L.dirty_off),
+                                                        (int64_t)(L.dirty_bytes / sizeof(unsigned)));
         rc = tf_check_launch("frame_prep_kernel");
         if (rc) return rc;
     }
@@ -1467,8 +1478,9 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
         const int exact_only = (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) ? 1 : 0;
         const int no_cull = (tf_debug_flags() & TF_DEBUG_NO_CULL) ? 1 : 0;
         if (do_prep) {
-            if (cudaMemsetAsync(count, 0, 128, stream) != cudaSuccess ||  // brick + queue counters
-                cudaMemsetAsync(ws + L.dirty_off, 0, L.dirty_bytes, stream) != cudaSuccess)
+            if (first > 0 &&  // chunk 0's were zeroed by frame_prep_kernel
+                (cudaMemsetAsync(count, 0, 128, stream) != cudaSuccess ||  // brick + queue counters
+                 cudaMemsetAsync(ws + L.dirty_off, 0, L.dirty_bytes, stream) != cudaSuccess))
                 return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
             int64_t macros_total = 0;
             for (int v = 0; v < cnt; ++v) {
