@@ -226,6 +226,10 @@ int tf_raymap_merge(double *dst_dist_dev, double *dst_vert_dev, double *dst_norm
  * (t, nx, ny, nz), 32-byte aligned; dst[p] = src[p] where _hit_wins(src, dst). */
 int tf_raymap_merge_packed(double *dst_dev, const double *src_dev, int64_t npixels, void *stream);
 
+/* RayMap.empty in place (tsdf.py:156-190): +inf distances, zero vertices and
+ * normals, in one launch. */
+int tf_raymap_reset(double *dist_dev, double *vert_dev, double *norm_dev, int64_t npixels, void *stream);
+
 /* Vertices of rows [row0, row0 + nrows) rebuilt from their hit distances
  * (dist_dev[i * dist_stride], row-major from row0): o + t d with the
  * raycast's own arithmetic (bit-identical to what tf_raycast writes), 0 where

@@ -104,6 +104,7 @@ _SIGNATURES = {
     "tf_brick_summary": (_c_int, [_VOL, _c_p]),
     "tf_raymap_merge": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p]),
     "tf_raymap_merge_packed": (_c_int, [_c_p, _c_p, _c_i64, _c_p]),
+    "tf_raymap_reset": (_c_int, [_c_p, _c_p, _c_p, _c_i64, _c_p]),
     "tf_raymap_vertices": (_c_int, [_c_p, _c_i64, _c_p, _CAM, _c_p, _c_p, _c_i64,
                                     _c_i64, _c_p]),
     "tf_vertex_normal_map": (_c_int, [_c_p, _c_i64, _c_i64, _c_int, _CAM, _c_p, _c_p, _c_p,

@@ -1058,16 +1058,12 @@ __device__ bool march_coop(const FastRay &fr, const RayRef &er, int j, const int
 
 // the rays raycast_kernel handed over: one warp per ray, every lane holds the
 // same ray state; lane 0 writes
-__global__ void __launch_bounds__(128) raycast_coop_kernel(
-    const __grid_constant__ VolumeTable vt, const __grid_constant__ RayGeom g,
-    double *__restrict__ out_dist, double *__restrict__ out_vert, double *__restrict__ out_norm,
-    unsigned long long *__restrict__ stats, const unsigned *__restrict__ rescue,
-    const unsigned *__restrict__ rescue_count, const unsigned first) {
+__device__ void coop_whole_rays(const VolumeTable &vt, const RayGeom &g, double *__restrict__ out_dist,
+                                double *__restrict__ out_vert, double *__restrict__ out_norm,
+                                const unsigned *__restrict__ rescue, const unsigned count, const unsigned first,
+                                const unsigned warp, const unsigned nwarps, unsigned long long &samples,
+                                unsigned long long &hits, unsigned long long &exact_samples) {
     const int lane = threadIdx.x & 31;
-    const unsigned count = *rescue_count;
-    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
-    unsigned long long samples = 0, hits = 0, exact_samples = 0;
     for (unsigned i = first + warp; i < count; i += nwarps) {
         const int64_t p = rescue[i];
         const int64_t py = p / g.width, px = p - py * g.width;
@@ -1119,13 +1115,6 @@ __global__ void __launch_bounds__(128) raycast_coop_kernel(
             out_norm[3 * p + 2] = best.nz;
         }
     }
-    if (stats && threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&stats[TF_STAT_COOP_RAYS], (unsigned long long)count);
-    if (stats && lane == 0) {  // every lane counted the same ray: lane 0 reports
-        atomicAdd(&stats[TF_STAT_RAY_SAMPLES], samples);
-        atomicAdd(&stats[TF_STAT_RAY_HITS], hits);
-        atomicAdd(&stats[TF_STAT_EXACT_SAMPLES], exact_samples & ((1ull << 40) - 1));
-        atomicAdd(&stats[TF_STAT_CERT_FAILURES], (exact_samples >> 40) & 15ull);
-    }
 }
 
 // The first `cap` handed-over rays, split into (ray, volume) items, one warp
@@ -1139,9 +1128,11 @@ __global__ void __launch_bounds__(128) raycast_coop_kernel(
 __global__ void __launch_bounds__(128) raycast_coop_items_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ RayGeom g,
     unsigned long long *__restrict__ stats, const unsigned *__restrict__ rescue,
-    const unsigned *__restrict__ rescue_count, const unsigned cap, double *__restrict__ slots) {
+    const unsigned *__restrict__ rescue_count, const unsigned cap, double *__restrict__ slots,
+    double *__restrict__ out_dist, double *__restrict__ out_vert, double *__restrict__ out_norm) {
     const int lane = threadIdx.x & 31;
-    const unsigned count = min(*rescue_count, cap);
+    const unsigned all = *rescue_count;
+    const unsigned count = min(all, cap);
     const unsigned nitems = count * (unsigned)vt.count;
     const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -1181,8 +1172,15 @@ __global__ void __launch_bounds__(128) raycast_coop_items_kernel(
             sl[6] = best.nz;
         }
     }
+    // rays beyond the split capacity (usually none): one warp per whole ray,
+    // written directly (they have no slots)
+    unsigned long long hits = 0;
+    coop_whole_rays(vt, g, out_dist, out_vert, out_norm, rescue, all, cap, warp, nwarps, samples, hits,
+                    exact_samples);
+    if (stats && threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&stats[TF_STAT_COOP_RAYS], (unsigned long long)all);
     if (stats && lane == 0) {  // every lane counted the same item: lane 0 reports
         atomicAdd(&stats[TF_STAT_RAY_SAMPLES], samples);
+        atomicAdd(&stats[TF_STAT_RAY_HITS], hits);
         atomicAdd(&stats[TF_STAT_EXACT_SAMPLES], exact_samples & ((1ull << 40) - 1));
         atomicAdd(&stats[TF_STAT_CERT_FAILURES], (exact_samples >> 40) & 15ull);
     }
@@ -1465,21 +1463,40 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
             void *pc = tf_profile_begin(TF_PROF_RAYCAST_COOP, stream);
             double *slots = (double *)(rescue + slot_off);
             raycast_coop_items_kernel<<<(unsigned)sms * 8, 128, 0, stream>>>(vt, g, st, rescue + 1, rescue,
-                                                                           kCoopSplitRays, slots);
+                                                                           kCoopSplitRays, slots, dist, vert,
+                                                                           norm);
             if ((rc = tf_check_launch("raycast_coop_items_kernel"))) return rc;
             raycast_coop_merge_kernel<<<kCoopSplitRays / 128, 128, 0, stream>>>(
                 vt.count, rescue + 1, rescue, kCoopSplitRays, slots, dist, vert, norm, st);
             if ((rc = tf_check_launch("raycast_coop_merge_kernel"))) return rc;
-            // rays beyond the split capacity: one warp per whole ray (usually
-            // none, so a small grid: the launch is nearly free when empty)
-            raycast_coop_kernel<<<(unsigned)sms, 128, 0, stream>>>(vt, g, dist, vert, norm, st, rescue + 1,
-                                                                     rescue, kCoopSplitRays);
             tf_profile_end(pc, stream);
-            if ((rc = tf_check_launch("raycast_coop_kernel"))) return rc;
         }
         tf_profile_end(prof, stream);
     }
     return TF_OK;
+}
+
+// RayMap.empty in place: +inf distances, zero vertices and normals (one
+// launch instead of three)
+__global__ void raymap_reset_kernel(double *__restrict__ dist, double *__restrict__ vert,
+                                    double *__restrict__ norm, int64_t npix) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * npix;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < npix) dist[i] = INFINITY;
+        vert[i] = 0.0;
+        norm[i] = 0.0;
+    }
+}
+
+extern "C" int tf_raymap_reset(double *dist_dev, double *vert_dev, double *norm_dev, int64_t npix,
+                               void *stream_) {
+    if (npix <= 0) return TF_OK;
+    if (!dist_dev || !vert_dev || !norm_dev) return tf_set_error(TF_EINVAL, "tf_raymap_reset: null argument");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    raymap_reset_kernel<<<(unsigned)sms * 4, 256, 0, (cudaStream_t)stream_>>>(dist_dev, vert_dev, norm_dev, npix);
+    return tf_check_launch("raymap_reset_kernel");
 }
 
 extern "C" int tf_raymap_merge_packed(double *dst_dev, const double *src_dev, int64_t npix, void *stream_) {

@@ -467,10 +467,15 @@ class RayMap:
             torch.full((h, w), float("inf"), dtype=torch.float64, device=dev)))
 
     def reset(self) -> "RayMap":
-        """Back to the empty state in place (no host round trip)."""
-        self.vertices_dev.zero_()
-        self.normals_dev.zero_()
-        self.distance_dev.fill_(float("inf"))
+        """Back to the empty state in place (no host round trip, one launch)."""
+        d, v, n = self.distance_dev, self.vertices_dev, self.normals_dev
+        if d.is_contiguous() and v.is_contiguous() and n.is_contiguous():
+            nat.check(nat.lib().tf_raymap_reset(d.data_ptr(), v.data_ptr(), n.data_ptr(), d.numel(),
+                                                nat.stream_handle()), "tf_raymap_reset")
+        else:
+            v.zero_()
+            n.zero_()
+            d.fill_(float("inf"))
         self._device_written()
         return self
 
