@@ -415,15 +415,29 @@ def run_e2e(args, tf, nat, torch, dist, rank, world, intr, spec, params, poses, 
     else:
         shard = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length,
                               params, intr, rank, world)
-        buf = torch.empty(host_frames[0].shape, dtype=torch.float64, device="cuda")
+        # the frame goes up (rank 0) and out (broadcast) on a side stream into
+        # one of two buffers, so the next frame's culling can start while this
+        # frame's raycast runs (ShardedFusion.step depth_ready)
+        bufs = [torch.empty(host_frames[0].shape, dtype=torch.float64, device="cuda") for _ in range(2)]
+        side = torch.cuda.Stream()
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        free = [torch.cuda.Event(), torch.cuda.Event()]
+        for e in free:
+            e.record()
 
         result = torch.empty(shard.stats.shape, dtype=shard.stats.dtype).pin_memory()
 
         def step(i):
-            if rank == 0:
-                buf.copy_(pinned[i], non_blocking=True)
-            broadcast_frame(buf)
-            shard.step(buf, poses[i])
+            slot = i & 1
+            side.wait_event(free[slot])
+            with torch.cuda.stream(side):
+                if rank == 0:
+                    bufs[slot].copy_(pinned[i], non_blocking=True)
+                broadcast_frame(bufs[slot])
+                ready[slot].record(side)
+            torch.cuda.current_stream().wait_event(ready[slot])
+            shard.step(bufs[slot], poses[i], depth_ready=ready[slot])
+            free[slot].record()
             result.copy_(shard.stats, non_blocking=True)
             return result
 
@@ -446,7 +460,7 @@ def run_e2e(args, tf, nat, torch, dist, rank, world, intr, spec, params, poses, 
             "h2d_bytes_per_step": int(host_frames[0].nbytes) if rank == 0 else 0,
             "d2h_bytes_per_step": int(out.numel() * out.element_size()), "steps": steps,
             "path": "FusionPipeline.step(pinned host frame)" if world == 1 else
-                    "rank-0 H2D + NCCL broadcast + ShardedFusion.step"}
+                    "rank-0 H2D + NCCL broadcast (side stream) + ShardedFusion.step"}
 
 
 def run_config2(args, tf, nat, torch, barrier, max_over_ranks) -> dict:
