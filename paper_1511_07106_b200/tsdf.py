@@ -353,11 +353,18 @@ class SplitIntegrator:
             self._ws_free, self._prepared = torch.cuda.Event(), torch.cuda.Event()
             self._ws_free.record(main)
         prep = self._prep
+        # the workspace is (re)allocated here, on the current stream, and marked
+        # as used by the side stream, so the caching allocator never hands a
+        # block one of the two streams still uses to the other
+        arr = _vol_array(volumes, params.truncation)
+        ws = nat.workspace.get(nat.lib().tf_integrate_workspace_size(arr, len(volumes), nat.camera(intr)),
+                               self._slot)
         if depth_ready is not True:
             prep.wait_event(depth_ready)
         prep.wait_event(self._ws_free)
         with torch.cuda.stream(prep):
             integrate_volumes(volumes, depth, pose, intr, params, phase="prepare", workspace_slot=self._slot)
+        ws.record_stream(prep)
         self._prepared.record(prep)
         main.wait_event(self._prepared)
         integrate_volumes(volumes, depth, pose, intr, params, stats, color=color, phase="finish",

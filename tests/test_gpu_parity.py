@@ -672,8 +672,8 @@ def test_pipeline_with_tracking_matches_the_reference(tmp_path, pinned):
     assert np.array_equal(res.cloud.normals, g["cloud_normals"])
 
 
-@pytest.mark.parametrize("tier", ["disk", "host"])
-def test_dynamic_placement_and_spill_match_the_reference(tmp_path, tier):
+@pytest.mark.parametrize("tier,pinned", [("disk", False), ("host", False), ("host", True)])
+def test_dynamic_placement_and_spill_match_the_reference(tmp_path, tier, pinned):
     """Dynamic placement down a corridor with tiles spilling (at most 4 tiles,
     3 resident), against the reference's own pipeline
     (tests/golden/dynamic_small.npz, pipeline.py:117-197, volumes.py:249-331):
@@ -687,7 +687,8 @@ def test_dynamic_placement_and_spill_match_the_reference(tmp_path, tier):
                        use_groundtruth=True, spill_tier=tier)
     pipe = tf.FusionPipeline(cfg, tmp_path)
     for i, (f, m) in enumerate(zip(g["frames"], g["poses"])):
-        r = pipe.step(tf.DepthFrame(f), Pose(m[:3, :3], m[:3, 3]))
+        frame = torch.from_numpy(np.ascontiguousarray(f)).pin_memory() if pinned else tf.DepthFrame(f)
+        r = pipe.step(frame, Pose(m[:3, :3], m[:3, 3]))
         want = [tuple(k) for k in g["keys"][g["offsets"][i]:g["offsets"][i + 1]].tolist()]
         assert list(pipe.volumes.keys()) == want, f"frame {i}"
         got = [r.volumes, r.resident, r.files_read, r.files_written, r.bytes_read, r.bytes_written]
