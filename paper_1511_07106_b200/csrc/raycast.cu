@@ -1125,7 +1125,7 @@ __device__ void coop_whole_rays(const VolumeTable &vt, const RayGeom &g, double 
 // _hit_wins — the same result, with the pass bounded by the slowest
 // ray-volume march instead of the slowest ray.  slots: 8 doubles per item
 // (t, hit xyz, normal xyz; t = +inf: no hit).
-__global__ void __launch_bounds__(128) raycast_coop_items_kernel(
+__global__ void __launch_bounds__(128, 4) raycast_coop_items_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ RayGeom g,
     unsigned long long *__restrict__ stats, const unsigned *__restrict__ rescue,
     const unsigned *__restrict__ rescue_count, const unsigned cap, double *__restrict__ slots,
