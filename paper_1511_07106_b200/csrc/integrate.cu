@@ -1509,7 +1509,7 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
             cudaEventRecord(side->fork, stream);
             cudaStreamWaitEvent(side->stream, side->fork, 0);
             void *pf = tf_profile_begin(TF_PROF_INTEGRATE_FREE, side->stream);
-            brick_free_kernel<<<(unsigned)sms * 8, 256, 0, side->stream>>>(vt, bt, f, active_free, fcount,
+            brick_free_kernel<<<(unsigned)sms * 4, 256, 0, side->stream>>>(vt, bt, f, active_free, fcount,
                                                                           fixed_point,
                                                                           (unsigned long long *)stats,
                                                                           changed);
@@ -1523,7 +1523,7 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
             tf_profile_end(pg, stream);
             if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
             void *pe = tf_profile_begin(TF_PROF_INTEGRATE_EXACT, stream);
-            exact_queue_kernel<<<(unsigned)sms * 16, 256, 0, stream>>>(vt, bt, f, table, queue, qcount,
+            exact_queue_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(vt, bt, f, table, queue, qcount,
                                                                      L.queue_cap,
                                                                      (unsigned long long *)stats, changed,
                                                                      count, fcount, (unsigned long long)off);
