@@ -1517,7 +1517,7 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
             if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
             cudaEventRecord(side->join, side->stream);
             void *pg = tf_profile_begin(TF_PROF_INTEGRATE_GENERAL, stream);
-            brick_update_kernel<<<(unsigned)sms * 6, 256, 0, stream>>>(
+            brick_update_kernel<<<(unsigned)sms * 9, 256, 0, stream>>>(
                 vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap,
                 fixed_point, (unsigned long long *)stats, changed);
             tf_profile_end(pg, stream);
