@@ -197,6 +197,16 @@ int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
                int64_t coarse_step, const double r_wc[9], const double cam_center[3],
                double *dist_dev, double *vert_dev, double *norm_dev,
                uint64_t *stats_dev, void *stream);
+/* tf_raycast with the cooperative pass's scratch (rescue list and per-(ray,
+ * volume) hit slots) taken from a caller workspace of at least
+ * tf_raycast_workspace_size(nvol, cam) bytes, 256-byte aligned, used by one
+ * stream at a time.  tf_raycast keeps an internal per-(device, stream)
+ * buffer instead (least recently used of 16 evicted). */
+size_t tf_raycast_workspace_size(int nvol, const TfCamera *cam);
+int tf_raycast_ws(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
+                  int64_t coarse_step, const double r_wc[9], const double cam_center[3],
+                  double *dist_dev, double *vert_dev, double *norm_dev, void *workspace_dev,
+                  size_t workspace_bytes, uint64_t *stats_dev, void *stream);
 
 /* ---- trilinear_sample (tsdf.py:147-153 / _kernels._sample :28-68) for
  * `npoints` world points (f64 [N][3]); writes value and validity per point. */
@@ -345,6 +355,10 @@ int tf_comm_link_local(TfComm *const *comms, int world);
 int tf_comm_reduce_raymap(TfComm *comm, unsigned flags, void *stream);
 /* Synchronous read of the region's error flag (1 = a wait timed out). */
 int tf_comm_error(const TfComm *comm, int *error);
+/* Non-blocking read of the error flag as of the last reduction that has
+ * completed on its stream (each tf_comm_reduce_raymap queues a copy of the
+ * flag into pinned host memory): the per-frame check of ShardedFusion. */
+int tf_comm_error_poll(const TfComm *comm, int *error);
 int tf_comm_destroy(TfComm *comm);
 
 #ifdef __cplusplus

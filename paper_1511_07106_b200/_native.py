@@ -99,6 +99,9 @@ _SIGNATURES = {
     "tf_raycast_colors": (_c_int, [_VOL, _c_int, _CAM, _c_p, _c_p, _c_p, _c_p, _c_p]),
     "tf_raycast": (_c_int, [_VOL, _c_int, _CAM, _c_d, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
                             _c_p, _c_p]),
+    "tf_raycast_workspace_size": (_c_sz, [_c_int, _CAM]),
+    "tf_raycast_ws": (_c_int, [_VOL, _c_int, _CAM, _c_d, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
+                               _c_p, _c_sz, _c_p, _c_p]),
     "tf_trilinear_sample": (_c_int, [_VOL, _c_p, _c_i64, _c_p, _c_p, _c_p]),
     "tf_good_threshold": (ctypes.c_float, [_c_d]),
     "tf_brick_summary": (_c_int, [_VOL, _c_p]),
@@ -124,6 +127,7 @@ _SIGNATURES = {
     "tf_comm_link_local": (_c_int, [_c_p, _c_int]),
     "tf_comm_reduce_raymap": (_c_int, [_c_p, ctypes.c_uint, _c_p]),
     "tf_comm_error": (_c_int, [_c_p, ctypes.POINTER(_c_int)]),
+    "tf_comm_error_poll": (_c_int, [_c_p, ctypes.POINTER(_c_int)]),
     "tf_comm_destroy": (_c_int, [_c_p]),
 }
 

@@ -47,6 +47,7 @@ struct TfComm {
     char *peer[TF_COMM_MAX_RANKS] = {};
     bool ipc_opened[TF_COMM_MAX_RANKS] = {};
     unsigned long long epoch = 0;
+    unsigned *err_host = nullptr;  // pinned copy of the error flag, refreshed after every reduction
 };
 
 namespace tf {
@@ -229,6 +230,13 @@ extern "C" int tf_comm_create(int rank, int world, int64_t width, int64_t height
         delete c;
         return cuda_fail(e, "tf_comm_create: init");
     }
+    e = cudaHostAlloc((void **)&c->err_host, sizeof(unsigned), cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+        cudaFree(c->base);
+        delete c;
+        return cuda_fail(e, "tf_comm_create: cudaHostAlloc");
+    }
+    *c->err_host = 0u;
     c->peer[rank] = c->base;
     *out = c;
     return TF_OK;
@@ -299,7 +307,19 @@ extern "C" int tf_comm_reduce_raymap(TfComm *c, unsigned flags, void *stream_) {
     int rc = tf_check_launch("raymap_reduce_kernel");
     if (rc || !wait) return rc;
     tf::comm_wait_done_kernel<<<1, 64, 0, stream>>>(pt);
-    return tf_check_launch("comm_wait_done_kernel");
+    rc = tf_check_launch("comm_wait_done_kernel");
+    if (rc) return rc;
+    // stream-ordered copy of the (sticky) error flag into pinned memory, so
+    // the host can poll it every frame without a synchronisation
+    const cudaError_t e = cudaMemcpyAsync(c->err_host, c->base + c->off[TF_COMM_FLAGS] + offsetof(tf::CommFlags, error),
+                                          sizeof(unsigned), cudaMemcpyDeviceToHost, stream);
+    return e == cudaSuccess ? TF_OK : cuda_fail(e, "tf_comm_reduce_raymap: error flag copy");
+}
+
+extern "C" int tf_comm_error_poll(const TfComm *c, int *error) {
+    if (!c || !error) return tf_set_error(TF_EINVAL, "tf_comm_error_poll: null argument");
+    *error = (int)*(volatile unsigned *)c->err_host;
+    return TF_OK;
 }
 
 extern "C" int tf_comm_error(const TfComm *c, int *error) {
@@ -317,6 +337,7 @@ extern "C" int tf_comm_destroy(TfComm *c) {
     for (int r = 0; r < c->world; ++r)
         if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->peer[r]);
     cudaFree(c->base);
+    if (c->err_host) cudaFreeHost(c->err_host);
     delete c;
     return TF_OK;
 }

@@ -1343,21 +1343,33 @@ __global__ void raycast_colors_kernel(const __grid_constant__ VolumeTable vt, co
 
 using namespace tf;
 
-// Rescue list of the cooperative pass: one persistent buffer per (device,
-// stream), grown on demand — launches on one stream are ordered, launches on
-// different streams never share a buffer, and no allocation sits on the
-// per-frame path (a stream-ordered pool would hand memory back to the driver
-// at every host synchronisation).
+// Rescue list + per-(ray, volume) hit slots of the cooperative pass.  They
+// come from the caller's workspace (tf_raycast_ws, sized by
+// tf_raycast_workspace_size); tf_raycast without a workspace keeps a small
+// per-(device, stream) table of buffers, least recently used evicted.
+namespace {
+constexpr unsigned kCoopSplitRays = 16384;
+
+int64_t rescue_slot_offset(int64_t npix) { return (npix + 1 + 63) / 64 * 64; }  // words, 256-B aligned
+
+int64_t rescue_words(int64_t npix, int nvol_launch) {
+    return rescue_slot_offset(npix) + (int64_t)kCoopSplitRays * nvol_launch * 16;
+}
+}  // namespace
+
 static unsigned *rescue_buffer(cudaStream_t stream, int64_t words) {
     struct Buf {
         int dev;
         cudaStream_t stream;
         unsigned *ptr;
         int64_t words;
+        unsigned long long used;
     };
+    constexpr int kBufs = 16;
     static std::mutex mu;
-    static Buf bufs[64];
+    static Buf bufs[kBufs];
     static int nbufs = 0;
+    static unsigned long long tick = 0;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> lock(mu);
@@ -1365,10 +1377,23 @@ static unsigned *rescue_buffer(cudaStream_t stream, int64_t words) {
     for (int i = 0; i < nbufs; ++i)
         if (bufs[i].dev == dev && bufs[i].stream == stream) b = &bufs[i];
     if (!b) {
-        if (nbufs == 64) return nullptr;
-        b = &bufs[nbufs++];
-        *b = Buf{dev, stream, nullptr, 0};
+        if (nbufs < kBufs) {
+            b = &bufs[nbufs++];
+        } else {  // evict the least recently used entry (its stream may still use it)
+            b = &bufs[0];
+            for (int i = 1; i < kBufs; ++i)
+                if (bufs[i].used < b->used) b = &bufs[i];
+            if (b->ptr) {
+                int cur = dev;
+                cudaSetDevice(b->dev);
+                cudaStreamSynchronize(b->stream);
+                cudaFree(b->ptr);
+                cudaSetDevice(cur);
+            }
+        }
+        *b = Buf{dev, stream, nullptr, 0, 0};
     }
+    b->used = ++tick;
     if (b->words < words) {
         if (b->ptr) {
             cudaStreamSynchronize(stream);  // the old buffer may still be in use on this stream
@@ -1382,10 +1407,38 @@ static unsigned *rescue_buffer(cudaStream_t stream, int64_t words) {
     return b->ptr;
 }
 
+extern "C" size_t tf_raycast_workspace_size(int nvol, const TfCamera *cam) {
+    if (!cam || nvol <= 0 || cam->width <= 0 || cam->height <= 0) return 0;
+    const int per = nvol < TFB200_MAX_VOLUMES_PER_LAUNCH ? nvol : TFB200_MAX_VOLUMES_PER_LAUNCH;
+    return (size_t)rescue_words(cam->width * cam->height, per) * sizeof(unsigned);
+}
+
+static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
+                        int64_t coarse_step, const double r_wc[9], const double cam_center[3],
+                        double *dist, double *vert, double *norm, void *workspace,
+                        size_t workspace_bytes, uint64_t *stats, void *stream_);
+
+extern "C" int tf_raycast_ws(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
+                             int64_t coarse_step, const double r_wc[9], const double cam_center[3],
+                             double *dist, double *vert, double *norm, void *workspace,
+                             size_t workspace_bytes, uint64_t *stats, void *stream_) {
+    if (!workspace && nvol > 0) return tf_set_error(TF_EINVAL, "tf_raycast_ws: null workspace");
+    return raycast_impl(vols, nvol, cam, tau, coarse_step, r_wc, cam_center, dist, vert, norm,
+                        workspace, workspace_bytes, stats, stream_);
+}
+
 extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
                           int64_t coarse_step, const double r_wc[9], const double cam_center[3],
                           double *dist, double *vert, double *norm, uint64_t *stats,
                           void *stream_) {
+    return raycast_impl(vols, nvol, cam, tau, coarse_step, r_wc, cam_center, dist, vert, norm,
+                        nullptr, 0, stats, stream_);
+}
+
+static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
+                        int64_t coarse_step, const double r_wc[9], const double cam_center[3],
+                        double *dist, double *vert, double *norm, void *workspace,
+                        size_t workspace_bytes, uint64_t *stats, void *stream_) {
     cudaStream_t stream = (cudaStream_t)stream_;
     if (nvol == 0) return TF_OK;
     if (!vols || nvol < 0 || !cam || !r_wc || !cam_center || !dist || !vert || !norm)
@@ -1432,9 +1485,16 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
         const int64_t npix = cam->width * cam->height;
         // [0] = count, then pixel indices; then the per-(ray, volume) hit slots
         // of the first kCoopSplitRays handed-over rays (8 doubles each)
-        constexpr unsigned kCoopSplitRays = 16384;
-        const int64_t slot_off = (npix + 1 + 63) / 64 * 64;  // words, 256-byte aligned
-        unsigned *rescue = rescue_buffer(stream, slot_off + (int64_t)kCoopSplitRays * vt.count * 16);
+        const int64_t slot_off = rescue_slot_offset(npix);
+        const int64_t words = rescue_words(npix, vt.count);
+        unsigned *rescue = nullptr;
+        if (workspace) {
+            if (workspace_bytes < (size_t)words * sizeof(unsigned) || ((uintptr_t)workspace & 255u))
+                return tf_set_error(TF_EINVAL, "tf_raycast_ws: workspace too small or not 256-byte aligned");
+            rescue = (unsigned *)workspace;
+        } else {
+            rescue = rescue_buffer(stream, words);
+        }
         if (!rescue || cudaMemsetAsync(rescue, 0, sizeof(unsigned), stream) != cudaSuccess)
             return tf_set_error(TF_ECUDA, "tf_raycast: cannot allocate the rescue list");
         auto launch = [&](auto kern, int bx, int by) {

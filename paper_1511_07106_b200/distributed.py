@@ -230,10 +230,23 @@ class PeerExchange:
         nat.check(nat.lib().tf_comm_link_local(arr, len(exchanges)), "tf_comm_link_local")
 
     def reduce(self, nowait: bool = False) -> RayMap:
+        # a wait that timed out leaves the flag raised for good and every later
+        # wait returns at once, so the merged maps would be folded unsynchronised:
+        # surface it on the next frame (the flag copy of the last completed
+        # reduction, no host synchronisation)
+        if self.poll_error():
+            raise RuntimeError("peer-memory ray-map reduction: a flag wait timed out "
+                               "(a peer stopped or its GPU is unreachable)")
         nat.check(nat.lib().tf_comm_reduce_raymap(self._h, nat.COMM_NOWAIT if nowait else 0,
                                                   nat.stream_handle()), "tf_comm_reduce_raymap")
         self.model._device_written()
         return self.model
+
+    def poll_error(self) -> int:
+        """The error flag as of the last completed reduction (non-blocking)."""
+        e = ctypes.c_int()
+        nat.check(nat.lib().tf_comm_error_poll(self._h, ctypes.byref(e)), "tf_comm_error_poll")
+        return e.value
 
     def error(self) -> int:
         """1 when a flag wait timed out (synchronous read)."""

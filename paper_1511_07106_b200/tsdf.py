@@ -343,8 +343,12 @@ class SplitIntegrator:
                  depth_ready=None) -> None:
         volumes = list(volumes)
         if (depth_ready is None or not volumes or len(volumes) > nat.MAX_VOLUMES_PER_LAUNCH
-                or not isinstance(depth, torch.Tensor) or not depth.is_cuda):
-            # nothing to overlap with: one call on the current stream
+                or not isinstance(depth, torch.Tensor) or not depth.is_cuda
+                or any(v._mirror.exposed for v in volumes)):
+            # nothing to overlap with, or a volume's host mirror is handed out
+            # (its upload and summary rebuild must stay ordered after the
+            # previous frame's raycast, which reads the same voxels): one call
+            # on the current stream
             integrate_volumes(volumes, depth, pose, intr, params, stats, color=color)
             return
         main = torch.cuda.current_stream(depth.device)
@@ -356,6 +360,9 @@ class SplitIntegrator:
         # the workspace is (re)allocated here, on the current stream, and marked
         # as used by the side stream, so the caching allocator never hands a
         # block one of the two streams still uses to the other
+        # brick summaries are (re)built here, on the current stream, so the
+        # side stream only reads the depth, the volumes' geometry and its
+        # own workspace
         arr = _vol_array(volumes, params.truncation)
         ws = nat.workspace.get(nat.lib().tf_integrate_workspace_size(arr, len(volumes), nat.camera(intr)),
                                self._slot)
@@ -545,12 +552,17 @@ def raycast_volumes(volumes: Sequence[TsdfSubvolume], pose: Pose, intr: CameraIn
     r = nat.mat9(pose.rotation)
     c = nat.vec3(pose.translation)
     st = stats if stats is not None else nat.stats.buffer()
+    L = nat.lib()
+    stream = nat.stream_handle()
     for coarse, vols in groups.items():
         arr = _vol_array(vols, params.truncation)
-        nat.check(nat.lib().tf_raycast(arr, len(vols), cam, float(params.truncation), int(coarse),
-                                       r, c, nat.ptr(raymap.distance_dev),
-                                       nat.ptr(raymap.vertices_dev), nat.ptr(raymap.normals_dev),
-                                       nat.ptr(st), nat.stream_handle()), "tf_raycast")
+        # the cooperative pass's scratch: one workspace per stream (launches on
+        # a stream are ordered; two streams never share one)
+        ws = nat.workspace.get(L.tf_raycast_workspace_size(len(vols), cam), f"raycast{stream}")
+        nat.check(L.tf_raycast_ws(arr, len(vols), cam, float(params.truncation), int(coarse),
+                                  r, c, nat.ptr(raymap.distance_dev),
+                                  nat.ptr(raymap.vertices_dev), nat.ptr(raymap.normals_dev),
+                                  nat.ptr(ws), ws.numel(), nat.ptr(st), stream), "tf_raycast_ws")
     raymap._device_written()
     return raymap
 

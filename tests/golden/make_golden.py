@@ -282,6 +282,210 @@ def dynamic_fixture():
           int(np.array(counters)[:, 3].sum()), "spill writes,", len(res.cloud.vertices), "cloud points")
 
 
+def _sha(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def config3_fixture():
+    """Config 3 at full size (BASELINE configs[2]): the 8 fixed 512^3 tiles of
+    init_grid(4.08, 1020, 510), 640x480 frames of the demo orbit, ground-truth
+    poses.  The reference's numba integrate_kernel runs frames 0, 9 and 18 into
+    every tile (each tile sees the three frames in order); after each frame the
+    SHA-256 of every tile's tsdf and weight bytes is recorded, and after frames 0
+    and 18 the merged raycast of all 8 tiles (reference tile order).  Hashes
+    only: the arrays are 8.6 GB.  Pins the GPU fused path (tests/test_gpu_parity.py)
+    and the oracle (tests/test_oracle_golden.py, slow) on the busy tiles too."""
+    cfg = tf.RunConfig()
+    intr = cfg.intrinsics()
+    spec = tf.init_grid(4.08, 1020, 510)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    scene = anchored_scene()
+    poses = tf.orbit_trajectory(np.array([0.0, 0.0, 1.5]), 1.5, 64)
+    frames_idx = [0, 9, 18]
+    tiles = [tf.TsdfSubvolume.empty(np.array(k), spec.voxels_per_side, spec.subvolume_side_length)
+             for k in spec.keys]
+    th, wh, upd = [], [], []
+    ray = {}
+    for f in frames_idx:
+        frame = scene.render_depth(poses[f], intr)
+        rt, rw, ru = [], [], []
+        for v in tiles:
+            w0 = v.weight.copy()
+            tf.integrate(v, frame, poses[f], intr, params)
+            ru.append(int(np.count_nonzero(v.weight != w0)))
+            rt.append(_sha(v.tsdf))
+            rw.append(_sha(v.weight))
+        th.append(rt)
+        wh.append(rw)
+        upd.append(ru)
+        if f in (0, 18):
+            rm = tf.RayMap.empty(intr)
+            for v in tiles:
+                tf.raycast(v, poses[f], intr, rm, params)
+            ray[f] = (_sha(rm.distance), _sha(rm.vertices), _sha(rm.normals),
+                      int(np.isfinite(rm.distance).sum()))
+        print("config3 frame", f, "updates", ru, flush=True)
+    np.savez_compressed(
+        OUT / "config3_hashes.npz",
+        keys=np.array(spec.keys, np.int64), frames=np.array(frames_idx, np.int64),
+        tsdf_sha=np.array(th), weight_sha=np.array(wh), changed=np.array(upd, np.int64),
+        ray_frames=np.array(sorted(ray), np.int64),
+        ray_sha=np.array([ray[f][:3] for f in sorted(ray)]),
+        ray_hits=np.array([ray[f][3] for f in sorted(ray)], np.int64),
+    )
+
+
+def icp_full_fixture():
+    """Config 2 at full resolution (BASELINE configs[1]): run_fusion's tracking
+    on one 256^3 tile (init_grid(3.0, 254, 254)), 640x480, the 1.5-degree orbit,
+    frames 0-5.  Every _solve_step of every track() call is recorded with its
+    inputs (estimate, level) and outputs (count, delta, rms), plus the SHA-256
+    of the model ray map each call tracks against and the reference's poses
+    (exact bits), so a GPU pipeline driven by those poses rebuilds the identical
+    model and replays every step (tests/test_gpu_parity.py)."""
+    import tempfile
+    cfg = tf.RunConfig(side_length=3.0, resolution=254, resident_resolution=254,
+                       use_groundtruth=False)
+    intr = cfg.intrinsics()
+    scene = anchored_scene()
+    poses = tf.orbit_trajectory(np.array([0.0, 0.0, 1.5]), 1.5, 240)[:6]
+    steps = []
+    models = []
+    real = tr._solve_step
+    frame_no = [0]
+
+    def spy(src_pts, src_nrm, src_valid, model_pts, model_nrm, model_valid, estimate,
+            ref_inv, intr_l, params_l, min_pairs):
+        out = real(src_pts, src_nrm, src_valid, model_pts, model_nrm, model_valid,
+                   estimate, ref_inv, intr_l, params_l, min_pairs)
+        rec = {"frame": frame_no[0], "level_w": intr_l.width, "estimate": estimate.matrix.copy(),
+               "min_pairs": min_pairs}
+        if out is None:
+            rec.update(count=-1, delta=np.full(6, np.nan), rms=np.nan)
+        else:
+            rec.update(count=out[1], delta=out[0].copy(), rms=out[2])
+        steps.append(rec)
+        return out
+
+    tr._solve_step = spy
+    import tilefusion.pipeline as tp
+    tp_track = tp.track
+
+    def track_spy(frame, intr_, model, ref_pose, params=tr.TrackingParams(), init=None):
+        models.append((frame_no[0], _sha(model.distance), _sha(model.vertices),
+                       _sha(model.normals), int(np.isfinite(model.distance).sum())))
+        return tp_track(frame, intr_, model, ref_pose, params, init)
+
+    tp.track = track_spy
+    out_poses, recs = [], []
+    try:
+        with tempfile.TemporaryDirectory() as tmp:
+            pipe = tf.FusionPipeline(cfg, tmp)
+            for i, p in enumerate(poses):
+                frame_no[0] = i
+                r = pipe.step(scene.render_depth(p, intr), p)
+                recs.append((r.tracked, r.correspondences, r.residual_rms))
+                print("icp_full frame", i, r.tracked, r.correspondences, flush=True)
+            out_poses = list(pipe.poses)
+    finally:
+        tr._solve_step = real
+        tp.track = tp_track
+    np.savez_compressed(
+        OUT / "icp_full.npz",
+        intr=intr_arr(intr), gt_poses=pose_arr(poses), poses=pose_arr(out_poses),
+        tracked=np.array([r[0] for r in recs]), correspondences=np.array([r[1] for r in recs], np.int64),
+        residual_rms=np.array([r[2] for r in recs], np.float64),
+        model_frame=np.array([m[0] for m in models], np.int64),
+        model_sha=np.array([m[1:4] for m in models]), model_hits=np.array([m[4] for m in models], np.int64),
+        step_frame=np.array([s["frame"] for s in steps], np.int64),
+        step_level_w=np.array([s["level_w"] for s in steps]),
+        step_estimate=np.stack([s["estimate"] for s in steps]),
+        step_min_pairs=np.array([s["min_pairs"] for s in steps]),
+        step_count=np.array([s["count"] for s in steps]),
+        step_delta=np.stack([s["delta"] for s in steps]),
+        step_rms=np.array([s["rms"] for s in steps]),
+    )
+    print("icp_full:", len(steps), "steps over", len(models), "track calls")
+
+
+CORRIDOR_BOXES = ((-0.85, 0.10, 3.0, -0.45, 0.50, 3.6),
+                  (0.40, 0.20, 6.5, 0.85, 0.50, 7.2),
+                  (-0.80, -0.30, 10.0, -0.50, 0.50, 10.4),
+                  (0.30, 0.00, 13.5, 0.80, 0.50, 14.5),
+                  (-0.70, 0.25, 17.0, -0.20, 0.50, 17.5))  # = synth.CORRIDOR_BOXES
+
+
+def corridor_scene():
+    prims = [tf.Plane(np.array([0.9, 0.0, 0.0]), np.array([-1.0, 0.0, 0.0])),
+             tf.Plane(np.array([-0.9, 0.0, 0.0]), np.array([1.0, 0.0, 0.0])),
+             tf.Plane(np.array([0.0, 0.5, 0.0]), np.array([0.0, -1.0, 0.0]))]
+    prims += [tf.Box(np.array(b[:3]), np.array(b[3:])) for b in CORRIDOR_BOXES]
+    return tf.Scene(tuple(prims))
+
+
+CONFIG4 = dict(frames=2000, length=20.0, block_voxels=258, block_side_length=1.024,
+               max_volumes=16, hysteresis=1.5)
+
+
+def _config4_hist(i):
+    cfg = tf.RunConfig(dynamic=True, block_voxels=CONFIG4["block_voxels"],
+                       block_side_length=CONFIG4["block_side_length"])
+    intr = cfg.intrinsics()
+    pose = tf.corridor_trajectory(CONFIG4["length"], CONFIG4["frames"])[i]
+    d = corridor_scene().render_depth(pose, intr).data.copy()
+    d[d > 4.0] = 0.0  # test_acceptance.py:241
+    spacing = CONFIG4["block_voxels"] - 2
+    c = tf.bin_endpoints(tf.DepthFrame(d), intr, pose, spacing,
+                         CONFIG4["block_side_length"] / spacing)
+    return sorted(c.items())
+
+
+def placement_fixture():
+    """Config 4's placement over ALL 2000 corridor frames at 640x480
+    (BASELINE configs[3]; pipeline.py:126-127, :175-184): per frame the
+    reference's bin_endpoints histogram (volumes.py:305-331) and the
+    update_allocation decision (volumes.py:358-389) given the allocation the
+    previous frames left (ground-truth poses, so placement does not depend on
+    the map).  Histograms are computed in a process pool (independent per
+    frame); the decisions run in frame order."""
+    import multiprocessing as mp
+    n = CONFIG4["frames"]
+    with mp.get_context("fork").Pool(min(8, os.cpu_count() or 1)) as pool:
+        hists = pool.map(_config4_hist, range(n), chunksize=8)
+    policy = tf.AllocationPolicy(max_volumes=CONFIG4["max_volumes"],
+                                 hysteresis=CONFIG4["hysteresis"])
+    current: list = []
+    hk, hc, ho = [], [], [0]
+    ak, ao, rk, ro = [], [0], [], [0]
+    for h in hists:
+        for k, c in h:
+            hk.append(k)
+            hc.append(c)
+        ho.append(len(hk))
+        added, removed = tf.update_allocation(tuple(current), dict(h), policy)
+        for k in removed:
+            current.remove(k)
+        current.extend(added)
+        ak.extend(added)
+        ao.append(len(ak))
+        rk.extend(removed)
+        ro.append(len(rk))
+    np.savez_compressed(
+        OUT / "placement_config4.npz",
+        frames=np.int64(n), length=np.float64(CONFIG4["length"]),
+        block_voxels=np.int64(CONFIG4["block_voxels"]),
+        block_side_length=np.float64(CONFIG4["block_side_length"]),
+        max_volumes=np.int64(CONFIG4["max_volumes"]), hysteresis=np.float64(CONFIG4["hysteresis"]),
+        hist_keys=np.array(hk, np.int64).reshape(-1, 3), hist_counts=np.array(hc, np.int64),
+        hist_offsets=np.array(ho, np.int64),
+        added=np.array(ak, np.int64).reshape(-1, 3), added_offsets=np.array(ao, np.int64),
+        removed=np.array(rk, np.int64).reshape(-1, 3), removed_offsets=np.array(ro, np.int64),
+        final_keys=np.array(current, np.int64).reshape(-1, 3),
+    )
+    print("placement_config4:", n, "frames,", len(hk), "cells,", len(ak), "adds,", len(rk), "removals")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:  # regenerate only the named fixtures
         for name in sys.argv[1:]:
@@ -293,5 +497,8 @@ if __name__ == "__main__":
     endpoints_fixture()
     pipeline_fixture()
     dynamic_fixture()
+    config3_fixture()
+    icp_full_fixture()
+    placement_fixture()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size, "bytes")
