@@ -7,21 +7,32 @@ on "at 1/2/4/8 B200"): 8 fixed 512^3 volumes tiling a 4.08 m cube at 4 mm
 (init_grid(4.08, 1020, 510)), 640x480 frames of the demo scene (sphere +
 floor + box) along orbit_trajectory((0,0,1.5), 1.5, 64), ground-truth poses.
 One step = one frame through the hot path: fused integration of every
-volume + fused raycast of every volume (+ all-gather / _hit_wins merge of
-the partial ray maps across ranks when N > 1).  With N GPUs the 8 volumes
-are owned by the ranks in checkerboard-spread chunks (total work fixed -> "strong").
+volume + fused raycast of every volume (+ the _hit_wins reduction of the
+partial ray maps across ranks when N > 1).
+
+Frame schedule (identical in every arm, independent of K): one untimed lap
+over the 64 orbit frames builds the map, W warm-up steps follow, then the K
+timed steps take frames spread uniformly over the orbit (frame
+floor(s * 64 / K) for K <= 64, s mod 64 beyond), so a short run times the
+same mix as a long one.
 
 value  = voxel updates per frame x frames/s, inputs resident in HBM, CUDA
-         events on the launching stream, L2 flushed (256 MiB write) between
-         timed steps, max over ranks.
+         events on the launching stream per step, L2 flushed (256 MiB write)
+         between timed steps, max over ranks.
 e2e    = the same through the public FusionPipeline.step API with the frame
          read from pinned host memory each step (H2D inside the timed region)
          and the step's counters read back (D2H).
-config2 (secondary): BASELINE configs[1] — one 256^3 volume with ICP
-         tracking on (integrate + raycast + projective ICP per frame).
+Extra legs (N = 1): config1 / config2 (BASELINE configs[0], [1]) with their
+CPU baselines, config4 (dynamic placement over the 2000-frame corridor),
+config5 (1024^3 tiles through the pinned-host spill tier), colour.
 
---impl reference times the reference algorithm on the host CPU (the C
-restatement in oracle/, all host threads) on the same workload and metric.
+--impl reference times the reference algorithm on the host CPU on the same
+frames and map state: the C restatement in oracle/ on all host threads (the
+headline CPU arm) and, as a second stated baseline, the unmodified reference
+package (numba, single core) from baseline/_ref on a bounded sample.
+
+--gpus N without a torchrun environment re-launches this script under
+torch.distributed.run with N ranks (127.0.0.1); rank 0 prints the line.
 """
 
 from __future__ import annotations
@@ -30,6 +41,7 @@ import argparse
 import gc
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -46,45 +58,85 @@ sys.path.insert(0, str(ROOT))
 METRIC = "TSDF voxel-updates/sec and frames/sec at 1/2/4/8 B200; % HBM roofline"
 BYTES_PER_UPDATE = 16  # read + write of f32 tsdf and f32 weight
 FALLBACK_HBM_GBS = 6650.0
+LAP = 64               # frames of the orbit (BASELINE configs[0..2])
 
 
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--steps", type=int, default=64)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-color", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--no-config2", action="store_true")
-    p.add_argument("--frames", type=int, default=64, help="distinct frames cycled through")
+    p.add_argument("--no-extra", action="store_true", help="skip the config1/2/4/5 legs")
+    p.add_argument("--no-numba", action="store_true", help="reference arm: skip the numba sample")
     return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# launcher
+# ---------------------------------------------------------------------------
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_if_needed(args) -> None:
+    """--gpus N > 1 outside torchrun: start N ranks of this script."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None:
+        if args.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                   f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+                   f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+            sys.exit(subprocess.call(cmd))
+        return
+    if int(env_world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}")
 
 
 # ---------------------------------------------------------------------------
 # workload
 # ---------------------------------------------------------------------------
 
-def workload(nframes: int):
+def workload():
     import paper_1511_07106_b200 as tf
     from paper_1511_07106_b200.synth import demo_scene
 
     intr = tf.RunConfig().intrinsics()
     spec = tf.init_grid(4.08, 1020, 510)
     params = tf.FusionParams.for_voxel_size(spec.voxel_size)
-    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)[:nframes]
-    scene = demo_scene()
-    return intr, spec, params, poses, scene
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, LAP)
+    return intr, spec, params, poses, demo_scene()
 
 
-def config_desc(n_gpus: int) -> dict:
-    return {"workload": "configs[2]: 8 fixed 512^3 TSDF volumes at 4 mm (init_grid(4.08, 1020, "
-                        "510)), 640x480 demo-scene orbit frames, ground-truth poses; step = "
-                        "integrate + raycast of every volume",
-            "volumes": 8, "voxels_per_side": 512, "voxel_size_m": 0.004, "image": "640x480",
-            "ownership": f"checkerboard-spread chunks over {n_gpus} rank(s) (distributed.owned_keys)",
-            "l2": "flushed between timed steps (256 MiB write); volumes 8.6 GB > L2"}
+def timed_frames(k: int) -> list[int]:
+    return [(s * LAP) // k for s in range(k)] if k <= LAP else [s % LAP for s in range(k)]
+
+
+def warm_frames(w: int) -> list[int]:
+    return [(LAP // 2 + s * 7) % LAP for s in range(w)]
+
+
+SCHEDULE_DESC = ("one untimed lap over the 64 orbit frames, W warm-up frames, then K timed frames "
+                 "spread uniformly over the orbit (floor(s*64/K)); identical in both arms")
+
+
+def config_desc(n_gpus: int, retile: int = 1) -> dict:
+    d = {"workload": "configs[2]: 8 fixed 512^3 TSDF volumes at 4 mm (init_grid(4.08, 1020, 510)), "
+                     "640x480 demo-scene orbit frames, ground-truth poses; step = integrate + "
+                     "raycast of every volume",
+         "volumes": 8, "voxels_per_side": 512, "voxel_size_m": 0.004, "image": "640x480",
+         "frames": SCHEDULE_DESC,
+         "l2": "flushed between timed steps (256 MiB write); volumes 8.6 GB > L2"}
+    if n_gpus > 1:
+        d["ownership"] = (f"each 512^3 tile re-tiled into {retile}^3 sub-tiles (2-voxel overlap), "
+                          f"sub-tiles owned by {n_gpus} ranks by balanced update counts")
+    return d
 
 
 def peak_hbm() -> tuple[float, str]:
@@ -98,58 +150,86 @@ def peak_hbm() -> tuple[float, str]:
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """NVML clock / throttle-reason sampling every 5 ms in a thread
+    (B200_PROFILING.md clocks line); summary over a marked time window."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int) -> None:
-        self.index = index
-        self.proc = None
-        self.lines: list[str] = []
+    def __init__(self, index: int, period: float = 0.005) -> None:
+        self.index, self.period = index, period
+        self.samples: list[tuple[float, float, float, int]] = []
+        self._stop = threading.Event()
+        self._t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._nv, self._h = pynvml, h
+            self._max = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
         except Exception:
-            self.proc = None
+            self._t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv, h = self._nv, self._h
+        while not self._stop.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                self.samples.append((time.perf_counter(), sm, self._max, rs))
+            except Exception:
+                pass
+            self._stop.wait(self.period)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._t is not None:
             self._t.join(timeout=2)
 
-    def summary(self) -> dict | None:
-        rows = []
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) == 6:
-                try:
-                    rows.append((float(parts[0]), float(parts[1]), parts[2:]))
-                except ValueError:
-                    pass
-        if not rows:
+    def summary(self, t0: float, t1: float) -> dict | None:
+        if not self.samples:
             return None
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        active = sorted({names[i] for _, _, flags in rows for i, f in enumerate(flags)
-                         if f.lower().startswith("active")})
-        return {"sm_mhz": statistics.median(r[0] for r in rows),
-                "sm_max_mhz": max(r[1] for r in rows), "reasons": active, "samples": len(rows)}
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        rows = inside if len(inside) >= 3 else self.samples
+        nv = self._nv
+        names = {nv.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                 nv.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                 nv.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                 nv.nvmlClocksEventReasonSwPowerCap: "sw_power_cap"}
+        active = sorted({n for _, _, _, rs in rows for bit, n in names.items() if rs & bit})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
+                "reasons": active, "samples": len(rows), "samples_in_timed_region": len(inside),
+                "window": "timed region" if len(inside) >= 3 else "warm-up + timed region",
+                "period_ms": 1e3 * self.period, "source": "NVML"}
+
+
+def render_frames(poses, intr, scene_fn="demo_scene", max_range=None, procs=None):
+    """Depth frames of the synthetic scene (host renderer, identical to the
+    reference's), rendered in a process pool; float64 arrays."""
+    import multiprocessing as mp
+    procs = procs or max(1, min(16, os.cpu_count() or 1))
+    mats = [p.matrix for p in poses]
+    args = [(m, (intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height), scene_fn, max_range)
+            for m in mats]
+    if len(args) <= 8 or procs == 1:
+        return [_render_one(a) for a in args]
+    with mp.get_context("spawn").Pool(procs) as pool:
+        return pool.map(_render_one, args, chunksize=max(1, len(args) // (4 * procs)))
+
+
+def _render_one(a):
+    from paper_1511_07106_b200 import geometry, synth
+    m, ci, scene_fn, max_range = a
+    intr = geometry.CameraIntrinsics(fx=ci[0], fy=ci[1], cx=ci[2], cy=ci[3], width=int(ci[4]),
+                                     height=int(ci[5]))
+    pose = geometry.Pose(m[:3, :3].copy(), m[:3, 3].copy())
+    d = getattr(synth, scene_fn)().render_depth(pose, intr).data
+    if max_range is not None:
+        d = d.copy()
+        d[d > max_range] = 0.0
+    return d
 
 
 # ---------------------------------------------------------------------------
@@ -175,14 +255,12 @@ def run_ours(args) -> None:
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    import paper_1511_07106_b200 as tf
     from paper_1511_07106_b200 import _native as nat
-    from paper_1511_07106_b200.distributed import ShardedFusion, broadcast_frame
+    from paper_1511_07106_b200.distributed import ShardedFusion, default_retile
 
     lib = nat.load_library()
-    intr, spec, params, poses, scene = workload(args.frames)
-    nframes = len(poses)
-    host_frames = [scene.render_depth(p, intr).data for p in poses]
+    intr, spec, params, poses, scene = workload()
+    host_frames = render_frames(poses, intr)
     dev_frames = torch.stack([torch.from_numpy(f) for f in host_frames]).cuda()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -205,15 +283,16 @@ def run_ours(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return int(t.item())
 
+    retile = default_retile(world)
     shard = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length, params,
-                          intr, rank, world)
+                          intr, rank, world, retile=retile)
 
-    # ---- warm-up (also the per-frame work cycle starts here) ----
-    for i in range(args.warmup):
-        shard.step(dev_frames[i % nframes], poses[i % nframes])
+    # ---- untimed lap (builds the map) + warm-up ----
+    for i in range(LAP):
+        shard.step(dev_frames[i], poses[i])
+    for i in warm_frames(args.warmup):
+        shard.step(dev_frames[i], poses[i])
     barrier()
-    if shard._peer is not None and shard._peer.error():
-        raise RuntimeError("peer-memory ray-map reduction: a flag wait timed out (warm-up)")
 
     # ---- timed region: resident inputs, per-step events, L2 flushed between ----
     shard.stats.zero_()
@@ -222,19 +301,20 @@ def run_ours(args) -> None:
     launches0 = lib.tf_launch_count()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    sched = timed_frames(args.steps)
     with ClockSampler(local) as clocks:
         barrier()
-        for s in range(args.steps):
+        t0 = time.perf_counter()
+        for s, i in enumerate(sched):
             flush.zero_()
-            i = (args.warmup + s) % nframes
             starts[s].record()
             shard.step(dev_frames[i], poses[i])
             stops[s].record()
         barrier()
+        t1 = time.perf_counter()
     lib.tf_profile_enable(0)
     launches = lib.tf_launch_count() - launches0
-    if shard._peer is not None and shard._peer.error():
-        raise RuntimeError("peer-memory ray-map reduction: a flag wait timed out")
+    shard.check_exchange()
     ms_total = sum(a.elapsed_time(b) for a, b in zip(starts, stops))
     prof = nat.profile_read()
     st = shard.stats.cpu().numpy()
@@ -247,31 +327,27 @@ def run_ours(args) -> None:
     updates_per_frame = updates / args.steps
     value = updates_per_frame * fps
 
-    # roofline of the dominant kernel (the voxel-update kernel), this rank
+    # roofline of the dominant kernel (the voxel-update bracket), this rank
     upd_ms, upd_launches = prof["integrate_update"]
     int_ms, _ = prof["integrate_all"]
     ray_ms, ray_launches = prof["raycast"]
     peak, peak_src = peak_hbm()
     achieved = (BYTES_PER_UPDATE * updates_local / max(upd_launches, 1)) / (
         upd_ms / max(upd_launches, 1) / 1e3) / 1e9 if upd_ms > 0 else 0.0
-    traffic = ray_traffic = None
-    tfile = ROOT / "profiles" / "traffic_r01.json"
+    traffic = ray_traffic = traffic_src = None
+    tfile = ROOT / "profiles" / "traffic_r02.json"
     if tfile.exists():
         try:
             tj = json.loads(tfile.read_text())
             traffic = tj.get("integrate_update_bracket_bytes_per_launch")
-            ray_traffic = next((v for k, v in tj.get("per_kernel_dram_bytes", {}).items()
-                                if k.startswith("raycast_kernel")), None)
+            ray_traffic = tj.get("raycast_bytes_per_launch")
+            traffic_src = tj.get("source")
         except Exception:
             traffic = ray_traffic = None
-    # raycast: not HBM-bound (gathers mostly hit L1/L2); reported
-    # against the same HBM peak for scale, with the nominal 64 B per evaluated
-    # (gathering) sample: certified-free samples read no voxels
     evaluated = samples - sum_over_ranks(int(st[nat.STAT_SUMMARY_SAMPLES]))
     ray_achieved = (64.0 * evaluated / max(ray_launches, 1)) / (ray_ms / max(ray_launches, 1) / 1e3) / 1e9 \
         if ray_ms > 0 else 0.0
 
-    # per-kernel sub-rooflines of the update bracket (16 B per update each)
     def comp(kind, n_updates):
         ms, n = prof[kind]
         if ms <= 0:
@@ -288,18 +364,23 @@ def run_ours(args) -> None:
         "exact_queue_kernel (near-surface band, reference arithmetic)": comp("integrate_exact", exact_upd),
     }
 
+    def per_frame(stat):
+        return sum_over_ranks(int(st[stat])) / args.steps
+
     result = {
         "metric": METRIC, "value": value, "unit": "voxel-updates/s",
         "frames_per_s": fps, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(config_desc(world), **({"raymap_exchange": {
+        "config": dict(config_desc(world, retile), **({"raymap_exchange": {
             "p2p": "peer-memory reduce kernel (csrc/comm.cu, CUDA IPC over NVLink)",
             "collective": "NCCL row-block all-to-all + merge + all-gather"}[shard.exchange]}
             if world > 1 else {})),
         "voxel_updates_per_frame": updates_per_frame,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "kernel": "integrate update bracket (brick_update_kernel + brick_free_kernel + "
                                "exact_queue_kernel, TF_PROF_INTEGRATE_UPDATE)", "peak_source": peak_src,
                      "bytes_per_update": BYTES_PER_UPDATE,
@@ -315,42 +396,53 @@ def run_ours(args) -> None:
         "breakdown_ms_per_step": {"integrate_update_kernel": upd_ms / args.steps,
                                   "integrate_total": int_ms / args.steps,
                                   "raycast": ray_ms / args.steps},
-        "integrate": {"noop_updates_per_frame": sum_over_ranks(int(st[nat.STAT_NOOP_UPDATES])) / args.steps, "swept_voxels_per_frame": sum_over_ranks(int(st[nat.STAT_SWEPT_VOXELS])) / args.steps,
-                      "exact_path_voxels_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_VOXELS])) / args.steps,
-                      "column_rejected_per_frame": sum_over_ranks(int(st[nat.STAT_COL_SKIPPED])) / args.steps,
-                      "depth_rejected_per_frame": sum_over_ranks(int(st[nat.STAT_DEPTH_SKIPPED])) / args.steps,
-                      "active_bricks_per_frame": sum_over_ranks(int(st[nat.STAT_ACTIVE_BRICKS])) / args.steps,
-                      "free_space_bricks_per_frame": sum_over_ranks(int(st[nat.STAT_FREE_BRICKS])) / args.steps,
-                      "general_bricks_all_free_per_frame": sum_over_ranks(int(st[nat.STAT_GENERAL_ALL_FREE])) / args.steps,
-                      "general_parts_all_free_per_frame": sum_over_ranks(int(st[nat.STAT_PART_ALL_FREE])) / args.steps,
-                      "general_parts_all_skip_per_frame": sum_over_ranks(int(st[nat.STAT_PART_ALL_SKIP])) / args.steps,
+        "integrate": {"noop_updates_per_frame": per_frame(nat.STAT_NOOP_UPDATES),
+                      "swept_voxels_per_frame": per_frame(nat.STAT_SWEPT_VOXELS),
+                      "exact_path_voxels_per_frame": per_frame(nat.STAT_EXACT_VOXELS),
+                      "column_rejected_per_frame": per_frame(nat.STAT_COL_SKIPPED),
+                      "depth_rejected_per_frame": per_frame(nat.STAT_DEPTH_SKIPPED),
+                      "active_bricks_per_frame": per_frame(nat.STAT_ACTIVE_BRICKS),
+                      "free_space_bricks_per_frame": per_frame(nat.STAT_FREE_BRICKS),
+                      "general_bricks_all_free_per_frame": per_frame(nat.STAT_GENERAL_ALL_FREE),
+                      "general_parts_all_free_per_frame": per_frame(nat.STAT_PART_ALL_FREE),
+                      "general_parts_all_skip_per_frame": per_frame(nat.STAT_PART_ALL_SKIP),
                       "total_bricks": sum_over_ranks(int(st[nat.STAT_TOTAL_BRICKS])) // max(args.steps, 1)},
-        "raycast": {"exact_samples_per_frame": sum_over_ranks(int(st[nat.STAT_EXACT_SAMPLES])) / args.steps,
+        "raycast": {"exact_samples_per_frame": per_frame(nat.STAT_EXACT_SAMPLES),
                     "certification_failures": sum_over_ranks(int(st[nat.STAT_CERT_FAILURES])),
-                    "summary_certified_samples_per_frame": sum_over_ranks(int(st[nat.STAT_SUMMARY_SAMPLES])) / args.steps,
+                    "summary_certified_samples_per_frame": per_frame(nat.STAT_SUMMARY_SAMPLES),
                     "samples_per_frame": samples / args.steps,
-                    "coop_rays_per_frame": sum_over_ranks(int(st[nat.STAT_COOP_RAYS])) / args.steps,
+                    "coop_rays_per_frame": per_frame(nat.STAT_COOP_RAYS),
                     "coop_pass_ms_per_frame": prof["raycast_coop"][0] / args.steps,
                     "samples_per_s": samples / (ms_total / 1e3)},
         "gpu_launches": int(launches),
+        "clocks": clocks.summary(t0, t1),
     }
-    cs = clocks.summary()
-    result["clocks"] = cs
-
-    # ---- the same step with colour (north_star; the reference has no colour) ----
-    if not args.no_color and world == 1:
-        result["color"] = run_color(args, tf, torch, spec, params, intr, poses, scene, barrier)
+    if world > 1:
+        result["balance"] = shard.balance_report()
 
     # ---- e2e through the public pipeline API, frames from pinned host memory ----
     if not args.no_e2e:
-        result["e2e"] = run_e2e(args, tf, nat, torch, dist, rank, world, intr, spec, params,
-                                poses, host_frames, barrier, max_over_ranks, sum_over_ranks)
-    del shard, dev_frames
+        del shard
+        torch.cuda.empty_cache()
+        result["e2e"] = run_e2e(args, torch, nat, dist, rank, world, intr, spec, params, poses,
+                                host_frames, barrier, max_over_ranks, sum_over_ranks)
+    else:
+        del shard
+    del dev_frames
     torch.cuda.empty_cache()
 
-    if not args.no_config2:
-        result["config2"] = run_config2(args, tf, nat, torch, barrier, max_over_ranks)
-
+    if world == 1 and not args.no_color:
+        result["color"] = run_color(args, torch, spec, params, intr, poses, scene, barrier)
+        torch.cuda.empty_cache()
+    if world == 1 and not args.no_extra:
+        for name, fn in (("config1", run_config1), ("config2", run_config2),
+                         ("config4", run_config4), ("config5", run_config5)):
+            try:
+                result[name] = fn(args, torch, nat, barrier, cpu=not args.no_cpu_baseline)
+            except Exception as exc:  # a leg must not take the headline line down
+                result[name] = {"error": f"{type(exc).__name__}: {exc}"}
+            gc.collect()
+            torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(intr, spec, params, poses, host_frames)
     if rank == 0:
@@ -360,126 +452,144 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-def run_color(args, tf, torch, spec, params, intr, poses, scene, barrier) -> dict:
-    """Config 3 with an RGB frame fused into a colour channel per volume (the
-    band voxels' running mean, tf_integrate_rgb) and the model colours
-    rendered (tf_raycast_colors) every step: device-resident inputs."""
+def run_color(args, torch, spec, params, intr, poses, scene, barrier) -> dict:
+    """Config 3 with an RGB frame fused into a colour channel per volume and
+    the model colours rendered every step: device-resident inputs, the same
+    frame schedule.  Colour is not in the reference (parity unpinned)."""
+    import paper_1511_07106_b200 as tf
     from paper_1511_07106_b200.distributed import ShardedFusion
     from paper_1511_07106_b200.synth import render_rgb
 
-    steps = args.steps  # the same frame mix as the device-timed loop (early frames are slower)
-    n = len(poses)
-    depth = [torch.from_numpy(scene.render_depth(p, intr).data).cuda() for p in poses]
-    rgb = [torch.from_numpy(render_rgb(scene, p, intr)).cuda() for p in poses]
+    depth = [torch.from_numpy(scene.render_depth(poses[i], intr).data).cuda() for i in range(LAP)]
+    rgb = [torch.from_numpy(render_rgb(scene, poses[i], intr)).cuda() for i in range(LAP)]
     shard = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length, params, intr,
                           color=True)
-    for i in range(args.warmup):
-        shard.step(depth[i % n], poses[i % n], color=rgb[i % n])
-        tf.raycast_colors(shard.tiles, shard.model, poses[i % n], intr)
+    for i in list(range(LAP)) + warm_frames(args.warmup):
+        shard.step(depth[i], poses[i], color=rgb[i])
+        tf.raycast_colors(shard.tiles, shard.model, poses[i], intr)
     barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for s in range(steps):
-        i = (args.warmup + s) % n
+    for i in timed_frames(args.steps):
         shard.step(depth[i], poses[i], color=rgb[i])
         tf.raycast_colors(shard.tiles, shard.model, poses[i], intr)
     b.record()
     barrier()
-    ms = a.elapsed_time(b) / steps
+    ms = a.elapsed_time(b) / args.steps
     del shard
-    torch.cuda.empty_cache()
-    return {"frames_per_s": 1000.0 / ms, "ms_per_step": ms, "steps": steps,
+    return {"frames_per_s": 1000.0 / ms, "ms_per_step": ms, "steps": args.steps,
             "path": "ShardedFusion.step(depth, pose, color=rgb) + raycast_colors, inputs resident",
-            "note": "colour is not in the reference; no L2 flush between steps"}
+            "note": "colour is not in the reference (parity unpinned); no L2 flush between steps"}
 
 
-def run_e2e(args, tf, nat, torch, dist, rank, world, intr, spec, params, poses, host_frames,
+def run_e2e(args, torch, nat, dist, rank, world, intr, spec, params, poses, host_frames,
             barrier, max_over_ranks, sum_over_ranks) -> dict:
-    from paper_1511_07106_b200.distributed import ShardedFusion, broadcast_frame
+    """The headline step through the public FusionPipeline.step API: every
+    rank passes its pinned host frame (rank 0's is broadcast when N > 1)."""
+    import paper_1511_07106_b200 as tf
 
-    nframes = len(poses)
     pinned = [torch.from_numpy(f).pin_memory() for f in host_frames]
-    steps = args.steps  # the same frame mix as the device-timed loop (early frames are slower)
-    if world == 1:
-        cfg = tf.RunConfig(side_length=4.08, resolution=1020, resident_resolution=510,
-                           use_groundtruth=True, max_resident=8)
-        spill = tempfile.mkdtemp(prefix="tfb200_spill_")
-        pipe = tf.FusionPipeline(cfg, spill)
+    cfg = tf.RunConfig(side_length=4.08, resolution=1020, resident_resolution=510,
+                       use_groundtruth=True, max_resident=8)
+    spill = tempfile.mkdtemp(prefix="tfb200_spill_")
+    pipe = tf.FusionPipeline(cfg, spill, rank=rank, world=world)
+    result = torch.empty(pipe.stats.shape, dtype=pipe.stats.dtype).pin_memory()
 
-        result = torch.empty(pipe.stats.shape, dtype=pipe.stats.dtype).pin_memory()
+    def step(i):
+        pipe.step(pinned[i], poses[i])               # public API: H2D inside step()
+        result.copy_(pipe.stats, non_blocking=True)  # D2H of the step's counters
+        return result
 
-        def step(i):
-            pipe.step(pinned[i], poses[i])          # public API: H2D inside step()
-            result.copy_(pipe.stats, non_blocking=True)  # D2H of the step's counters
-            return result
-    else:
-        shard = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length,
-                              params, intr, rank, world)
-        # the frame goes up (rank 0) and out (broadcast) on a side stream into
-        # one of two buffers, so the next frame's culling can start while this
-        # frame's raycast runs (ShardedFusion.step depth_ready)
-        bufs = [torch.empty(host_frames[0].shape, dtype=torch.float64, device="cuda") for _ in range(2)]
-        side = torch.cuda.Stream()
-        ready = [torch.cuda.Event(), torch.cuda.Event()]
-        free = [torch.cuda.Event(), torch.cuda.Event()]
-        for e in free:
-            e.record()
-
-        result = torch.empty(shard.stats.shape, dtype=shard.stats.dtype).pin_memory()
-
-        def step(i):
-            slot = i & 1
-            side.wait_event(free[slot])
-            with torch.cuda.stream(side):
-                if rank == 0:
-                    bufs[slot].copy_(pinned[i], non_blocking=True)
-                broadcast_frame(bufs[slot])
-                ready[slot].record(side)
-            torch.cuda.current_stream().wait_event(ready[slot])
-            shard.step(bufs[slot], poses[i], depth_ready=ready[slot])
-            free[slot].record()
-            result.copy_(shard.stats, non_blocking=True)
-            return result
-
-    for i in range(args.warmup):
-        out = step(i % nframes)
+    for i in list(range(LAP)) + warm_frames(args.warmup):
+        out = step(i)
     torch.cuda.synchronize()
     barrier()
     before = int(out[nat.STAT_VOXEL_UPDATES])
     # every step uploads its frame from pinned memory and reads its counters
-    # back into pinned memory, both stream-ordered; the host does not wait per
-    # step, only once at the end (the last read has landed when the clock stops)
+    # back into pinned memory, both stream-ordered; the host waits once at
+    # the end (the last read has landed when the clock stops)
     t0 = time.perf_counter()
-    for s in range(steps):
-        out = step((args.warmup + s) % nframes)
+    for i in timed_frames(args.steps):
+        out = step(i)
     torch.cuda.synchronize()
     barrier()
     sec = max_over_ranks(time.perf_counter() - t0)
     updates = sum_over_ranks(int(out[nat.STAT_VOXEL_UPDATES]) - before)
-    return {"value": updates / sec, "unit": "voxel-updates/s", "frames_per_s": steps / sec,
+    del pipe
+    return {"value": updates / sec, "unit": "voxel-updates/s", "frames_per_s": args.steps / sec,
             "h2d_bytes_per_step": int(host_frames[0].nbytes) if rank == 0 else 0,
-            "d2h_bytes_per_step": int(out.numel() * out.element_size()), "steps": steps,
-            "path": "FusionPipeline.step(pinned host frame)" if world == 1 else
-                    "rank-0 H2D + NCCL broadcast (side stream) + ShardedFusion.step"}
+            "d2h_bytes_per_step": int(out.numel() * out.element_size()), "steps": args.steps,
+            "path": "FusionPipeline.step(pinned host frame)" +
+                    (f" at world {world} (rank-0 H2D + broadcast)" if world > 1 else "")}
 
 
-def run_config2(args, tf, nat, torch, barrier, max_over_ranks) -> dict:
-    """BASELINE configs[1]: one 256^3 volume, ICP tracking on, 1.5-degree orbit."""
-    from paper_1511_07106_b200.synth import demo_scene
+# ---------------------------------------------------------------------------
+# extra legs (N = 1): the other BASELINE configs
+# ---------------------------------------------------------------------------
+
+def _pipeline_run(torch, pipe, frames_pinned, poses, first_gt=True):
+    """Frames through FusionPipeline.step (pinned host frames), host waits
+    once at the end; returns seconds."""
+    t0 = time.perf_counter()
+    for i, f in enumerate(frames_pinned):
+        pipe.step(f, poses[i])
+    torch.cuda.synchronize()
+    return time.perf_counter() - t0
+
+
+def run_config1(args, torch, nat, barrier, cpu: bool) -> dict:
+    """BASELINE configs[0]: one 256^3 volume (init_grid(3.0, 254, 254)), 64
+    orbit frames, ground-truth poses, through FusionPipeline.step from pinned
+    host frames; frames/s excludes frame 0 (evaluation.py:112-119).  CPU: the
+    oracle over the same 64 frames on all host threads."""
+    import paper_1511_07106_b200 as tf
+
+    cfg = tf.RunConfig(side_length=3.0, resolution=254, resident_resolution=254,
+                       use_groundtruth=True)
+    intr = cfg.intrinsics()
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, LAP)
+    host = render_frames(poses, intr)
+    pinned = [torch.from_numpy(f).pin_memory() for f in host]
+    warm = tf.FusionPipeline(cfg, tempfile.mkdtemp(prefix="tfb200_c1w_"))
+    _pipeline_run(torch, warm, pinned, poses)
+    del warm
+    pipe = tf.FusionPipeline(cfg, tempfile.mkdtemp(prefix="tfb200_c1_"))
+    pipe.step(pinned[0], poses[0])
+    torch.cuda.synchronize()
+    pipe.stats.zero_()
+    gc.disable()
+    sec = _pipeline_run(torch, pipe, pinned[1:], poses[1:])
+    gc.enable()
+    ks = pipe.kernel_stats()
+    out = {"workload": "configs[0]: one 256^3 volume (init_grid(3.0, 254, 254)), 640x480, 64 orbit "
+                       "frames, ground-truth poses, FusionPipeline.step from pinned host frames",
+           "frames": LAP - 1, "frames_per_s": (LAP - 1) / sec,
+           "voxel_updates_per_s": ks["voxel_updates"] / sec,
+           "voxel_updates_per_frame": ks["voxel_updates"] / (LAP - 1)}
+    if cpu:
+        import oracle
+        spec = tf.init_grid(3.0, 254, 254)
+        params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+        out["cpu"] = _cpu_static(oracle, spec, params, intr, poses, host, list(range(1, LAP)),
+                                 warm=[0], kind="full 64-frame run (frame 0 untimed)")
+    return out
+
+
+def run_config2(args, torch, nat, barrier, cpu: bool) -> dict:
+    """BASELINE configs[1]: one 256^3 volume, ICP tracking on, 1.5-degree orbit
+    (64 frames).  CPU: the oracle's integrate / raycast / track on all host
+    threads over the first 9 frames (8 tracked), per frame."""
+    import paper_1511_07106_b200 as tf
 
     cfg = tf.RunConfig(side_length=3.0, resolution=254, resident_resolution=254,
                        use_groundtruth=False)
     intr = cfg.intrinsics()
-    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 240)[:64]
-    scene = demo_scene()
-    steps = min(args.steps, 63)
-    frames = [torch.from_numpy(scene.render_depth(p, intr).data).cuda() for p in poses[:steps + 1]]
-    # an untimed pass over the same frames first (allocator growth, workspaces,
-    # first launches), then the timed pass with a fresh pipeline
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 240)[:LAP]
+    host = render_frames(poses, intr)
+    frames = [torch.from_numpy(f).cuda() for f in host]
     warm = tf.FusionPipeline(cfg, tempfile.mkdtemp(prefix="tfb200_c2w_"))
-    warm.step(frames[0], poses[0])
-    for i in range(1, steps + 1):
-        warm.step(frames[i])
+    for i, f in enumerate(frames):
+        warm.step(f, poses[i] if i == 0 else None)
     torch.cuda.synchronize()
     del warm
     pipe = tf.FusionPipeline(cfg, tempfile.mkdtemp(prefix="tfb200_c2_"))
@@ -487,79 +597,373 @@ def run_config2(args, tf, nat, torch, barrier, max_over_ranks) -> dict:
     gc.collect()
     barrier()
     pipe.stats.zero_()
-    gc.disable()  # no collector pause inside the 60-80 ms timed pass
+    gc.disable()  # no collector pause inside the short timed pass
     t0 = time.perf_counter()
-    for i in range(1, steps + 1):
+    for i in range(1, LAP):
         pipe.step(frames[i])
-        if os.environ.get("TFB200_C2_TRACE"):
-            torch.cuda.synchronize()
-            print(f"config2 frame {i}: {1e3 * (time.perf_counter() - t0):.2f} ms", file=sys.stderr)
     barrier()
-    sec = max_over_ranks(time.perf_counter() - t0)
+    sec = time.perf_counter() - t0
     gc.enable()
     ks = pipe.kernel_stats()
     lost = sum(1 for r in pipe.records[1:] if not r.tracked)
-    err = max(float(np.abs(p.translation - q.translation).max())
-              for p, q in zip(pipe.poses, poses[:steps + 1]))
-    return {"workload": "configs[1]: one 256^3 volume (init_grid(3.0, 254, 254)), 640x480, "
-                        "1.5-degree orbit, ICP tracking on", "frames": steps,
-            "frames_per_s": steps / sec, "voxel_updates_per_s": ks["voxel_updates"] / sec,
-            "lost_frames": lost, "max_translation_error_m": err}
+    err = max(float(np.abs(p.translation - q.translation).max()) for p, q in zip(pipe.poses, poses))
+    out = {"workload": "configs[1]: one 256^3 volume (init_grid(3.0, 254, 254)), 640x480, "
+                       "1.5-degree orbit, ICP tracking on (frames resident)", "frames": LAP - 1,
+           "frames_per_s": (LAP - 1) / sec, "voxel_updates_per_s": ks["voxel_updates"] / sec,
+           "lost_frames": lost, "max_translation_error_m": err}
+    if cpu:
+        import oracle
+        spec = tf.init_grid(3.0, 254, 254)
+        params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+        out["cpu"] = _cpu_tracked(oracle, spec, params, intr, poses, host, 9)
+    return out
+
+
+CONFIG4 = dict(frames=2000, length=20.0, block_voxels=258, block_side_length=1.024,
+               max_volumes=16, hysteresis=1.5, max_range=4.0)
+
+
+def run_config4(args, torch, nat, barrier, cpu: bool) -> dict:
+    """BASELINE configs[3]: dynamic placement over the 2000-frame corridor
+    (synth.corridor_scene, corridor_trajectory(20, 2000), depth > 4 m zeroed,
+    258^3 tiles at 4 mm, at most 16 tiles, hysteresis 1.5, ground-truth poses),
+    every frame through FusionPipeline.step from pinned host frames: placement
+    (device endpoint histogram + host update_allocation), integration and
+    raycast of the allocated tiles, removal (extraction of retired tiles)."""
+    import paper_1511_07106_b200 as tf
+
+    c = CONFIG4
+    cfg = tf.RunConfig(dynamic=True, block_voxels=c["block_voxels"],
+                       block_side_length=c["block_side_length"], max_volumes=c["max_volumes"],
+                       hysteresis=c["hysteresis"], max_resident=c["max_volumes"], use_groundtruth=True)
+    intr = cfg.intrinsics()
+    poses = tf.corridor_trajectory(c["length"], c["frames"])
+    t_r = time.perf_counter()
+    host = render_frames(poses, intr, "corridor_scene", c["max_range"])
+    render_s = time.perf_counter() - t_r
+    pinned = [torch.from_numpy(f).pin_memory() for f in host]
+    warm = tf.FusionPipeline(cfg, tempfile.mkdtemp(prefix="tfb200_c4w_"))
+    _pipeline_run(torch, warm, pinned[:50], poses[:50])
+    del warm
+    torch.cuda.empty_cache()
+    pipe = tf.FusionPipeline(cfg, tempfile.mkdtemp(prefix="tfb200_c4_"))
+    pipe.step(pinned[0], poses[0])
+    torch.cuda.synchronize()
+    pipe.stats.zero_()
+    gc.disable()
+    sec = _pipeline_run(torch, pipe, pinned[1:], poses[1:])
+    gc.enable()
+    ks = pipe.kernel_stats()
+    n = c["frames"] - 1
+    vols = [r.volumes for r in pipe.records]
+    out = {"workload": "configs[3]: dynamic placement, corridor_trajectory(20.0, 2000), 640x480, "
+                       "258^3 tiles at 4 mm, max_volumes 16, hysteresis 1.5, depth > 4 m zeroed, "
+                       "ground-truth poses, pinned host frames", "frames": n,
+           "frames_per_s": n / sec, "voxel_updates_per_s": ks["voxel_updates"] / sec,
+           "voxel_updates_per_frame": ks["voxel_updates"] / n, "max_live_tiles": max(vols),
+           "distinct_tiles": len(set(k for k in pipe.volumes.keys())) + len(pipe._archive),
+           "host_render_s": render_s}
+    if cpu:
+        import oracle
+        out["cpu"] = _cpu_dynamic(oracle, cfg, intr, poses, host, 50)
+    del pipe
+    return out
+
+
+def run_config5(args, torch, nat, barrier, cpu: bool) -> dict:
+    """BASELINE configs[4], one GPU's share: 4 of the 32 1024^3 tiles (~1 mm
+    voxels; the 4x4x2 key block, spacing 1022) — the 4 rank 0 owns at N = 8 —
+    with max_resident = 2, so every frame evicts tiles to the pinned-host
+    spill tier (async D2H/H2D side stream) and brings others back.  Reports
+    frames/s, spill GB/s and the pinned copy bandwidth measured alongside."""
+    import psutil
+
+    import paper_1511_07106_b200 as tf
+    from paper_1511_07106_b200.distributed import owned_keys
+    from paper_1511_07106_b200.volumes import VolumeSet
+
+    n = 1024
+    tile_bytes = n ** 3 * 8
+    if psutil.virtual_memory().available < 6 * tile_bytes:
+        return {"skipped": f"needs ~{6 * tile_bytes / 1e9:.0f} GB free host memory for the spill tier"}
+    vs = 0.001
+    keys = [(x * 1022, y * 1022, z * 1022) for x in (-2, -1, 0, 1) for y in (-2, -1, 0, 1)
+            for z in (0, 1)]
+    mine = owned_keys(keys, 0, 8)
+    params = tf.FusionParams.for_voxel_size(vs)
+    intr = tf.RunConfig().intrinsics()
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, LAP)
+    frame_ids = [0, 16, 32, 48]
+    host = render_frames([poses[i] for i in frame_ids], intr)
+    pinned = [torch.from_numpy(f).pin_memory() for f in host]
+    # pinned copy bandwidth on this box, for the spill rate's denominator
+    src = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+    dst = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
+    for _ in range(2):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    d2h = (1 << 30) / (time.perf_counter() - t0) / 1e9
+    t0 = time.perf_counter()
+    src.copy_(dst, non_blocking=True)
+    torch.cuda.synchronize()
+    h2d = (1 << 30) / (time.perf_counter() - t0) / 1e9
+    del src, dst
+    vset = VolumeSet(params, voxels_per_side=n, voxel_size=vs, max_resident=2,
+                     spill_dir=tempfile.mkdtemp(prefix="tfb200_c5_"), spill_tier="host")
+    for k in mine:
+        vset.add(k)
+    stats = nat.stats.buffer()
+
+    def frame(j):
+        depth = torch.empty(host[j].shape, dtype=torch.float64, device="cuda")
+        depth.copy_(pinned[j], non_blocking=True)
+        rm = tf.RayMap.empty(intr)
+        for k in vset.keys():
+            tile = vset.acquire(k)
+            tf.integrate_volumes([tile], depth, poses[frame_ids[j]], intr, params, stats)
+            tf.raycast_volumes([tile], poses[frame_ids[j]], intr, rm, params, stats)
+            vset.release(k)
+        return rm
+
+    frame(0)
+    torch.cuda.synchronize()
+    stats.zero_()
+    b0 = (vset.bytes_read, vset.bytes_written)
+    t0 = time.perf_counter()
+    for j in range(1, len(frame_ids)):
+        frame(j)
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    moved = (vset.bytes_read - b0[0]) + (vset.bytes_written - b0[1])
+    upd = int(stats[nat.STAT_VOXEL_UPDATES].item())
+    nf = len(frame_ids) - 1
+    out = {"workload": "configs[4], one GPU's share at N = 8: 4 tiles of 1024^3 at 1 mm (4x4x2 key "
+                       "block, spacing 1022; rank 0's of 8), max_resident 2 -> pinned-host spill "
+                       "every frame; orbit frames 16, 32, 48 timed (0 untimed)",
+           "tiles": len(mine), "tile_bytes": tile_bytes, "frames": nf, "frames_per_s": nf / sec,
+           "voxel_updates_per_s": upd / sec, "spill_bytes_per_frame": moved / nf,
+           "spill_gbs": moved / sec / 1e9, "pinned_d2h_gbs": d2h, "pinned_h2d_gbs": h2d,
+           "bound": "host link (each frame moves every tile through the spill tier)"}
+    del vset
+    return out
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (oracle restatement of the reference kernels, all host threads)
+# CPU baselines (oracle restatement of the reference kernels, all host threads)
 # ---------------------------------------------------------------------------
 
-def cpu_frame_sample(intr, spec, params, poses, host_frames, volumes: int, threads: int,
-                     first: int = 0) -> dict:
-    import oracle
+def _coarse(params, vs):
+    return max(2, int(round(0.5 * params.truncation / vs)))
 
-    n = spec.voxels_per_side
-    vs = spec.voxel_size
-    coarse = max(2, int(round(0.5 * params.truncation / vs)))
-    keys = [spec.keys[(first + i) % len(spec.keys)] for i in range(volumes)]
-    tiles = [(np.zeros((n, n, n), np.float32), np.zeros((n, n, n), np.float32)) for _ in keys]
-    p0, p1 = poses[0], poses[1]
-    for (t, w), k in zip(tiles, keys):
-        inv = p0.invert()
-        oracle.integrate(t, w, k, vs, host_frames[0], inv.rotation, inv.translation,
-                         p0.translation, intr.fx, intr.fy, intr.cx, intr.cy, params.truncation,
-                         params.max_weight, params.sample_weight, threads=threads)
-    inv = p1.invert()
+
+def _oracle_frame(oracle, tiles, keys, vs, params, intr, pose, depth, threads, raycast=True):
+    inv = pose.invert()
     t0 = time.perf_counter()
     updates = 0
     for (t, w), k in zip(tiles, keys):
-        updates += oracle.integrate(t, w, k, vs, host_frames[1], inv.rotation, inv.translation,
-                                    p1.translation, intr.fx, intr.fy, intr.cx, intr.cy,
+        updates += oracle.integrate(t, w, k, vs, depth, inv.rotation, inv.translation,
+                                    pose.translation, intr.fx, intr.fy, intr.cx, intr.cy,
                                     params.truncation, params.max_weight, params.sample_weight,
                                     threads=threads)
     t_int = time.perf_counter() - t0
-    d = np.full((intr.height, intr.width), np.inf)
-    v = np.zeros((intr.height, intr.width, 3))
-    nn = np.zeros_like(v)
-    t0 = time.perf_counter()
-    for (t, w), k in zip(tiles, keys):
-        oracle.raycast(t, w, k, vs, params.truncation, coarse, p1.rotation, p1.translation,
-                       intr.fx, intr.fy, intr.cx, intr.cy, d, v, nn, threads=threads)
-    t_ray = time.perf_counter() - t0
-    return {"updates": updates, "t_integrate": t_int, "t_raycast": t_ray, "volumes": volumes}
+    maps = None
+    t_ray = 0.0
+    if raycast:
+        d = np.full((intr.height, intr.width), np.inf)
+        v = np.zeros((intr.height, intr.width, 3))
+        nn = np.zeros_like(v)
+        t0 = time.perf_counter()
+        for (t, w), k in zip(tiles, keys):
+            oracle.raycast(t, w, k, vs, params.truncation, _coarse(params, vs), pose.rotation,
+                           pose.translation, intr.fx, intr.fy, intr.cx, intr.cy, d, v, nn,
+                           threads=threads)
+        t_ray = time.perf_counter() - t0
+        maps = (d, v, nn)
+    return updates, t_int, t_ray, maps
+
+
+def _cpu_static(oracle, spec, params, intr, poses, frames, timed, warm=(), kind=""):
+    threads = oracle.default_threads()
+    n = spec.voxels_per_side
+    tiles = [(np.zeros((n, n, n), np.float32), np.zeros((n, n, n), np.float32)) for _ in spec.keys]
+    for i in warm:
+        _oracle_frame(oracle, tiles, spec.keys, spec.voxel_size, params, intr, poses[i], frames[i],
+                      threads, raycast=False)
+    tot, ups = 0.0, 0
+    for i in timed:
+        u, ti, tr, _ = _oracle_frame(oracle, tiles, spec.keys, spec.voxel_size, params, intr, poses[i],
+                                     frames[i], threads)
+        tot += ti + tr
+        ups += u
+    return {"frames_per_s": len(timed) / tot, "voxel_updates_per_s": ups / tot, "cores": threads,
+            "kind": "port", "sample": kind}
+
+
+def _cpu_tracked(oracle, spec, params, intr, poses, frames, nframes):
+    """Config 2 on the CPU: per frame oracle.track against the previous model,
+    then integrate + raycast at the tracked pose (pipeline.py:117-172)."""
+    import paper_1511_07106_b200 as tf
+    threads = oracle.default_threads()
+    n = spec.voxels_per_side
+    vs = spec.voxel_size
+    tiles = [(np.zeros((n, n, n), np.float32), np.zeros((n, n, n), np.float32)) for _ in spec.keys]
+    pose = poses[0]
+    _, _, _, model = _oracle_frame(oracle, tiles, spec.keys, vs, params, intr, pose, frames[0], threads)
+    tot, t_track, lost = 0.0, 0.0, 0
+    for i in range(1, nframes):
+        t0 = time.perf_counter()
+        rot, t, is_lost, _, _ = oracle.track(frames[i], intr.fx, intr.fy, intr.cx, intr.cy, *model,
+                                             pose.rotation, pose.translation, pose.rotation,
+                                             pose.translation)
+        dt = time.perf_counter() - t0
+        t_track += dt
+        if is_lost:
+            lost += 1
+        else:
+            pose = tf.Pose(rot, t)
+        _, ti, tr, model = _oracle_frame(oracle, tiles, spec.keys, vs, params, intr, pose, frames[i],
+                                         threads)
+        tot += dt + ti + tr
+    k = nframes - 1
+    return {"frames_per_s": k / tot, "track_s_per_frame": t_track / k, "lost_frames": lost,
+            "cores": threads, "kind": "port",
+            "sample": f"frames 1-{k} of the run (frame 0 untimed): oracle.track + integrate + raycast"}
+
+
+def _cpu_dynamic(oracle, cfg, intr, poses, frames, nframes):
+    """Config 4's first frames on the CPU: placement (oracle endpoint cells +
+    the reference's histogram and update_allocation), then integrate + raycast
+    of every allocated tile (tiles retired by placement are dropped; the
+    extraction of retired tiles is not timed here)."""
+    from paper_1511_07106_b200.volumes import AllocationPolicy, update_allocation
+    threads = oracle.default_threads()
+    spacing = cfg.block_voxels - 2
+    vs = cfg.block_side_length / spacing
+    n = cfg.block_voxels
+    params = cfg.fusion_params(vs)
+    policy = AllocationPolicy(max_volumes=cfg.max_volumes, hysteresis=cfg.hysteresis)
+    tiles: dict = {}
+    tot, ups = 0.0, 0
+    for i in range(nframes):
+        t0 = time.perf_counter()
+        p = poses[i]
+        counts = oracle.bin_endpoints(frames[i], intr.fx, intr.fy, intr.cx, intr.cy, p.rotation,
+                                      p.translation, spacing, vs)
+        added, removed = update_allocation(tuple(tiles), counts, policy)
+        for k in removed:
+            del tiles[k]
+        for k in added:
+            tiles[k] = (np.zeros((n, n, n), np.float32), np.zeros((n, n, n), np.float32))
+        dt = time.perf_counter() - t0
+        u, ti, tr, _ = _oracle_frame(oracle, list(tiles.values()), list(tiles), vs, params, intr, p,
+                                     frames[i], threads)
+        if i > 0:
+            tot += dt + ti + tr
+            ups += u
+    k = nframes - 1
+    return {"frames_per_s": k / tot, "voxel_updates_per_s": ups / tot, "cores": threads,
+            "kind": "port", "sample": f"frames 1-{k} of the 2000 (frame 0 untimed)"}
+
+
+class OracleMap:
+    """The config-3 map on the host (oracle arrays), advanced through the same
+    frame schedule as the GPU arm."""
+
+    def __init__(self, oracle, intr, spec, params, poses, frames, threads):
+        self.o, self.intr, self.spec, self.params = oracle, intr, spec, params
+        self.poses, self.frames, self.threads = poses, frames, threads
+        n = spec.voxels_per_side
+        self.tiles = [(np.zeros((n, n, n), np.float32), np.zeros((n, n, n), np.float32))
+                      for _ in spec.keys]
+
+    def integrate_only(self, i):
+        _oracle_frame(self.o, self.tiles, self.spec.keys, self.spec.voxel_size, self.params,
+                      self.intr, self.poses[i], self.frames[i], self.threads, raycast=False)
+
+    def step(self, i, subset=None):
+        """integrate every tile (the map state must follow the GPU arm's),
+        raycast the tiles in ``subset``; returns (updates, integrate s, raycast s
+        scaled to all tiles)."""
+        ups, ti, _, _ = _oracle_frame(self.o, self.tiles, self.spec.keys, self.spec.voxel_size,
+                                      self.params, self.intr, self.poses[i], self.frames[i],
+                                      self.threads, raycast=False)
+        idx = list(range(len(self.tiles))) if subset is None else subset
+        _, _, tr, _ = _oracle_frame(self.o, [self.tiles[j] for j in idx],
+                                    [self.spec.keys[j] for j in idx], self.spec.voxel_size,
+                                    self.params, self.intr, self.poses[i], self.frames[i],
+                                    self.threads)
+        return ups, ti, tr * len(self.tiles) / len(idx)
 
 
 def cpu_baseline(intr, spec, params, poses, host_frames) -> dict:
+    """The oracle on all host threads on a bounded sample of the same workload:
+    the lap that builds the map, then 3 frames of the timed schedule."""
     import oracle
 
     threads = oracle.default_threads()
-    vols = 8 if threads >= 16 else 2
-    s = cpu_frame_sample(intr, spec, params, poses, host_frames, vols, threads)
-    frame_s = (s["t_integrate"] + s["t_raycast"]) * 8 / vols
-    updates_frame = s["updates"] * 8 / vols
-    return {"value": updates_frame / frame_s, "unit": "voxel-updates/s", "cores": threads,
-            "kind": "port", "frames_per_s": 1.0 / frame_s,
-            "sample": f"frame 1 of the same workload, {vols} of 8 volumes (integrate + raycast, "
-                      f"C oracle on {threads} host threads), scaled to 8 volumes",
-            "integrate_s_per_volume": s["t_integrate"] / vols,
-            "raycast_s_per_volume": s["t_raycast"] / vols}
+    m = OracleMap(oracle, intr, spec, params, poses, host_frames, threads)
+    t0 = time.perf_counter()
+    for i in range(LAP):
+        m.integrate_only(i)
+    lap_s = time.perf_counter() - t0
+    times, ups = [], []
+    for i in timed_frames(3):
+        u, ti, tr = m.step(i)
+        times.append(ti + tr)
+        ups.append(u)
+    frame_s = sum(times) / len(times)
+    return {"value": sum(ups) / sum(times), "unit": "voxel-updates/s", "cores": threads, "kind": "port",
+            "frames_per_s": 1.0 / frame_s,
+            "sample": f"the map after the 64-frame lap (integrated untimed, {lap_s:.0f} s), then 3 "
+                      f"frames of the timed schedule (integrate + raycast of all 8 volumes), C oracle "
+                      f"on {threads} host threads"}
+
+
+def numba_sample(intr, spec, params, poses, host_frames, m: OracleMap, frame: int, tiles: list) -> dict:
+    """The unmodified reference package (baseline/_ref, numba, single core)
+    on a bounded sample: its public integrate + raycast on ``tiles`` of the
+    map state ``m`` holds (copied), frame ``frame``; scaled to 8 tiles."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "tilefusion").exists():
+        return {"unavailable": "baseline/_ref not installed"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="tfb200_numba_"))
+    sys.path.insert(0, str(ref))
+    import tilefusion as rtf
+
+    rintr = rtf.CameraIntrinsics(fx=intr.fx, fy=intr.fy, cx=intr.cx, cy=intr.cy, width=intr.width,
+                                 height=intr.height)
+    rparams = rtf.FusionParams.for_voxel_size(spec.voxel_size)
+    # JIT warm-up on a tiny volume (compilation excluded, SURVEY.md App. A.10)
+    small = rtf.TsdfSubvolume.empty(np.array([-8, -8, 100]), 16, 16 * spec.voxel_size)
+    f0 = rtf.DepthFrame(host_frames[frame])
+    p = poses[frame]
+    rpose = rtf.Pose(p.rotation.copy(), p.translation.copy())
+    rtf.integrate(small, f0, rpose, rintr, rparams)
+    rtf.raycast(small, rpose, rintr, rtf.RayMap.empty(rintr), rparams)
+    t_int = t_ray = 0.0
+    rm = rtf.RayMap.empty(rintr)
+    for j in tiles:
+        vol = rtf.TsdfSubvolume.empty(np.array(spec.keys[j]), spec.voxels_per_side,
+                                      spec.subvolume_side_length)
+        np.copyto(vol.tsdf, m.tiles[j][0])
+        np.copyto(vol.weight, m.tiles[j][1])
+        t0 = time.perf_counter()
+        rtf.integrate(vol, f0, rpose, rintr, rparams)
+        t_int += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rtf.raycast(vol, rpose, rintr, rm, rparams)
+        t_ray += time.perf_counter() - t0
+        del vol
+    scale = len(spec.keys) / len(tiles)
+    frame_s = (t_int + t_ray) * scale
+    return {"frames_per_s": 1.0 / frame_s, "integrate_s_per_volume": t_int / len(tiles),
+            "raycast_s_per_volume": t_ray / len(tiles), "cores": 1, "kind": "reference",
+            "sample": f"unmodified reference (baseline/_ref, numba, single core): tilefusion.integrate + "
+                      f"tilefusion.raycast of frame {frame} into tiles {tiles} of the same map state "
+                      f"(copied from the oracle arm), scaled to 8 tiles; JIT excluded"}
 
 
 def run_reference(args) -> None:
@@ -570,40 +974,54 @@ def run_reference(args) -> None:
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     threads = oracle.default_threads()
-    intr, spec, params, poses, scene = workload(2)
-    host_frames = [scene.render_depth(p, intr).data for p in poses]
-    # exactly --warmup untimed and --steps timed samples; each sample is
-    # bounded (volumes per sample shrink as K + W grow: ~120 volume-samples in
-    # all, ~0.5 s each) and the samples walk round-robin over the 8 volumes
+    intr, spec, params, poses, scene = workload()
+    host_frames = render_frames(poses, intr)
+    m = OracleMap(oracle, intr, spec, params, poses, host_frames, threads)
+    t0 = time.perf_counter()
+    for i in range(LAP):
+        m.integrate_only(i)
+    lap_s = time.perf_counter() - t0
     steps, warmup = max(1, args.steps), max(0, args.warmup)
-    cap = 8 if threads >= 32 else (4 if threads >= 8 else 1)
-    vols = max(1, min(cap, 120 // (steps + warmup)))
-    for i in range(warmup):
-        cpu_frame_sample(intr, spec, params, poses, host_frames, vols, threads, first=i * vols)
+    # every step integrates all 8 tiles (the map follows the GPU arm's); the
+    # raycast is timed on a round-robin subset when K is large, scaled to 8
+    per = max(1, min(8, 512 // steps))
+    for i in warm_frames(warmup):
+        m.integrate_only(i)
     times, ups = [], []
-    for i in range(steps):
-        s = cpu_frame_sample(intr, spec, params, poses, host_frames, vols, threads,
-                             first=(warmup + i) * vols)
-        times.append((s["t_integrate"] + s["t_raycast"]) * 8 / vols)
-        ups.append(s["updates"] * 8 / vols)
+    for s, i in enumerate(timed_frames(steps)):
+        subset = [(s * per + j) % 8 for j in range(per)]
+        u, ti, tr = m.step(i, subset)
+        times.append(ti + tr)
+        ups.append(u)
     frame_s = sum(times) / len(times)
-    value = (sum(ups) / len(ups)) / frame_s
-    sample = (f"per step: frame 1 of the workload on {vols} of the 8 volumes (round-robin over the "
-              f"steps; integrate + raycast), C restatement of the reference kernels on {threads} "
-              f"host threads, scaled to 8")
-    print(json.dumps({
+    value = sum(ups) / sum(times)
+    sample = (f"per step: the GPU arm's frame on the same map state (64-frame lap + warm-up "
+              f"frames integrated untimed first, {lap_s:.0f} s); integrate of all 8 volumes + raycast "
+              f"of {per} of 8 (round-robin, scaled to 8); C restatement of the reference kernels on "
+              f"{threads} host threads")
+    line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "voxel-updates/s",
         "frames_per_s": 1.0 / frame_s, "n_gpus": world, "steps": steps, "warmup": warmup,
-        "ms_per_step": frame_s * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_desc(world),
+        "ms_per_step": frame_s * 1e3, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_desc(1),
         "cpu_baseline": {"value": value, "unit": "voxel-updates/s", "cores": threads,
                          "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "voxel-updates/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0}}), flush=True)
+                "d2h_bytes_per_step": 0}}
+    if not args.no_numba:
+        try:
+            nb = numba_sample(intr, spec, params, poses, host_frames, m, timed_frames(steps)[-1],
+                              [2, 6])
+        except Exception as exc:
+            nb = {"error": f"{type(exc).__name__}: {exc}"}
+        line["cpu_baseline_reference_numba"] = nb
+    print(json.dumps(line), flush=True)
 
 
 def main() -> None:
     args = parse_args()
+    relaunch_if_needed(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -214,3 +214,79 @@ def solve_from_sums(sums: np.ndarray, min_pairs: int):
     if not np.all(np.isfinite(delta)):
         return None
     return delta, count, float(np.sqrt(sums[27] / count))
+
+
+# ---------------------------------------------------------------------------
+# tracking.track (tracking.py:123-196) over the oracle's per-pixel pieces
+# ---------------------------------------------------------------------------
+
+def _rodrigues(axis, angle: float) -> np.ndarray:
+    """rotation_from_axis_angle (geometry.py:211-219)."""
+    import math
+    axis = np.asarray(axis, dtype=np.float64)
+    norm = np.linalg.norm(axis)
+    if norm == 0.0 or angle == 0.0:
+        return np.eye(3)
+    x, y, z = axis / norm
+    k = np.array([[0.0, -z, y], [z, 0.0, -x], [-y, x, 0.0]])
+    return np.eye(3) + math.sin(angle) * k + (1.0 - math.cos(angle)) * (k @ k)
+
+
+def _orthonormalized(rot: np.ndarray) -> np.ndarray:
+    """Pose.orthonormalized (geometry.py:169-176)."""
+    u, _, vt = np.linalg.svd(rot)
+    r = u @ vt
+    if np.linalg.det(r) < 0:
+        u[:, -1] = -u[:, -1]
+        r = u @ vt
+    return r
+
+
+def track(depth, fx, fy, cx, cy, model_dist, model_vert, model_norm, ref_rot, ref_t,
+          seed_rot, seed_t, max_distance=0.10, max_angle_deg=20.0, iterations=(10, 5, 4),
+          min_correspondences=1000, step_eps=1.0e-10):
+    """tracking.track (tracking.py:123-196): stride-2 pyramids of the frame and
+    the model (geometry.py:256-258, :326-332; CameraIntrinsics.scaled :44-57),
+    coarsest level first, per step icp_reduce + solve_from_sums + the Rodrigues
+    update re-orthonormalised (:178-183).  Returns (rot, t, lost, count, rms)."""
+    depth = np.asarray(depth, np.float64)
+    ref_rot = np.asarray(ref_rot, np.float64)
+    ref_t = np.asarray(ref_t, np.float64)
+    inv_r = ref_rot.T.copy()
+    inv_t = -(inv_r @ ref_t)
+    est_r, est_t = np.asarray(seed_rot, np.float64), np.asarray(seed_t, np.float64)
+    cos_min = float(np.cos(np.deg2rad(max_angle_deg)))
+    levels = len(iterations)
+    h, w = depth.shape
+    count, rms, lost = 0, float("inf"), False
+    for level in range(levels - 1, -1, -1):
+        s = 1 << level
+        d = depth[::s, ::s]
+        lw = max(1, int(round(w * 0.5 ** level)))
+        lh = max(1, int(round(h * 0.5 ** level)))
+        lfx, lfy, lcx, lcy = fx, fy, cx, cy
+        for _ in range(level):  # scaled(0.5) applied level times
+            lfx, lfy, lcx, lcy = lfx * 0.5, lfy * 0.5, lcx * 0.5, lcy * 0.5
+        sv, sn, sok = vertex_normal_map(d, lfx, lfy, lcx, lcy)
+        sok = sok & np.all(np.isfinite(sn), axis=-1)
+        md = model_dist[::s, ::s]
+        mv, mn = model_vert[::s, ::s], model_norm[::s, ::s]
+        mok = np.isfinite(md)
+        min_pairs = max(6, min_correspondences // 4 ** level)
+        for _ in range(iterations[level]):
+            sums = icp_reduce(sv, sn, sok, mv, mn, mok, est_r, est_t, inv_r, inv_t, lfx, lfy,
+                              lcx, lcy, lw, lh, max_distance ** 2, cos_min)
+            step = solve_from_sums(sums, min_pairs)
+            if step is None:
+                lost = True
+                break
+            delta, count, rms = step
+            rot = _rodrigues(delta[:3], float(np.linalg.norm(delta[:3])))
+            est_r, est_t = _orthonormalized(rot @ est_r), rot @ est_t + delta[3:]
+            if float(np.linalg.norm(delta)) < step_eps:
+                break
+        if lost:
+            break
+    if lost:
+        return np.asarray(seed_rot, np.float64), np.asarray(seed_t, np.float64), True, count, rms
+    return est_r, est_t, False, count, rms

@@ -1,0 +1,226 @@
+"""Parity at the sizes the metric is quoted on (BASELINE configs[1..3]).
+
+* config 3 (8 x 512^3 at 4 mm, 640x480): the fused CUDA integrate / raycast
+  against the REFERENCE's own numba kernels on all 8 tiles, busy tiles 2 and
+  6 included (SHA-256 of every tile after frames 0, 9, 18 and of the merged
+  ray maps, tests/golden/config3_hashes.npz), and against the oracle over the
+  whole 64-frame lap (bit-exact tsdf, weights and maps at frames 0, 9, 18,
+  40, 63; equal update counts every frame);
+* config 2 (256^3, 640x480, ICP on): every _solve_step of the reference's
+  run_fusion over frames 0-5 replayed at full resolution against the
+  identical model (its SHA-256 pinned to the reference's), counts exact,
+  deltas within 1e-5 m / 1e-6 rad (tests/golden/icp_full.npz);
+* config 4 (2000 corridor frames): the device bin_endpoints histogram and the
+  update_allocation decisions of every frame equal the reference's
+  (tests/golden/placement_config4.npz).
+"""
+
+import hashlib
+import multiprocessing as mp
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1511_07106_b200 as tf
+from paper_1511_07106_b200 import tracking as trk
+from paper_1511_07106_b200 import _native as nat
+from paper_1511_07106_b200.geometry import Pose
+from paper_1511_07106_b200.synth import corridor_depth, corridor_scene, demo_scene
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _pose(m) -> Pose:
+    return Pose(m[:3, :3], m[:3, 3])
+
+
+def _tile_hashes(tile):
+    pair = tile.voxels.cpu().numpy()
+    return _sha(pair[..., 0]), _sha(pair[..., 1])
+
+
+def test_config3_all_tiles_match_reference_kernels():
+    g = load_golden("config3_hashes.npz")
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(4.08, 1020, 510)
+    assert [tuple(k) for k in g["keys"].tolist()] == list(spec.keys)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    tiles = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length)
+             for k in spec.keys]
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)
+    scene = demo_scene()
+    ray_frames = g["ray_frames"].tolist()
+    try:
+        for fi, f in enumerate(g["frames"].tolist()):
+            frame = scene.render_depth(poses[f], intr)
+            tf.integrate_volumes(tiles, frame, poses[f], intr, params)
+            for t, tile in enumerate(tiles):
+                th, wh = _tile_hashes(tile)
+                assert th == g["tsdf_sha"][fi][t], f"tsdf of tile {t} {spec.keys[t]} after frame {f}"
+                assert wh == g["weight_sha"][fi][t], f"weight of tile {t} {spec.keys[t]} after frame {f}"
+            if f in ray_frames:
+                r = ray_frames.index(f)
+                rm = tf.RayMap.empty(intr)
+                tf.raycast_volumes(tiles, poses[f], intr, rm, params)
+                assert int(np.isfinite(rm.distance).sum()) == int(g["ray_hits"][r])
+                assert _sha(rm.distance) == g["ray_sha"][r][0], f"ray distances, frame {f}"
+                assert _sha(rm.vertices) == g["ray_sha"][r][1], f"ray vertices, frame {f}"
+                assert _sha(rm.normals) == g["ray_sha"][r][2], f"ray normals, frame {f}"
+    finally:
+        del tiles
+        torch.cuda.empty_cache()
+
+
+def test_config3_whole_lap_matches_oracle():
+    """64 frames into the 8 tiles on the GPU and in the oracle (all host
+    threads); per frame equal update counts, at frames 0, 9, 18, 40, 63 every
+    tile bit-exact and the merged maps bit-exact."""
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(4.08, 1020, 510)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    n, vs = spec.voxels_per_side, spec.voxel_size
+    tiles = [tf.TsdfSubvolume.empty(k, n, spec.subvolume_side_length) for k in spec.keys]
+    host = [(np.zeros((n, n, n), np.float32), np.zeros((n, n, n), np.float32)) for _ in spec.keys]
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)
+    scene = demo_scene()
+    threads = oracle.default_threads()
+    coarse = tf.tsdf.coarse_step(params, vs)
+    stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
+    check = {0, 9, 18, 40, 63}
+    try:
+        for f, pose in enumerate(poses):
+            frame = scene.render_depth(pose, intr)
+            stats.zero_()
+            tf.integrate_volumes(tiles, frame, pose, intr, params, stats)
+            inv = pose.invert()
+            want = sum(oracle.integrate(t, w, k, vs, frame.data, inv.rotation, inv.translation,
+                                        pose.translation, intr.fx, intr.fy, intr.cx, intr.cy,
+                                        params.truncation, params.max_weight, params.sample_weight,
+                                        threads=threads)
+                       for (t, w), k in zip(host, spec.keys))
+            assert int(stats[nat.STAT_VOXEL_UPDATES].item()) == want, f"updates, frame {f}"
+            if f not in check:
+                continue
+            for i, tile in enumerate(tiles):
+                pair = tile.voxels.cpu().numpy()
+                assert np.array_equal(pair[..., 0], host[i][0]), f"tsdf tile {i} frame {f}"
+                assert np.array_equal(pair[..., 1], host[i][1]), f"weight tile {i} frame {f}"
+                del pair
+            rm = tf.RayMap.empty(intr)
+            tf.raycast_volumes(tiles, pose, intr, rm, params)
+            d = np.full((intr.height, intr.width), np.inf)
+            v = np.zeros((intr.height, intr.width, 3))
+            nn = np.zeros_like(v)
+            for (t, w), k in zip(host, spec.keys):
+                oracle.raycast(t, w, k, vs, params.truncation, coarse, pose.rotation,
+                               pose.translation, intr.fx, intr.fy, intr.cx, intr.cy, d, v, nn,
+                               threads=threads)
+            assert np.isfinite(d).sum() > 200000
+            assert np.array_equal(rm.distance, d), f"distances frame {f}"
+            assert np.array_equal(rm.vertices, v), f"vertices frame {f}"
+            assert np.array_equal(rm.normals, nn), f"normals frame {f}"
+    finally:
+        del tiles, host
+        torch.cuda.empty_cache()
+
+
+def test_config2_icp_full_resolution_matches_reference_steps(tmp_path):
+    """Every _solve_step of the reference's tracked run (640x480, 256^3) on
+    the identical model: our pipeline is driven through the reference's own
+    poses (exact bits), so each model it renders must hash to the model the
+    reference tracked against; then each step at the reference's estimate
+    gives the same inlier count and the same increment to 1e-5 m / 1e-6 rad,
+    and our device track() ends at the reference's pose."""
+    g = load_golden("icp_full.npz")
+    cfg = tf.RunConfig(side_length=3.0, resolution=254, resident_resolution=254,
+                       use_groundtruth=True)
+    intr = cfg.intrinsics()
+    scene = demo_scene()
+    ref_poses = [_pose(m) for m in g["poses"]]
+    gt = [_pose(m) for m in g["gt_poses"]]
+    params = tf.TrackingParams()
+    pipe = tf.FusionPipeline(cfg, tmp_path)
+    steps_checked = 0
+    for f in range(len(ref_poses)):
+        frame = scene.render_depth(gt[f], intr)
+        calls = np.flatnonzero(g["model_frame"] == f)
+        if len(calls):
+            c = int(calls[0])
+            model = pipe.model
+            assert int(np.isfinite(model.distance).sum()) == int(g["model_hits"][c])
+            assert _sha(model.distance) == g["model_sha"][c][0], f"model distances before frame {f}"
+            assert _sha(model.vertices) == g["model_sha"][c][1], f"model vertices before frame {f}"
+            assert _sha(model.normals) == g["model_sha"][c][2], f"model normals before frame {f}"
+            depth = torch.as_tensor(frame.data, device="cuda")
+            levels = {}
+            li = intr
+            for level in range(3):
+                levels[li.width] = trk.source_level(depth, li, level)
+                li = li.scaled(0.5)
+            ref_inv = ref_poses[f - 1].invert()
+            for k in np.flatnonzero(g["step_frame"] == f):
+                src = levels[int(g["step_level_w"][k])]
+                step = trk.solve_step(src, model, _pose(g["step_estimate"][k]), ref_inv, params,
+                                      int(g["step_min_pairs"][k]))
+                if g["step_count"][k] < 0:
+                    assert step is None
+                    continue
+                delta, count, rms = step
+                assert count == g["step_count"][k], f"frame {f} step {k}: inlier count"
+                assert np.abs(delta[:3] - g["step_delta"][k][:3]).max() <= 1e-6
+                assert np.abs(delta[3:] - g["step_delta"][k][3:]).max() <= 1e-5
+                assert rms == pytest.approx(float(g["step_rms"][k]), rel=1e-6)
+                steps_checked += 1
+            res = tf.track(depth, intr, model, ref_poses[f - 1], params)
+            assert not res.lost and bool(g["tracked"][f])
+            assert res.correspondences == int(g["correspondences"][f])
+            assert np.abs(res.pose.matrix - g["poses"][f]).max() < 1e-9
+        pipe.step(frame, ref_poses[f])
+    assert steps_checked == int((g["step_count"] >= 0).sum()) >= 50
+
+
+def _corridor_frame(i):
+    c = dict(frames=2000, length=20.0)
+    intr = tf.RunConfig(dynamic=True).intrinsics()
+    pose = tf.corridor_trajectory(c["length"], c["frames"])[i]
+    return corridor_depth(corridor_scene(), pose, intr).data
+
+
+def test_config4_placement_over_all_2000_frames():
+    g = load_golden("placement_config4.npz")
+    n = int(g["frames"])
+    cfg = tf.RunConfig(dynamic=True, block_voxels=int(g["block_voxels"]),
+                       block_side_length=float(g["block_side_length"]),
+                       max_volumes=int(g["max_volumes"]), hysteresis=float(g["hysteresis"]))
+    intr = cfg.intrinsics()
+    spacing = cfg.block_voxels - 2
+    vs = cfg.block_side_length / spacing
+    policy = cfg.allocation_policy()
+    poses = tf.corridor_trajectory(float(g["length"]), n)
+    procs = max(1, min(16, os.cpu_count() or 1))
+    with mp.get_context("spawn").Pool(procs) as pool:
+        frames = pool.map(_corridor_frame, range(n), chunksize=16)
+    current: list = []
+    for i in range(n):
+        got = tf.bin_endpoints(torch.as_tensor(frames[i], device="cuda"), intr, poses[i], spacing, vs)
+        lo, hi = g["hist_offsets"][i], g["hist_offsets"][i + 1]
+        want = {tuple(k): int(c) for k, c in zip(g["hist_keys"][lo:hi].tolist(),
+                                                 g["hist_counts"][lo:hi].tolist())}
+        assert got == want, f"endpoint histogram, frame {i}"
+        added, removed = tf.update_allocation(tuple(current), got, policy)
+        wa = [tuple(k) for k in g["added"][g["added_offsets"][i]:g["added_offsets"][i + 1]].tolist()]
+        wr = [tuple(k) for k in g["removed"][g["removed_offsets"][i]:g["removed_offsets"][i + 1]].tolist()]
+        assert added == wa and removed == wr, f"allocation decision, frame {i}"
+        for k in removed:
+            current.remove(k)
+        current.extend(added)
+    assert current == [tuple(k) for k in g["final_keys"].tolist()]
