@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define TFB200_ABI_VERSION 1
+#define TFB200_ABI_VERSION 2
 #define TFB200_MAX_VOLUMES_PER_LAUNCH 64
 
 enum {
@@ -72,6 +72,11 @@ typedef struct TfVolume {
                             voxel while it lay in the truncation band, w their
                             count (saturating at 255).  Not in the reference
                             (SPEC.md:8): the rule is this library's own. */
+    uint64_t *counters_dev; /* optional (NULL = none): uint64[2] accumulated by
+                               tf_integrate's culling stage: [0] general bricks
+                               (8^3, swept voxel by voxel), [1] certified
+                               free-space bricks — the per-volume work measure
+                               the multi-GPU ownership balances on */
 } TfVolume;
 
 /* Pinhole intrinsics of one pyramid level (geometry.py:27-57). */

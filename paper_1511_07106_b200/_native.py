@@ -17,7 +17,7 @@ import torch
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ["TFB200_LIB"]) if os.environ.get("TFB200_LIB") else _PKG / "libtfb200.so"  # override: A/B runs only
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_VOLUMES_PER_LAUNCH = 64  # TFB200_MAX_VOLUMES_PER_LAUNCH
 
 _c_d = ctypes.c_double
@@ -31,7 +31,7 @@ class TfVolume(ctypes.Structure):
     _fields_ = [("voxels_dev", _c_p), ("n", _c_i64), ("origin", _c_i64 * 3),
                 ("voxel_size", _c_d), ("brick_state_dev", _c_p), ("brick_flags_dev", _c_p),
                 ("summary_threshold", ctypes.c_float),
-                ("reserved", ctypes.c_int32), ("color_dev", _c_p)]
+                ("reserved", ctypes.c_int32), ("color_dev", _c_p), ("counters_dev", _c_p)]
 
 
 class TfCamera(ctypes.Structure):
@@ -216,12 +216,14 @@ def camera(intr) -> TfCamera:
 
 def volume_struct(voxels: torch.Tensor, n: int, origin, voxel_size: float,
                   brick_state: torch.Tensor | None = None, brick_flags: torch.Tensor | None = None,
-                  threshold: float = 0.0, color: torch.Tensor | None = None) -> TfVolume:
+                  threshold: float = 0.0, color: torch.Tensor | None = None,
+                  counters: torch.Tensor | None = None) -> TfVolume:
     o = np.asarray(origin, dtype=np.int64)
     return TfVolume(ptr(voxels), int(n), (_c_i64 * 3)(int(o[0]), int(o[1]), int(o[2])),
                     float(voxel_size), ptr(brick_state) if brick_state is not None else None,
                     ptr(brick_flags) if brick_flags is not None else None, float(threshold), 0,
-                    ptr(color) if color is not None else None)
+                    ptr(color) if color is not None else None,
+                    ptr(counters) if counters is not None else None)
 
 
 class _Workspace:

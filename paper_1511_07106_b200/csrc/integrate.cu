@@ -451,6 +451,7 @@ __global__ void __launch_bounds__(256) macro_cull_kernel(
         }
         const unsigned base = atomicAdd(free_count, cnt);
         for (unsigned k = 0; k < cnt; ++k) active_free[base + k] = ids[k];
+        if (vt.vol[v].counters_dev) atomicAdd((unsigned long long *)&vt.vol[v].counters_dev[1], (unsigned long long)cnt);
     }
     const int lane = threadIdx.x & 31;
     const unsigned mg = __ballot_sync(0xffffffffu, kind == 1);
@@ -481,13 +482,14 @@ __global__ void __launch_bounds__(256) brick_cull_kernel(
     const int lane = threadIdx.x & 31;
     for (unsigned t0 = blockIdx.x * blockDim.x; t0 < total; t0 += gridDim.x * blockDim.x) {
         const unsigned t = t0 + threadIdx.x;
-        int kind = 0;
+        int kind = 0, vol_of = 0;
         uint32_t gb = 0;
         if (t < total) {
             const int64_t gm = macros[t >> 6];
             const int sub = t & 63;
             int v = 0;
             while (gm >= mfirst[v + 1]) ++v;
+            vol_of = v;
             const int64_t nb = bt.nb[v], nm = (nb + kMacro - 1) / kMacro, local = gm - mfirst[v];
             const int64_t bx = (local % nm) * kMacro + (sub & 3), by = ((local / nm) % nm) * kMacro + ((sub >> 2) & 3),
                           bz = (local / (nm * nm)) * kMacro + (sub >> 4);
@@ -495,6 +497,18 @@ __global__ void __launch_bounds__(256) brick_cull_kernel(
                 gb = (uint32_t)(bt.offset[v] + (bz * nb + by) * nb + bx);
                 kind = brick_may_update(vt.vol[v], bx, by, bz, f, mip, qmip, m, allow_free != 0);
                 if (no_cull && kind == 0) kind = 1;
+            }
+        }
+        // per-volume work counters (ownership balance): one atomic per volume
+        // present in the warp
+        {
+            const unsigned peers = __match_any_sync(0xffffffffu, kind ? vol_of : -1);
+            if (kind && vt.vol[vol_of].counters_dev) {
+                const unsigned g1 = __ballot_sync(peers, kind == 1) & peers, g2 = peers & ~g1;
+                if (lane == __ffs(peers) - 1) {
+                    if (g1) atomicAdd((unsigned long long *)&vt.vol[vol_of].counters_dev[0], (unsigned long long)__popc(g1));
+                    if (g2) atomicAdd((unsigned long long *)&vt.vol[vol_of].counters_dev[1], (unsigned long long)__popc(g2));
+                }
             }
         }
         // warp-aggregated appends (list order is irrelevant: voxels are independent)

@@ -281,36 +281,187 @@ def _connect_peers(intr: CameraIntrinsics, rank: int, world: int, group, require
     return None
 
 
+# ---------------------------------------------------------------------------
+# re-tiling and load-balanced ownership (hard part 4)
+# ---------------------------------------------------------------------------
+
+def valid_retile(voxels_per_side: int, k: int) -> bool:
+    """A tile of n voxels splits into k^3 cubic sub-tiles with the reference's
+    2-voxel overlap iff k divides n - 2 (spacing (n - 2) / k, size spacing + 2)."""
+    return k >= 1 and (voxels_per_side - 2) % k == 0 and (voxels_per_side - 2) // k >= 2
+
+
+def default_retile(world: int, voxels_per_side: int = 512) -> int:
+    """Sub-tiles per axis at ``world`` ranks: none on one GPU; enough that the
+    sub-tiles outnumber the ranks several times over (k^3 >= 4 world per tile
+    group of 8) — the largest valid k <= the target."""
+    if world <= 1:
+        return 1
+    target = 2 if world <= 4 else 3
+    for k in range(target, 0, -1):
+        if valid_retile(voxels_per_side, k):
+            return k
+    return 1
+
+
+def retile(keys: Sequence, voxels_per_side: int, voxel_size: float, k: int) -> tuple[list, int]:
+    """Split every tile into k^3 sub-tiles with a 2-voxel overlap.
+
+    Tile ``key`` (origin voxel o, n voxels per side, volumes.py:117-153)
+    covers global voxels o .. o + n - 1; sub-tile (i, j, l) covers
+    o + (i, j, l) * s .. + s + 1 with s = (n - 2) / k, so neighbours share two
+    voxel layers exactly like the reference's tiles (_kernels.py:8-14) and
+    the union is the tile.  Every voxel's update depends only on its global
+    lattice coordinate (_kernels.py:99-133), so each sub-tile's voxels equal
+    the tile's bit for bit; the merged raycast of the sub-tiles moves by the
+    rounding of the local coordinates only.  Returns
+    (sub-tile keys in tile order, sub-tile voxels per side)."""
+    n = int(voxels_per_side)
+    if k == 1:
+        return [tuple(int(x) for x in key) for key in keys], n
+    if not valid_retile(n, k):
+        raise ValueError(f"cannot split {n}-voxel tiles into {k}^3 sub-tiles with a 2-voxel overlap")
+    s = (n - 2) // k
+    m = s + 2
+    if (m * voxel_size) / m != voxel_size:
+        raise ValueError("sub-tile side length does not round-trip the voxel size")
+    out = []
+    for key in keys:
+        o = [int(x) for x in key]
+        for i in range(k):
+            for j in range(k):
+                for l in range(k):
+                    out.append((o[0] + i * s, o[1] + j * s, o[2] + l * s))
+    return out, m
+
+
+_retile = retile  # ShardedFusion's keyword argument shadows the name
+
+
+def balanced_owners(costs: Sequence[float], world: int, current: Sequence[int] | None = None,
+                    slack: float = 0.05) -> list[int]:
+    """Sticky longest-processing-time assignment of units to ranks.
+
+    Units in decreasing cost (ties: lower index first) go to the least-loaded
+    rank (ties: lower rank), except that a unit stays with its current owner
+    while that owner's load after taking it stays within ``slack`` x the mean
+    load of the least-loaded choice — so a balanced assignment is kept and a
+    rebalance moves few units.  Deterministic: every rank computes the same
+    result from the same (all-reduced) costs."""
+    nunits = len(costs)
+    if world <= 1:
+        return [0] * nunits
+    load = [0.0] * world
+    owner = [0] * nunits
+    mean = sum(costs) / world if nunits else 0.0
+    for u in sorted(range(nunits), key=lambda i: (-costs[i], i)):
+        best = min(range(world), key=lambda r: (load[r], r))
+        r = best
+        if current is not None:
+            c = current[u]
+            if load[c] + costs[u] <= load[best] + costs[u] + slack * mean:
+                r = c
+        owner[u] = r
+        load[r] += costs[u]
+    return owner
+
+
+def initial_owners(keys: Sequence, world: int) -> list[int]:
+    """Owners before any work was measured: contiguous chunks of the
+    checkerboard spread order (spread_order)."""
+    spread = spread_order(keys)
+    pos = {k: i for i, k in enumerate(spread)}
+    n = len(keys)
+    return [pos[k] * world // n for k in keys] if n else []
+
+
+def move_units(moves: Sequence[tuple], rank: int, payloads: dict, alloc: Callable,
+               group=None) -> dict:
+    """Point-to-point moves of whole units between ranks (collective over the
+    ranks that take part).  ``moves`` = [(unit, src, dst)] in the same order
+    on every rank; ``payloads[unit]`` = the tensors this rank sends (src ==
+    rank); ``alloc(unit)`` = empty tensors of the same shapes for a unit it
+    receives (dst == rank).  Returns {unit: received tensors}.  NCCL moves
+    device tensors directly (NVLink); gloo has no device send / recv, so the
+    tensors go through host memory there."""
+    staged = dist.get_backend(group) == "gloo"
+    ops, out, host_in = [], {}, {}
+    for u, a, b in moves:
+        if a == b:
+            continue
+        if rank == a:
+            for t in payloads[u]:
+                t = t.contiguous()
+                ops.append(dist.P2POp(dist.isend, t.cpu() if staged else t, b, group=group))
+        elif rank == b:
+            bufs = alloc(u)
+            out[u] = bufs
+            host_in[u] = [t.new_empty(t.shape, device="cpu") if staged else t for t in bufs]
+            for t in host_in[u]:
+                ops.append(dist.P2POp(dist.irecv, t, a, group=group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    if staged:
+        for u, bufs in out.items():
+            for dev_t, host_t in zip(bufs, host_in[u]):
+                dev_t.copy_(host_t)
+    return out
+
+
+WORK_GENERAL_BRICK = 4.0  # relative cost of a general brick vs a certified free-space one
+
+
 class ShardedFusion:
     """The per-rank slice of a static multi-volume map.
 
-    ``step(depth, pose)`` integrates this rank's volumes, raycasts them into a
-    partial map and merges all ranks' partials into ``model`` on every rank:
-    over peer memory (``exchange="p2p"``, one kernel, the default when every
-    pair of the ranks' GPUs can map each other) or with the NCCL row-block
-    exchange (``exchange="collective"``).
+    The map's tiles are split into ``retile``^3 sub-tiles each (``retile``;
+    1 keeps the tiles), and every sub-tile is owned by one rank.
+    ``step(depth, pose)`` integrates this rank's sub-tiles, raycasts them
+    into a partial map and merges all ranks' partials into ``model`` on
+    every rank: over peer memory (``exchange="p2p"``, one kernel, the
+    default when every pair of the ranks' GPUs can map each other) or with
+    the NCCL row-block exchange (``exchange="collective"``).
+
+    Ownership follows the work: the culling stage counts, per sub-tile, the
+    bricks it sweeps (TfVolume.counters_dev); every ``rebalance_every``
+    frames the counts are all-reduced, ``balanced_owners`` recomputes the
+    assignment (sticky LPT) and the sub-tiles that change owner move between
+    GPUs (NCCL send / recv of their voxels).  Integration has no data-path
+    collective; a migration moves 8 B per voxel of the moved sub-tiles.
     """
 
     def __init__(self, keys: Sequence, voxels_per_side: int, side_length: float,
                  params: FusionParams, intr: CameraIntrinsics, rank: int = 0, world: int = 1,
-                 group=None, color: bool = False, exchange: str = "auto") -> None:
+                 group=None, color: bool = False, exchange: str = "auto", retile: int = 1,
+                 rebalance_every: int = 8) -> None:
         if exchange not in ("auto", "p2p", "collective"):
             raise ValueError(f"exchange must be 'auto', 'p2p' or 'collective', not {exchange!r}")
         self.rank, self.world, self.group = rank, world, group
         self.params, self.intr = params, intr
-        self.keys = owned_keys(keys, rank, world)
-        self.tiles = [TsdfSubvolume.empty(k, voxels_per_side, side_length) for k in self.keys]
-        if color:
-            for t in self.tiles:
-                t.enable_color()
+        self.parent_keys = [tuple(int(x) for x in k) for k in keys]
+        vs = side_length / voxels_per_side
+        self.voxel_size = vs
+        self.units, self.unit_n = _retile(self.parent_keys, voxels_per_side, vs, retile)
+        self.retile_k = retile
+        self.color = color
+        self.owner = initial_owners(self.units, world)
+        self.rebalance_every = rebalance_every if world > 1 else 0
+        self._dev = torch.device("cuda", torch.cuda.current_device())
+        self._tiles: dict[int, TsdfSubvolume] = {}
+        # per-unit work counters (general, free bricks), one row per unit
+        self._counters = torch.zeros((len(self.units), 2), dtype=torch.int64, device=self._dev)
+        for u in range(len(self.units)):
+            if self.owner[u] == rank:
+                self._tiles[u] = self._new_tile(u)
+        self._refresh()
         self.partial = RayMap.empty(intr)
         self.model = RayMap.empty(intr)
-        self.stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device=self.partial.distance_dev.device)
+        self.stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device=self._dev)
         # row-block exchange buffer: (t, n) records, rows padded to world * B; the
         # padding rows stay "no hit"
         b = row_block(intr.height, world)
-        self._packed = torch.zeros((world * b, intr.width, 4), dtype=torch.float64,
-                                   device=self.partial.distance_dev.device)
+        self._packed = torch.zeros((world * b, intr.width, 4), dtype=torch.float64, device=self._dev)
         self._packed[..., 0] = float("inf")
         self._integrator = SplitIntegrator()
         self.exchange = "none" if world == 1 else exchange
@@ -323,11 +474,137 @@ class ShardedFusion:
                 self.exchange = "collective"
             else:
                 self.partial, self.model = self._peer.partial, self._peer.model
+        self.frames = 0
+        self.migrations = 0
+        self._last_costs: list[float] | None = None
 
+    # ---- ownership -------------------------------------------------------------
+    def _new_tile(self, u: int, voxels: torch.Tensor | None = None) -> TsdfSubvolume:
+        side = self.unit_n * self.voxel_size
+        t = (TsdfSubvolume.empty(self.units[u], self.unit_n, side) if voxels is None
+             else TsdfSubvolume(self.units[u], self.unit_n, side, voxels=voxels))
+        if self.color and t.color is None:
+            t.enable_color()
+        t.counters = self._counters[u]
+        return t
+
+    def _refresh(self) -> None:
+        self.keys = [self.units[u] for u in sorted(self._tiles)]
+        self.tiles = [self._tiles[u] for u in sorted(self._tiles)]
+
+    def unit_costs(self) -> list[float]:
+        """Work per unit since the last rebalance, summed over ranks (collective)."""
+        c = self._counters.to(torch.float64)
+        cost = c[:, 0] * WORK_GENERAL_BRICK + c[:, 1]
+        if self.world > 1:
+            dist.all_reduce(cost, op=dist.ReduceOp.SUM, group=self.group)
+        return cost.cpu().tolist()
+
+    def rebalance(self) -> int:
+        """Recompute the owners from the measured work and migrate; returns
+        the number of units that moved.  Collective: every rank calls it."""
+        costs = self.unit_costs()
+        self._last_costs = costs
+        new = balanced_owners(costs, self.world, self.owner)
+        moved = self.migrate(new)
+        self._counters.zero_()
+        return moved
+
+    def migrate(self, new_owner: Sequence[int]) -> int:
+        """Move every unit whose owner changes (move_units: NCCL send / recv
+        of its voxels, and colours); collective."""
+        moves = [(u, self.owner[u], new_owner[u]) for u in range(len(self.units))
+                 if self.owner[u] != new_owner[u]]
+        if not moves:
+            return 0
+        payloads = {}
+        for u, a, _ in moves:
+            if a == self.rank:
+                t = self._tiles.pop(u)
+                t._device_read()
+                payloads[u] = [t.voxels] + ([t.color] if self.color else [])
+        n = self.unit_n
+
+        def alloc(u):
+            bufs = [torch.empty((n, n, n, 2), dtype=torch.float32, device=self._dev)]
+            if self.color:
+                bufs.append(torch.empty((n, n, n, 4), dtype=torch.uint8, device=self._dev))
+            return bufs
+
+        got = move_units(moves, self.rank, payloads, alloc, self.group)
+        for u, bufs in got.items():
+            t = self._new_tile(u, bufs[0])
+            if self.color:
+                t.color = bufs[1]
+            self._tiles[u] = t
+        self.owner = list(new_owner)
+        self._refresh()
+        self.migrations += len(moves)
+        return len(moves)
+
+    # ---- dynamic placement (whole tiles, retile 1) --------------------------------
+    def add_unit(self, key) -> None:
+        """Allocate a tile (replicated decision, every rank calls it): owned by
+        the rank with the fewest units (ties: lowest rank)."""
+        if self.retile_k != 1:
+            raise ValueError("dynamic tiles are not re-tiled")
+        key = tuple(int(x) for x in key)
+        counts = [self.owner.count(r) for r in range(self.world)]
+        r = min(range(self.world), key=lambda q: (counts[q], q))
+        self.units.append(key)
+        self.owner.append(r)
+        c = torch.zeros((len(self.units), 2), dtype=torch.int64, device=self._dev)
+        c[:-1] = self._counters
+        self._counters = c
+        for u, t in self._tiles.items():
+            t.counters = self._counters[u]
+        if r == self.rank:
+            self._tiles[len(self.units) - 1] = self._new_tile(len(self.units) - 1)
+        self._refresh()
+
+    def remove_unit(self, key) -> TsdfSubvolume | None:
+        """Retire a tile (every rank calls it); returns it on its owner."""
+        key = tuple(int(x) for x in key)
+        u = self.units.index(key)
+        tile = self._tiles.pop(u, None)
+        keep = [i for i in range(len(self.units)) if i != u]
+        self.units = [self.units[i] for i in keep]
+        self.owner = [self.owner[i] for i in keep]
+        self._counters = self._counters[keep].clone()
+        self._tiles = {keep.index(i): t for i, t in self._tiles.items()}
+        for i, t in self._tiles.items():
+            t.counters = self._counters[i]
+        if tile is not None:
+            tile.counters = None
+        self._refresh()
+        return tile
+
+    def balance_report(self) -> dict:
+        """Per-rank share of the last measured work (collective)."""
+        costs = self._last_costs if self._last_costs is not None else self.unit_costs()
+        load = [0.0] * self.world
+        for u, c in enumerate(costs):
+            load[self.owner[u]] += c
+        mean = sum(load) / self.world if self.world else 0.0
+        return {"units": len(self.units), "unit_voxels_per_side": self.unit_n,
+                "retile": self.retile_k, "rebalance_every": self.rebalance_every,
+                "load_per_rank": load, "imbalance_max_over_mean": (max(load) / mean) if mean else None,
+                "units_per_rank": [self.owner.count(r) for r in range(self.world)],
+                "migrations": self.migrations,
+                "work_measure": f"bricks swept per unit (general x {WORK_GENERAL_BRICK:g} + free-space)"}
+
+    def check_exchange(self) -> None:
+        if self._peer is not None and self._peer.error():
+            raise RuntimeError("peer-memory ray-map reduction: a flag wait timed out")
+
+    # ---- one frame ---------------------------------------------------------------
     def step(self, depth: torch.Tensor, pose: Pose, color=None, depth_ready=None) -> RayMap:
         """One frame.  ``depth_ready`` (see SplitIntegrator): an event after
         which ``depth`` is valid, True for a frame with no pending producer,
         or None (the integration's first half then waits for the stream)."""
+        if self.rebalance_every and self.frames and self.frames % self.rebalance_every == 0:
+            self.rebalance()
+        self.frames += 1
         self._integrator(self.tiles, depth, pose, self.intr, self.params, self.stats, color=color,
                          depth_ready=depth_ready)
         self.partial.reset()
@@ -335,6 +612,10 @@ class ShardedFusion:
         if self.world == 1:
             self.model, self.partial = self.partial, self.model
             return self.model
+        return self.reduce(pose)
+
+    def reduce(self, pose: Pose) -> RayMap:
+        """Merge every rank's partial into ``model`` on every rank (collective)."""
         if self._peer is not None:
             return self._peer.reduce()
         h, w = self.intr.height, self.intr.width

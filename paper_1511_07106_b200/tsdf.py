@@ -135,6 +135,9 @@ class TsdfSubvolume:
         self._summary_t: float | None = None
         # optional colour (not in the reference): uint8 [n, n, n, 4] = (r, g, b, count)
         self.color: torch.Tensor | None = None
+        # optional per-volume work counters (TfVolume.counters_dev, int64[2]:
+        # general / free-space bricks swept), set by the multi-GPU ownership
+        self.counters: torch.Tensor | None = None
 
     def enable_color(self) -> "TsdfSubvolume":
         """Give the volume a colour channel (all unobserved); returns it."""
@@ -226,10 +229,11 @@ class TsdfSubvolume:
         """ABI descriptor; with ``tau`` it carries the brick summary for that truncation."""
         if tau is None:
             return nat.volume_struct(self.voxels, self.voxels_per_side, self.origin_voxel,
-                                     self.voxel_size, color=self.color)
+                                     self.voxel_size, color=self.color, counters=self.counters)
         bad, thr = self._summary_for(tau)
         return nat.volume_struct(self.voxels, self.voxels_per_side, self.origin_voxel,
-                                 self.voxel_size, bad, self.brick_flags, thr, color=self.color)
+                                 self.voxel_size, bad, self.brick_flags, thr, color=self.color,
+                                 counters=self.counters)
 
     def __repr__(self) -> str:
         return (f"TsdfSubvolume(origin_voxel={self.origin_voxel!r}, "

