@@ -35,6 +35,7 @@ struct RayGeom {
     int exact_only;      // TF_DEBUG_EXACT_ONLY: plain reference march for every ray
     int lane0_only;      // TF_DEBUG_LANE0_ONLY: only lane 0 of each warp traces (timing studies)
     float good_t;        // brick-summary threshold for this tau
+    int uniform_vs;      // every volume of the launch has the same voxel size
 };
 
 struct Hit {
@@ -728,6 +729,8 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
     double *__restrict__ out_dist, double *__restrict__ out_vert, double *__restrict__ out_norm,
     unsigned long long *__restrict__ stats, int64_t *__restrict__ clocks, unsigned *__restrict__ rescue,
     unsigned *__restrict__ rescue_count, long long budget) {
+    constexpr int kList = 4;
+    __shared__ int2 s_list[kList][kBX * kBY];
     const long long t_start = clock64();
     const long long deadline = budget > 0 ? t_start + budget : LLONG_MAX;
     long long t_start_ns = 0;
@@ -755,37 +758,78 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
         ray_direction(g, px, py, d);
         const double o[3] = {g.cam.v[0], g.cam.v[1], g.cam.v[2]};
 
-        // entry intervals of every volume, visited nearest-entry first
-        int64_t jlo[TFB200_MAX_VOLUMES_PER_LAUNCH], jhi[TFB200_MAX_VOLUMES_PER_LAUNCH];
-        uint64_t pending = 0;  // bit v set = volume v still to march
-        for (int v = 0; v < vt.count; ++v)
-            if (ray_interval(vt.vol[v], o, d, jlo[v], jhi[v])) pending |= 1ull << v;
+        // Volumes are visited nearest entry first (the skip test below then
+        // prunes whatever lies behind a hit; any order gives the same map, the
+        // merge is order-free).  The order comes in batches of kList entries
+        // (lattice entry index, exit index | volume << 26) kept sorted in
+        // shared memory, one column per thread: no per-thread local arrays.
+        // A ray crossing more than kList volumes rebuilds the next batch from
+        // the ones after the last entry marched.  Launches mixing voxel sizes,
+        // or lattice indices beyond 2^26, take the volumes in index order.
         bool changed = false, aborted = false;
-        while (pending) {
-            int pick = -1;
-            for (int v = 0; v < vt.count; ++v)
-                if (((pending >> v) & 1ull) &&
-                    (pick < 0 || dmul((double)(jlo[v] - 1), vt.vol[v].voxel_size) <
-                                     dmul((double)(jlo[pick] - 1), vt.vol[pick].voxel_size)))
-                    pick = v;
-            pending &= ~(1ull << pick);
-            const TfVolume &vol = vt.vol[pick];
+        // n entries in the current batch, bi the next one to march; flags:
+        // bit 0 = more volumes after the batch, bit 1 = index order (the
+        // cursor of a rebuild is the batch's last entry, read back from smem)
+        int n = 0, bi = 0, flags = g.uniform_vs ? 1 : 3;
+        while (!aborted) {
+            int v;
+            int64_t lo, hi;
+            if (!(flags & 2) && bi == n) {
+                if (!(flags & 1)) break;
+                int cur_lo = -1, cur_v = -1;
+                if (n > 0) {
+                    const int2 c = s_list[n - 1][threadIdx.x];
+                    cur_lo = c.x;
+                    cur_v = (int)((unsigned)c.y >> 26);
+                }
+                n = bi = 0;
+                flags = 0;
+                for (int u = 0; u < vt.count; ++u) {
+                    int64_t a, b;
+                    if (!ray_interval(vt.vol[u], o, d, a, b)) continue;
+                    if (b >= (1ll << 26) || a >= (1ll << 30)) {  // decided on the first build
+                        flags = 2;
+                        break;
+                    }
+                    const int ia = (int)a;
+                    if (ia < cur_lo || (ia == cur_lo && u <= cur_v)) continue;  // an earlier batch
+                    int pos = n;
+                    while (pos > 0 && s_list[pos - 1][threadIdx.x].x > ia) {
+                        if (pos < kList) s_list[pos][threadIdx.x] = s_list[pos - 1][threadIdx.x];
+                        --pos;
+                    }
+                    if (pos < kList) s_list[pos][threadIdx.x] = make_int2(ia, (int)b | (u << 26));
+                    if (n < kList) ++n;
+                    else flags = 1;
+                }
+                if (!(flags & 2) && n == 0) break;
+            }
+            if (!(flags & 2)) {
+                const int2 e = s_list[bi++][threadIdx.x];
+                v = (int)((unsigned)e.y >> 26);
+                lo = e.x;
+                hi = e.y & ((1 << 26) - 1);
+            } else {  // index order; bi walks the volumes
+                while (bi < vt.count && !ray_interval(vt.vol[bi], o, d, lo, hi)) ++bi;
+                if (bi == vt.count) break;
+                v = bi++;
+            }
+            const TfVolume &vol = vt.vol[v];
             // no hit of this volume can have tstar below (j0 - 1) * delta
-            if (dmul((double)(jlo[pick] - 1), vol.voxel_size) > best.t) continue;
+            if (dmul((double)(lo - 1), vol.voxel_size) > best.t) continue;
             Ray r;
             FastRay fr;
-            if (setup_volume(g, vol, o, d, jhi[pick], r, fr)) {
+            if (setup_volume(g, vol, o, d, hi, r, fr)) {
 #ifdef TF_RAY_DIAG
                 int64_t *diag = clocks ? clocks + 12 * p + 4 : nullptr;
                 if (!diag) __trap();
 #endif
                 DIAG_T0
-                changed |= march_fast(fr, RayRef{&vol, &g}, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best,
+                changed |= march_fast(fr, RayRef{&vol, &g}, (int)lo, (int)hi, (int)g.coarse, best,
                                       samples, exact_samples, deadline, aborted DIAG_ARG);
                 DIAG_ACC(3)
-                if (aborted) break;
             } else {  // forced, or coordinates too large to certify: the exact reference march
-                changed |= march_volume(r, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
+                changed |= march_volume(r, lo, hi, g.coarse, g.near_thresh, best);
                 samples += r.samples;
                 exact_samples += r.samples;
             }
@@ -1078,28 +1122,36 @@ __device__ void coop_whole_rays(const VolumeTable &vt, const RayGeom &g, double 
         double d[3];
         ray_direction(g, px, py, d);
         const double o[3] = {g.cam.v[0], g.cam.v[1], g.cam.v[2]};
-        int64_t jlo[TFB200_MAX_VOLUMES_PER_LAUNCH], jhi[TFB200_MAX_VOLUMES_PER_LAUNCH];
-        uint64_t pending = 0;
-        for (int v = 0; v < vt.count; ++v)
-            if (ray_interval(vt.vol[v], o, d, jlo[v], jhi[v])) pending |= 1ull << v;
+        // volumes nearest entry first, each pick re-scanning the intervals (a
+        // rare path: rays beyond the split capacity; no per-lane arrays)
         bool changed = false;
-        while (pending) {
+        int64_t cur_lo = -1;
+        int cur_v = -1;
+        while (true) {
             int pick = -1;
-            for (int v = 0; v < vt.count; ++v)
-                if (((pending >> v) & 1ull) &&
-                    (pick < 0 || dmul((double)(jlo[v] - 1), vt.vol[v].voxel_size) <
-                                     dmul((double)(jlo[pick] - 1), vt.vol[pick].voxel_size)))
-                    pick = v;
-            pending &= ~(1ull << pick);
+            int64_t lo = 0, hi = 0;
+            for (int u = 0; u < vt.count; ++u) {
+                int64_t a, b;
+                if (!ray_interval(vt.vol[u], o, d, a, b)) continue;
+                if (a < cur_lo || (a == cur_lo && u <= cur_v)) continue;
+                if (pick < 0 || a < lo) {
+                    pick = u;
+                    lo = a;
+                    hi = b;
+                }
+            }
+            if (pick < 0) break;
+            cur_lo = lo;
+            cur_v = pick;
             const TfVolume &vol = vt.vol[pick];
-            if (dmul((double)(jlo[pick] - 1), vol.voxel_size) > best.t) continue;
+            if (dmul((double)(lo - 1), vol.voxel_size) > best.t) continue;
             Ray r;
             FastRay fr;
-            if (setup_volume(g, vol, o, d, jhi[pick], r, fr)) {
-                changed |= march_coop(fr, RayRef{&vol, &g}, (int)jlo[pick], (int)jhi[pick], (int)g.coarse, best,
+            if (setup_volume(g, vol, o, d, hi, r, fr)) {
+                changed |= march_coop(fr, RayRef{&vol, &g}, (int)lo, (int)hi, (int)g.coarse, best,
                                       samples, exact_samples);
             } else {
-                changed |= march_volume(r, jlo[pick], jhi[pick], g.coarse, g.near_thresh, best);
+                changed |= march_volume(r, lo, hi, g.coarse, g.near_thresh, best);
                 samples += r.samples;
                 exact_samples += r.samples;
             }
@@ -1459,6 +1511,9 @@ static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, dou
     g.exact_only = (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) ? 1 : 0;
     g.lane0_only = (tf_debug_flags() & TF_DEBUG_LANE0_ONLY) ? 1 : 0;
     g.good_t = good_threshold(tau);
+    g.uniform_vs = 1;
+    for (int v = 1; v < nvol; ++v)
+        if (vols[v].voxel_size != vols[0].voxel_size) g.uniform_vs = 0;
     for (int first = 0; first < nvol; first += TFB200_MAX_VOLUMES_PER_LAUNCH) {
         VolumeTable vt{};
         vt.count = nvol - first < TFB200_MAX_VOLUMES_PER_LAUNCH ? nvol - first
