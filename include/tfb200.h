@@ -315,6 +315,21 @@ int tf_endpoint_cells(const double *depth_dev, const TfCamera *cam, const double
                       const double t_wc[3], double block_side, int64_t *cells_dev,
                       void *stream);
 
+/* ---- the whole of volumes.bin_endpoints' arithmetic (volumes.py:305-331)
+ * on the device: the endpoint cell of every valid pixel (tf_endpoint_cells'
+ * arithmetic) counted in a hash table in the workspace (np.unique(...,
+ * return_counts=True), :327), compacted into out_dev = int64 [2 + 4 *
+ * capacity]: out[0] = distinct cells n, out[1] = overflow (1: a cell beyond
+ * +-2^20 blocks, or more than `capacity` cells — bin on the host instead),
+ * then n records (cx, cy, cz, count) in no particular order.  Stream-ordered,
+ * no host synchronisation: one small D2H of out_dev per frame.  The
+ * workspace (tf_bin_endpoints_workspace_size(capacity) bytes, 256-byte
+ * aligned) must be zero before the first call; each call leaves it zero. */
+size_t tf_bin_endpoints_workspace_size(int64_t capacity);
+int tf_bin_endpoints(const double *depth_dev, const TfCamera *cam, const double r_wc[9],
+                     const double t_wc[3], double block_side, int64_t capacity, void *workspace_dev,
+                     size_t workspace_bytes, int64_t *out_dev, void *stream);
+
 /* ---- multi-GPU ray-map reduction over peer memory (the
  * survey's tf_comm_init / tf_exchange_* rows).  One process per GPU.  Each
  * rank owns a "region" in its own HBM holding its partial ray map (what its

@@ -10,6 +10,8 @@
 //   endpoint_* — the per-pixel part of volumes.bin_endpoints (volumes.py:318-326).
 #include <math.h>
 
+#include <algorithm>
+
 #include "tf_common.cuh"
 
 namespace tf {
@@ -161,6 +163,128 @@ struct EndpointGeom {
     int64_t width, height;
 };
 
+// the endpoint cell of pixel p (valid depth): volumes.py:318-326
+__device__ __forceinline__ void endpoint_cell(const double *__restrict__ depth, const EndpointGeom &g,
+                                              int64_t p, double d, int64_t c[3]) {
+    const int64_t x = p % g.width, y = p / g.width;
+    const double ray[3] = {ddiv(dsub((double)x, g.cx), g.fx), ddiv(dsub((double)y, g.cy), g.fy), 1.0};
+    double rr[3];
+    // pixel_rays() @ R.T through OpenBLAS: FMA chain over k
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        rr[i] = dfma(ray[2], g.r.m[3 * i + 2], dfma(ray[1], g.r.m[3 * i + 1], dmul(ray[0], g.r.m[3 * i])));
+    const double nn = dsqrt(dadd(dadd(dmul(rr[0], rr[0]), dmul(rr[1], rr[1])), dmul(rr[2], rr[2])));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double pt = dadd(g.t.v[a], dmul(d, ddiv(rr[a], nn)));  // :319, :324
+        const double q = floor(ddiv(pt, g.block_side));            // :326
+        // int64 conversion of the reference; saturate far outside any key range
+        c[a] = q >= 9.0e18 ? INT64_MAX : (q <= -9.0e18 ? INT64_MIN + 1 : (int64_t)q);
+    }
+}
+
+// ---- endpoint histogram: np.unique(cells, axis=0, return_counts=True)
+// (volumes.py:327) as a hash table in the workspace.  Keys pack the cell's
+// three coordinates in 21 bits each (|c| < 2^20: 1 km at 1 mm blocks), top
+// bit set so an empty slot (0) never matches; a cell out of that range or a
+// full table raises the overflow flag (the caller then bins on the host).
+constexpr int kCellBits = 21;
+constexpr long long kCellLim = 1ll << (kCellBits - 1);
+
+struct HistHeader {
+    unsigned long long n;         // distinct cells compacted
+    unsigned long long overflow;  // 1: a cell out of range or the table / output full
+};
+
+__device__ __forceinline__ unsigned long long pack_cell(const int64_t c[3], bool &ok) {
+    ok = c[0] >= -kCellLim && c[0] < kCellLim && c[1] >= -kCellLim && c[1] < kCellLim &&
+         c[2] >= -kCellLim && c[2] < kCellLim;
+    const unsigned long long m = (1ull << kCellBits) - 1ull;
+    return (1ull << 63) | (((unsigned long long)c[0] & m) << (2 * kCellBits)) |
+           (((unsigned long long)c[1] & m) << kCellBits) | ((unsigned long long)c[2] & m);
+}
+
+__device__ __forceinline__ int64_t unpack_coord(unsigned long long key, int shift) {
+    const long long v = (long long)((key >> shift) & ((1ull << kCellBits) - 1ull));
+    return v >= kCellLim ? v - 2 * kCellLim : v;
+}
+
+__global__ void __launch_bounds__(256) endpoint_hist_kernel(const double *__restrict__ depth,
+                                                            const EndpointGeom g,
+                                                            unsigned long long *__restrict__ keys,
+                                                            unsigned long long *__restrict__ counts,
+                                                            const unsigned long long tmask,
+                                                            HistHeader *__restrict__ hdr) {
+    const int64_t npix = g.width * g.height;
+    for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x; p0 < npix; p0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = p0 + threadIdx.x;
+        const double d = p < npix ? depth[p] : 0.0;
+        const bool valid = d > 0.0;  // volumes.py:322
+        unsigned long long key = 0;
+        if (valid) {
+            int64_t c[3];
+            endpoint_cell(depth, g, p, d, c);
+            bool ok;
+            key = pack_cell(c, ok);
+            if (!ok) {
+                atomicExch(&hdr->overflow, 1ull);
+                key = 0;
+            }
+        }
+        // lanes with the same cell add once (neighbouring pixels share cells)
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (key && (threadIdx.x & 31) == __ffs(peers) - 1) {
+            const unsigned long long cnt = __popc(peers);
+            unsigned long long h = (key * 0x9E3779B97F4A7C15ull) >> 20;
+            for (unsigned long long probe = 0;; ++probe) {
+                if (probe > tmask) {
+                    atomicExch(&hdr->overflow, 1ull);
+                    break;
+                }
+                const unsigned long long slot = (h + probe) & tmask;
+                const unsigned long long prev = atomicCAS(&keys[slot], 0ull, key);
+                if (prev == 0ull || prev == key) {
+                    atomicAdd(&counts[slot], cnt);
+                    break;
+                }
+            }
+        }
+    }
+}
+
+// occupied slots -> out records (cx, cy, cz, count); the table is left empty
+__global__ void __launch_bounds__(256) endpoint_compact_kernel(unsigned long long *__restrict__ keys,
+                                                               unsigned long long *__restrict__ counts,
+                                                               const unsigned long long tsize,
+                                                               HistHeader *__restrict__ hdr,
+                                                               int64_t *__restrict__ out,
+                                                               const int64_t cap) {
+    for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < tsize;
+         s += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long key = keys[s];
+        if (!key) continue;
+        const unsigned long long i = atomicAdd(&hdr->n, 1ull);
+        if ((int64_t)i < cap) {
+            int64_t *r = out + 2 + 4 * i;
+            r[0] = unpack_coord(key, 2 * kCellBits);
+            r[1] = unpack_coord(key, kCellBits);
+            r[2] = unpack_coord(key, 0);
+            r[3] = (int64_t)counts[s];
+        } else {
+            atomicExch(&hdr->overflow, 1ull);
+        }
+        keys[s] = 0ull;
+        counts[s] = 0ull;
+    }
+}
+
+__global__ void endpoint_header_kernel(HistHeader *__restrict__ hdr, int64_t *__restrict__ out) {
+    out[0] = (int64_t)hdr->n;
+    out[1] = (int64_t)hdr->overflow;
+    hdr->n = 0ull;
+    hdr->overflow = 0ull;
+}
+
 __global__ void endpoint_cells_kernel(const double *__restrict__ depth, const EndpointGeom g,
                                       int64_t *__restrict__ cells) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -257,4 +381,56 @@ extern "C" int tf_endpoint_cells(const double *depth, const TfCamera *cam, const
     endpoint_cells_kernel<<<(unsigned)((npix + 255) / 256), 256, 0, (cudaStream_t)stream_>>>(depth, g,
                                                                                              cells);
     return tf_check_launch("endpoint_cells_kernel");
+}
+
+// table slots: the power of two >= 2 x capacity (load factor <= 1/2)
+static unsigned long long hist_slots(int64_t capacity) {
+    unsigned long long t = 64;
+    while (t < 2ull * (unsigned long long)capacity) t <<= 1;
+    return t;
+}
+
+extern "C" size_t tf_bin_endpoints_workspace_size(int64_t capacity) {
+    if (capacity < 1) return 0;
+    return 256 + (size_t)hist_slots(capacity) * 16;
+}
+
+extern "C" int tf_bin_endpoints(const double *depth, const TfCamera *cam, const double r_wc[9],
+                                const double t_wc[3], double block_side, int64_t capacity,
+                                void *workspace, size_t workspace_bytes, int64_t *out, void *stream_) {
+    if (!depth || !cam || !r_wc || !t_wc || !out || !workspace || !(block_side > 0.0) || capacity < 1)
+        return tf_set_error(TF_EINVAL, "tf_bin_endpoints: bad argument");
+    if (workspace_bytes < tf_bin_endpoints_workspace_size(capacity) || ((uintptr_t)workspace & 255u))
+        return tf_set_error(TF_EINVAL, "tf_bin_endpoints: workspace too small or not 256-byte aligned");
+    EndpointGeom g{};
+    for (int i = 0; i < 9; ++i) g.r.m[i] = r_wc[i];
+    for (int i = 0; i < 3; ++i) g.t.v[i] = t_wc[i];
+    g.fx = cam->fx;
+    g.fy = cam->fy;
+    g.cx = cam->cx;
+    g.cy = cam->cy;
+    g.block_side = block_side;
+    g.width = cam->width;
+    g.height = cam->height;
+    const unsigned long long tsize = hist_slots(capacity);
+    HistHeader *hdr = (HistHeader *)workspace;
+    unsigned long long *keys = (unsigned long long *)((char *)workspace + 256);
+    unsigned long long *counts = keys + tsize;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t npix = cam->width * cam->height;
+    if (npix > 0) {
+        const unsigned blocks = (unsigned)std::min<int64_t>((npix + 255) / 256, (int64_t)sms * 8);
+        endpoint_hist_kernel<<<blocks, 256, 0, stream>>>(depth, g, keys, counts, tsize - 1, hdr);
+        int rc = tf_check_launch("endpoint_hist_kernel");
+        if (rc) return rc;
+    }
+    endpoint_compact_kernel<<<(unsigned)std::min<unsigned long long>((tsize + 255) / 256, 1024ull), 256, 0,
+                              stream>>>(keys, counts, tsize, hdr, out, capacity);
+    int rc = tf_check_launch("endpoint_compact_kernel");
+    if (rc) return rc;
+    endpoint_header_kernel<<<1, 1, 0, stream>>>(hdr, out);
+    return tf_check_launch("endpoint_header_kernel");
 }

@@ -4,6 +4,7 @@ both spill tiers — the reference's files ("disk") and pinned host memory
 ("host", same LRU order and whole-image counters; files only on persist())."""
 
 import numpy as np
+import torch
 import pytest
 
 import paper_1511_07106_b200 as tf
@@ -153,3 +154,27 @@ def test_bin_endpoints_negative_cells(small_intr):
 
 def test_bin_endpoints_empty_frame(small_intr):
     assert tf.bin_endpoints(DepthFrame(np.zeros((60, 80))), small_intr, Pose.identity(), 30, 0.05) == {}
+
+
+def test_device_endpoint_histogram_equals_sorted_unique():
+    """tf_bin_endpoints (hash-table histogram, one read-back) == the per-pixel
+    cells + sort-based unique, on corridor frames, on a frame with more cells
+    than the table holds (host fallback) and with cells beyond the packed key
+    range (fallback)."""
+    import paper_1511_07106_b200 as tf
+    from paper_1511_07106_b200 import volumes as vm
+    from paper_1511_07106_b200.synth import corridor_depth, corridor_scene
+    intr = tf.RunConfig().intrinsics()
+    scene = corridor_scene()
+    poses = tf.corridor_trajectory(20.0, 2000)
+    for i in (0, 333, 1000, 1999):
+        f = torch.as_tensor(corridor_depth(scene, poses[i], intr).data, device="cuda")
+        for spacing, vs in ((256, 0.004), (30, 0.004), (8, 0.004), (4, 0.0001)):
+            got = vm.bin_endpoints(f, intr, poses[i], spacing, vs)
+            want = vm._bin_endpoints_sorted(f, intr, poses[i], spacing, vs)
+            assert got == want and list(got) == list(want), (i, spacing)
+    far = tf.Pose(np.eye(3), np.array([5.0e3, 0.0, 0.0]))  # cells beyond +-2^20 blocks
+    f = torch.full((intr.height, intr.width), 2.0, dtype=torch.float64, device="cuda")
+    assert vm.bin_endpoints(f, intr, far, 1, 0.001) == vm._bin_endpoints_sorted(f, intr, far, 1, 0.001)
+    empty = torch.zeros((intr.height, intr.width), dtype=torch.float64, device="cuda")
+    assert vm.bin_endpoints(empty, intr, poses[0], 256, 0.004) == {}
