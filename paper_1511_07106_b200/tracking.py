@@ -3,18 +3,24 @@
 Drop-in for tilefusion/tracking.py.  ``track`` keeps the reference's
 control flow exactly (pyramid of stride-2 levels, coarsest first, per-level
 iteration counts and pair minimums, Rodrigues update + SVD
-re-orthonormalisation, loss semantics; tracking.py:123-196).  What moved to
-the device:
+re-orthonormalisation, loss semantics; tracking.py:123-196) and runs all of
+it on the device in one call (tf_icp_track):
 
 * the source vertex / normal maps of every level (tf_vertex_normal_map,
   read straight from the full-resolution depth at stride 2^level);
 * every ``_solve_step``'s per-pixel work — transform, projective
-  association, distance / angle gates, and the reduction of A^T A, A^T r,
-  sum r^2 and the inlier count (tf_icp_reduce, 29 doubles per step).
+  association, distance / angle gates, and a deterministic warp-shuffle
+  reduction of A^T A, A^T r, sum r^2 and the inlier count (29 doubles);
+* the host part of ``_solve_step`` (tracking.py:100-120: pair minimum, the
+  cond > 1e12 gate, LU solve with partial pivoting, finiteness) and the
+  pose update (:178-183), in a single-warp kernel per step; steps after a
+  loss or convergence return at once.
 
-Only those 29 doubles cross to the host per iteration, where the 6x6
-conditioning gate and solve run in numpy exactly as in the reference
-(tracking.py:100-120).
+One read-back per frame (the final pose, loss flag, count and rms).
+``track_host`` is the same loop with one host round trip per step (the 6x6
+part in numpy, operation for operation as the reference); ``icp_sums`` /
+``solve_step`` expose a single step (parity tests replay the reference's
+steps through them).
 """
 
 from __future__ import annotations
