@@ -536,6 +536,83 @@ __device__ __forceinline__ unsigned free_state_delta(float2 old, float2 nv, floa
 // mean (_kernels.py:128-133 with clamped == tau).  Pure streaming: 16-byte
 // voxel pairs, four lanes per 64-byte row, eight rows per warp instruction,
 // four rows' loads in flight per lane.
+// One certified free-space brick (global brick id g) by one warp.
+__device__ __forceinline__ void free_brick(const VolumeTable &vt, const BrickTable &bt, const FrameGeom &f,
+                                           const unsigned g, const int lane, const int fixed_point,
+                                           const double2 *rcp, const ChangedList &changed,
+                                           unsigned &updates, unsigned &nop) {
+    const float2 fixed = make_float2(f.tau32, (float)f.max_w);
+    const int vi = find_volume(bt, g);
+    const TfVolume &vol = vt.vol[vi];
+    const unsigned n = (unsigned)vol.n, nb = (unsigned)bt.nb[vi];
+    const unsigned local = g - (unsigned)bt.offset[vi];
+    const unsigned x = (local % nb) * kBrick + 2 * (lane & 3);
+    const unsigned y0 = ((local / nb) % nb) * kBrick, z0 = (local / (nb * nb)) * kBrick;
+    float2 *vox = (float2 *)vol.voxels_dev;
+    const bool keep = keeps_summary(vol, f);
+    unsigned dbad = 0;
+    if ((n & 1u) == 0u && n - z0 >= (unsigned)kBrick && n - y0 >= (unsigned)kBrick &&
+        n - (x - 2 * (lane & 3)) >= (unsigned)kBrick) {
+        // interior brick, even n: 16-byte pairs, never split
+#pragma unroll 1
+        for (int h = 0; h < 8; h += 4) {
+            float4 o[4];
+            size_t lin[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const unsigned r = (unsigned)(lane >> 2) + 8u * (h + k);  // row = y + 8 z
+                lin[k] = ((size_t)(z0 + (r >> 3)) * n + (y0 + (r & 7u))) * n + x;
+                o[k] = *reinterpret_cast<const float4 *>(vox + lin[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 a = make_float2(o[k].x, o[k].y), b = make_float2(o[k].z, o[k].w);
+                const bool na = fixed_point && a.x == fixed.x && a.y == fixed.y;
+                const bool nbq = fixed_point && b.x == fixed.x && b.y == fixed.y;
+                updates += 2;
+                nop += (na ? 1u : 0u) + (nbq ? 1u : 0u);
+                if (na && nbq) continue;  // provably unchanged (host-verified fixed point)
+                const float2 ua = na ? a : free_update(a, f, rcp);
+                const float2 ub = nbq ? b : free_update(b, f, rcp);
+                if (keep) dbad += free_state_delta(a, ua, f.good_t) + free_state_delta(b, ub, f.good_t);
+                *reinterpret_cast<float4 *>(vox + lin[k]) = make_float4(ua.x, ua.y, ub.x, ub.y);
+            }
+        }
+    } else {
+        // edge brick or odd n: per voxel
+#pragma unroll 1
+        for (int it = 0; it < 8; ++it) {
+            const unsigned r = (unsigned)(lane >> 2) + 8u * it;
+            const unsigned y = y0 + (r & 7u), z = z0 + (r >> 3);
+            if (y >= n || z >= n) continue;
+            for (unsigned xx = x; xx < x + 2 && xx < n; ++xx) {
+                const size_t lin = ((size_t)z * n + y) * n + xx;
+                const float2 a = vox[lin];
+                ++updates;
+                if (fixed_point && a.x == fixed.x && a.y == fixed.y) {
+                    ++nop;
+                    continue;
+                }
+                const float2 ua = free_update(a, f, rcp);
+                if (keep) dbad += free_state_delta(a, ua, f.good_t);
+                vox[lin] = ua;
+            }
+        }
+    }
+    if (keep) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
+        if (lane == 0 && dbad) {
+            atomicAdd(&vol.brick_state_dev[local], dbad);
+            mark_changed(changed, g);
+        }
+    }
+}
+
+// Certified free-space bricks: every voxel gets the clamped-to-tau running
+// mean (_kernels.py:128-133 with clamped == tau).  Pure streaming: 16-byte
+// voxel pairs, four lanes per 64-byte row, eight rows per warp instruction,
+// four rows' loads in flight per lane.
 __global__ void __launch_bounds__(256, 4) brick_free_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const uint32_t *__restrict__ list,
@@ -547,77 +624,12 @@ __global__ void __launch_bounds__(256, 4) brick_free_kernel(
     const int lane = threadIdx.x & 31;
     const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
-    const float2 fixed = make_float2(f.tau32, (float)f.max_w);
     unsigned updates = 0, nop = 0;
     unsigned g_next = warp < count ? list[warp] : 0u;  // next brick id, loaded one brick ahead
     for (unsigned i = warp; i < count; i += nwarps) {
         const unsigned g = g_next;
         if (i + nwarps < count) g_next = list[i + nwarps];
-        const int vi = find_volume(bt, g);
-        const TfVolume &vol = vt.vol[vi];
-        const unsigned n = (unsigned)vol.n, nb = (unsigned)bt.nb[vi];
-        const unsigned local = g - (unsigned)bt.offset[vi];
-        const unsigned x = (local % nb) * kBrick + 2 * (lane & 3);
-        const unsigned y0 = ((local / nb) % nb) * kBrick, z0 = (local / (nb * nb)) * kBrick;
-        float2 *vox = (float2 *)vol.voxels_dev;
-        const bool keep = keeps_summary(vol, f);
-        unsigned dbad = 0;
-        if ((n & 1u) == 0u && n - z0 >= (unsigned)kBrick && n - y0 >= (unsigned)kBrick &&
-            n - (x - 2 * (lane & 3)) >= (unsigned)kBrick) {
-            // interior brick, even n: 16-byte pairs, never split
-#pragma unroll 1
-            for (int h = 0; h < 8; h += 4) {
-                float4 o[4];
-                size_t lin[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const unsigned r = (unsigned)(lane >> 2) + 8u * (h + k);  // row = y + 8 z
-                    lin[k] = ((size_t)(z0 + (r >> 3)) * n + (y0 + (r & 7u))) * n + x;
-                    o[k] = *reinterpret_cast<const float4 *>(vox + lin[k]);
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const float2 a = make_float2(o[k].x, o[k].y), b = make_float2(o[k].z, o[k].w);
-                    const bool na = fixed_point && a.x == fixed.x && a.y == fixed.y;
-                    const bool nbq = fixed_point && b.x == fixed.x && b.y == fixed.y;
-                    updates += 2;
-                    nop += (na ? 1u : 0u) + (nbq ? 1u : 0u);
-                    if (na && nbq) continue;  // provably unchanged (host-verified fixed point)
-                    const float2 ua = na ? a : free_update(a, f, rcp);
-                    const float2 ub = nbq ? b : free_update(b, f, rcp);
-                    if (keep) dbad += free_state_delta(a, ua, f.good_t) + free_state_delta(b, ub, f.good_t);
-                    *reinterpret_cast<float4 *>(vox + lin[k]) = make_float4(ua.x, ua.y, ub.x, ub.y);
-                }
-            }
-        } else {
-            // edge brick or odd n: per voxel
-#pragma unroll 1
-            for (int it = 0; it < 8; ++it) {
-                const unsigned r = (unsigned)(lane >> 2) + 8u * it;
-                const unsigned y = y0 + (r & 7u), z = z0 + (r >> 3);
-                if (y >= n || z >= n) continue;
-                for (unsigned xx = x; xx < x + 2 && xx < n; ++xx) {
-                    const size_t lin = ((size_t)z * n + y) * n + xx;
-                    const float2 a = vox[lin];
-                    ++updates;
-                    if (fixed_point && a.x == fixed.x && a.y == fixed.y) {
-                        ++nop;
-                        continue;
-                    }
-                    const float2 ua = free_update(a, f, rcp);
-                    if (keep) dbad += free_state_delta(a, ua, f.good_t);
-                    vox[lin] = ua;
-                }
-            }
-        }
-        if (keep) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
-            if (lane == 0 && dbad) {
-                atomicAdd(&vol.brick_state_dev[local], dbad);
-                mark_changed(changed, g);
-            }
-        }
+        free_brick(vt, bt, f, g, lane, fixed_point, rcp, changed, updates, nop);
     }
     if (stats) {
         warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
@@ -864,16 +876,32 @@ constexpr int kZBatch = 4;  // voxels in flight per thread
 // batches, so a warp instruction touches four 64-byte rows.  Column-level
 // work (float64 base, error bounds, whole-column rejection) is amortised over
 // the column; per voxel the screen is ~25 float32 instructions.
+// The general-brick list as virtual items p; with kMixed the certified
+// free-space bricks are interleaved into the same item space in proportion
+// (item p is general iff floor((p + 1) G / N) > floor(p G / N)), so every
+// warp streams free bricks between its general ones: the memory-bound and
+// the issue-bound work share the SMs inside one kernel instead of two
+// kernels time-slicing the register file.
+__device__ __forceinline__ unsigned mixed_item(unsigned p, unsigned ng, unsigned total, bool &is_free) {
+    const unsigned g0 = (unsigned)(((unsigned long long)p * ng) / total);
+    const unsigned g1 = (unsigned)(((unsigned long long)(p + 1) * ng) / total);
+    is_free = g1 == g0;
+    return is_free ? p - g0 : g0;
+}
+
+template <bool kMixed>
 __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const double2 *__restrict__ table,
     const float2 *__restrict__ table32, const uint32_t *__restrict__ active,
     const unsigned int *__restrict__ active_count, unsigned long long *__restrict__ queue,
     unsigned long long *__restrict__ queue_count, const unsigned long long queue_cap,
-    const int fixed_point, unsigned long long *__restrict__ stats, const ChangedList changed) {
+    const int fixed_point, unsigned long long *__restrict__ stats, const ChangedList changed,
+    const uint32_t *__restrict__ free_list, const unsigned int *__restrict__ free_count) {
     __shared__ double2 rcp[257];
     fill_rcp(rcp);
-    const unsigned count = *active_count;
+    const unsigned ngen = *active_count;
+    const unsigned count = kMixed ? ngen + *free_count : ngen;
     const int lane = threadIdx.x & 31;
     const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -884,11 +912,25 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const float k3u = 9.6e-7f * f.fx32, k3v = 9.6e-7f * f.fy32;
     const float k2u = 9.6e-7f * (fabsf(f.cx32) + 2.f), k2v = 9.6e-7f * (fabsf(f.cy32) + 2.f);
     unsigned updates = 0, swept = 0, nop = 0, col_skipped = 0, depth_skipped = 0, all_free = 0;
-    unsigned part_free = 0, part_skip = 0;
-    unsigned g_next = warp < count ? active[warp] : 0u;  // next brick id, loaded one brick ahead
+    unsigned part_free = 0, part_skip = 0, free_updates = 0;
+    bool next_free = false;
+    auto item_id = [&](unsigned p, bool &is_free) -> unsigned {
+        if (!kMixed) {
+            is_free = false;
+            return active[p];
+        }
+        const unsigned k = mixed_item(p, ngen, count, is_free);
+        return is_free ? free_list[k] : active[k];
+    };
+    unsigned g_next = warp < count ? item_id(warp, next_free) : 0u;  // next brick id, loaded one ahead
     for (unsigned i = warp; i < count; i += nwarps) {
         const unsigned g = g_next;
-        if (i + nwarps < count) g_next = active[i + nwarps];
+        const bool this_free = next_free;
+        if (i + nwarps < count) g_next = item_id(i + nwarps, next_free);
+        if (kMixed && this_free) {
+            free_brick(vt, bt, f, g, lane, fixed_point, rcp, changed, free_updates, nop);
+            continue;
+        }
         const int vi = find_volume(bt, g);
         const TfVolume &vol = vt.vol[vi];
         const unsigned n = (unsigned)vol.n, nb = (unsigned)bt.nb[vi];
@@ -954,6 +996,12 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                 brick_vox += nz;
             }
             if (row_in && !col_live) col_skipped += nz;
+            // every column of the warp outside the image / behind the camera:
+            // nothing of this half-brick can update (its parts are all-skip)
+            if (!__any_sync(0xffffffffu, col_live)) {
+                part_skip += kBrick / kZBatch;
+                continue;
+            }
             const float hu = 0.5f - du, hv = 0.5f - dv;
             const bool fast = front && hu > 0.f && hv > 0.f;
             unsigned exact_mask = 0;
@@ -1091,8 +1139,9 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
             ++all_free;  // (counted on every lane; lane 0's count is reported)
     }
     if (stats) {
-        warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
-        warp_count_add(&stats[TF_STAT_SWEPT_VOXELS], swept);
+        warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates + free_updates);
+        warp_count_add(&stats[TF_STAT_SWEPT_VOXELS], swept + free_updates);
+        if (kMixed) warp_count_add(&stats[TF_STAT_FREE_KERNEL_UPDATES], free_updates);
         warp_count_add(&stats[TF_STAT_NOOP_UPDATES], nop);
         warp_count_add(&stats[TF_STAT_COL_SKIPPED], col_skipped);
         warp_count_add(&stats[TF_STAT_DEPTH_SKIPPED], depth_skipped);
@@ -1517,25 +1566,47 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
         } else {
             // the certified free-space bricks (bandwidth-bound) run on a side
             // stream next to the general bricks (issue-bound): disjoint bricks
-            SideStream *side = side_stream();
-            if (!side) return tf_set_error(TF_ECUDA, "tf_integrate: cannot create the side stream");
-            std::unique_lock<std::mutex> side_lock(side->mu);
-            cudaEventRecord(side->fork, stream);
-            cudaStreamWaitEvent(side->stream, side->fork, 0);
-            void *pf = tf_profile_begin(TF_PROF_INTEGRATE_FREE, side->stream);
-            brick_free_kernel<<<(unsigned)sms * 4, 256, 0, side->stream>>>(vt, bt, f, active_free, fcount,
-                                                                          fixed_point,
-                                                                          (unsigned long long *)stats,
-                                                                          changed);
-            tf_profile_end(pf, side->stream);
-            if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
-            cudaEventRecord(side->join, side->stream);
-            void *pg = tf_profile_begin(TF_PROF_INTEGRATE_GENERAL, stream);
-            brick_update_kernel<<<(unsigned)sms * 9, 256, 0, stream>>>(
-                vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap,
-                fixed_point, (unsigned long long *)stats, changed);
-            tf_profile_end(pg, stream);
-            if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
+            static const int free_mode = [] {
+                // tuning knob (A/B): 1 (default) the free-brick kernel on a side
+                // stream next to the general kernel; 2 the same in stream order
+                // (0.423 vs 0.371 ms update bracket, config 3); 0 free bricks
+                // interleaved into the general kernel's items (0.471 ms: the
+                // streaming loses its memory parallelism at the general
+                // kernel's 3 blocks / SM)
+                const char *e = getenv("TFB200_FREE_MODE");
+                return e ? atoi(e) : 1;
+            }();
+            if (free_mode == 0) {
+                void *pg = tf_profile_begin(TF_PROF_INTEGRATE_GENERAL, stream);
+                brick_update_kernel<true><<<(unsigned)sms * 9, 256, 0, stream>>>(
+                    vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap, fixed_point,
+                    (unsigned long long *)stats, changed, active_free, fcount);
+                tf_profile_end(pg, stream);
+                if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
+            }
+            SideStream *side = free_mode == 1 ? side_stream() : nullptr;
+            if (free_mode == 1 && !side) return tf_set_error(TF_ECUDA, "tf_integrate: cannot create the side stream");
+            std::unique_lock<std::mutex> side_lock;
+            if (side) side_lock = std::unique_lock<std::mutex>(side->mu);
+            if (free_mode != 0) {
+                const cudaStream_t fs = side ? side->stream : stream;
+                if (side) {
+                    cudaEventRecord(side->fork, stream);
+                    cudaStreamWaitEvent(side->stream, side->fork, 0);
+                }
+                void *pf = tf_profile_begin(TF_PROF_INTEGRATE_FREE, fs);
+                brick_free_kernel<<<(unsigned)sms * 4, 256, 0, fs>>>(vt, bt, f, active_free, fcount, fixed_point,
+                                                                    (unsigned long long *)stats, changed);
+                tf_profile_end(pf, fs);
+                if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
+                if (side) cudaEventRecord(side->join, fs);
+                void *pg = tf_profile_begin(TF_PROF_INTEGRATE_GENERAL, stream);
+                brick_update_kernel<false><<<(unsigned)sms * 9, 256, 0, stream>>>(
+                    vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap, fixed_point,
+                    (unsigned long long *)stats, changed, nullptr, nullptr);
+                tf_profile_end(pg, stream);
+                if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
+            }
             void *pe = tf_profile_begin(TF_PROF_INTEGRATE_EXACT, stream);
             exact_queue_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(vt, bt, f, table, queue, qcount,
                                                                      L.queue_cap,
@@ -1543,7 +1614,7 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
                                                                      count, fcount, (unsigned long long)off);
             tf_profile_end(pe, stream);
             if ((rc = tf_check_launch("exact_queue_kernel"))) return rc;
-            cudaStreamWaitEvent(stream, side->join, 0);
+            if (side) cudaStreamWaitEvent(stream, side->join, 0);
         }
         tf_profile_end(prof, stream);
         if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
