@@ -293,18 +293,16 @@ __device__ __forceinline__ int find_volume(const BrickTable &bt, int64_t g) {
 // a free-space update: in front of the camera, projecting inside the image
 // onto pixels with depth, and closer than (d - tau) * ray_scale for every pixel
 // its projection box covers -> sdf >= tau, clamped value exactly tau).
-__device__ int brick_may_update(const TfVolume &vol, int64_t bx, int64_t by, int64_t bz,
-                                const FrameGeom &f, const unsigned long long *__restrict__ mip,
-                                const unsigned *__restrict__ qmip, const MipDesc &m, bool allow_free,
-                                int span = 1) {
-    // box of span^3 bricks starting at brick (bx, by, bz)
+__device__ int box_may_update(const TfVolume &vol, const int64_t i0[3], const int64_t len[3],
+                              const FrameGeom &f, const unsigned long long *__restrict__ mip,
+                              const unsigned *__restrict__ qmip, const MipDesc &m, bool allow_free) {
+    // the voxel box i0 .. i0 + len - 1 (clipped to the volume)
     const int64_t n = vol.n;
-    const int64_t i0[3] = {bx * kBrick, by * kBrick, bz * kBrick};
     double g0[3];
     float ext[3], gmin[3], gmax[3];
     float gabs = 0.f;
     for (int a = 0; a < 3; ++a) {
-        const int64_t i1 = min(i0[a] + (int64_t)kBrick * span - 1, n - 1);
+        const int64_t i1 = min(i0[a] + len[a] - 1, n - 1);
         // the reference's voxel centres (i + ht) * vs are monotone in i
         g0[a] = (double)(i0[a] + vol.origin[a]) * vol.voxel_size;
         const double g1 = (double)(i1 + vol.origin[a]) * vol.voxel_size;
@@ -404,6 +402,44 @@ __device__ int brick_may_update(const TfVolume &vol, int64_t bx, int64_t by, int
         if (qmin > 0.f && dist_ub <= qmin * 0.99998f) return 2;
     }
     return 1;
+}
+
+// box of span^3 bricks starting at brick (bx, by, bz)
+__device__ __forceinline__ int brick_may_update(const TfVolume &vol, int64_t bx, int64_t by, int64_t bz,
+                                                const FrameGeom &f, const unsigned long long *__restrict__ mip,
+                                                const unsigned *__restrict__ qmip, const MipDesc &m,
+                                                bool allow_free, int span = 1) {
+    const int64_t i0[3] = {bx * kBrick, by * kBrick, bz * kBrick};
+    const int64_t len[3] = {(int64_t)kBrick * span, (int64_t)kBrick * span, (int64_t)kBrick * span};
+    return box_may_update(vol, i0, len, f, mip, qmip, m, allow_free);
+}
+
+// Stage 3: classes of every general brick's four 8x4x4 parts (part p = hy +
+// 2 zh: y rows 4 hy .. 4 hy + 3, z layers 4 zh .. 4 zh + 3 — the general
+// kernel's lane layout), one thread per part: part_class[4 k + p] =
+// box_may_update of the part (0 no voxel can update, 1 maybe, 2 every voxel a
+// free-space update).  The general kernel skips class-0 parts and streams
+// class-2 parts without screening.
+__global__ void __launch_bounds__(256) part_cull_kernel(
+    const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
+    const __grid_constant__ FrameGeom f, const __grid_constant__ MipDesc m,
+    const unsigned long long *__restrict__ mip, const unsigned *__restrict__ qmip,
+    const uint32_t *__restrict__ active, const unsigned int *__restrict__ active_count,
+    uint8_t *__restrict__ part_class, const int allow_free) {
+    const unsigned total = *active_count * 4u;
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const unsigned g = active[t >> 2];
+        const int p = (int)(t & 3u);
+        const int v = find_volume(bt, g);
+        const TfVolume &vol = vt.vol[v];
+        const int64_t nb = bt.nb[v], local = (int64_t)g - bt.offset[v];
+        const int64_t bx = local % nb, by = (local / nb) % nb, bz = local / (nb * nb);
+        const int64_t i0[3] = {bx * kBrick, by * kBrick + 4 * (p & 1), bz * kBrick + 4 * (p >> 1)};
+        const int64_t len[3] = {kBrick, 4, 4};
+        int c = 0;
+        if (i0[1] < vol.n && i0[2] < vol.n) c = box_may_update(vol, i0, len, f, mip, qmip, m, allow_free != 0);
+        part_class[t] = (uint8_t)c;
+    }
 }
 
 constexpr int kMacro = 4;  // macro cull box: 4^3 bricks = 32^3 voxels
@@ -876,20 +912,6 @@ constexpr int kZBatch = 4;  // voxels in flight per thread
 // batches, so a warp instruction touches four 64-byte rows.  Column-level
 // work (float64 base, error bounds, whole-column rejection) is amortised over
 // the column; per voxel the screen is ~25 float32 instructions.
-// The general-brick list as virtual items p; with kMixed the certified
-// free-space bricks are interleaved into the same item space in proportion
-// (item p is general iff floor((p + 1) G / N) > floor(p G / N)), so every
-// warp streams free bricks between its general ones: the memory-bound and
-// the issue-bound work share the SMs inside one kernel instead of two
-// kernels time-slicing the register file.
-__device__ __forceinline__ unsigned mixed_item(unsigned p, unsigned ng, unsigned total, bool &is_free) {
-    const unsigned g0 = (unsigned)(((unsigned long long)p * ng) / total);
-    const unsigned g1 = (unsigned)(((unsigned long long)(p + 1) * ng) / total);
-    is_free = g1 == g0;
-    return is_free ? p - g0 : g0;
-}
-
-template <bool kMixed>
 __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const double2 *__restrict__ table,
@@ -897,11 +919,10 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const unsigned int *__restrict__ active_count, unsigned long long *__restrict__ queue,
     unsigned long long *__restrict__ queue_count, const unsigned long long queue_cap,
     const int fixed_point, unsigned long long *__restrict__ stats, const ChangedList changed,
-    const uint32_t *__restrict__ free_list, const unsigned int *__restrict__ free_count) {
+    const uint8_t *__restrict__ part_class) {
     __shared__ double2 rcp[257];
     fill_rcp(rcp);
-    const unsigned ngen = *active_count;
-    const unsigned count = kMixed ? ngen + *free_count : ngen;
+    const unsigned count = *active_count;
     const int lane = threadIdx.x & 31;
     const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -912,24 +933,22 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const float k3u = 9.6e-7f * f.fx32, k3v = 9.6e-7f * f.fy32;
     const float k2u = 9.6e-7f * (fabsf(f.cx32) + 2.f), k2v = 9.6e-7f * (fabsf(f.cy32) + 2.f);
     unsigned updates = 0, swept = 0, nop = 0, col_skipped = 0, depth_skipped = 0, all_free = 0;
-    unsigned part_free = 0, part_skip = 0, free_updates = 0;
-    bool next_free = false;
-    auto item_id = [&](unsigned p, bool &is_free) -> unsigned {
-        if (!kMixed) {
-            is_free = false;
-            return active[p];
-        }
-        const unsigned k = mixed_item(p, ngen, count, is_free);
-        return is_free ? free_list[k] : active[k];
+    unsigned part_free = 0, part_skip = 0;
+    unsigned g_next = warp < count ? active[warp] : 0u;  // next brick id, loaded one brick ahead
+    auto classes = [&](unsigned k) -> unsigned {
+        const uchar4 c = reinterpret_cast<const uchar4 *>(part_class)[k];
+        return (unsigned)c.x | ((unsigned)c.y << 2) | ((unsigned)c.z << 4) | ((unsigned)c.w << 6);
     };
-    unsigned g_next = warp < count ? item_id(warp, next_free) : 0u;  // next brick id, loaded one ahead
+    unsigned pc_next = part_class && warp < count ? classes(warp) : 0x55u;
     for (unsigned i = warp; i < count; i += nwarps) {
         const unsigned g = g_next;
-        const bool this_free = next_free;
-        if (i + nwarps < count) g_next = item_id(i + nwarps, next_free);
-        if (kMixed && this_free) {
-            free_brick(vt, bt, f, g, lane, fixed_point, rcp, changed, free_updates, nop);
-            continue;
+        // classes of the brick's four 8x4x4 parts (2 bits each, part = hy + 2 zh:
+        // 0 no voxel can update, 1 screen voxel by voxel, 2 every voxel a
+        // free-space update), certified by the culling stage
+        const unsigned pcls = pc_next;
+        if (i + nwarps < count) {
+            g_next = active[i + nwarps];
+            if (part_class) pc_next = classes(i + nwarps);
         }
         const int vi = find_volume(bt, g);
         const TfVolume &vol = vt.vol[vi];
@@ -955,6 +974,12 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         for (int hy = 0; hy < 2; ++hy) {
             const unsigned y = y_base + 4 * hy;
             const bool row_in = x < n && y < n;
+            // classes of this half's two parts (z layers 0-3, 4-7); warp-uniform
+            const unsigned pc_lo = (pcls >> (2 * hy)) & 3u, pc_hi = (pcls >> (2 * hy + 4)) & 3u;
+            if (pc_lo == 0u && pc_hi == 0u) {  // no voxel of the half-brick can update
+                part_skip += kBrick / kZBatch;
+                continue;
+            }
             const double gy = dmul((double)((int64_t)y + vol.origin[1]), vs);
             // float32 column bases at z0 (plain float64, then rounded)
             const float pbx = (float)(R[0] * gx + R[1] * gy + R[2] * gz0 + f.t_cw.v[0]);
@@ -1007,6 +1032,36 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
             unsigned exact_mask = 0;
 #pragma unroll 1
             for (int zb = 0; zb < kBrick; zb += kZBatch) {
+                const unsigned pc = zb < kZBatch ? pc_lo : pc_hi;
+                const unsigned nzb = (unsigned)zb < nz ? min(nz - (unsigned)zb, (unsigned)kZBatch) : 0u;
+                if (pc == 0u) {  // certified: no voxel of the part can update
+                    if (row_in) swept -= nzb;
+                    ++part_skip;
+                    continue;
+                }
+                if (pc == 2u) {  // certified: every voxel of the part is a free-space update
+                    const size_t row = ((size_t)(z0 + zb) * n + y) * n + x;
+                    float2 old[kZBatch];
+#pragma unroll
+                    for (int j = 0; j < kZBatch; ++j)
+                        old[j] = row_in && (unsigned)j < nzb ? vox[(size_t)row + (size_t)j * n * n]
+                                                            : make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int j = 0; j < kZBatch; ++j) {
+                        if (!(row_in && (unsigned)j < nzb)) continue;
+                        ++updates;
+                        ++brick_free;
+                        if (fixed_point && old[j].x == fixed.x && old[j].y == fixed.y) {
+                            ++nop;
+                        } else {
+                            const float2 nv = free_update(old[j], f, rcp);
+                            vox[(size_t)row + (size_t)j * n * n] = nv;
+                            if (keep) dbad += free_state_delta(old[j], nv, f.good_t);
+                        }
+                    }
+                    ++part_free;
+                    continue;
+                }
                 int cls[kZBatch];
                 unsigned pix[kZBatch];
                 // A: pixel of every voxel of the batch
@@ -1139,9 +1194,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
             ++all_free;  // (counted on every lane; lane 0's count is reported)
     }
     if (stats) {
-        warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates + free_updates);
-        warp_count_add(&stats[TF_STAT_SWEPT_VOXELS], swept + free_updates);
-        if (kMixed) warp_count_add(&stats[TF_STAT_FREE_KERNEL_UPDATES], free_updates);
+        warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
+        warp_count_add(&stats[TF_STAT_SWEPT_VOXELS], swept);
         warp_count_add(&stats[TF_STAT_NOOP_UPDATES], nop);
         warp_count_add(&stats[TF_STAT_COL_SKIPPED], col_skipped);
         warp_count_add(&stats[TF_STAT_DEPTH_SKIPPED], depth_skipped);
@@ -1314,7 +1368,7 @@ __global__ void __launch_bounds__(256) brick_summary_kernel(const TfVolume vol) 
 
 struct IntegrateLayout {
     size_t table_off, table32_off, mip_off, qmip_off, count_off, active_off, free_off, macro_off, queue_off,
-        changed_off, dirty_off, dirty_bytes, total;
+        changed_off, dirty_off, dirty_bytes, part_off, total;
     unsigned long long queue_cap;
 };
 
@@ -1351,6 +1405,8 @@ static IntegrateLayout layout_for(int64_t total_bricks_max, const TfCamera *cam)
     L.dirty_off = off;
     L.dirty_bytes = (size_t)((total_bricks_max + 31) / 32) * sizeof(uint32_t);
     off = align_up(off + L.dirty_bytes, 256);
+    L.part_off = off;  // part classes of the general bricks, 4 bytes per active entry
+    off = align_up(off + (size_t)total_bricks_max * 4, 256);
     L.total = off;
     return L;
 }
@@ -1448,6 +1504,11 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
     unsigned long long *qcount = (unsigned long long *)(ws + L.count_off + 64);
     unsigned long long *queue = (unsigned long long *)(ws + L.queue_off);
     uint32_t *active = (uint32_t *)(ws + L.active_off);
+    uint8_t *part_class = (uint8_t *)(ws + L.part_off);
+    static const int use_parts = [] {
+        const char *e = getenv("TFB200_PARTS");  // tuning knob (A/B): part classes from the cull stage
+        return e ? atoi(e) : 1;
+    }();
     const MipDesc m = make_mip(cam->width, cam->height);
     bool do_prep = (phases & 1) != 0;
     const bool do_fin = (phases & 2) != 0;
@@ -1557,6 +1618,11 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
                 vt, bt, f, m, mip, qmip, macros, mcount, active, count, active_free, fcount, no_cull,
                 exact_only ? 0 : 1);
             if ((rc = tf_check_launch("brick_cull_kernel"))) return rc;
+            if (use_parts && !no_cull) {
+                part_cull_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(vt, bt, f, m, mip, qmip, active, count,
+                                                                       part_class, exact_only ? 0 : 1);
+                if ((rc = tf_check_launch("part_cull_kernel"))) return rc;
+            }
         }
         if (!do_fin) continue;
         void *prof = tf_profile_begin(TF_PROF_INTEGRATE_UPDATE, stream);
@@ -1566,47 +1632,36 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
         } else {
             // the certified free-space bricks (bandwidth-bound) run on a side
             // stream next to the general bricks (issue-bound): disjoint bricks
-            static const int free_mode = [] {
-                // tuning knob (A/B): 1 (default) the free-brick kernel on a side
-                // stream next to the general kernel; 2 the same in stream order
-                // (0.423 vs 0.371 ms update bracket, config 3); 0 free bricks
-                // interleaved into the general kernel's items (0.471 ms: the
-                // streaming loses its memory parallelism at the general
-                // kernel's 3 blocks / SM)
-                const char *e = getenv("TFB200_FREE_MODE");
-                return e ? atoi(e) : 1;
+            static const int free_serial = [] {
+                // tuning knob (A/B): the free-brick kernel in stream order
+                // instead of on a side stream next to the general kernel (0.423
+                // vs 0.371 ms update bracket, config 3); interleaving free bricks
+                // into the general kernel's work items measured 0.471 ms (the
+                // streaming loses its memory parallelism at 3 blocks / SM)
+                const char *e = getenv("TFB200_FREE_SERIAL");
+                return e ? atoi(e) : 0;
             }();
-            if (free_mode == 0) {
-                void *pg = tf_profile_begin(TF_PROF_INTEGRATE_GENERAL, stream);
-                brick_update_kernel<true><<<(unsigned)sms * 9, 256, 0, stream>>>(
-                    vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap, fixed_point,
-                    (unsigned long long *)stats, changed, active_free, fcount);
-                tf_profile_end(pg, stream);
-                if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
-            }
-            SideStream *side = free_mode == 1 ? side_stream() : nullptr;
-            if (free_mode == 1 && !side) return tf_set_error(TF_ECUDA, "tf_integrate: cannot create the side stream");
+            SideStream *side = free_serial ? nullptr : side_stream();
+            if (!free_serial && !side) return tf_set_error(TF_ECUDA, "tf_integrate: cannot create the side stream");
             std::unique_lock<std::mutex> side_lock;
             if (side) side_lock = std::unique_lock<std::mutex>(side->mu);
-            if (free_mode != 0) {
-                const cudaStream_t fs = side ? side->stream : stream;
-                if (side) {
-                    cudaEventRecord(side->fork, stream);
-                    cudaStreamWaitEvent(side->stream, side->fork, 0);
-                }
-                void *pf = tf_profile_begin(TF_PROF_INTEGRATE_FREE, fs);
-                brick_free_kernel<<<(unsigned)sms * 4, 256, 0, fs>>>(vt, bt, f, active_free, fcount, fixed_point,
-                                                                    (unsigned long long *)stats, changed);
-                tf_profile_end(pf, fs);
-                if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
-                if (side) cudaEventRecord(side->join, fs);
-                void *pg = tf_profile_begin(TF_PROF_INTEGRATE_GENERAL, stream);
-                brick_update_kernel<false><<<(unsigned)sms * 9, 256, 0, stream>>>(
-                    vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap, fixed_point,
-                    (unsigned long long *)stats, changed, nullptr, nullptr);
-                tf_profile_end(pg, stream);
-                if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
+            const cudaStream_t fs = side ? side->stream : stream;
+            if (side) {
+                cudaEventRecord(side->fork, stream);
+                cudaStreamWaitEvent(side->stream, side->fork, 0);
             }
+            void *pf = tf_profile_begin(TF_PROF_INTEGRATE_FREE, fs);
+            brick_free_kernel<<<(unsigned)sms * 4, 256, 0, fs>>>(vt, bt, f, active_free, fcount, fixed_point,
+                                                                (unsigned long long *)stats, changed);
+            tf_profile_end(pf, fs);
+            if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
+            if (side) cudaEventRecord(side->join, fs);
+            void *pg = tf_profile_begin(TF_PROF_INTEGRATE_GENERAL, stream);
+            brick_update_kernel<<<(unsigned)sms * 9, 256, 0, stream>>>(
+                vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap, fixed_point,
+                (unsigned long long *)stats, changed, use_parts && !no_cull ? part_class : nullptr);
+            tf_profile_end(pg, stream);
+            if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
             void *pe = tf_profile_begin(TF_PROF_INTEGRATE_EXACT, stream);
             exact_queue_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(vt, bt, f, table, queue, qcount,
                                                                      L.queue_cap,
