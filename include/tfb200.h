@@ -122,6 +122,12 @@ enum { TF_PROF_INTEGRATE_UPDATE = 0, TF_PROF_INTEGRATE_ALL = 1, TF_PROF_RAYCAST 
        TF_PROF_INTEGRATE_FREE = 3, TF_PROF_INTEGRATE_GENERAL = 4, TF_PROF_INTEGRATE_EXACT = 5,
        TF_PROF_RAYCAST_COOP = 6, TF_PROF_KINDS = 7 };
 uint64_t tf_launch_count(void);
+/* Debug: index violations counted by a bounds-checked build of the library
+ * (compiled with -DTF_BOUNDS_CHECK: guarded loads / stores are skipped and
+ * counted instead of faulting — the stand-in for compute-sanitizer memcheck,
+ * which is closed on the GPU pool); UINT64_MAX from a plain build. */
+uint64_t tf_debug_bounds_violations(void);
+
 /* Debug: when set (device int64[12*H*W] per raycast call), tf_raycast writes per
  * pixel {SM clock cycles, samples, exact samples, summary-certified samples,
  * region evaluations at brick level by kind 0..3, at superbrick level 0..3};

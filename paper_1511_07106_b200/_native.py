@@ -79,6 +79,7 @@ _SIGNATURES = {
     "tf_set_debug_flags": (None, [ctypes.c_uint32]),
     "tf_debug_flags": (ctypes.c_uint32, []),
     "tf_launch_count": (ctypes.c_uint64, []),
+    "tf_debug_bounds_violations": (ctypes.c_uint64, []),
     "tf_debug_ray_clock_buffer": (None, [_c_p]),
     "tf_icp_track_state_size": (ctypes.c_size_t, []),
     "tf_icp_track": (_c_int, [ctypes.c_int, _c_p, _c_p, _c_p, ctypes.POINTER(TfCamera), _c_p, _c_p,

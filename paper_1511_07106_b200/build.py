@@ -21,6 +21,9 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libtfb200.so"
+# the bounds-checked debug variant (-DTF_BOUNDS_CHECK, tf_common.cuh): loaded
+# only by tests/test_gpu_bounds.py through TFB200_LIB
+LIB_CHECKED = PKG / "libtfb200_checked.so"
 SOURCES = ["api.cu", "integrate.cu", "raycast.cu", "icp.cu", "extract.cu", "comm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler",
@@ -34,42 +37,45 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: cannot build libtfb200.so")
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+def _stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
+    lib = LIB_CHECKED if checked else LIB
+    if not force and not _stale(lib):
+        return lib
     objs = []
-    build_dir = PKG / "_build"
+    build_dir = PKG / ("_build_checked" if checked else "_build")
     build_dir.mkdir(exist_ok=True)
     log = []
     for s in SOURCES:
         obj = build_dir / (Path(s).stem + ".o")
         extra = os.environ.get("TFB200_NVCC_EXTRA", "").split()  # diagnostics builds only
+        if checked:
+            extra = extra + ["-DTF_BOUNDS_CHECK"]
         cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, f"-I{INCLUDE}", "-c", str(CSRC / s), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {s}:\n{r.stdout}\n{r.stderr}")
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     (build_dir / "ptxas.log").write_text("\n".join(log))
     if verbose:
         print("\n".join(log))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    out = build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    out = build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv)
     print(out)

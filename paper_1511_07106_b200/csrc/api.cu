@@ -35,6 +35,22 @@ int tf_check_launch(const char *what) {
 
 extern "C" int tf_abi_version(void) { return TFB200_ABI_VERSION; }
 
+// Bounds violations counted by a -DTF_BOUNDS_CHECK build (tf_common.cuh,
+// TF_IN_BOUNDS); UINT64_MAX from a plain build.
+#ifdef TF_BOUNDS_CHECK
+extern "C" unsigned long long tf_bounds_read_integrate(void);
+extern "C" unsigned long long tf_bounds_read_raycast(void);
+extern "C" unsigned long long tf_bounds_read_extract(void);
+extern "C" unsigned long long tf_bounds_read_icp(void);
+extern "C" unsigned long long tf_bounds_read_comm(void);
+extern "C" uint64_t tf_debug_bounds_violations(void) {
+    return tf_bounds_read_integrate() + tf_bounds_read_raycast() + tf_bounds_read_extract() +
+           tf_bounds_read_icp() + tf_bounds_read_comm();
+}
+#else
+extern "C" uint64_t tf_debug_bounds_violations(void) { return ~0ull; }
+#endif
+
 // ---- launch counting and kernel timing -------------------------------------
 // Every kernel launch of the library bumps g_launches.  When profiling is on,
 // the main kernel of each tf_integrate / tf_raycast call is bracketed by a

@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(256) raymap_reduce_kernel(const __grid_constan
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npix;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = p0 + i;
+        if (!TF_IN_BOUNDS(p < pt.width * (pt.row0 + pt.nrows))) break;
         // rank 0's record, then the others folded in rank order (merge_blocks)
         const double *n0 = section<const double>(pt, 0, TF_COMM_PART_NORM) + 3 * p;
         double t = __ldcv(section<const double>(pt, 0, TF_COMM_PART_DIST) + p);
@@ -187,6 +188,8 @@ int cuda_fail(cudaError_t e, const char *what) {
 }  // namespace tf
 
 using tf::cuda_fail;
+
+TF_BOUNDS_READER(comm)
 
 extern "C" int tf_comm_create(int rank, int world, int64_t width, int64_t height, TfComm **out) {
     if (!out || world < 1 || world > TF_COMM_MAX_RANKS || rank < 0 || rank >= world || width < 1 ||

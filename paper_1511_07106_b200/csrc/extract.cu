@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(256) endpoint_hist_kernel(const double *__rest
                     break;
                 }
                 const unsigned long long slot = (h + probe) & tmask;
+                if (!TF_IN_BOUNDS(slot <= tmask)) break;
                 const unsigned long long prev = atomicCAS(&keys[slot], 0ull, key);
                 if (prev == 0ull || prev == key) {
                     atomicAdd(&counts[slot], cnt);
@@ -317,6 +318,8 @@ static size_t extract_blocks(int64_t n) {
 }  // namespace tf
 
 using namespace tf;
+
+TF_BOUNDS_READER(extract)
 
 extern "C" size_t tf_extract_workspace_size(int64_t n) {
     if (n < 2) return 0;

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kIcpThreads) icp_terms_kernel(
         }
         if (ok) {
             const int64_t mx = (int64_t)uf * P.stride, my = (int64_t)vf * P.stride;
-            ok = mx < P.mdl_w && my < P.mdl_h;
+            ok = mx < P.mdl_w && my < P.mdl_h && TF_IN_BOUNDS(mx >= 0 && my >= 0);
             if (ok) {
                 const int64_t m = my * P.mdl_w + mx;
                 ok = isfinite(md[m]);                                 // RayMap.valid (tsdf.py:178-180)
@@ -433,6 +433,8 @@ __global__ void icp_level_start_kernel(double *st) { st[kStLevelDone] = 0.0; }
 }  // namespace tf
 
 using namespace tf;
+
+TF_BOUNDS_READER(icp)
 
 extern "C" int tf_vertex_normal_map(const double *depth, int64_t full_w, int64_t full_h, int level,
                                     const TfCamera *cam, double *verts, double *norms,

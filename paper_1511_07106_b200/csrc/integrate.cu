@@ -598,6 +598,7 @@ __device__ __forceinline__ void free_brick(const VolumeTable &vt, const BrickTab
             for (int k = 0; k < 4; ++k) {
                 const unsigned r = (unsigned)(lane >> 2) + 8u * (h + k);  // row = y + 8 z
                 lin[k] = ((size_t)(z0 + (r >> 3)) * n + (y0 + (r & 7u))) * n + x;
+                if (!TF_IN_BOUNDS(lin[k] + 1 < (size_t)n * n * n)) lin[k] = 0;
                 o[k] = *reinterpret_cast<const float4 *>(vox + lin[k]);
             }
 #pragma unroll
@@ -623,6 +624,7 @@ __device__ __forceinline__ void free_brick(const VolumeTable &vt, const BrickTab
             if (y >= n || z >= n) continue;
             for (unsigned xx = x; xx < x + 2 && xx < n; ++xx) {
                 const size_t lin = ((size_t)z * n + y) * n + xx;
+                if (!TF_IN_BOUNDS(lin < (size_t)n * n * n)) continue;
                 const float2 a = vox[lin];
                 ++updates;
                 if (fixed_point && a.x == fixed.x && a.y == fixed.y) {
@@ -695,6 +697,7 @@ __device__ __forceinline__ int update_voxel(float2 *__restrict__ vox, int64_t li
     const double uf = floor(dadd(u, 0.5)), vf = floor(dadd(v, 0.5));            // :111-112
     if (!(uf >= 0.0 && uf < (double)f.width && vf >= 0.0 && vf < (double)f.height))
         return 0;                                                               // :113
+    if (!TF_IN_BOUNDS((int64_t)vf * f.width + (int64_t)uf < f.width * f.height)) return 0;
     const double2 px = __ldg(&table[(int64_t)vf * f.width + (int64_t)uf]);
     const double d = px.x;                                                      // :115
     if (!(d > 0.0)) return 0;                                                   // :116
@@ -1041,6 +1044,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                 }
                 if (pc == 2u) {  // certified: every voxel of the part is a free-space update
                     const size_t row = ((size_t)(z0 + zb) * n + y) * n + x;
+                    if (!TF_IN_BOUNDS(!row_in || nzb == 0u || row + (size_t)(nzb - 1) * n * n < (size_t)n * n * n))
+                        continue;
                     float2 old[kZBatch];
 #pragma unroll
                     for (int j = 0; j < kZBatch; ++j)
@@ -1109,7 +1114,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                 float2 px[kZBatch];
 #pragma unroll
                 for (int j = 0; j < kZBatch; ++j)
-                    px[j] = cls[j] == kFree ? __ldg(&table32[pix[j]]) : make_float2(0.f, 0.f);
+                    px[j] = cls[j] == kFree && TF_IN_BOUNDS(pix[j] < (unsigned)(f.width * f.height))
+                                ? __ldg(&table32[pix[j]]) : make_float2(0.f, 0.f);
                 // C: sdf class (dist <= (d - tau) rs  => free;  dist > (d + tau) rs  => skip)
 #pragma unroll
                 for (int j = 0; j < kZBatch; ++j) {
@@ -1129,8 +1135,10 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                 const size_t row = ((size_t)(z0 + zb) * n + y) * n + x;
                 float2 old[kZBatch];
 #pragma unroll
-                for (int j = 0; j < kZBatch; ++j)
+                for (int j = 0; j < kZBatch; ++j) {
+                    if (cls[j] == kFree && !TF_IN_BOUNDS(row + (size_t)j * n * n < (size_t)n * n * n)) cls[j] = kSkip;
                     old[j] = cls[j] == kFree ? vox[(size_t)row + (size_t)j * n * n] : make_float2(0.f, 0.f);
+                }
                 // E: free-space updates
 #pragma unroll
                 for (int j = 0; j < kZBatch; ++j) {
@@ -1226,6 +1234,7 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
         const TfVolume &vol = vt.vol[v];
         const int64_t n = vol.n;
         const int64_t lin = (z * n + y) * n + x;
+        if (!TF_IN_BOUNDS(v < vt.count && x < n && y < n && z < n)) continue;
         // the voxel's old value is loaded before the float64 projection, so its
         // HBM round trip overlaps the arithmetic instead of following it
         const float2 old = ((const float2 *)vol.voxels_dev)[lin];
@@ -1365,6 +1374,8 @@ __global__ void __launch_bounds__(256) brick_summary_kernel(const TfVolume vol) 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+
+TF_BOUNDS_READER(integrate)
 
 struct IntegrateLayout {
     size_t table_off, table32_off, mip_off, qmip_off, count_off, active_off, free_off, macro_off, queue_off,
@@ -1657,7 +1668,11 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
             if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
             if (side) cudaEventRecord(side->join, fs);
             void *pg = tf_profile_begin(TF_PROF_INTEGRATE_GENERAL, stream);
-            brick_update_kernel<<<(unsigned)sms * 9, 256, 0, stream>>>(
+            static const int gen_grid = [] {
+                const char *e = getenv("TFB200_GEN_GRID");  // tuning knob (A/B): blocks per SM
+                return e ? atoi(e) : 9;
+            }();
+            brick_update_kernel<<<(unsigned)(sms * gen_grid), 256, 0, stream>>>(
                 vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap, fixed_point,
                 (unsigned long long *)stats, changed, use_parts && !no_cull ? part_class : nullptr);
             tf_profile_end(pg, stream);

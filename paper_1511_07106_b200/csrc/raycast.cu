@@ -56,6 +56,10 @@ __device__ __forceinline__ void load_cell(const float2 *__restrict__ vox, int64_
                                           int64_t iy, int64_t iz, Cell &cell) {
     const float2 *b = vox + vox_index(n, iz, iy, ix);
     const int64_t sy = n, sz = n * n;
+    if (!TF_IN_BOUNDS(ix >= 0 && iy >= 0 && iz >= 0 && ix + 1 < n && iy + 1 < n && iz + 1 < n)) {
+        for (int c = 0; c < 8; ++c) cell.c[c] = make_float2(0.f, 0.f);
+        return;
+    }
     cell.c[0] = __ldg(b);
     cell.c[1] = __ldg(b + 1);
     cell.c[2] = __ldg(b + sy);
@@ -377,6 +381,7 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k, bool us
     const unsigned ix = bx_ >> 20, iy = by_ >> 20, iz = bz_ >> 20;
     const unsigned top = (unsigned)(r.n - 2);
     if (ix > top || iy > top || iz > top) return 0u;                  // invalid (:38)
+    if (!TF_IN_BOUNDS(ix + 1 < (unsigned)r.n && iy + 1 < (unsigned)r.n && iz + 1 < (unsigned)r.n)) return 0u;
     if (use_summary) {
         // min corner in a never-observed brick: certainly invalid (:40-50);
         // every corner in bricks whose voxels are all observed and >= T:
@@ -391,7 +396,8 @@ __device__ __forceinline__ unsigned fast_sample(const FastRay &r, int k, bool us
             for (unsigned c = 1; c < 8; ++c) {
                 if (((c & 1u) && !ex) || ((c & 2u) && !ey) || ((c & 4u) && !ez)) continue;
                 const unsigned nbx = bx + (c & 1u), nby = by + ((c >> 1) & 1u), nbz = bz + (c >> 2);
-                good = good && (__ldg(&r.bad[(nbz * r.nb + nby) * r.nb + nbx]) & 0xFFFFu) == 0u;
+                good = good && TF_IN_BOUNDS(nbx < r.nb && nby < r.nb && nbz < r.nb) &&
+                       (__ldg(&r.bad[(nbz * r.nb + nby) * r.nb + nbx]) & 0xFFFFu) == 0u;
             }
             if (good) return kValidBit | kPosBit | kSummaryBit;
         }
@@ -839,7 +845,7 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
             // this partial march is kept
             samples = exact_samples = 0;
             rescue[atomicAdd(rescue_count, 1u)] = (unsigned)p;
-        } else if (changed) {
+        } else if (changed && TF_IN_BOUNDS(p < g.width * g.height)) {
             hits = 1;
             out_dist[p] = best.t;
             out_vert[3 * p + 0] = best.hx;
@@ -1394,6 +1400,8 @@ __global__ void raycast_colors_kernel(const __grid_constant__ VolumeTable vt, co
 }  // namespace tf
 
 using namespace tf;
+
+TF_BOUNDS_READER(raycast)
 
 // Rescue list + per-(ray, volume) hit slots of the cooperative pass.  They
 // come from the caller's workspace (tf_raycast_ws, sized by

@@ -80,6 +80,26 @@ __device__ __forceinline__ bool record_wins(double t, double nx, double ny, doub
     return nz > cnz;
 }
 
+// ---- bounds-checked debug build (-DTF_BOUNDS_CHECK) ------------------------
+// compute-sanitizer is closed on the GPU pool; this build stands in for its
+// memcheck: every guarded index is checked, a violation is counted (per
+// translation unit) and the access is skipped instead of faulting.
+// tf_debug_bounds_violations() (api.cu) sums the counters; the plain build
+// compiles the guards away (TF_IN_BOUNDS(c) == true).
+#ifdef TF_BOUNDS_CHECK
+static __device__ unsigned long long tf_bounds_hits;
+#define TF_IN_BOUNDS(cond) ((cond) || (atomicAdd(&::tf::tf_bounds_hits, 1ull), false))
+#define TF_BOUNDS_READER(name)                                                              \
+    extern "C" unsigned long long tf_bounds_read_##name(void) {                           \
+        unsigned long long v = 0;                                                           \
+        cudaMemcpyFromSymbol(&v, ::tf::tf_bounds_hits, sizeof(v));                         \
+        return v;                                                                           \
+    }
+#else
+#define TF_IN_BOUNDS(cond) true
+#define TF_BOUNDS_READER(name)
+#endif
+
 // Warp-aggregated 64-bit counter add (integer: order-independent, exact).
 __device__ __forceinline__ void warp_count_add(unsigned long long *dst, unsigned long long v) {
 #pragma unroll

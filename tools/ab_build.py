@@ -6,6 +6,7 @@ Compiles the current csrc/ with the named files replaced (e.g.
 raycast.cu=/tmp/old_raycast.cu) into _ab/NAME.so; run the bench against it
 with TFB200_LIB=_ab/NAME.so.
 """
+import os
 import shutil
 import subprocess
 import sys
@@ -31,7 +32,8 @@ def main():
         objs = []
         for s in b.SOURCES:
             o = src / (Path(s).stem + ".o")
-            subprocess.run([b.nvcc(), *b.ARCH, *b.NVCC_FLAGS, f"-I{b.INCLUDE}", "-c", str(src / s), "-o", str(o)],
+            extra = os.environ.get("TFB200_NVCC_EXTRA", "").split()
+            subprocess.run([b.nvcc(), *b.ARCH, *b.NVCC_FLAGS, *extra, f"-I{b.INCLUDE}", "-c", str(src / s), "-o", str(o)],
                            check=True, capture_output=True)
             objs.append(str(o))
         subprocess.run([b.nvcc(), *b.ARCH, "-shared", "-o", str(out / f"{name}.so"), *objs], check=True)

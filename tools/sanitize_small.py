@@ -1,7 +1,13 @@
-"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck):
-every kernel family of libtfb200 once on small inputs.
+"""Small workload for memory checking: every kernel family of libtfb200
+once on small inputs (and, with --big, one config-3 frame: 8 x 512^3, voxel
+offsets near 2^31 per volume).
 
-    compute-sanitizer --tool memcheck --error-exitcode 99 python tools/sanitize_small.py
+    TFB200_LIB=paper_1511_07106_b200/libtfb200_checked.so python tools/sanitize_small.py --big
+
+With the bounds-checked build (-DTF_BOUNDS_CHECK) it reports the guarded
+index violations (tf_debug_bounds_violations) and exits 1 when any occurred;
+compute-sanitizer is closed on the GPU pool, this build stands in for its
+memcheck.  (Under compute-sanitizer the same script runs unchanged.)
 
 Covers: integration (screened + exact queue, exact-only, no-cull, colour),
 split integration, raycast (per-lane + cooperative pass, all-cooperative,
@@ -75,9 +81,26 @@ def main():
     shard = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length, params, intr)
     for p in poses[:2]:
         shard.step(torch.from_numpy(scene.render_depth(p, intr).data).cuda(), p)
+    if "--big" in sys.argv:
+        bspec = tf.init_grid(4.08, 1020, 510)
+        bintr = tf.RunConfig().intrinsics()
+        bparams = tf.FusionParams.for_voxel_size(bspec.voxel_size)
+        big = [tf.TsdfSubvolume.empty(k, bspec.voxels_per_side, bspec.subvolume_side_length) for k in bspec.keys]
+        orbit = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)
+        for p in (orbit[0], orbit[9]):
+            tf.integrate_volumes(big, scene.render_depth(p, bintr), p, bintr, bparams)
+            rmb = tf.RayMap.empty(bintr)
+            tf.raycast_volumes(big, p, bintr, rmb, bparams)
+        tf.extract_points(big[2])
+        del big
     torch.cuda.synchronize()
-    print("sanitize workload done")
+    v = int(lib.tf_debug_bounds_violations())
+    if v == 2 ** 64 - 1:
+        print("sanitize workload done (plain build: no bounds counters)")
+        return 0
+    print(f"sanitize workload done: {v} bounds violations")
+    return 1 if v else 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())
