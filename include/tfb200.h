@@ -336,6 +336,17 @@ int tf_bin_endpoints(const double *depth_dev, const TfCamera *cam, const double 
                      const double t_wc[3], double block_side, int64_t capacity, void *workspace_dev,
                      size_t workspace_bytes, int64_t *out_dev, void *stream);
 
+/* ---- packed spill images: the opt-in capacity mode of the pinned-host spill
+ * tier (spill_tier="host_packed"; not the parity format, SURVEY.md §7 hard
+ * part 5).  (tsdf, weight) f32 pairs -> tsdf IEEE half (round to nearest,
+ * |error| <= 2^-11 |tsdf| <= 4.9e-4 tau) + weight uint8 (round to nearest,
+ * saturating at 255: exact for integral weights <= 255) in two planes of
+ * `count` entries: 3 B per voxel crosses the host link instead of 8. */
+int tf_pack_voxels(const void *voxels_dev, int64_t count, void *tsdf_half_dev, uint8_t *weight_dev,
+                   void *stream);
+int tf_unpack_voxels(const void *tsdf_half_dev, const uint8_t *weight_dev, int64_t count,
+                     void *voxels_dev, void *stream);
+
 /* ---- multi-GPU ray-map reduction over peer memory (the
  * survey's tf_comm_init / tf_exchange_* rows).  One process per GPU.  Each
  * rank owns a "region" in its own HBM holding its partial ray map (what its

@@ -121,6 +121,8 @@ _SIGNATURES = {
     "tf_extract_count": (_c_int, [_VOL, _c_p, _c_sz, _c_p, _c_p]),
     "tf_extract_emit": (_c_int, [_VOL, _c_p, _c_sz, _c_p, _c_p, _c_p]),
     "tf_endpoint_cells": (_c_int, [_c_p, _CAM, _c_p, _c_p, _c_d, _c_p, _c_p]),
+    "tf_pack_voxels": (_c_int, [_c_p, _c_i64, _c_p, _c_p, _c_p]),
+    "tf_unpack_voxels": (_c_int, [_c_p, _c_p, _c_i64, _c_p, _c_p]),
     "tf_bin_endpoints_workspace_size": (_c_sz, [_c_i64]),
     "tf_bin_endpoints": (_c_int, [_c_p, _CAM, _c_p, _c_p, _c_d, _c_i64, _c_p, _c_sz, _c_p, _c_p]),
     "tf_comm_create": (_c_int, [_c_int, _c_int, _c_i64, _c_i64, ctypes.POINTER(_c_p)]),

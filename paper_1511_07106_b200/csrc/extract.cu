@@ -437,3 +437,56 @@ extern "C" int tf_bin_endpoints(const double *depth, const TfCamera *cam, const 
     endpoint_header_kernel<<<1, 1, 0, stream>>>(hdr, out);
     return tf_check_launch("endpoint_header_kernel");
 }
+
+// ---- packed spill images (opt-in capacity mode, not the parity format) -----
+// tsdf as IEEE half (round to nearest: |error| <= 2^-11 |tsdf| <= 4.9e-4 tau),
+// weight as uint8 (round to nearest, saturating at 255: exact for the
+// reference's integral weights up to 255; max_weight defaults to 128) — 3 B
+// per voxel instead of 8 in two planes.  SURVEY.md §7 hard part 5: the
+// parity format stays f32 / f32; this only shrinks what crosses the host link.
+#include <cuda_fp16.h>
+
+namespace tf {
+__global__ void pack_voxels_kernel(const float2 *__restrict__ vox, int64_t count, __half *__restrict__ t,
+                                   uint8_t *__restrict__ w) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 v = vox[i];
+        t[i] = __float2half_rn(v.x);
+        w[i] = (uint8_t)fminf(fmaxf(rintf(v.y), 0.0f), 255.0f);
+    }
+}
+
+__global__ void unpack_voxels_kernel(const __half *__restrict__ t, const uint8_t *__restrict__ w,
+                                     int64_t count, float2 *__restrict__ vox) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        vox[i] = make_float2(__half2float(t[i]), (float)w[i]);
+}
+}  // namespace tf
+
+static unsigned pack_grid(int64_t count) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (count + 255) / 256;
+    return (unsigned)(want < (int64_t)sms * 8 ? (want > 0 ? want : 1) : (int64_t)sms * 8);
+}
+
+extern "C" int tf_pack_voxels(const void *voxels_dev, int64_t count, void *tsdf_half_dev, uint8_t *weight_dev,
+                              void *stream) {
+    if (count <= 0) return TF_OK;
+    if (!voxels_dev || !tsdf_half_dev || !weight_dev) return tf_set_error(TF_EINVAL, "tf_pack_voxels: null argument");
+    tf::pack_voxels_kernel<<<pack_grid(count), 256, 0, (cudaStream_t)stream>>>(
+        (const float2 *)voxels_dev, count, (__half *)tsdf_half_dev, weight_dev);
+    return tf_check_launch("pack_voxels_kernel");
+}
+
+extern "C" int tf_unpack_voxels(const void *tsdf_half_dev, const uint8_t *weight_dev, int64_t count,
+                                void *voxels_dev, void *stream) {
+    if (count <= 0) return TF_OK;
+    if (!voxels_dev || !tsdf_half_dev || !weight_dev) return tf_set_error(TF_EINVAL, "tf_unpack_voxels: null argument");
+    tf::unpack_voxels_kernel<<<pack_grid(count), 256, 0, (cudaStream_t)stream>>>(
+        (const __half *)tsdf_half_dev, weight_dev, count, (float2 *)voxels_dev);
+    return tf_check_launch("unpack_voxels_kernel");
+}

@@ -178,3 +178,61 @@ def test_device_endpoint_histogram_equals_sorted_unique():
     assert vm.bin_endpoints(f, intr, far, 1, 0.001) == vm._bin_endpoints_sorted(f, intr, far, 1, 0.001)
     empty = torch.zeros((intr.height, intr.width), dtype=torch.float64, device="cuda")
     assert vm.bin_endpoints(empty, intr, poses[0], 256, 0.004) == {}
+
+
+def test_packed_spill_images_round_trip_bounds():
+    """tf_pack_voxels / tf_unpack_voxels (the host_packed capacity mode):
+    tsdf within half rounding (<= 2^-11 |tsdf|), integral weights <= 255 exact,
+    larger weights saturate at 255."""
+    from paper_1511_07106_b200 import _native as nat
+    g = torch.Generator(device="cpu").manual_seed(5)
+    n = 1 << 20
+    t = (torch.rand(n, generator=g) * 2 - 1) * 0.05
+    w = torch.randint(0, 300, (n,), generator=g).float()
+    vox = torch.stack([t, w], -1).cuda()
+    ht = torch.empty(n, dtype=torch.float16, device="cuda")
+    hw = torch.empty(n, dtype=torch.uint8, device="cuda")
+    back = torch.empty_like(vox)
+    L = nat.lib()
+    nat.check(L.tf_pack_voxels(nat.ptr(vox), n, nat.ptr(ht), nat.ptr(hw), nat.stream_handle()), "pack")
+    nat.check(L.tf_unpack_voxels(nat.ptr(ht), nat.ptr(hw), n, nat.ptr(back), nat.stream_handle()), "unpack")
+    back = back.cpu()
+    err = (back[:, 0] - t).abs()
+    assert bool((err <= t.abs() * 2.0 ** -11 + 6e-8).all())
+    assert torch.equal(back[:, 1], torch.clamp(w, max=255.0))
+
+
+def test_host_packed_tier_keeps_placement_and_bounds_the_error(tmp_path):
+    """The dynamic corridor run (tests/golden/dynamic_small.npz) with the lossy
+    packed spill tier: allocation, residency and spill counters equal the
+    reference's; weights equal the exact host tier's; tsdf within the half
+    rounding of every spill the tile went through."""
+    import paper_1511_07106_b200 as tf
+    from conftest import load_golden
+    g = load_golden("dynamic_small.npz")
+    fx, fy, cx, cy, w, h = g["intr"]
+    runs = {}
+    for tier in ("host", "host_packed"):
+        cfg = tf.RunConfig(fx=fx, fy=fy, cx=cx, cy=cy, width=int(w), height=int(h), dynamic=True,
+                           block_voxels=34, block_side_length=0.64, max_volumes=4, max_resident=3,
+                           use_groundtruth=True, spill_tier=tier)
+        pipe = tf.FusionPipeline(cfg, tmp_path / tier)
+        recs = []
+        for i, (f, m) in enumerate(zip(g["frames"], g["poses"])):
+            r = pipe.step(tf.DepthFrame(f), Pose(m[:3, :3], m[:3, 3]))
+            recs.append([r.volumes, r.resident, r.files_read, r.files_written, r.bytes_read, r.bytes_written])
+        assert recs == g["counters"].tolist()
+        vols = {}
+        for k in pipe.volumes.keys():
+            v = pipe.volumes.acquire(k)
+            vols[k] = v.voxels.cpu()
+            pipe.volumes.release(k)
+        runs[tier] = (vols, pipe.volumes.link_bytes_written, pipe.volumes.files_written)
+    exact, packed = runs["host"][0], runs["host_packed"][0]
+    assert exact.keys() == packed.keys()
+    tau = tf.FusionParams.for_voxel_size(0.64 / 32).truncation
+    spills = runs["host"][2]
+    for k in exact:
+        assert torch.equal(exact[k][..., 1], packed[k][..., 1])
+        assert float((exact[k][..., 0] - packed[k][..., 0]).abs().max()) <= spills * 4.9e-4 * tau
+    assert runs["host_packed"][1] * 8 == runs["host"][1] * 3  # 3 B per voxel instead of 8
