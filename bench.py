@@ -72,6 +72,8 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extra", action="store_true", help="skip the config1/2/4/5 legs")
     p.add_argument("--no-numba", action="store_true", help="reference arm: skip the numba sample")
+    p.add_argument("--only", choices=["config1", "config2", "config4", "config5"],
+                   help="run just this extra leg (debugging)")
     return p.parse_args()
 
 
@@ -437,9 +439,15 @@ def run_ours(args) -> None:
     if world == 1 and not args.no_extra:
         for name, fn in (("config1", run_config1), ("config2", run_config2),
                          ("config4", run_config4), ("config5", run_config5)):
+            if args.only and name != args.only:
+                continue
+            print(f"bench: {name} leg, {torch.cuda.memory_allocated() / 1e9:.1f} GB allocated before",
+                  file=sys.stderr, flush=True)
             try:
                 result[name] = fn(args, torch, nat, barrier, cpu=not args.no_cpu_baseline)
             except Exception as exc:  # a leg must not take the headline line down
+                import traceback
+                traceback.print_exc()
                 result[name] = {"error": f"{type(exc).__name__}: {exc}"}
             gc.collect()
             torch.cuda.empty_cache()
@@ -735,6 +743,8 @@ def run_config5(args, torch, nat, barrier, cpu: bool) -> dict:
 
         frame(0)
         torch.cuda.synchronize()
+        print(f"bench: config5 {tier}: {torch.cuda.memory_allocated() / 1e9:.1f} GB allocated after frame 0",
+              file=sys.stderr, flush=True)
         stats.zero_()
         b0 = (vset.link_bytes_read, vset.link_bytes_written)
         t0 = time.perf_counter()

@@ -20,6 +20,7 @@ and the operators running in libtfb200 (include/tfb200.h):
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass
 from typing import Iterable, Sequence
 
@@ -61,24 +62,27 @@ class _Mirror:
     """
 
     def __init__(self, download, upload) -> None:
-        self._download = download  # () -> dict[str, np.ndarray]
-        self._upload = upload      # (dict) -> None
+        # the owner's bound methods, held weakly: a strong reference would make
+        # owner -> mirror -> method -> owner a cycle, and a dropped volume's
+        # device memory would then wait for the cyclic garbage collector
+        self._download = weakref.WeakMethod(download)  # () -> dict[str, np.ndarray]
+        self._upload = weakref.WeakMethod(upload)      # (dict) -> None
         self.host: dict | None = None
         self.exposed = False
 
     def fetch(self) -> dict:
         if self.host is None:
-            self.host = self._download()
+            self.host = self._download()()
         self.exposed = True
         return self.host
 
     def before_read(self) -> None:
         if self.exposed and self.host is not None:
-            self._upload(self.host)
+            self._upload()(self.host)
 
     def after_write(self) -> None:
         if self.exposed and self.host is not None:
-            fresh = self._download()
+            fresh = self._download()()
             for k, v in fresh.items():
                 np.copyto(self.host[k], v)
         else:

@@ -236,3 +236,39 @@ def test_host_packed_tier_keeps_placement_and_bounds_the_error(tmp_path):
         assert torch.equal(exact[k][..., 1], packed[k][..., 1])
         assert float((exact[k][..., 0] - packed[k][..., 0]).abs().max()) <= spills * 4.9e-4 * tau
     assert runs["host_packed"][1] * 8 == runs["host"][1] * 3  # 3 B per voxel instead of 8
+
+
+@pytest.mark.parametrize("tier", ["host", "host_packed"])
+def test_dropped_tiles_free_their_memory_without_the_gc(tmp_path, tier):
+    """Volumes and ray maps hold no reference cycle: a tile evicted to the host
+    tier, or dropped, releases its device memory at once (with the cyclic
+    garbage collector off), so a long spill sequence does not pile up."""
+    import gc
+    import paper_1511_07106_b200 as tf
+    from paper_1511_07106_b200.volumes import VolumeSet
+    torch.cuda.synchronize()
+    gc.collect()
+    gc.disable()
+    try:
+        base = torch.cuda.memory_allocated()
+        params = tf.FusionParams.for_voxel_size(0.004)
+        vset = VolumeSet(params, voxels_per_side=128, voxel_size=0.004, max_resident=2,
+                         spill_dir=tmp_path, spill_tier=tier)
+        for k in range(4):
+            vset.add((k * 126, 0, 0))
+        tile_bytes = 128 ** 3 * 8
+        for _ in range(3):
+            for k in vset.keys():
+                vset.acquire(k)
+                tf.raycast_volumes([vset._resident[k]], tf.Pose.identity(),
+                                   tf.CameraIntrinsics(50.0, 50.0, 31.5, 23.5, 64, 48),
+                                   tf.RayMap.empty(tf.CameraIntrinsics(50.0, 50.0, 31.5, 23.5, 64, 48)),
+                                   params)
+                vset.release(k)
+                torch.cuda.synchronize()
+                assert torch.cuda.memory_allocated() - base < 3.5 * tile_bytes
+        del vset
+        torch.cuda.synchronize()
+        assert torch.cuda.memory_allocated() - base < 0.5 * tile_bytes
+    finally:
+        gc.enable()
