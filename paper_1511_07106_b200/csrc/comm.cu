@@ -11,9 +11,10 @@
 // the merge are the same loads and stores.  Synchronisation is two flag
 // waves through the same mappings (release / acquire at system scope):
 //
-//   ready  block 0 of the reduce kernel tells every peer "my partial is
-//          final" (the raycast precedes it on the stream); every block
-//          waits for all ranks' ready before reading;
+//   ready  every block of the reduce kernel tells every peer "my partial
+//          is final" (the raycast precedes it on the stream; the first
+//          resident block raises it); every block waits for all ranks'
+//          ready before reading;
 //   done   the reduce kernel's last block (grid-wide counter) tells every
 //          peer "my rows are in your model and I have stopped reading your
 //          partial"; comm_wait_done_kernel (one warp) waits for all ranks'
@@ -109,7 +110,12 @@ __device__ void wait_flag(const unsigned long long *flag, unsigned long long epo
 __global__ void __launch_bounds__(256) raymap_reduce_kernel(const __grid_constant__ PeerTable pt) {
     CommFlags *mine = section<CommFlags>(pt, pt.rank, TF_COMM_FLAGS);
     if (pt.wait) {
-        if (blockIdx.x == 0 && threadIdx.x < pt.world) {  // my partial is final -> every rank
+        // my partial is final (the raycast precedes this kernel on the stream)
+        // -> every rank.  Every block raises it (the same value, idempotent),
+        // so the flag goes up as soon as ANY block of the grid is resident —
+        // no rank waits on a block of another rank that is still queued behind
+        // whatever else that GPU runs
+        if (threadIdx.x < pt.world) {
             __threadfence_system();
             st_release_sys(&section<CommFlags>(pt, threadIdx.x, TF_COMM_FLAGS)->ready[pt.rank], pt.epoch);
         }

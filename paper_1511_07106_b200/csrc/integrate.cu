@@ -1168,10 +1168,23 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                     part_skip += ls;
                 }
             }
-            // undecided voxels of the column go to the exact kernel
-            if (__any_sync(0xffffffffu, exact_mask != 0u) && exact_mask) {
+            // undecided voxels of the column go to the exact kernel; one queue
+            // reservation per warp (a lane-order scan of the counts): per-lane
+            // atomics on the one counter serialise when many columns are
+            // undecided (axis-aligned views put whole voxel planes on pixel
+            // edges: 1.1 ms instead of 0.3 for the general kernel)
+            if (__any_sync(0xffffffffu, exact_mask != 0u)) {
                 const unsigned c = __popc(exact_mask);
-                const unsigned long long base = atomicAdd(queue_count, (unsigned long long)c);
+                unsigned incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                unsigned long long wbase = 0;
+                if (lane == 31) wbase = atomicAdd(queue_count, (unsigned long long)incl);
+                wbase = __shfl_sync(0xffffffffu, wbase, 31);
+                const unsigned long long base = wbase + (incl - c);
                 unsigned k = 0;
                 for (unsigned m = exact_mask; m; m &= m - 1, ++k) {
                     const unsigned zz = __ffs(m) - 1;
