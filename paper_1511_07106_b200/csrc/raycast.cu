@@ -872,11 +872,11 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
         clocks[q + 3] = (int64_t)(exact_samples >> 44);
     }
     if (stats) {
-        warp_count_add(&stats[TF_STAT_RAY_SAMPLES], samples);
-        warp_count_add(&stats[TF_STAT_RAY_HITS], hits);
-        warp_count_add(&stats[TF_STAT_EXACT_SAMPLES], exact_samples & ((1ull << 40) - 1));
-        warp_count_add(&stats[TF_STAT_CERT_FAILURES], (exact_samples >> 40) & 15ull);
-        warp_count_add(&stats[TF_STAT_SUMMARY_SAMPLES], exact_samples >> 44);
+        unsigned long long *const dst[5] = {&stats[TF_STAT_RAY_SAMPLES], &stats[TF_STAT_RAY_HITS],
+                                            &stats[TF_STAT_EXACT_SAMPLES], &stats[TF_STAT_CERT_FAILURES],
+                                            &stats[TF_STAT_SUMMARY_SAMPLES]};
+        block_count_add<5>(dst, {samples, hits, exact_samples & ((1ull << 40) - 1),
+                                 (exact_samples >> 40) & 15ull, exact_samples >> 44});
     }
 }
 

@@ -107,6 +107,28 @@ __device__ __forceinline__ void warp_count_add(unsigned long long *dst, unsigned
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
 }
 
+// Block-aggregated counter adds for the end of a persistent kernel: every
+// warp of the grid finishes at about the same time, and per-warp atomics on a
+// handful of addresses then queue up behind each other; here the warps' sums
+// meet in shared memory and one thread per block adds each counter.  Every
+// thread of the block must call it.
+template <int N>
+__device__ __forceinline__ void block_count_add(unsigned long long *const (&dst)[N],
+                                                const unsigned long long (&v)[N]) {
+    __shared__ unsigned long long part[N];
+    if (threadIdx.x < N) part[threadIdx.x] = 0ull;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        unsigned long long s = v[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if ((threadIdx.x & 31) == 0 && s) atomicAdd_block(&part[i], s);
+    }
+    __syncthreads();
+    if (threadIdx.x < N && part[threadIdx.x]) atomicAdd(dst[threadIdx.x], part[threadIdx.x]);
+}
+
 }  // namespace tf
 
 // ---- host-side error plumbing (api.cu) --------------------------------------
