@@ -1536,12 +1536,19 @@ static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, dou
             const char *e = getenv("TFB200_RAY_SHAPE");  // tuning knob: block shape variant
             return e ? atoi(e) : 0;
         }();
-        static const long long budget = [] {
+        static const long long base_budget = [] {
             // cycles a warp of the per-lane march may run before its unfinished
-            // rays move to the cooperative pass (0: never)
+            // rays move to the cooperative pass (0: never), for up to 8 volumes
             const char *e = getenv("TFB200_RAY_BUDGET");
             return e ? atoll(e) : 1400000ll;
         }();
+        // the bulk of the per-lane work grows with the volumes a ray crosses:
+        // the budget scales with the square root of the launch's volumes beyond
+        // 8 (config 3, 8 volumes: 1.4 M cycles optimal, 2.0 M 30 % slower;
+        // config 4, 16 volumes: 1.4 M -> 1.90 ms, 2.0 M -> 1.45, 2.5 M -> 1.49,
+        // 2.8 M -> 1.54, 4 M -> 1.70 ms)
+        const long long budget =
+            vt.count > 8 ? (long long)((double)base_budget * sqrt(vt.count / 8.0)) : base_budget;
         const bool coop_all = (tf_debug_flags() & TF_DEBUG_COOP_ALL) != 0;
         unsigned long long *st = (unsigned long long *)stats;
         int64_t *clk = tf_ray_clock_buffer();
