@@ -741,7 +741,9 @@ def run_config5(args, torch, nat, barrier, cpu: bool) -> dict:
                 vset.release(k)
             return rm
 
+        counts = []
         frame(0)
+        counts.append((vset.files_read, vset.files_written))
         torch.cuda.synchronize()
         print(f"bench: config5 {tier}: {torch.cuda.memory_allocated() / 1e9:.1f} GB allocated after frame 0",
               file=sys.stderr, flush=True)
@@ -750,8 +752,10 @@ def run_config5(args, torch, nat, barrier, cpu: bool) -> dict:
         t0 = time.perf_counter()
         for j in range(1, len(frame_ids)):
             frame(j)
+            counts.append((vset.files_read, vset.files_written))
         torch.cuda.synchronize()
         sec = time.perf_counter() - t0
+        run.counts = counts
         moved = (vset.link_bytes_read - b0[0]) + (vset.link_bytes_written - b0[1])
         nf = len(frame_ids) - 1
         return vset, {"frames_per_s": nf / sec,
@@ -759,7 +763,9 @@ def run_config5(args, torch, nat, barrier, cpu: bool) -> dict:
                       "link_bytes_per_frame": moved / nf, "link_gbs": moved / sec / 1e9}
 
     exact_set, exact = run("host")
+    schedule = run.counts
     packed_set, packed = run("host_packed")
+    ref_schedule = reference_spill_schedule(mine, len(frame_ids))
     tau = params.truncation
     err, wdiff = 0.0, 0
     for k in exact_set.keys():  # tile by tile, both resident at once
@@ -780,7 +786,38 @@ def run_config5(args, torch, nat, barrier, cpu: bool) -> dict:
             "frames_per_s": exact["frames_per_s"], "voxel_updates_per_s": exact["voxel_updates_per_s"],
             "spill_bytes_per_frame": exact["link_bytes_per_frame"], "spill_gbs": exact["link_gbs"],
             "pinned_d2h_gbs": d2h, "pinned_h2d_gbs": h2d, "packed_tier": packed,
+            "spill_schedule": {"files_read_written_after_each_frame": schedule,
+                               "reference": ref_schedule,
+                               "matches_reference": ref_schedule is None or ref_schedule == schedule,
+                               "how": "the unmodified reference VolumeSet (baseline/_ref) driven through the "
+                                      "same acquire / release sequence on 8^3 stand-in tiles"},
             "bound": "host link (each frame moves every tile through the spill tier)"}
+
+
+def reference_spill_schedule(keys, nframes):
+    """(files_read, files_written) after each frame from the reference's own
+    VolumeSet (volumes.py:156-302) for config 5's acquire / release order, on
+    tiny stand-in tiles (the counts do not depend on the tile size); None when
+    baseline/_ref is absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "tilefusion").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="tfb200_numba_"))
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import tilefusion as rtf
+    vs = 0.001
+    rset = rtf.VolumeSet(rtf.FusionParams.for_voxel_size(vs), voxels_per_side=8, voxel_size=vs,
+                         max_resident=2, spill_dir=tempfile.mkdtemp(prefix="tfb200_refspill_"))
+    for k in keys:
+        rset.add(k)
+    out = []
+    for _ in range(nframes):
+        for k in rset.keys():
+            rset.acquire(k)
+            rset.release(k)
+        out.append((rset.files_read, rset.files_written))
+    return out
 
 
 # ---------------------------------------------------------------------------
