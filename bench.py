@@ -341,9 +341,13 @@ def run_ours(args) -> None:
     if tfile.exists():
         try:
             tj = json.loads(tfile.read_text())
-            traffic = tj.get("integrate_update_bracket_bytes_per_launch")
+            # the capture is one launch (one frame): its DRAM bytes per update,
+            # times this run's updates per launch
+            bpu = tj.get("integrate_update_bracket_bytes_per_update")
+            traffic = bpu * updates_local / max(upd_launches, 1) if bpu else None
             ray_traffic = tj.get("raycast_bytes_per_launch")
-            traffic_src = tj.get("source")
+            traffic_src = (f"{tj.get('source')}: {bpu:.2f} DRAM bytes per update x this run's updates per "
+                           f"launch" if bpu else tj.get("source"))
         except Exception:
             traffic = ray_traffic = None
     evaluated = samples - sum_over_ranks(int(st[nat.STAT_SUMMARY_SAMPLES]))

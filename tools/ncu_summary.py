@@ -85,10 +85,11 @@ def main():
         for d in rs:
             by.setdefault(d["kernel"], []).append(d.get("dram_read", 0) + d.get("dram_write", 0))
         avg = {k: sum(v) / len(v) for k, v in by.items()}
-        bracket = sum(avg.get(k, 0.0) for k in ("tf::brick_update_kernel", "tf::brick_free_kernel",
-                                                "tf::exact_queue_kernel"))
+        bracket = sum(v for k, v in avg.items()
+                      if k.split("::")[-1] in ("brick_update_kernel", "brick_free_kernel", "exact_queue_kernel"))
         ray = next((v for k, v in avg.items() if "raycast_kernel" in k), None)
-        json.dump({"source": f"ncu --set full capture {rep.split('/')[-1]}, one timed-region launch per kernel",
+        json.dump({"source": f"ncu --set full capture {rep.split('/')[-1]}, one timed-region launch per kernel "
+                             "(frame 0 of the orbit, 36.9 M updates: 590 MB algorithmic)",
                    "integrate_update_bracket_bytes_per_launch": bracket, "raycast_bytes_per_launch": ray,
                    "per_kernel_dram_bytes": avg}, open(out, "w"), indent=1)
         return
