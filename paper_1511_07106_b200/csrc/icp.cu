@@ -123,6 +123,38 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+constexpr int kFoldThreads = 256;
+
+// The 29 sums over the block partials ([nblocks][29] doubles) by one block of
+// kFoldThreads threads, in a fixed order: thread t folds blocks t, t + 256,
+// ... (all 29 terms at once: independent loads, many in flight), then the
+// shuffle tree per warp, then the warps in order.  Deterministic; the same
+// function serves tf_icp_reduce and tf_icp_track.
+__device__ void fold_partials(const double *__restrict__ partials, int64_t nblocks, double *sums) {
+    __shared__ double wpart[kFoldThreads / 32][kIcpTerms];
+    double acc[kIcpTerms];
+#pragma unroll
+    for (int k = 0; k < kIcpTerms; ++k) acc[k] = 0.0;
+    for (int64_t b = threadIdx.x; b < nblocks; b += kFoldThreads) {
+        const double *p = partials + b * kIcpTerms;
+#pragma unroll
+        for (int k = 0; k < kIcpTerms; ++k) acc[k] = dadd(acc[k], p[k]);
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < kIcpTerms; ++k) {
+        const double s = warp_sum(acc[k]);
+        if (lane == 0) wpart[w][k] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < kIcpTerms) {
+        double s = 0.0;
+        for (int i = 0; i < kFoldThreads / 32; ++i) s = dadd(s, wpart[i][threadIdx.x]);
+        sums[threadIdx.x] = s;
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(kIcpThreads) icp_terms_kernel(
     const double *__restrict__ sv, const double *__restrict__ sn, const uint8_t *__restrict__ sok,
     const double *__restrict__ md, const double *__restrict__ mv, const double *__restrict__ mn,
@@ -212,15 +244,12 @@ __global__ void __launch_bounds__(kIcpThreads) icp_terms_kernel(
     }
 }
 
-// warp k sums term k over all block partials in a fixed order
-__global__ void icp_finish_kernel(const double *__restrict__ partials, int64_t nblocks,
-                                  double *__restrict__ out) {
-    const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
-    if (k >= kIcpTerms) return;
-    double s = 0.0;
-    for (int64_t b = lane; b < nblocks; b += 32) s = dadd(s, partials[b * kIcpTerms + k]);
-    s = warp_sum(s);
-    if (lane == 0) out[k] = s;
+// the 29 sums of tf_icp_reduce (fold_partials' order)
+__global__ void __launch_bounds__(kFoldThreads) icp_finish_kernel(const double *__restrict__ partials,
+                                                                  int64_t nblocks, double *__restrict__ out) {
+    __shared__ double sums[kIcpTerms];
+    fold_partials(partials, nblocks, sums);
+    if (threadIdx.x < kIcpTerms) out[threadIdx.x] = sums[threadIdx.x];
 }
 
 
@@ -363,19 +392,12 @@ __device__ void polar3(double X[9]) {
     }
 }
 
-__global__ void __launch_bounds__(32 * kIcpTerms, 1) icp_step_kernel(const double *__restrict__ partials, int64_t nblocks, int min_pairs,
-                                double step_eps, double *__restrict__ st) {
-    const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
-    if (st[kStLost] != 0.0 || st[kStLevelDone] != 0.0) return;
-    __shared__ double sums[kIcpTerms];
-    if (k < kIcpTerms) {
-        double s = 0.0;
-        for (int64_t b = lane; b < nblocks; b += 32) s = dadd(s, partials[b * kIcpTerms + k]);
-        s = warp_sum(s);
-        if (lane == 0) sums[k] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
+__device__ void icp_apply_delta(const double b[6], double step_eps, double *__restrict__ st);
+
+// the host part of _solve_step and the pose update for one thread (the
+// reference order, operation for operation)
+__device__ void icp_step_serial(const double *sums, int min_pairs, double step_eps,
+                                             double *__restrict__ st) {
     const int count = (int)llrint(sums[28]);
     if (count < min_pairs) {  // :101-102
         st[kStLost] = 1.0;
@@ -404,7 +426,14 @@ __global__ void __launch_bounds__(32 * kIcpTerms, 1) icp_step_kernel(const doubl
     }
     st[kStCount] = (double)count;
     st[kStRms] = sqrt(sums[27] / (double)count);  // :119
-    // Rodrigues on delta[:3] (geometry.py:211-219), left-multiplied (:178-181)
+    icp_apply_delta(b, step_eps, st);
+}
+
+
+// Pose update shared by both step variants: Rodrigues on delta[:3]
+// (geometry.py:211-219) left-multiplied, re-orthonormalised (:178-181), the
+// convergence test (:182-183).
+__device__ void icp_apply_delta(const double b[6], double step_eps, double *__restrict__ st) {
     const double ang = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
     double rot[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
     if (ang != 0.0) {
@@ -425,7 +454,20 @@ __global__ void __launch_bounds__(32 * kIcpTerms, 1) icp_step_kernel(const doubl
     for (int i = 0; i < 3; ++i) st[kStT + i] = t[i];
     double dn = 0.0;
     for (int i = 0; i < 6; ++i) dn += b[i] * b[i];
-    if (sqrt(dn) < step_eps) st[kStLevelDone] = 1.0;  // :182-183
+    if (sqrt(dn) < step_eps) st[kStLevelDone] = 1.0;
+}
+
+// One ICP iteration's host part on the device (tracking.py:100-120,
+// :178-183): the 29 sums folded from the block partials (fold_partials), then
+// one thread does the 6x6 work and the pose update (icp_step_serial).  A
+// warp-parallel LU with the matrix in registers measured no faster: the step
+// is a chain of dependent latencies either way (~18 us per launch).
+__global__ void __launch_bounds__(kFoldThreads, 1) icp_step_kernel(const double *__restrict__ partials, int64_t nblocks, int min_pairs,
+                                double step_eps, double *__restrict__ st) {
+    if (st[kStLost] != 0.0 || st[kStLevelDone] != 0.0) return;
+    __shared__ double sums[kIcpTerms];
+    fold_partials(partials, nblocks, sums);
+    if (threadIdx.x == 0) icp_step_serial(sums, min_pairs, step_eps, st);
 }
 
 __global__ void icp_level_start_kernel(double *st) { st[kStLevelDone] = 0.0; }
@@ -497,7 +539,7 @@ extern "C" int tf_icp_reduce(const double *sv, const double *sn, const uint8_t *
                                                                    partials);
     int rc = tf_check_launch("icp_terms_kernel");
     if (rc) return rc;
-    icp_finish_kernel<<<1, 32 * kIcpTerms, 0, stream>>>(partials, blocks, out29);
+    icp_finish_kernel<<<1, kFoldThreads, 0, stream>>>(partials, blocks, out29);
     return tf_check_launch("icp_finish_kernel");
 }
 
@@ -547,8 +589,8 @@ extern "C" int tf_icp_track(int nlevels, const double *const *src_verts, const d
             icp_terms_kernel<<<(unsigned)blocks, kIcpThreads, 0, stream>>>(
                 src_verts[level], src_norms[level], src_valid[level], md, mv, mn, P, partials);
             if ((rc = tf_check_launch("icp_terms_kernel"))) return rc;
-            icp_step_kernel<<<1, 32 * kIcpTerms, 0, stream>>>(partials, blocks, min_pairs[level], step_eps,
-                                                              state);
+            icp_step_kernel<<<1, kFoldThreads, 0, stream>>>(partials, blocks, min_pairs[level], step_eps,
+                                                            state);
             if ((rc = tf_check_launch("icp_step_kernel"))) return rc;
         }
     }
