@@ -33,11 +33,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _setup(nframes=4):
+def _setup(nframes=4, grid=(3.0, 124, 62)):
     import paper_1511_07106_b200 as tf
     from paper_1511_07106_b200.synth import demo_scene
     intr = tf.CameraIntrinsics(131.25, 131.25, 79.5, 59.5, 160, 120)
-    spec = tf.init_grid(3.0, 124, 62)  # 8 tiles of 64^3
+    spec = tf.init_grid(*grid)  # default: 8 tiles of 64^3; (3.0, 254, 254): config 1's one 256^3
     params = tf.FusionParams.for_voxel_size(spec.voxel_size)
     poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 24)
     frames = [torch.from_numpy(demo_scene().render_depth(p, intr).data.astype(np.float64)).cuda()
@@ -52,11 +52,11 @@ def _init(rank, world, port):
     torch.cuda.set_device(0)
 
 
-def _shard_worker(rank, world, port, retile, rebalance_every, out):
+def _shard_worker(rank, world, port, retile, rebalance_every, out, grid=(3.0, 124, 62)):
     _init(rank, world, port)
     try:
         from paper_1511_07106_b200.distributed import ShardedFusion
-        tf, intr, spec, params, poses, frames = _setup()
+        tf, intr, spec, params, poses, frames = _setup(grid=grid)
         shard = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length, params,
                               intr, rank, world, retile=retile, rebalance_every=rebalance_every)
         for f, p in zip(frames, poses):
@@ -71,17 +71,17 @@ def _shard_worker(rank, world, port, retile, rebalance_every, out):
         dist.destroy_process_group()
 
 
-def _run(world, retile, rebalance_every=0):
+def _run(world, retile, rebalance_every=0, grid=(3.0, 124, 62)):
     mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
-    mp.spawn(_shard_worker, args=(world, _free_port(), retile, rebalance_every, out), nprocs=world,
+    mp.spawn(_shard_worker, args=(world, _free_port(), retile, rebalance_every, out, grid), nprocs=world,
              join=True)
     return [out[r] for r in range(world)]
 
 
-def _single(retile):
+def _single(retile, grid=(3.0, 124, 62)):
     from paper_1511_07106_b200.distributed import ShardedFusion
-    tf, intr, spec, params, poses, frames = _setup()
+    tf, intr, spec, params, poses, frames = _setup(grid=grid)
     s = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length, params, intr,
                       0, 1, retile=retile)
     for f, p in zip(frames, poses):
@@ -89,17 +89,20 @@ def _single(retile):
     return s, [m.distance_dev.cpu(), m.vertices_dev.cpu(), m.normals_dev.cpu()], params
 
 
-@pytest.mark.parametrize("rebalance_every", [0, 1])
-def test_retiled_two_ranks(rebalance_every):
-    ranks = _run(2, 2, rebalance_every)
-    sub, sub_model, _ = _single(2)
-    whole, whole_model, params = _single(1)
+@pytest.mark.parametrize("rebalance_every,grid", [(0, (3.0, 124, 62)), (1, (3.0, 124, 62)),
+                                                   (1, (3.0, 254, 254))])
+def test_retiled_two_ranks(rebalance_every, grid):
+    """(3.0, 254, 254) is config 1's one 256^3 tile split into 8 sub-tiles of
+    129^3, the others 8 tiles of 64^3 into 64 of 33^3."""
+    ranks = _run(2, 2, rebalance_every, grid)
+    sub, sub_model, _ = _single(2, grid)
+    whole, whole_model, params = _single(1, grid)
     # every sub-tile is owned once, and its voxels are the untiled tile's
     got_tiles = {}
     for r in ranks:
         assert not set(r["tiles"]) & set(got_tiles)
         got_tiles.update(r["tiles"])
-    assert len(got_tiles) == len(sub.units) == 64
+    assert len(got_tiles) == len(sub.units) == 8 * len(whole.units)
     m = ranks[0]["unit_n"]
     n = whole.unit_n
     for key, vox in got_tiles.items():
