@@ -304,13 +304,23 @@ def run_ours(args) -> None:
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     sched = timed_frames(args.steps)
+    # at N > 1 every timed step includes the frame's broadcast from rank 0
+    # (NCCL over NVLink) into the ranks' frame buffer
+    from paper_1511_07106_b200.distributed import broadcast_frame
+    frame_buf = torch.empty_like(dev_frames[0])
     with ClockSampler(local) as clocks:
         barrier()
         t0 = time.perf_counter()
         for s, i in enumerate(sched):
             flush.zero_()
             starts[s].record()
-            shard.step(dev_frames[i], poses[i])
+            if world > 1:
+                if rank == 0:
+                    frame_buf.copy_(dev_frames[i])
+                broadcast_frame(frame_buf)
+                shard.step(frame_buf, poses[i])
+            else:
+                shard.step(dev_frames[i], poses[i])
             stops[s].record()
         barrier()
         t1 = time.perf_counter()
