@@ -769,16 +769,14 @@ def run_config5(args, torch, nat, barrier, cpu: bool) -> dict:
             counts.append((vset.files_read, vset.files_written))
         torch.cuda.synchronize()
         sec = time.perf_counter() - t0
-        run.counts = counts
         moved = (vset.link_bytes_read - b0[0]) + (vset.link_bytes_written - b0[1])
         nf = len(frame_ids) - 1
         return vset, {"frames_per_s": nf / sec,
                       "voxel_updates_per_s": int(stats[nat.STAT_VOXEL_UPDATES].item()) / sec,
-                      "link_bytes_per_frame": moved / nf, "link_gbs": moved / sec / 1e9}
+                      "link_bytes_per_frame": moved / nf, "link_gbs": moved / sec / 1e9}, counts
 
-    exact_set, exact = run("host")
-    schedule = run.counts
-    packed_set, packed = run("host_packed")
+    exact_set, exact, schedule = run("host")
+    packed_set, packed, _ = run("host_packed")
     ref_schedule = reference_spill_schedule(mine, len(frame_ids))
     tau = params.truncation
     err, wdiff = 0.0, 0
