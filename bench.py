@@ -72,7 +72,7 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extra", action="store_true", help="skip the config1/2/4/5 legs")
     p.add_argument("--no-numba", action="store_true", help="reference arm: skip the numba sample")
-    p.add_argument("--only", choices=["config1", "config2", "config4", "config5"],
+    p.add_argument("--only", choices=["config1", "config2", "config4", "config5", "scaling_projection"],
                    help="run just this extra leg (debugging)")
     return p.parse_args()
 
@@ -128,14 +128,17 @@ SCHEDULE_DESC = ("one untimed lap over the 64 orbit frames, W warm-up frames, th
                  "spread uniformly over the orbit (floor(s*64/K)); identical in both arms")
 
 
-def config_desc(n_gpus: int, retile: int = 1) -> dict:
+def config_desc(n_gpus: int, retile: int = 1, mode: str = "volumes") -> dict:
     d = {"workload": "configs[2]: 8 fixed 512^3 TSDF volumes at 4 mm (init_grid(4.08, 1020, 510)), "
                      "640x480 demo-scene orbit frames, ground-truth poses; step = integrate + "
                      "raycast of every volume",
          "volumes": 8, "voxels_per_side": 512, "voxel_size_m": 0.004, "image": "640x480",
          "frames": SCHEDULE_DESC,
          "l2": "flushed between timed steps (256 MiB write); volumes 8.6 GB > L2"}
-    if n_gpus > 1:
+    if n_gpus > 1 and mode == "replicated":
+        d["ownership"] = (f"replicated: every rank holds and integrates the 8 volumes and traces every "
+                          f"{n_gpus}th 8-pixel block row over all of them; partial maps merged by _hit_wins")
+    elif n_gpus > 1:
         d["ownership"] = (f"each 512^3 tile re-tiled into {retile}^3 sub-tiles (2-voxel overlap), "
                           f"sub-tiles owned by {n_gpus} ranks by balanced update counts")
     return d
@@ -287,7 +290,7 @@ def run_ours(args) -> None:
 
     retile = default_retile(world)
     shard = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length, params,
-                          intr, rank, world, retile=retile)
+                          intr, rank, world, retile=retile, mode=os.environ.get("TFB200_SHARD_MODE", "auto"))
 
     # ---- untimed lap (builds the map) + warm-up ----
     for i in range(LAP):
@@ -332,7 +335,8 @@ def run_ours(args) -> None:
     st = shard.stats.cpu().numpy()
     updates_local = int(st[nat.STAT_VOXEL_UPDATES])
     ms_total = max_over_ranks(ms_total)
-    updates = sum_over_ranks(updates_local)
+    # replicated mode integrates every volume on every rank: count once
+    updates = updates_local if shard.replicated else sum_over_ranks(updates_local)
     samples = sum_over_ranks(int(st[nat.STAT_RAY_SAMPLES]))
     ms_per_step = ms_total / args.steps
     fps = 1000.0 / ms_per_step
@@ -383,13 +387,16 @@ def run_ours(args) -> None:
     def per_frame(stat):
         return sum_over_ranks(int(st[stat])) / args.steps
 
+    def per_frame_int(stat):  # integration counters: every rank integrates everything when replicated
+        return (int(st[stat]) if shard.replicated else sum_over_ranks(int(st[stat]))) / args.steps
+
     result = {
         "metric": METRIC, "value": value, "unit": "voxel-updates/s",
         "frames_per_s": fps, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(config_desc(world, retile), **({"raymap_exchange": {
+        "config": dict(config_desc(world, retile, shard.mode), **({"raymap_exchange": {
             "p2p": "peer-memory reduce kernel (csrc/comm.cu, CUDA IPC over NVLink)",
             "collective": "NCCL row-block all-to-all + merge + all-gather"}[shard.exchange]}
             if world > 1 else {})),
@@ -412,17 +419,17 @@ def run_ours(args) -> None:
         "breakdown_ms_per_step": {"integrate_update_kernel": upd_ms / args.steps,
                                   "integrate_total": int_ms / args.steps,
                                   "raycast": ray_ms / args.steps},
-        "integrate": {"noop_updates_per_frame": per_frame(nat.STAT_NOOP_UPDATES),
-                      "swept_voxels_per_frame": per_frame(nat.STAT_SWEPT_VOXELS),
-                      "exact_path_voxels_per_frame": per_frame(nat.STAT_EXACT_VOXELS),
-                      "column_rejected_per_frame": per_frame(nat.STAT_COL_SKIPPED),
-                      "depth_rejected_per_frame": per_frame(nat.STAT_DEPTH_SKIPPED),
-                      "active_bricks_per_frame": per_frame(nat.STAT_ACTIVE_BRICKS),
-                      "free_space_bricks_per_frame": per_frame(nat.STAT_FREE_BRICKS),
-                      "general_bricks_all_free_per_frame": per_frame(nat.STAT_GENERAL_ALL_FREE),
-                      "general_parts_all_free_per_frame": per_frame(nat.STAT_PART_ALL_FREE),
-                      "general_parts_all_skip_per_frame": per_frame(nat.STAT_PART_ALL_SKIP),
-                      "total_bricks": sum_over_ranks(int(st[nat.STAT_TOTAL_BRICKS])) // max(args.steps, 1)},
+        "integrate": {"noop_updates_per_frame": per_frame_int(nat.STAT_NOOP_UPDATES),
+                      "swept_voxels_per_frame": per_frame_int(nat.STAT_SWEPT_VOXELS),
+                      "exact_path_voxels_per_frame": per_frame_int(nat.STAT_EXACT_VOXELS),
+                      "column_rejected_per_frame": per_frame_int(nat.STAT_COL_SKIPPED),
+                      "depth_rejected_per_frame": per_frame_int(nat.STAT_DEPTH_SKIPPED),
+                      "active_bricks_per_frame": per_frame_int(nat.STAT_ACTIVE_BRICKS),
+                      "free_space_bricks_per_frame": per_frame_int(nat.STAT_FREE_BRICKS),
+                      "general_bricks_all_free_per_frame": per_frame_int(nat.STAT_GENERAL_ALL_FREE),
+                      "general_parts_all_free_per_frame": per_frame_int(nat.STAT_PART_ALL_FREE),
+                      "general_parts_all_skip_per_frame": per_frame_int(nat.STAT_PART_ALL_SKIP),
+                      "total_bricks": int(per_frame_int(nat.STAT_TOTAL_BRICKS))},
         "raycast": {"exact_samples_per_frame": per_frame(nat.STAT_EXACT_SAMPLES),
                     "certification_failures": sum_over_ranks(int(st[nat.STAT_CERT_FAILURES])),
                     "summary_certified_samples_per_frame": per_frame(nat.STAT_SUMMARY_SAMPLES),
@@ -452,7 +459,8 @@ def run_ours(args) -> None:
         torch.cuda.empty_cache()
     if world == 1 and not args.no_extra:
         for name, fn in (("config1", run_config1), ("config2", run_config2),
-                         ("config4", run_config4), ("config5", run_config5)):
+                         ("config4", run_config4), ("config5", run_config5),
+                         ("scaling_projection", run_scaling_projection)):
             if args.only and name != args.only:
                 continue
             print(f"bench: {name} leg, {torch.cuda.memory_allocated() / 1e9:.1f} GB allocated before",
@@ -536,7 +544,8 @@ def run_e2e(args, torch, nat, dist, rank, world, intr, spec, params, poses, host
     torch.cuda.synchronize()
     barrier()
     sec = max_over_ranks(time.perf_counter() - t0)
-    updates = sum_over_ranks(int(out[nat.STAT_VOXEL_UPDATES]) - before)
+    upd = int(out[nat.STAT_VOXEL_UPDATES]) - before
+    updates = upd if (pipe._shard is not None and pipe._shard.replicated) else sum_over_ranks(upd)
     del pipe
     return {"value": updates / sec, "unit": "voxel-updates/s", "frames_per_s": args.steps / sec,
             "h2d_bytes_per_step": int(host_frames[0].nbytes) if rank == 0 else 0,
@@ -804,6 +813,96 @@ def run_config5(args, torch, nat, barrier, cpu: bool) -> dict:
                                "how": "the unmodified reference VolumeSet (baseline/_ref) driven through the "
                                       "same acquire / release sequence on 8^3 stand-in tiles"},
             "bound": "host link (each frame moves every tile through the spill tier)"}
+
+
+def run_scaling_projection(args, torch, nat, barrier, cpu: bool) -> dict:
+    """A projection, not a measurement (this pool has one GPU): config 3
+    re-tiled and owned as N ranks would own it (distributed.retile,
+    balanced_owners on the work the culling stage measured over the lap),
+    then every timed frame runs each rank's share — integrate + raycast of its
+    sub-tiles into a partial map — one rank after the other on this GPU, with
+    CUDA events around each.  The frame's projected time is the slowest
+    rank's; the ray-map reduction (peer memory over NVLink, ~9 MB per rank per
+    frame) and the frame broadcast are not included."""
+    import paper_1511_07106_b200 as tf
+    from paper_1511_07106_b200.distributed import balanced_owners, default_retile, retile
+
+    intr, spec, params, poses, scene = workload()
+    host = render_frames(poses, intr)
+    frames = [torch.from_numpy(f).cuda() for f in host]
+    out = {"note": "projection from one GPU: per-rank shares timed one after the other; the exchange "
+                   "and the broadcast are not included; the driver's SCALE run measures the real thing"}
+    # replicated mode (ShardedFusion's default when the map fits): every rank
+    # integrates all 8 volumes and traces every n-th block row over them
+    tiles = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in spec.keys]
+    for i in range(LAP):
+        tf.integrate_volumes(tiles, frames[i], poses[i], intr, params)
+    torch.cuda.synchronize()
+    rep = {n: [] for n in (2, 4, 8)}
+    for i in timed_frames(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        tf.integrate_volumes(tiles, frames[i], poses[i], intr, params)
+        b.record()
+        ev = []
+        for n in (2, 4, 8):
+            for r in range(n):
+                c, d = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                rm = tf.RayMap.empty(intr)
+                c.record()
+                tf.raycast_volumes(tiles, poses[i], intr, rm, params, rows=(r, n))
+                d.record()
+                ev.append((n, r, c, d))
+        torch.cuda.synchronize()
+        t_int = a.elapsed_time(b)
+        for n in (2, 4, 8):
+            rep[n].append(t_int + max(c.elapsed_time(d) for m, r, c, d in ev if m == n))
+    for n in (2, 4, 8):
+        mean = sum(rep[n]) / len(rep[n])
+        out[f"replicated_n{n}"] = {"projected_ms_per_frame": mean, "projected_frames_per_s": 1000.0 / mean}
+    del tiles
+    torch.cuda.empty_cache()
+    for n in (2, 4, 8):
+        k = default_retile(n, spec.voxels_per_side)
+        units, m = retile(spec.keys, spec.voxels_per_side, spec.voxel_size, k)
+        counters = torch.zeros((len(units), 2), dtype=torch.int64, device="cuda")
+        tiles = []
+        for u, key in enumerate(units):
+            t = tf.TsdfSubvolume.empty(key, m, m * spec.voxel_size)
+            t.counters = counters[u]
+            tiles.append(t)
+        for i in range(LAP):
+            tf.integrate_volumes(tiles, frames[i], poses[i], intr, params)
+        c = counters.to(torch.float64)
+        costs = (c[:, 0] * 4.0 + c[:, 1]).cpu().tolist()
+        owners = balanced_owners(costs, n)
+        shares = [[tiles[u] for u in range(len(units)) if owners[u] == r] for r in range(n)]
+        torch.cuda.synchronize()
+        per_frame = []
+        per_rank = [0.0] * n
+        for i in timed_frames(args.steps):
+            times = []
+            for r in range(n):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                rm = tf.RayMap.empty(intr)
+                a.record()
+                tf.integrate_volumes(shares[r], frames[i], poses[i], intr, params)
+                tf.raycast_volumes(shares[r], poses[i], intr, rm, params)
+                b.record()
+                times.append((a, b))
+            torch.cuda.synchronize()
+            ms = [a.elapsed_time(b) for a, b in times]
+            per_frame.append(max(ms))
+            for r in range(n):
+                per_rank[r] += ms[r] / len(timed_frames(args.steps))
+        mean = sum(per_frame) / len(per_frame)
+        out[f"volumes_n{n}"] = {"retile": k, "sub_tiles": len(units), "sub_tile_voxels": m,
+                        "projected_ms_per_frame": mean, "projected_frames_per_s": 1000.0 / mean,
+                        "per_rank_ms": per_rank,
+                        "imbalance_max_over_mean": max(per_rank) / (sum(per_rank) / n)}
+        del tiles, shares, counters
+        torch.cuda.empty_cache()
+    return out
 
 
 def reference_spill_schedule(keys, nframes):

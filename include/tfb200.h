@@ -218,6 +218,16 @@ int tf_raycast_ws(const TfVolume *vols, int nvol, const TfCamera *cam, double ta
                   int64_t coarse_step, const double r_wc[9], const double cam_center[3],
                   double *dist_dev, double *vert_dev, double *norm_dev, void *workspace_dev,
                   size_t workspace_bytes, uint64_t *stats_dev, void *stream);
+/* tf_raycast_ws over a subset of the image: only the rows of the 8-pixel
+ * block rows ty with ty % row_mod == row_rem are traced (the others are left
+ * as they are) — the image-partitioned raycast of the replicated multi-GPU
+ * mode, where every rank holds every volume and traces 1/row_mod of the
+ * rows; the ranks' maps merge into the full-image result bit for bit. */
+int tf_raycast_rows(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
+                    int64_t coarse_step, const double r_wc[9], const double cam_center[3],
+                    double *dist_dev, double *vert_dev, double *norm_dev, void *workspace_dev,
+                    size_t workspace_bytes, int row_mod, int row_rem, uint64_t *stats_dev,
+                    void *stream);
 
 /* ---- trilinear_sample (tsdf.py:147-153 / _kernels._sample :28-68) for
  * `npoints` world points (f64 [N][3]); writes value and validity per point. */

@@ -103,6 +103,8 @@ _SIGNATURES = {
     "tf_raycast_workspace_size": (_c_sz, [_c_int, _CAM]),
     "tf_raycast_ws": (_c_int, [_VOL, _c_int, _CAM, _c_d, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
                                _c_p, _c_sz, _c_p, _c_p]),
+    "tf_raycast_rows": (_c_int, [_VOL, _c_int, _CAM, _c_d, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                 _c_p, _c_sz, _c_int, _c_int, _c_p, _c_p]),
     "tf_trilinear_sample": (_c_int, [_VOL, _c_p, _c_i64, _c_p, _c_p, _c_p]),
     "tf_good_threshold": (ctypes.c_float, [_c_d]),
     "tf_brick_summary": (_c_int, [_VOL, _c_p]),

@@ -36,6 +36,7 @@ struct RayGeom {
     int lane0_only;      // TF_DEBUG_LANE0_ONLY: only lane 0 of each warp traces (timing studies)
     float good_t;        // brick-summary threshold for this tau
     int uniform_vs;      // every volume of the launch has the same voxel size
+    int row_mod, row_rem;  // trace only the block rows ty with ty % row_mod == row_rem
 };
 
 struct Hit {
@@ -746,8 +747,10 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
     const int64_t px = (int64_t)blockIdx.x * kBX + (w % (kBX / 8)) * 8 + (lane & 7);
     // tile rows are dispatched centre-out: rays near the image centre row run
     // longest in typical scenes, so they start first and the tail is short
+    // block rows are dispatched centre-out over this launch's subset of rows
+    // (every row_mod-th from row_rem; all rows by default)
     const int by = (int)blockIdx.y, mid = (int)(gridDim.y >> 1);
-    const int ty = (by & 1) ? mid - ((by + 1) >> 1) : mid + (by >> 1);
+    const int ty = g.row_rem + g.row_mod * ((by & 1) ? mid - ((by + 1) >> 1) : mid + (by >> 1));
     const int64_t py = (int64_t)ty * kBY + (w / (kBX / 8)) * 4 + (lane >> 3);
     unsigned long long samples = 0, hits = 0, exact_samples = 0;
     if (px < g.width && py < g.height && !(g.lane0_only && lane != 0)) {
@@ -1476,7 +1479,7 @@ extern "C" size_t tf_raycast_workspace_size(int nvol, const TfCamera *cam) {
 static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
                         int64_t coarse_step, const double r_wc[9], const double cam_center[3],
                         double *dist, double *vert, double *norm, void *workspace,
-                        size_t workspace_bytes, uint64_t *stats, void *stream_);
+                        size_t workspace_bytes, uint64_t *stats, void *stream_, int row_mod, int row_rem);
 
 extern "C" int tf_raycast_ws(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
                              int64_t coarse_step, const double r_wc[9], const double cam_center[3],
@@ -1484,7 +1487,19 @@ extern "C" int tf_raycast_ws(const TfVolume *vols, int nvol, const TfCamera *cam
                              size_t workspace_bytes, uint64_t *stats, void *stream_) {
     if (!workspace && nvol > 0) return tf_set_error(TF_EINVAL, "tf_raycast_ws: null workspace");
     return raycast_impl(vols, nvol, cam, tau, coarse_step, r_wc, cam_center, dist, vert, norm,
-                        workspace, workspace_bytes, stats, stream_);
+                        workspace, workspace_bytes, stats, stream_, 1, 0);
+}
+
+extern "C" int tf_raycast_rows(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
+                               int64_t coarse_step, const double r_wc[9], const double cam_center[3],
+                               double *dist, double *vert, double *norm, void *workspace,
+                               size_t workspace_bytes, int row_mod, int row_rem, uint64_t *stats,
+                               void *stream_) {
+    if (!workspace && nvol > 0) return tf_set_error(TF_EINVAL, "tf_raycast_rows: null workspace");
+    if (row_mod < 1 || row_rem < 0 || row_rem >= row_mod)
+        return tf_set_error(TF_EINVAL, "tf_raycast_rows: bad row subset");
+    return raycast_impl(vols, nvol, cam, tau, coarse_step, r_wc, cam_center, dist, vert, norm,
+                        workspace, workspace_bytes, stats, stream_, row_mod, row_rem);
 }
 
 extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
@@ -1492,13 +1507,13 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
                           double *dist, double *vert, double *norm, uint64_t *stats,
                           void *stream_) {
     return raycast_impl(vols, nvol, cam, tau, coarse_step, r_wc, cam_center, dist, vert, norm,
-                        nullptr, 0, stats, stream_);
+                        nullptr, 0, stats, stream_, 1, 0);
 }
 
 static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
                         int64_t coarse_step, const double r_wc[9], const double cam_center[3],
                         double *dist, double *vert, double *norm, void *workspace,
-                        size_t workspace_bytes, uint64_t *stats, void *stream_) {
+                        size_t workspace_bytes, uint64_t *stats, void *stream_, int row_mod, int row_rem) {
     cudaStream_t stream = (cudaStream_t)stream_;
     if (nvol == 0) return TF_OK;
     if (!vols || nvol < 0 || !cam || !r_wc || !cam_center || !dist || !vert || !norm)
@@ -1519,6 +1534,8 @@ static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, dou
     g.exact_only = (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) ? 1 : 0;
     g.lane0_only = (tf_debug_flags() & TF_DEBUG_LANE0_ONLY) ? 1 : 0;
     g.good_t = good_threshold(tau);
+    g.row_mod = row_mod;
+    g.row_rem = row_rem;
     g.uniform_vs = 1;
     for (int v = 1; v < nvol; ++v)
         if (vols[v].voxel_size != vols[0].voxel_size) g.uniform_vs = 0;
@@ -1547,8 +1564,18 @@ static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, dou
         // 8 (config 3, 8 volumes: 1.4 M cycles optimal, 2.0 M 30 % slower;
         // config 4, 16 volumes: 1.4 M -> 1.90 ms, 2.0 M -> 1.45, 2.5 M -> 1.49,
         // 2.8 M -> 1.54, 4 M -> 1.70 ms)
-        const long long budget =
-            vt.count > 8 ? (long long)((double)base_budget * sqrt(vt.count / 8.0)) : base_budget;
+        static const double row_exp = [] {
+            const char *e = getenv("TFB200_RAY_ROW_EXP");  // tuning knob (A/B): budget ~ row_mod^-exp
+            return e ? atof(e) : 0.5;
+        }();
+        // a launch over 1/row_mod of the rows ends sooner: its budget shrinks
+        // with it, or its slowest warps (not the rows' work) set its length
+        // (projected replicated-mode rates at 2 / 4 / 8 ranks, exponent 1.0:
+        // 836 / 326 / 242 frames/s — the cooperative pass drowns; 0.7: 948 /
+        // 783 / 653; 0.5: 896 / 954 / 929; 0: 782 / 788 / 790)
+        const long long budget = (long long)(
+            (vt.count > 8 ? (double)base_budget * sqrt(vt.count / 8.0) : (double)base_budget) /
+            pow((double)g.row_mod, row_exp));
         const bool coop_all = (tf_debug_flags() & TF_DEBUG_COOP_ALL) != 0;
         unsigned long long *st = (unsigned long long *)stats;
         int64_t *clk = tf_ray_clock_buffer();
@@ -1568,7 +1595,9 @@ static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, dou
         if (!rescue || cudaMemsetAsync(rescue, 0, sizeof(unsigned), stream) != cudaSuccess)
             return tf_set_error(TF_ECUDA, "tf_raycast: cannot allocate the rescue list");
         auto launch = [&](auto kern, int bx, int by) {
-            dim3 grid((unsigned)((cam->width + bx - 1) / bx), (unsigned)((cam->height + by - 1) / by));
+            const int rows = (int)((cam->height + by - 1) / by);  // block rows of the image
+            dim3 grid((unsigned)((cam->width + bx - 1) / bx),
+                      (unsigned)((rows - g.row_rem + g.row_mod - 1) / g.row_mod));
             kern<<<grid, bx * by, 0, stream>>>(vt, g, dist, vert, norm, st, clk, rescue + 1, rescue,
                                                coop_all ? 1ll : budget);
         };

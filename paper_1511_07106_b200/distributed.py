@@ -409,6 +409,15 @@ def move_units(moves: Sequence[tuple], rank: int, payloads: dict, alloc: Callabl
     return out
 
 
+def fits_replicated(ntiles: int, voxels_per_side: int, color: bool = False, share: float = 0.4) -> bool:
+    """Whether every rank can hold the whole map: its voxels (8 B, + 4 B of
+    colour) within ``share`` of this GPU's memory."""
+    per = 8 + (4 if color else 0)
+    need = ntiles * voxels_per_side ** 3 * per
+    total = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory
+    return need <= share * total
+
+
 WORK_GENERAL_BRICK = 4.0  # relative cost of a general brick vs a certified free-space one
 
 
@@ -431,22 +440,37 @@ class ShardedFusion:
     collective; a migration moves 8 B per voxel of the moved sub-tiles.
     """
 
+    MODES = ("auto", "volumes", "replicated")
+
     def __init__(self, keys: Sequence, voxels_per_side: int, side_length: float,
                  params: FusionParams, intr: CameraIntrinsics, rank: int = 0, world: int = 1,
                  group=None, color: bool = False, exchange: str = "auto", retile: int = 1,
-                 rebalance_every: int = 8) -> None:
+                 rebalance_every: int = 8, mode: str = "volumes") -> None:
         if exchange not in ("auto", "p2p", "collective"):
             raise ValueError(f"exchange must be 'auto', 'p2p' or 'collective', not {exchange!r}")
+        if mode not in self.MODES:
+            raise ValueError(f"mode must be one of {self.MODES}, not {mode!r}")
         self.rank, self.world, self.group = rank, world, group
         self.params, self.intr = params, intr
         self.parent_keys = [tuple(int(x) for x in k) for k in keys]
         vs = side_length / voxels_per_side
         self.voxel_size = vs
+        if mode == "auto":
+            mode = "replicated" if world > 1 and fits_replicated(len(keys), voxels_per_side, color) else "volumes"
+        # replicated: every rank holds and integrates every tile and traces
+        # 1/world of the image rows over all of them — each pixel is traced
+        # over every volume by exactly one rank, so the merged model is the
+        # single-GPU one bit for bit (and occluded volumes are skipped as on
+        # one GPU); volumes: the tiles, re-tiled, are owned by the ranks
+        self.mode = mode if world > 1 else "volumes"
+        self.replicated = self.mode == "replicated"
+        if self.replicated:
+            retile = 1
         self.units, self.unit_n = _retile(self.parent_keys, voxels_per_side, vs, retile)
         self.retile_k = retile
         self.color = color
-        self.owner = initial_owners(self.units, world)
-        self.rebalance_every = rebalance_every if world > 1 else 0
+        self.owner = [rank] * len(self.units) if self.replicated else initial_owners(self.units, world)
+        self.rebalance_every = rebalance_every if world > 1 and not self.replicated else 0
         self._dev = torch.device("cuda", torch.cuda.current_device())
         self._tiles: dict[int, TsdfSubvolume] = {}
         # per-unit work counters (general, free bricks), one row per unit
@@ -550,7 +574,7 @@ class ShardedFusion:
             raise ValueError("dynamic tiles are not re-tiled")
         key = tuple(int(x) for x in key)
         counts = [self.owner.count(r) for r in range(self.world)]
-        r = min(range(self.world), key=lambda q: (counts[q], q))
+        r = self.rank if self.replicated else min(range(self.world), key=lambda q: (counts[q], q))
         self.units.append(key)
         self.owner.append(r)
         c = torch.zeros((len(self.units), 2), dtype=torch.int64, device=self._dev)
@@ -581,6 +605,9 @@ class ShardedFusion:
 
     def balance_report(self) -> dict:
         """Per-rank share of the last measured work (collective)."""
+        if self.replicated:
+            return {"mode": "replicated", "tiles": len(self.units),
+                    "rows": f"block rows b with b % {self.world} == rank (8-pixel rows)"}
         costs = self._last_costs if self._last_costs is not None else self.unit_costs()
         load = [0.0] * self.world
         for u, c in enumerate(costs):
@@ -608,7 +635,8 @@ class ShardedFusion:
         self._integrator(self.tiles, depth, pose, self.intr, self.params, self.stats, color=color,
                          depth_ready=depth_ready)
         self.partial.reset()
-        raycast_volumes(self.tiles, pose, self.intr, self.partial, self.params, self.stats)
+        raycast_volumes(self.tiles, pose, self.intr, self.partial, self.params, self.stats,
+                        rows=(self.rank, self.world) if self.replicated else None)
         if self.world == 1:
             self.model, self.partial = self.partial, self.model
             return self.model

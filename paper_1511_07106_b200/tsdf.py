@@ -539,8 +539,11 @@ def coarse_step(params: FusionParams, voxel_size: float) -> int:
 
 def raycast_volumes(volumes: Sequence[TsdfSubvolume], pose: Pose, intr: CameraIntrinsics,
                     raymap: RayMap, params: FusionParams,
-                    stats: torch.Tensor | None = None) -> RayMap:
+                    stats: torch.Tensor | None = None, rows: tuple[int, int] | None = None) -> RayMap:
     """Render every volume into ``raymap`` with one fused launch.
+
+    ``rows`` = (rank, world): trace only the 8-pixel block rows b with
+    b % world == rank (tf_raycast_rows; the rest of the map is untouched).
 
     Volumes are grouped by coarse stride (the reference computes it per
     volume, tsdf.py:207); the merge is order-free so grouping is exact.
@@ -567,10 +570,17 @@ def raycast_volumes(volumes: Sequence[TsdfSubvolume], pose: Pose, intr: CameraIn
         # the cooperative pass's scratch: one workspace per stream (launches on
         # a stream are ordered; two streams never share one)
         ws = nat.workspace.get(L.tf_raycast_workspace_size(len(vols), cam), f"raycast{stream}")
-        nat.check(L.tf_raycast_ws(arr, len(vols), cam, float(params.truncation), int(coarse),
-                                  r, c, nat.ptr(raymap.distance_dev),
-                                  nat.ptr(raymap.vertices_dev), nat.ptr(raymap.normals_dev),
-                                  nat.ptr(ws), ws.numel(), nat.ptr(st), stream), "tf_raycast_ws")
+        if rows is None:
+            nat.check(L.tf_raycast_ws(arr, len(vols), cam, float(params.truncation), int(coarse),
+                                      r, c, nat.ptr(raymap.distance_dev),
+                                      nat.ptr(raymap.vertices_dev), nat.ptr(raymap.normals_dev),
+                                      nat.ptr(ws), ws.numel(), nat.ptr(st), stream), "tf_raycast_ws")
+        else:
+            nat.check(L.tf_raycast_rows(arr, len(vols), cam, float(params.truncation), int(coarse),
+                                        r, c, nat.ptr(raymap.distance_dev),
+                                        nat.ptr(raymap.vertices_dev), nat.ptr(raymap.normals_dev),
+                                        nat.ptr(ws), ws.numel(), int(rows[1]), int(rows[0]), nat.ptr(st),
+                                        stream), "tf_raycast_rows")
     raymap._device_written()
     return raymap
 

@@ -173,3 +173,37 @@ def test_pipeline_two_ranks_tracked(retile):
                 [x[1] for x in want["records"]][1:], rel=2e-3)
             assert np.abs(got["poses"] - want["poses"]).max() < 1e-6
     assert np.array_equal(out[0]["poses"], out[1]["poses"])  # replicated tracking agrees
+
+
+def _rep_worker(rank, world, port, out):
+    _init(rank, world, port)
+    try:
+        from paper_1511_07106_b200.distributed import ShardedFusion
+        tf, intr, spec, params, poses, frames = _setup()
+        shard = ShardedFusion(spec.keys, spec.voxels_per_side, spec.subvolume_side_length, params,
+                              intr, rank, world, mode="replicated")
+        assert shard.replicated and len(shard.tiles) == len(spec.keys)
+        for f, p in zip(frames, poses):
+            model = shard.step(f, p)
+        torch.cuda.synchronize()
+        out[rank] = [model.distance_dev.cpu(), model.vertices_dev.cpu(), model.normals_dev.cpu(),
+                     shard.tiles[3].voxels.cpu()]
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_replicated_mode_equals_one_process(world):
+    """Replicated mode: every rank integrates every volume and traces every
+    world-th block row over all of them; the merged model equals the
+    single-process raycast bit for bit (each pixel traced by one rank over all
+    volumes), and the ranks' volumes are identical."""
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.spawn(_rep_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    whole, whole_model, _ = _single(1)
+    assert torch.isfinite(whole_model[0]).sum().item() > 3000
+    for r in range(world):
+        for got, want in zip(out[r][:3], whole_model):
+            assert torch.equal(got, want)
+        assert torch.equal(out[r][3], whole.tiles[3].voxels.cpu())
