@@ -724,3 +724,50 @@ def test_split_integration_equals_one_call():
             assert torch.equal(x.brick_bad, y.brick_bad)
             assert torch.equal(x.brick_flags, y.brick_flags)
     assert float(b[0].voxels[..., 1].max()) > 0
+
+
+_HANDOVER_SCRIPT = r"""
+import torch, paper_1511_07106_b200 as tf
+from paper_1511_07106_b200 import _native as nat
+from paper_1511_07106_b200.synth import demo_scene
+intr = tf.RunConfig().intrinsics()
+spec = tf.init_grid(4.08, 1020, 510)
+params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+tiles = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in spec.keys]
+scene = demo_scene()
+poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)
+for pose in poses[:10]:
+    tf.integrate_volumes(tiles, scene.render_depth(pose, intr), pose, intr, params)
+lib = nat.load_library()
+stats = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
+for pose in (poses[4], poses[11], poses[30]):
+    fast = tf.RayMap.empty(intr)
+    tf.raycast_volumes(tiles, pose, intr, fast, params, stats)
+    exact = tf.RayMap.empty(intr)
+    lib.tf_set_debug_flags(nat.DEBUG_EXACT_ONLY)
+    tf.raycast_volumes(tiles, pose, intr, exact, params)
+    lib.tf_set_debug_flags(0)
+    assert torch.isfinite(exact.distance_dev).sum().item() > 30000
+    assert torch.equal(fast.distance_dev, exact.distance_dev)
+    assert torch.equal(fast.vertices_dev, exact.vertices_dev)
+    assert torch.equal(fast.normals_dev, exact.normals_dev)
+print("coop_rays", stats[nat.STAT_COOP_RAYS].item(), "cert_failures", stats[nat.STAT_CERT_FAILURES].item())
+"""
+
+
+@pytest.mark.parametrize("budget", [2000, 60000])
+def test_mid_march_handover_equals_exact_march(budget):
+    """Rays handed to the cooperative pass mid-march (tiny per-warp budgets) resume
+    from the per-lane march's state and still equal the exact march bit for bit."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TFB200_RAY_BUDGET=str(budget))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _HANDOVER_SCRIPT], env=env, cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    words = r.stdout.split()
+    coop = int(words[words.index("coop_rays") + 1])
+    assert coop > 5000, r.stdout          # the hand-over really happened, many times
+    assert int(words[words.index("cert_failures") + 1]) == 0
