@@ -293,10 +293,14 @@ def run_ours(args) -> None:
                           intr, rank, world, retile=retile, mode=os.environ.get("TFB200_SHARD_MODE", "auto"))
 
     # ---- untimed lap (builds the map) + warm-up ----
+    # resident frames have no pending producer (depth_ready=True): each step's
+    # culling half runs on the integrator's side stream next to the previous
+    # step's raycast, as in the pipeline; at N > 1 the broadcast is the
+    # producer (an event after it)
     for i in range(LAP):
-        shard.step(dev_frames[i], poses[i])
+        shard.step(dev_frames[i], poses[i], depth_ready=True)
     for i in warm_frames(args.warmup):
-        shard.step(dev_frames[i], poses[i])
+        shard.step(dev_frames[i], poses[i], depth_ready=True)
     barrier()
 
     # ---- timed region: resident inputs, per-step events, L2 flushed between ----
@@ -321,9 +325,11 @@ def run_ours(args) -> None:
                 if rank == 0:
                     frame_buf.copy_(dev_frames[i])
                 broadcast_frame(frame_buf)
-                shard.step(frame_buf, poses[i])
+                arrived = torch.cuda.Event()
+                arrived.record()
+                shard.step(frame_buf, poses[i], depth_ready=arrived)
             else:
-                shard.step(dev_frames[i], poses[i])
+                shard.step(dev_frames[i], poses[i], depth_ready=True)
             stops[s].record()
         barrier()
         t1 = time.perf_counter()
