@@ -915,6 +915,15 @@ constexpr int kZBatch = 4;  // voxels in flight per thread
 // batches, so a warp instruction touches four 64-byte rows.  Column-level
 // work (float64 base, error bounds, whole-column rejection) is amortised over
 // the column; per voxel the screen is ~25 float32 instructions.
+//
+// kClassify: the screen alone.  No voxel is read or written: the decisions
+// depend only on the frame (depth tables) and the geometry, so this runs in
+// tf_integrate_prepare, next to the previous frame's raycast.  Each lane
+// stores one word per brick (masks[32 i + lane]): bit hy*8 + z = a
+// free-space update of voxel (x, y_base + 4 hy, z0 + z); bit 16 + hy*8 + z
+// = an undecided voxel the full queue could not take (exact, in place, by
+// brick_apply_kernel); undecided voxels go to the exact queue as here.
+template <bool kClassify>
 __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
     const __grid_constant__ FrameGeom f, const double2 *__restrict__ table,
@@ -922,7 +931,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     const unsigned int *__restrict__ active_count, unsigned long long *__restrict__ queue,
     unsigned long long *__restrict__ queue_count, const unsigned long long queue_cap,
     const int fixed_point, unsigned long long *__restrict__ stats, const ChangedList changed,
-    const uint8_t *__restrict__ part_class) {
+    const uint8_t *__restrict__ part_class, uint32_t *__restrict__ masks) {
     __shared__ double2 rcp[257];
     fill_rcp(rcp);
     const unsigned count = *active_count;
@@ -973,6 +982,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
         const bool keep = keeps_summary(vol, f);
         unsigned dbad = 0;  // change of this brick's packed state (summary)
         unsigned brick_free = 0, brick_vox = 0;  // free-space class / voxels of this brick (lane)
+        uint32_t fmask = 0;  // kClassify: this lane's word
 #pragma unroll 1
         for (int hy = 0; hy < 2; ++hy) {
             const unsigned y = y_base + 4 * hy;
@@ -1043,6 +1053,14 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                     continue;
                 }
                 if (pc == 2u) {  // certified: every voxel of the part is a free-space update
+                    if (kClassify) {
+                        if (row_in) {
+                            fmask |= ((1u << nzb) - 1u) << (8 * hy + zb);
+                            brick_free += nzb;
+                        }
+                        ++part_free;
+                        continue;
+                    }
                     const size_t row = ((size_t)(z0 + zb) * n + y) * n + x;
                     if (!TF_IN_BOUNDS(!row_in || nzb == 0u || row + (size_t)(nzb - 1) * n * n < (size_t)n * n * n))
                         continue;
@@ -1131,6 +1149,16 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                     depth_skipped += c == kSkip;
                     cls[j] = c;
                 }
+                if (kClassify) {
+#pragma unroll
+                    for (int j = 0; j < kZBatch; ++j) {
+                        if (cls[j] == kFree) {
+                            fmask |= 1u << (8 * hy + zb + j);
+                            ++brick_free;
+                        }
+                        if (cls[j] == kExact) exact_mask |= 1u << (zb + j);
+                    }
+                } else {
                 // D: load the voxels with a free-space update
                 const size_t row = ((size_t)(z0 + zb) * n + y) * n + x;
                 float2 old[kZBatch];
@@ -1154,6 +1182,7 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                         }
                     }
                     if (cls[j] == kExact) exact_mask |= 1u << (zb + j);
+                }
                 }
                 if (stats) {  // the batch is one 8x4x4 part of the brick
                     bool lf = true, ls = true;
@@ -1193,6 +1222,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                         // (volume, z, y, x) packed 6 / 16 / 16 / 16 bits (n <= 65535)
                         queue[base + k] = ((unsigned long long)vi << 48) | ((unsigned long long)(z0 + zz) << 32) |
                                           ((unsigned long long)y << 16) | x;
+                    } else if (kClassify) {  // queue full: brick_apply_kernel updates it in place
+                        fmask |= 1u << (16 + 8 * hy + zz);
                     } else {  // queue full: exact update in place (still exact)
                         const double gz = dmul((double)((int64_t)(z0 + zz) + vol.origin[2]), vs);
                         unsigned db = 0;
@@ -1203,7 +1234,8 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
                 }
             }
         }
-        if (keep) {  // one atomic per brick and warp
+        if (kClassify) masks[(size_t)i * 32 + lane] = fmask;
+        if (keep && !kClassify) {  // one atomic per brick and warp
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
             if (lane == 0 && dbad) {
@@ -1226,6 +1258,95 @@ __global__ void __launch_bounds__(256, 3) brick_update_kernel(
     }
 }
 
+// The voxel updates of the general bricks classified by
+// brick_update_kernel<true> in the prepare phase: the masked free-space
+// updates (and, only when the exact queue overflowed, the exact updates of
+// the voxels it could not take).  Streaming like brick_free_kernel: the
+// lane's 16 voxels' loads are issued before any update.
+__global__ void __launch_bounds__(256, 4) brick_apply_kernel(
+    const __grid_constant__ VolumeTable vt, const __grid_constant__ BrickTable bt,
+    const __grid_constant__ FrameGeom f, const double2 *__restrict__ table,
+    const uint32_t *__restrict__ active, const unsigned int *__restrict__ active_count,
+    const uint32_t *__restrict__ masks, const int fixed_point, unsigned long long *__restrict__ stats,
+    const ChangedList changed) {
+    __shared__ double2 rcp[257];
+    fill_rcp(rcp);
+    const unsigned count = *active_count;
+    const int lane = threadIdx.x & 31;
+    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+    const float2 fixed = make_float2(f.tau32, (float)f.max_w);
+    unsigned updates = 0, nop = 0;
+    for (unsigned i = warp; i < count; i += nwarps) {
+        const uint32_t w = masks[(size_t)i * 32 + lane];
+        if (!__any_sync(0xffffffffu, w != 0u)) continue;
+        const unsigned g = active[i];
+        const int vi = find_volume(bt, g);
+        const TfVolume &vol = vt.vol[vi];
+        const unsigned n = (unsigned)vol.n, nb = (unsigned)bt.nb[vi];
+        const unsigned local = g - (unsigned)bt.offset[vi];
+        const unsigned bxy = local % (nb * nb);
+        const unsigned x = (bxy % nb) * kBrick + (lane & 7);
+        const unsigned z0 = (local / (nb * nb)) * kBrick;
+        const unsigned y_base = (bxy / nb) * kBrick + (lane >> 3);
+        float2 *vox = (float2 *)vol.voxels_dev;
+        const bool keep = keeps_summary(vol, f);
+        unsigned dbad = 0;
+#pragma unroll 1
+        for (int hy = 0; hy < 2; ++hy) {
+            const unsigned fm = (w >> (8 * hy)) & 0xffu;
+            if (!__any_sync(0xffffffffu, fm != 0u)) continue;
+            const size_t row = ((size_t)z0 * n + (y_base + 4 * hy)) * n + x;
+            float2 old[kBrick];
+#pragma unroll
+            for (int z = 0; z < kBrick; ++z) {
+                const bool on = (fm >> z) & 1u;
+                const size_t lin = row + (size_t)z * n * n;
+                old[z] = on && TF_IN_BOUNDS(lin < (size_t)n * n * n) ? vox[lin] : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int z = 0; z < kBrick; ++z) {
+                if (!((fm >> z) & 1u)) continue;
+                const size_t lin = row + (size_t)z * n * n;
+                if (!TF_IN_BOUNDS(lin < (size_t)n * n * n)) continue;
+                ++updates;
+                if (fixed_point && old[z].x == fixed.x && old[z].y == fixed.y) {
+                    ++nop;  // (tau32, max_w) is a host-verified fixed point
+                } else {
+                    const float2 nv = free_update(old[z], f, rcp);
+                    vox[lin] = nv;
+                    if (keep) dbad += free_state_delta(old[z], nv, f.good_t);
+                }
+            }
+        }
+        if (w >> 16) {  // the exact queue was full (rare): exact updates in place
+            const double vs = vol.voxel_size;
+            const double gx = dmul((double)((int64_t)x + vol.origin[0]), vs);
+            for (uint32_t m = w >> 16; m; m &= m - 1) {
+                const unsigned b = __ffs(m) - 1, hy = b >> 3, z = z0 + (b & 7u), y = y_base + 4 * hy;
+                const int64_t lin = ((int64_t)z * n + y) * n + x;
+                unsigned db = 0;
+                updates += update_voxel_slow(vox, lin, gx, dmul((double)((int64_t)y + vol.origin[1]), vs),
+                                             dmul((double)((int64_t)z + vol.origin[2]), vs), table, f, &db,
+                                             vol.color_dev);
+                dbad += db;
+            }
+        }
+        if (keep) {  // one atomic per brick and warp
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dbad += __shfl_xor_sync(0xffffffffu, dbad, o);
+            if (lane == 0 && dbad) {
+                atomicAdd(&vol.brick_state_dev[local], dbad);
+                mark_changed(changed, g);
+            }
+        }
+    }
+    if (stats) {
+        warp_count_add(&stats[TF_STAT_VOXEL_UPDATES], updates);
+        warp_count_add(&stats[TF_STAT_NOOP_UPDATES], nop);
+    }
+}
+
 // The exact reference arithmetic for every queued (undecided) voxel; one
 // thread per voxel, so the float64 path runs without divergence.
 __global__ void __launch_bounds__(256) exact_queue_kernel(
@@ -1235,7 +1356,7 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
     const unsigned long long *__restrict__ queue_count, const unsigned long long queue_cap,
     unsigned long long *__restrict__ stats, const ChangedList changed,
     const unsigned *__restrict__ active_count, const unsigned *__restrict__ free_count,
-    const unsigned long long total_bricks) {
+    const unsigned long long total_bricks, const unsigned long long *__restrict__ prep_stats) {
     const unsigned long long total = min(*queue_count, queue_cap);
     unsigned long long updates = 0;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -1270,6 +1391,10 @@ __global__ void __launch_bounds__(256) exact_queue_kernel(
             stats[TF_STAT_ACTIVE_BRICKS] += *active_count + *free_count;
             stats[TF_STAT_FREE_BRICKS] += *free_count;
             stats[TF_STAT_TOTAL_BRICKS] += total_bricks;
+            if (prep_stats)  // the screen's counters, counted in the prepare phase (atomics:
+                             // other blocks are adding to the same counters)
+                for (int k = 0; k < TF_STAT_COUNT; ++k)
+                    if (prep_stats[k]) atomicAdd(&stats[k], prep_stats[k]);
         }
     }
 }
@@ -1392,9 +1517,19 @@ TF_BOUNDS_READER(integrate)
 
 struct IntegrateLayout {
     size_t table_off, table32_off, mip_off, qmip_off, count_off, active_off, free_off, macro_off, queue_off,
-        changed_off, dirty_off, dirty_bytes, part_off, total;
+        changed_off, dirty_off, dirty_bytes, part_off, mask_off, mask_bytes, total;
     unsigned long long queue_cap;
 };
+
+// counters area (count_off): brick / free / macro / changed counts at 0, 8,
+// 16, 24, the queue count at 64; the prepare phase's screen counters
+// (TF_STAT_COUNT words) at kPrepStatsOff; zeroed by frame_prep_kernel
+constexpr size_t kPrepStatsOff = 256, kCountBytes = 512;
+
+// the screen's per-brick masks (128 bytes per general brick) are kept for
+// launches of up to 8 M bricks (1 GB); larger launches screen and update in
+// one kernel in the finish phase
+constexpr int64_t kMaskMaxBricks = 8ll << 20;
 
 // capacity of the exact-voxel queue; overflow is handled inline (still exact)
 constexpr unsigned long long kQueueCap = 8ull << 20;
@@ -1414,7 +1549,7 @@ static IntegrateLayout layout_for(int64_t total_bricks_max, const TfCamera *cam)
     L.qmip_off = off;
     off = align_up(off + (size_t)m.total * sizeof(unsigned), 256);
     L.count_off = off;
-    off = align_up(off + 256, 256);
+    off = align_up(off + kCountBytes, 256);
     L.active_off = off;
     off = align_up(off + (size_t)total_bricks_max * sizeof(uint32_t), 256);
     L.free_off = off;
@@ -1431,6 +1566,9 @@ static IntegrateLayout layout_for(int64_t total_bricks_max, const TfCamera *cam)
     off = align_up(off + L.dirty_bytes, 256);
     L.part_off = off;  // part classes of the general bricks, 4 bytes per active entry
     off = align_up(off + (size_t)total_bricks_max * 4, 256);
+    L.mask_off = off;  // screen masks of the general bricks, 32 words per active entry
+    L.mask_bytes = total_bricks_max <= kMaskMaxBricks ? (size_t)total_bricks_max * 128 : 0;
+    off = align_up(off + L.mask_bytes, 256);
     L.total = off;
     return L;
 }
@@ -1529,6 +1667,22 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
     unsigned long long *queue = (unsigned long long *)(ws + L.queue_off);
     uint32_t *active = (uint32_t *)(ws + L.active_off);
     uint8_t *part_class = (uint8_t *)(ws + L.part_off);
+    uint32_t *masks = (uint32_t *)(ws + L.mask_off);
+    unsigned long long *prep_stats = (unsigned long long *)(ws + L.count_off + kPrepStatsOff);
+    static const int use_split = [] {
+        // tuning knob (A/B): the screen of the general bricks in the prepare
+        // phase (brick_update_kernel<true> + brick_apply_kernel) instead of
+        // one kernel in the finish phase
+        const char *e = getenv("TFB200_SPLIT_SCREEN");
+        return e ? atoi(e) : 1;
+    }();
+    static const unsigned long long queue_cap_env = [] {
+        // test knob: a smaller exact queue, so the overflow paths (exact
+        // updates in place) run (tests/test_gpu_parity.py)
+        const char *e = getenv("TFB200_QUEUE_CAP");
+        return e ? strtoull(e, nullptr, 10) : ~0ull;
+    }();
+    const unsigned long long queue_cap = L.queue_cap < queue_cap_env ? L.queue_cap : queue_cap_env;
     static const int use_parts = [] {
         const char *e = getenv("TFB200_PARTS");  // tuning knob (A/B): part classes from the cull stage
         return e ? atoi(e) : 1;
@@ -1551,7 +1705,8 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
         dim3 pgrid((unsigned)((cam->width + kTile - 1) / kTile), (unsigned)((cam->height + kTile - 1) / kTile));
         frame_prep_kernel<<<pgrid, pblock, 0, stream>>>(depth, table, table32, mip, qmip, tau, m, cam->fx,
                                                         cam->fy, cam->cx, cam->cy, cam->width,
-                                                        cam->height, count, 32, (unsigned *)(ws + L.dirty_off),
+                                                        cam->height, count, (int)(kCountBytes / 4),
+                                                        (unsigned *)(ws + L.dirty_off),
                                                         (int64_t)(L.dirty_bytes / sizeof(unsigned)));
         rc = tf_check_launch("frame_prep_kernel");
         if (rc) return rc;
@@ -1625,9 +1780,14 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
                                   (unsigned *)(ws + L.dirty_off)};
         const int exact_only = (tf_debug_flags() & TF_DEBUG_EXACT_ONLY) ? 1 : 0;
         const int no_cull = (tf_debug_flags() & TF_DEBUG_NO_CULL) ? 1 : 0;
+        const bool split = use_split && L.mask_bytes > 0 && !exact_only;
+        static const int gen_grid = [] {
+            const char *e = getenv("TFB200_GEN_GRID");  // tuning knob (A/B): blocks per SM
+            return e ? atoi(e) : 9;
+        }();
         if (do_prep) {
             if (first > 0 &&  // chunk 0's were zeroed by frame_prep_kernel
-                (cudaMemsetAsync(count, 0, 128, stream) != cudaSuccess ||  // brick + queue counters
+                (cudaMemsetAsync(count, 0, kCountBytes, stream) != cudaSuccess ||  // counters
                  cudaMemsetAsync(ws + L.dirty_off, 0, L.dirty_bytes, stream) != cudaSuccess))
                 return tf_set_error(TF_ECUDA, "tf_integrate: memset failed");
             int64_t macros_total = 0;
@@ -1646,6 +1806,12 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
                 part_cull_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(vt, bt, f, m, mip, qmip, active, count,
                                                                        part_class, exact_only ? 0 : 1);
                 if ((rc = tf_check_launch("part_cull_kernel"))) return rc;
+            }
+            if (split) {  // the screen: masks + exact queue, no voxel touched
+                brick_update_kernel<true><<<(unsigned)(sms * gen_grid), 256, 0, stream>>>(
+                    vt, bt, f, table, table32, active, count, queue, qcount, queue_cap, fixed_point, prep_stats,
+                    changed, use_parts && !no_cull ? part_class : nullptr, masks);
+                if ((rc = tf_check_launch("brick_update_kernel<screen>"))) return rc;
             }
         }
         if (!do_fin) continue;
@@ -1681,20 +1847,24 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
             if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
             if (side) cudaEventRecord(side->join, fs);
             void *pg = tf_profile_begin(TF_PROF_INTEGRATE_GENERAL, stream);
-            static const int gen_grid = [] {
-                const char *e = getenv("TFB200_GEN_GRID");  // tuning knob (A/B): blocks per SM
-                return e ? atoi(e) : 9;
-            }();
-            brick_update_kernel<<<(unsigned)(sms * gen_grid), 256, 0, stream>>>(
-                vt, bt, f, table, table32, active, count, queue, qcount, L.queue_cap, fixed_point,
-                (unsigned long long *)stats, changed, use_parts && !no_cull ? part_class : nullptr);
-            tf_profile_end(pg, stream);
-            if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
+            if (split) {
+                brick_apply_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(
+                    vt, bt, f, table, active, count, masks, fixed_point, (unsigned long long *)stats, changed);
+                tf_profile_end(pg, stream);
+                if ((rc = tf_check_launch("brick_apply_kernel"))) return rc;
+            } else {
+                brick_update_kernel<false><<<(unsigned)(sms * gen_grid), 256, 0, stream>>>(
+                    vt, bt, f, table, table32, active, count, queue, qcount, queue_cap, fixed_point,
+                    (unsigned long long *)stats, changed, use_parts && !no_cull ? part_class : nullptr, nullptr);
+                tf_profile_end(pg, stream);
+                if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
+            }
             void *pe = tf_profile_begin(TF_PROF_INTEGRATE_EXACT, stream);
             exact_queue_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(vt, bt, f, table, queue, qcount,
-                                                                     L.queue_cap,
+                                                                     queue_cap,
                                                                      (unsigned long long *)stats, changed,
-                                                                     count, fcount, (unsigned long long)off);
+                                                                     count, fcount, (unsigned long long)off,
+                                                                     split ? prep_stats : nullptr);
             tf_profile_end(pe, stream);
             if ((rc = tf_check_launch("exact_queue_kernel"))) return rc;
             if (side) cudaStreamWaitEvent(stream, side->join, 0);

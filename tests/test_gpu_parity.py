@@ -771,3 +771,53 @@ def test_mid_march_handover_equals_exact_march(budget):
     coop = int(words[words.index("coop_rays") + 1])
     assert coop > 5000, r.stdout          # the hand-over really happened, many times
     assert int(words[words.index("cert_failures") + 1]) == 0
+
+
+_SCREEN_SCRIPT = r"""
+import torch, paper_1511_07106_b200 as tf
+from paper_1511_07106_b200 import _native as nat
+from paper_1511_07106_b200.synth import demo_scene
+intr = tf.RunConfig().intrinsics()
+spec = tf.init_grid(4.08, 1020, 510)
+params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+keys = [spec.keys[k] for k in (2, 5, 6)]          # the busiest tiles and a quiet one
+fast = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in keys]
+exact = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length) for k in keys]
+scene = demo_scene()
+lib = nat.load_library()
+sf = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
+se = torch.zeros(nat.STAT_COUNT, dtype=torch.int64, device="cuda")
+for pose in tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)[0:24:6]:
+    depth = scene.render_depth(pose, intr)
+    tf.integrate_volumes(fast, depth, pose, intr, params, sf)
+    lib.tf_set_debug_flags(nat.DEBUG_EXACT_ONLY)
+    tf.integrate_volumes(exact, depth, pose, intr, params, se)
+    lib.tf_set_debug_flags(0)
+    for a, b in zip(fast, exact):
+        assert torch.equal(a.voxels.view(torch.int32), b.voxels.view(torch.int32))
+    assert sf[nat.STAT_VOXEL_UPDATES].item() == se[nat.STAT_VOXEL_UPDATES].item()
+print("updates", sf[nat.STAT_VOXEL_UPDATES].item(), "exact_voxels", sf[nat.STAT_EXACT_VOXELS].item())
+"""
+
+
+@pytest.mark.parametrize("split,queue_cap", [("1", None), ("0", None), ("1", "2000"), ("0", "2000")])
+def test_screen_modes_and_queue_overflow_equal_exact(split, queue_cap):
+    """The general bricks' screen in the prepare phase (masks + brick_apply_kernel,
+    the default) and the one-kernel screen+update (TFB200_SPLIT_SCREEN=0) equal the
+    reference-order exact kernel bit for bit on config 3's busiest tiles — also with
+    the exact queue capped at 2000 entries, so the overflow paths (exact updates in
+    place; in the split screen, marked in the masks) carry most undecided voxels."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TFB200_SPLIT_SCREEN=split)
+    if queue_cap:
+        env["TFB200_QUEUE_CAP"] = queue_cap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _SCREEN_SCRIPT], env=env, cwd=root,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    words = r.stdout.split()
+    assert int(words[words.index("updates") + 1]) > 1_000_000
+    if queue_cap:  # far more undecided voxels than queue entries
+        assert int(words[words.index("exact_voxels") + 1]) > 10 * int(queue_cap)
