@@ -383,12 +383,23 @@ def run_ours(args) -> None:
                 "achieved_gbs": gbs, "frac": gbs / peak if peak else None}
     free_upd = int(st[nat.STAT_FREE_KERNEL_UPDATES])
     exact_upd = int(st[nat.STAT_EXACT_UPDATES])
+    screen_ms, screen_launches = prof["integrate_screen"]
     components = {
         "brick_free_kernel (certified free-space bricks, bandwidth-bound)": comp("integrate_free", free_upd),
-        "brick_update_kernel (general bricks: float32 screen + exact FP64 update)":
+        ("brick_apply_kernel (general bricks: the masked free-space updates)" if screen_launches else
+         "brick_update_kernel (general bricks: float32 screen + update in one kernel)"):
             comp("integrate_general", updates_local - free_upd - exact_upd),
         "exact_queue_kernel (near-surface band, reference arithmetic)": comp("integrate_exact", exact_upd),
     }
+    # the general bricks' screen runs in the prepare phase (no voxel traffic),
+    # on the integrator's side stream next to the previous frame's raycast
+    screen = ({"kernel": "brick_update_kernel<true> (float32 screen of the general bricks: masks + exact "
+                         "queue; reads the depth tables, not the voxels)",
+               "ms_per_launch": screen_ms / screen_launches, "launches": screen_launches,
+               "overlaps": "the previous frame's raycast (prepare phase, side stream)",
+               "frac_if_serial": (BYTES_PER_UPDATE * updates_local / max(upd_launches, 1)) /
+               ((upd_ms + screen_ms) / max(upd_launches, 1) / 1e3) / 1e9 / peak if peak else None}
+              if screen_launches else None)
 
     def per_frame(stat):
         return sum_over_ranks(int(st[stat])) / args.steps
@@ -410,8 +421,10 @@ def run_ours(args) -> None:
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
                      "traffic_source": traffic_src,
-                     "kernel": "integrate update bracket (brick_update_kernel + brick_free_kernel + "
-                               "exact_queue_kernel, TF_PROF_INTEGRATE_UPDATE)", "peak_source": peak_src,
+                     "kernel": "integrate update bracket (brick_apply_kernel + brick_free_kernel + "
+                               "exact_queue_kernel, TF_PROF_INTEGRATE_UPDATE): every voxel read/write of "
+                               "the frame's integration", "peak_source": peak_src,
+                     "screen": screen,
                      "bytes_per_update": BYTES_PER_UPDATE,
                      "launches": upd_launches, "kernel_ms_per_launch": upd_ms / max(upd_launches, 1),
                      "updates_per_launch": updates_local / max(upd_launches, 1),
@@ -423,6 +436,7 @@ def run_ours(args) -> None:
                              "evaluated_samples_per_launch": evaluated / max(ray_launches, 1),
                              "kernel_ms_per_launch": ray_ms / max(ray_launches, 1)},
         "breakdown_ms_per_step": {"integrate_update_kernel": upd_ms / args.steps,
+                                  "integrate_screen_overlapped": screen_ms / args.steps,
                                   "integrate_total": int_ms / args.steps,
                                   "raycast": ray_ms / args.steps},
         "integrate": {"noop_updates_per_frame": per_frame_int(nat.STAT_NOOP_UPDATES),

@@ -120,7 +120,7 @@ const char *tf_last_error(void);
  * 0 = integration voxel-update kernel, 1 = whole tf_integrate, 2 = raycast. */
 enum { TF_PROF_INTEGRATE_UPDATE = 0, TF_PROF_INTEGRATE_ALL = 1, TF_PROF_RAYCAST = 2,
        TF_PROF_INTEGRATE_FREE = 3, TF_PROF_INTEGRATE_GENERAL = 4, TF_PROF_INTEGRATE_EXACT = 5,
-       TF_PROF_RAYCAST_COOP = 6, TF_PROF_KINDS = 7 };
+       TF_PROF_RAYCAST_COOP = 6, TF_PROF_INTEGRATE_SCREEN = 7, TF_PROF_KINDS = 8 };
 uint64_t tf_launch_count(void);
 /* Debug: index violations counted by a bounds-checked build of the library
  * (compiled with -DTF_BOUNDS_CHECK: guarded loads / stores are skipped and

@@ -44,7 +44,7 @@ DEBUG_EXACT_ONLY = 2
 DEBUG_NO_FIXEDPOINT = 4
 DEBUG_LANE0_ONLY = 8
 DEBUG_COOP_ALL = 16
-PROF_INTEGRATE_UPDATE, PROF_INTEGRATE_ALL, PROF_RAYCAST, PROF_KINDS = 0, 1, 2, 7
+PROF_INTEGRATE_UPDATE, PROF_INTEGRATE_ALL, PROF_RAYCAST, PROF_KINDS = 0, 1, 2, 8
 
 
 def profile_read() -> dict:
@@ -53,7 +53,7 @@ def profile_read() -> dict:
     cnt = (ctypes.c_int64 * PROF_KINDS)()
     check(lib().tf_profile_read(ms, cnt, PROF_KINDS), "tf_profile_read")
     names = ("integrate_update", "integrate_all", "raycast", "integrate_free", "integrate_general",
-             "integrate_exact", "raycast_coop")
+             "integrate_exact", "raycast_coop", "integrate_screen")
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(names)}
 
 # TF_STAT_* slots (tfb200.h)

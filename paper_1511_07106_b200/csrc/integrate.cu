@@ -1808,9 +1808,11 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
                 if ((rc = tf_check_launch("part_cull_kernel"))) return rc;
             }
             if (split) {  // the screen: masks + exact queue, no voxel touched
+                void *ps = tf_profile_begin(TF_PROF_INTEGRATE_SCREEN, stream);
                 brick_update_kernel<true><<<(unsigned)(sms * gen_grid), 256, 0, stream>>>(
                     vt, bt, f, table, table32, active, count, queue, qcount, queue_cap, fixed_point, prep_stats,
                     changed, use_parts && !no_cull ? part_class : nullptr, masks);
+                tf_profile_end(ps, stream);
                 if ((rc = tf_check_launch("brick_update_kernel<screen>"))) return rc;
             }
         }

@@ -18,7 +18,7 @@ import json,sys
 d=json.loads(open('gpurun_out/ab_${tag}_${r}.json').read().strip().splitlines()[-1])
 b=d['breakdown_ms_per_step']
 e=d.get('e2e',{}).get('frames_per_s',0.0)
-print('%-28s fps %7.1f  e2e %7.1f  step %.4f  upd %.4f  int %.4f  ray %.4f  coop %.4f' % ('$spec', d['frames_per_s'], e, d['ms_per_step'], b['integrate_update_kernel'], b['integrate_total'], b['raycast'], d['raycast']['coop_pass_ms_per_frame']))
+print('%-28s fps %7.1f  e2e %7.1f  step %.4f  upd %.4f  scr %.4f  int %.4f  ray %.4f  coop %.4f' % ('$spec', d['frames_per_s'], e, d['ms_per_step'], b['integrate_update_kernel'], b.get('integrate_screen_overlapped', 0.0), b['integrate_total'], b['raycast'], d['raycast']['coop_pass_ms_per_frame']))
 "
   done
 done
