@@ -357,7 +357,7 @@ def run_ours(args) -> None:
     achieved = (BYTES_PER_UPDATE * updates_local / max(upd_launches, 1)) / (
         upd_ms / max(upd_launches, 1) / 1e3) / 1e9 if upd_ms > 0 else 0.0
     traffic = ray_traffic = traffic_src = None
-    tfile = ROOT / "profiles" / "traffic_r02.json"
+    tfile = ROOT / "profiles" / "traffic_r02b.json"
     if tfile.exists():
         try:
             tj = json.loads(tfile.read_text())
@@ -897,6 +897,10 @@ def run_scaling_projection(args, torch, nat, barrier, cpu: bool) -> dict:
         costs = (c[:, 0] * 4.0 + c[:, 1]).cpu().tolist()
         owners = balanced_owners(costs, n)
         shares = [[tiles[u] for u in range(len(units)) if owners[u] == r] for r in range(n)]
+        for i in warm_frames(args.warmup):  # untimed: each share's first raycast sizes its scratch
+            for r in range(n):
+                tf.integrate_volumes(shares[r], frames[i], poses[i], intr, params)
+                tf.raycast_volumes(shares[r], poses[i], intr, tf.RayMap.empty(intr), params)
         torch.cuda.synchronize()
         per_frame = []
         per_rank = [0.0] * n

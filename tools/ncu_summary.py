@@ -85,13 +85,25 @@ def main():
         for d in rs:
             by.setdefault(d["kernel"], []).append(d.get("dram_read", 0) + d.get("dram_write", 0))
         avg = {k: sum(v) / len(v) for k, v in by.items()}
+        def short(k):
+            return k.split("::")[-1].replace("void ", "")
+
+        def screen(k):  # the prepare-phase screen (no voxel traffic; not in the bracket)
+            return any(f"brick_update_kernel<{t}>" in short(k) for t in ("true", "(bool)1", "1"))
+
         bracket = sum(v for k, v in avg.items()
-                      if k.split("::")[-1] in ("brick_update_kernel", "brick_free_kernel", "exact_queue_kernel"))
+                      if short(k).split("<")[0] in ("brick_update_kernel", "brick_apply_kernel",
+                                                    "brick_free_kernel", "exact_queue_kernel") and not screen(k))
         ray = next((v for k, v in avg.items() if "raycast_kernel" in k), None)
+        scr = next((v for k, v in avg.items() if screen(k)), None)
+        frame_updates = float(sys.argv[sys.argv.index("--updates") + 1]) if "--updates" in sys.argv else None
         json.dump({"source": f"ncu --set full capture {rep.split('/')[-1]}, one timed-region launch per kernel "
-                             "(frame 0 of the orbit, 36.9 M updates: 590 MB algorithmic)",
+                             "(frame 0 of the orbit)",
                    "integrate_update_bracket_bytes_per_launch": bracket, "raycast_bytes_per_launch": ray,
-                   "per_kernel_dram_bytes": avg}, open(out, "w"), indent=1)
+                   "screen_bytes_per_launch": scr, "per_kernel_dram_bytes": avg,
+                   "captured_frame_updates": frame_updates,
+                   "integrate_update_bracket_bytes_per_update": bracket / frame_updates if frame_updates else None},
+                  open(out, "w"), indent=1)
         return
     seen = set()
     for d in rs:
