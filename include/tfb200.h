@@ -179,10 +179,11 @@ int tf_integrate_rgb(const TfVolume *vols, int nvol, const double *depth_dev,
 
 /* tf_integrate_rgb in two halves, so the first can run on another stream
  * while the previous frame's raycast still occupies the GPU:
- * tf_integrate_prepare builds the per-frame pixel tables, depth mips and the
- * culled brick lists in the workspace (it reads the depth frame and the
- * volumes' geometry, never their voxels or summaries); tf_integrate_finish
- * then runs the voxel updates and the summary upkeep.  finish must follow a
+ * tf_integrate_prepare builds the per-frame pixel tables, depth mips, the
+ * culled brick lists and the float32 screen of the general bricks' voxels
+ * (free-space masks and the exact-voxel queue) in the workspace (it reads the
+ * depth frame and the volumes' geometry, never their voxels or summaries);
+ * tf_integrate_finish then runs the voxel updates and the summary upkeep.  finish must follow a
  * prepare with the same arguments on the same workspace (the caller orders
  * the two streams), and no other integrate call may use that workspace in
  * between.  With more volumes than one launch holds, prepare does nothing
