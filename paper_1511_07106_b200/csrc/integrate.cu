@@ -1842,15 +1842,38 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
                 cudaEventRecord(side->fork, stream);
                 cudaStreamWaitEvent(side->stream, side->fork, 0);
             }
+            static const int free_grid = [] {  // tuning knob (A/B): blocks per SM
+                const char *e = getenv("TFB200_FREE_GRID");
+                return e ? atoi(e) : 4;
+            }();
+            static const int apply_grid = [] {  // tuning knob (A/B): blocks per SM
+                const char *e = getenv("TFB200_APPLY_GRID");
+                return e ? atoi(e) : 4;
+            }();
+            static const int exact_first = [] {  // tuning knob (A/B): exact queue before the masked updates
+                const char *e = getenv("TFB200_EXACT_FIRST");
+                return e ? atoi(e) : 0;
+            }();
+            auto launch_exact = [&]() -> int {
+                void *pe = tf_profile_begin(TF_PROF_INTEGRATE_EXACT, stream);
+                exact_queue_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(vt, bt, f, table, queue, qcount,
+                                                                         queue_cap,
+                                                                         (unsigned long long *)stats, changed,
+                                                                         count, fcount, (unsigned long long)off,
+                                                                         split ? prep_stats : nullptr);
+                tf_profile_end(pe, stream);
+                return tf_check_launch("exact_queue_kernel");
+            };
+            if (split && exact_first && (rc = launch_exact())) return rc;
             void *pf = tf_profile_begin(TF_PROF_INTEGRATE_FREE, fs);
-            brick_free_kernel<<<(unsigned)sms * 4, 256, 0, fs>>>(vt, bt, f, active_free, fcount, fixed_point,
+            brick_free_kernel<<<(unsigned)(sms * free_grid), 256, 0, fs>>>(vt, bt, f, active_free, fcount, fixed_point,
                                                                 (unsigned long long *)stats, changed);
             tf_profile_end(pf, fs);
             if ((rc = tf_check_launch("brick_free_kernel"))) return rc;
             if (side) cudaEventRecord(side->join, fs);
             void *pg = tf_profile_begin(TF_PROF_INTEGRATE_GENERAL, stream);
             if (split) {
-                brick_apply_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(
+                brick_apply_kernel<<<(unsigned)(sms * apply_grid), 256, 0, stream>>>(
                     vt, bt, f, table, active, count, masks, fixed_point, (unsigned long long *)stats, changed);
                 tf_profile_end(pg, stream);
                 if ((rc = tf_check_launch("brick_apply_kernel"))) return rc;
@@ -1861,14 +1884,7 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
                 tf_profile_end(pg, stream);
                 if ((rc = tf_check_launch("brick_update_kernel"))) return rc;
             }
-            void *pe = tf_profile_begin(TF_PROF_INTEGRATE_EXACT, stream);
-            exact_queue_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(vt, bt, f, table, queue, qcount,
-                                                                     queue_cap,
-                                                                     (unsigned long long *)stats, changed,
-                                                                     count, fcount, (unsigned long long)off,
-                                                                     split ? prep_stats : nullptr);
-            tf_profile_end(pe, stream);
-            if ((rc = tf_check_launch("exact_queue_kernel"))) return rc;
+            if (!(split && exact_first) && (rc = launch_exact())) return rc;
             if (side) cudaStreamWaitEvent(stream, side->join, 0);
         }
         tf_profile_end(prof, stream);
