@@ -138,6 +138,10 @@ void tf_debug_ray_clock_buffer(int64_t *buffer_dev);
  * through the table-driven correctly rounded division of the running-mean
  * update vs. IEEE division; returns the number of mismatches (-1 on error). */
 int64_t tf_debug_weight_division_check(int64_t n, uint64_t seed);
+/* Test hook (synchronous): n random and adversarial (volume, ray) pairs
+ * through the raycast's division-free ray/box interval vs. the reference's
+ * (_kernels.py:299-348); returns the number of mismatches (-1 on error). */
+int64_t tf_debug_ray_interval_check(int64_t n, uint64_t seed);
 void tf_profile_enable(int on);
 int tf_profile_read(double *ms_by_kind, int64_t *launches_by_kind, int nkinds);
 

@@ -36,6 +36,7 @@ struct RayGeom {
     int lane0_only;      // TF_DEBUG_LANE0_ONLY: only lane 0 of each warp traces (timing studies)
     float good_t;        // brick-summary threshold for this tau
     int uniform_vs;      // every volume of the launch has the same voxel size
+    double inv_vs;       // 1 / that voxel size (uniform_vs only)
     int row_mod, row_rem;  // trace only the block rows ty with ty % row_mod == row_rem
 };
 
@@ -219,6 +220,52 @@ __device__ __forceinline__ bool ray_interval(const TfVolume &vol, const double o
     j0 = (int64_t)ceil(ddiv(t_lo, vs));
     if (j0 < 0) j0 = 0;
     j_end = (int64_t)floor(ddiv(t_hi, vs));
+    return true;
+}
+
+// ray_interval with its eight divisions replaced by products with 1/d (per
+// ray) and 1/vs: every candidate t is then within 2^-50 |t| of the reference's
+// quotient, so t_lo / t_hi are within E = 2^-46 max|t| of the reference's (max
+// and min are 1-Lipschitz), and j0 / j_end = ceil / floor of t / vs within
+// (E + 2^-52 |t|) / vs.  When the hit-or-miss test or a ceil / floor is closer
+// than that to flipping, the exact ray_interval decides.  Same (j0, j_end) and
+// result as ray_interval, bit for bit.
+__device__ __forceinline__ bool ray_interval_fast(const TfVolume &vol, const double o[3], const double d[3],
+                                                  const double inv_d[3], const double inv_vs, int64_t &j0,
+                                                  int64_t &j_end) {
+    double t_lo = 0.0, t_hi = 1.0e30, tmax = 0.0;
+    const double vs = vol.voxel_size;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double mn = dmul((double)vol.origin[a], vs);
+        const double mx = dmul((double)(vol.origin[a] + vol.n - 1), vs);
+        if (fabs(d[a]) < 1.0e-15) {
+            if (o[a] < mn || o[a] > mx) return false;
+        } else {
+            double t1 = dmul(dsub(mn, o[a]), inv_d[a]);
+            double t2 = dmul(dsub(mx, o[a]), inv_d[a]);
+            if (t1 > t2) {
+                const double tmp = t1;
+                t1 = t2;
+                t2 = tmp;
+            }
+            tmax = fmax(tmax, fmax(fabs(t1), fabs(t2)));
+            if (t1 > t_lo) t_lo = t1;
+            if (t2 < t_hi) t_hi = t2;
+        }
+    }
+    const double e = 0x1p-46 * tmax;
+    if (t_lo - t_hi > 2.0 * e) return false;                   // certainly a miss
+    bool sure = t_hi - t_lo > 2.0 * e;                         // certainly not a miss
+    const double xl = dmul(t_lo, inv_vs), xh = dmul(t_hi, inv_vs);
+    const double ml = (e + 0x1p-52 * fabs(t_lo)) * inv_vs * 2.0, mh = (e + 0x1p-52 * fabs(t_hi)) * inv_vs * 2.0;
+    const double cl = ceil(xl), fh = floor(xh);
+    // t_lo == 0 exactly iff the reference's is (the candidates' signs are exact)
+    sure = sure && (t_lo == 0.0 || (cl - xl > ml && xl - (cl - 1.0) > ml)) && xh - fh > mh && fh + 1.0 - xh > mh;
+    if (!sure) return ray_interval(vol, o, d, j0, j_end);
+    j0 = (int64_t)cl;
+    if (j0 < 0) j0 = 0;
+    j_end = (int64_t)fh;
     return true;
 }
 
@@ -793,9 +840,12 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
                 }
                 n = bi = 0;
                 flags = 0;
+                double inv_d[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) inv_d[c] = fabs(d[c]) < 1.0e-15 ? 0.0 : ddiv(1.0, d[c]);
                 for (int u = 0; u < vt.count; ++u) {
                     int64_t a, b;
-                    if (!ray_interval(vt.vol[u], o, d, a, b)) continue;
+                    if (!ray_interval_fast(vt.vol[u], o, d, inv_d, g.inv_vs, a, b)) continue;
                     if (b >= (1ll << 26) || a >= (1ll << 30)) {  // decided on the first build
                         flags = 2;
                         break;
@@ -1470,6 +1520,72 @@ static unsigned *rescue_buffer(cudaStream_t stream, int64_t words) {
     return b->ptr;
 }
 
+namespace tf {
+// test hook: random and adversarial (volume, ray) pairs through
+// ray_interval_fast vs ray_interval; counts result / (j0, j_end) mismatches
+// and how often the fast path fell back (out[0], out[1])
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+    x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 27; x *= 0x94D049BB133111EBull; x ^= x >> 33;
+    return x;
+}
+__device__ __forceinline__ double unif(unsigned long long &st) {  // [0, 1)
+    st = mix64(st + 0x9E3779B97F4A7C15ull);
+    return (double)(st >> 11) * 0x1p-53;
+}
+__global__ void ray_interval_check_kernel(int64_t n, unsigned long long seed, unsigned long long *out) {
+    const double vss[5] = {0.004, 0.001, 0.0029296875, 0.1, 0.0117647058823529};
+    unsigned long long bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long st = seed ^ (0xD1B54A32D192ED03ull * (unsigned long long)(i + 1));
+        TfVolume vol{};
+        vol.voxel_size = vss[(int)(unif(st) * 5.0)];
+        vol.n = 2 + (int64_t)(unif(st) * 600.0);
+        for (int a = 0; a < 3; ++a) vol.origin[a] = (int64_t)(unif(st) * 1200.0) - 600;
+        double d[3], o[3];
+        double nn = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            d[a] = unif(st) * 2.0 - 1.0;
+            const double r = unif(st);
+            if (r < 0.1) d[a] = 0.0;
+            else if (r < 0.13) d[a] = 1e-16;
+            nn += d[a] * d[a];
+        }
+        if (nn == 0.0) d[0] = nn = 1.0;
+        nn = sqrt(nn);
+        for (int a = 0; a < 3; ++a) d[a] /= nn;
+        const double vs = vol.voxel_size, lo0 = (double)vol.origin[0] * vs;
+        for (int a = 0; a < 3; ++a)
+            o[a] = ((double)vol.origin[a] + (unif(st) * 1.6 - 0.3) * (double)vol.n) * vs;
+        const double r = unif(st);
+        if (r < 0.2) {  // on a face of the box
+            const int a = (int)(unif(st) * 3.0);
+            o[a] = dmul((double)(vol.origin[a] + (unif(st) < 0.5 ? 0 : vol.n - 1)), vs);
+        } else if (r < 0.4 && fabs(d[0]) > 0.1) {  // the x-entry t an integer multiple of vs
+            const double k = floor(unif(st) * 400.0) + 1.0;
+            o[0] = dsub(lo0, dmul(dmul(k, vs), d[0]));
+        }
+        int64_t a0 = -7, a1 = -7, b0 = -7, b1 = -7;
+        double inv_d[3];
+        for (int c = 0; c < 3; ++c) inv_d[c] = fabs(d[c]) < 1.0e-15 ? 0.0 : ddiv(1.0, d[c]);
+        const bool h0 = ray_interval(vol, o, d, a0, a1);
+        const bool h1 = ray_interval_fast(vol, o, d, inv_d, 1.0 / vs, b0, b1);
+        bad += h0 != h1 || (h0 && (a0 != b0 || a1 != b1));
+    }
+    if (bad) atomicAdd(&out[0], bad);
+}
+}  // namespace tf
+
+extern "C" int64_t tf_debug_ray_interval_check(int64_t n, uint64_t seed) {
+    unsigned long long *d = nullptr, h = 0;
+    if (n <= 0) return 0;
+    if (cudaMalloc(&d, sizeof(h)) != cudaSuccess) return -1;
+    cudaMemset(d, 0, sizeof(h));
+    tf::ray_interval_check_kernel<<<1184, 256>>>(n, seed, d);
+    const bool ok = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(d);
+    return ok ? (int64_t)h : -1;
+}
+
 extern "C" size_t tf_raycast_workspace_size(int nvol, const TfCamera *cam) {
     if (!cam || nvol <= 0 || cam->width <= 0 || cam->height <= 0) return 0;
     const int per = nvol < TFB200_MAX_VOLUMES_PER_LAUNCH ? nvol : TFB200_MAX_VOLUMES_PER_LAUNCH;
@@ -1537,6 +1653,7 @@ static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, dou
     g.row_mod = row_mod;
     g.row_rem = row_rem;
     g.uniform_vs = 1;
+    g.inv_vs = 1.0 / vols[0].voxel_size;
     for (int v = 1; v < nvol; ++v)
         if (vols[v].voxel_size != vols[0].voxel_size) g.uniform_vs = 0;
     for (int first = 0; first < nvol; first += TFB200_MAX_VOLUMES_PER_LAUNCH) {

@@ -236,6 +236,17 @@ def test_table_division_is_ieee():
         assert lib.tf_debug_weight_division_check(100_000_000, seed) == 0
 
 
+def test_division_free_ray_interval_is_exact():
+    """The raycast's ray/box interval from products with 1/d and 1/vs (with its
+    certified margins and exact fallback) equals the reference's divisions
+    (_kernels.py:299-348) on 400 M random and adversarial (volume, ray) pairs:
+    origins on box faces, zero and 1e-16 direction components, entry t an
+    integer multiple of the voxel size."""
+    lib = nat.load_library()
+    for seed in (1, 2, 3, 4):
+        assert lib.tf_debug_ray_interval_check(100_000_000, seed) == 0
+
+
 @pytest.mark.parametrize("sw,max_w", [(0.75, 128.0), (1.0, 5.0), (2.5, 10.0)])
 def test_fractional_and_capped_weights(sw, max_w):
     """Non-integral running-mean denominators (the division falls back from
