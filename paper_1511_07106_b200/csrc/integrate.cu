@@ -1477,11 +1477,20 @@ __global__ void __launch_bounds__(256) super_flags_kernel(const __grid_constant_
         const unsigned char *bf = vol.brick_flags_dev;
         unsigned acc = 3u;
         // 64 (y, z) rows of 8 x bricks; lane handles rows lane and lane + 32
+        const int64_t bx0 = sx * 8;
+        const bool whole = (nb & 7) == 0 && ((uintptr_t)bf & 7) == 0;  // full aligned rows: one load each
+#pragma unroll
         for (int r = lane; r < 64; r += 32) {
             const int64_t by = sy * 8 + (r & 7), bz = sz * 8 + (r >> 3);
             if (by >= nb || bz >= nb) continue;
-            const int64_t bx0 = sx * 8;
-            for (int k = 0; k < 8 && bx0 + k < nb; ++k) acc &= bf[(bz * nb + by) * nb + bx0 + k];
+            const int64_t row = (bz * nb + by) * nb + bx0;
+            if (whole) {
+                const unsigned long long q = *reinterpret_cast<const unsigned long long *>(bf + row);
+                const unsigned lo = (unsigned)q & (unsigned)(q >> 32);
+                acc &= lo & (lo >> 8) & (lo >> 16) & (lo >> 24);
+            } else {
+                for (int k = 0; k < 8 && bx0 + k < nb; ++k) acc &= bf[row + k];
+            }
         }
         acc = __reduce_and_sync(0xffffffffu, acc);
         if (lane == 0) vol.brick_flags_dev[nb * nb * nb + sb] = (unsigned char)acc;
