@@ -98,9 +98,9 @@ if not os.environ.get("RAY_LANE0") and allc[..., 5].any():
     T = en0.max()
     grid = np.linspace(0, T, 400)
     active = np.array([((st0 <= t) & (en0 > t)).sum() for t in grid])
-    print("kernel %.0f us; warps active (of 2368 slots): " % T +
+    print("kernel %.0f us; warps active (of 2960 slots): " % T +
           " ".join("%d%%:%d" % (p, active[int(p / 100 * 399)]) for p in (10, 30, 50, 70, 80, 90, 95, 99)))
     dur = en0 - st0
     late = np.argsort(en0)[-5:]
     print("last warps to finish: start/dur us", [(round(st0[i]), round(dur[i])) for i in late])
-    print("time with < 50%% of slots busy: %.0f us" % ((active < 1184).mean() * T))
+    print("time with < 50%% of slots busy: %.0f us" % ((active < 1480).mean() * T))
