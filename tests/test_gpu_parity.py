@@ -832,3 +832,17 @@ def test_screen_modes_and_queue_overflow_equal_exact(split, queue_cap):
     assert int(words[words.index("updates") + 1]) > 1_000_000
     if queue_cap:  # far more undecided voxels than queue entries
         assert int(words[words.index("exact_voxels") + 1]) > 10 * int(queue_cap)
+
+
+def test_tma_staged_free_bricks_equal_exact():
+    """The TMA-staged free-space kernel (TFB200_FREE_TMA=1: 8x8x8 tensor-map box loads
+    into shared memory, mbarrier double buffering) gives the same voxels as the
+    reference-order exact kernel on config 3's busiest tiles."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TFB200_FREE_TMA="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _SCREEN_SCRIPT], env=env, cwd=root,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
