@@ -233,6 +233,15 @@ int tf_raycast_rows(const TfVolume *vols, int nvol, const TfCamera *cam, double 
                     double *dist_dev, double *vert_dev, double *norm_dev, void *workspace_dev,
                     size_t workspace_bytes, int row_mod, int row_rem, uint64_t *stats_dev,
                     void *stream);
+/* tf_raycast_rows with flags.  TF_RAYCAST_FRESH: the map is taken as empty
+ * (RayMap.empty / tf_raymap_reset) without reading it — every pixel is
+ * written, so no reset launch is needed first; requires row_mod == 1. */
+#define TF_RAYCAST_FRESH 1
+int tf_raycast_ex(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
+                  int64_t coarse_step, const double r_wc[9], const double cam_center[3],
+                  double *dist_dev, double *vert_dev, double *norm_dev, void *workspace_dev,
+                  size_t workspace_bytes, int row_mod, int row_rem, int flags, uint64_t *stats_dev,
+                  void *stream);
 
 /* ---- trilinear_sample (tsdf.py:147-153 / _kernels._sample :28-68) for
  * `npoints` world points (f64 [N][3]); writes value and validity per point. */

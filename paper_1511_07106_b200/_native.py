@@ -44,6 +44,7 @@ DEBUG_EXACT_ONLY = 2
 DEBUG_NO_FIXEDPOINT = 4
 DEBUG_LANE0_ONLY = 8
 DEBUG_COOP_ALL = 16
+RAYCAST_FRESH = 1  # tf_raycast_ex flag (tfb200.h TF_RAYCAST_FRESH)
 PROF_INTEGRATE_UPDATE, PROF_INTEGRATE_ALL, PROF_RAYCAST, PROF_KINDS = 0, 1, 2, 8
 
 
@@ -106,6 +107,8 @@ _SIGNATURES = {
                                _c_p, _c_sz, _c_p, _c_p]),
     "tf_raycast_rows": (_c_int, [_VOL, _c_int, _CAM, _c_d, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
                                  _c_p, _c_sz, _c_int, _c_int, _c_p, _c_p]),
+    "tf_raycast_ex": (_c_int, [_VOL, _c_int, _CAM, _c_d, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
+                               _c_p, _c_sz, _c_int, _c_int, _c_int, _c_p, _c_p]),
     "tf_trilinear_sample": (_c_int, [_VOL, _c_p, _c_i64, _c_p, _c_p, _c_p]),
     "tf_good_threshold": (ctypes.c_float, [_c_d]),
     "tf_brick_summary": (_c_int, [_VOL, _c_p]),

@@ -38,6 +38,7 @@ struct RayGeom {
     int uniform_vs;      // every volume of the launch has the same voxel size
     double inv_vs;       // 1 / that voxel size (uniform_vs only)
     int row_mod, row_rem;  // trace only the block rows ty with ty % row_mod == row_rem
+    int fresh;           // the map starts empty: not read, every traced pixel written
 };
 
 struct Hit {
@@ -802,14 +803,16 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
     unsigned long long samples = 0, hits = 0, exact_samples = 0;
     if (px < g.width && py < g.height && !(g.lane0_only && lane != 0)) {
         const int64_t p = py * g.width + px;
-        Hit best;
-        best.t = out_dist[p];
-        best.hx = out_vert[3 * p + 0];
-        best.hy = out_vert[3 * p + 1];
-        best.hz = out_vert[3 * p + 2];
-        best.nx = out_norm[3 * p + 0];
-        best.ny = out_norm[3 * p + 1];
-        best.nz = out_norm[3 * p + 2];
+        Hit best{INFINITY, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // RayMap.empty's record
+        if (!g.fresh) {
+            best.t = out_dist[p];
+            best.hx = out_vert[3 * p + 0];
+            best.hy = out_vert[3 * p + 1];
+            best.hz = out_vert[3 * p + 2];
+            best.nx = out_norm[3 * p + 0];
+            best.ny = out_norm[3 * p + 1];
+            best.nz = out_norm[3 * p + 2];
+        }
         double d[3];
         ray_direction(g, px, py, d);
         const double o[3] = {g.cam.v[0], g.cam.v[1], g.cam.v[2]};
@@ -895,11 +898,15 @@ __global__ void __launch_bounds__(kBX * kBY, kMinBlocks) raycast_kernel(
         }
         if (aborted) {
             // finished by raycast_coop_kernel (one warp per ray); nothing of
-            // this partial march is kept
+            // this partial march is kept (a fresh map gets the empty record,
+            // which the cooperative pass merges into)
             samples = exact_samples = 0;
             rescue[atomicAdd(rescue_count, 1u)] = (unsigned)p;
-        } else if (changed && TF_IN_BOUNDS(p < g.width * g.height)) {
-            hits = 1;
+            changed = false;
+            if (g.fresh) best = Hit{INFINITY, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        }
+        if ((changed || g.fresh) && TF_IN_BOUNDS(p < g.width * g.height)) {
+            hits = changed ? 1 : 0;
             out_dist[p] = best.t;
             out_vert[3 * p + 0] = best.hx;
             out_vert[3 * p + 1] = best.hy;
@@ -1592,10 +1599,14 @@ extern "C" size_t tf_raycast_workspace_size(int nvol, const TfCamera *cam) {
     return (size_t)rescue_words(cam->width * cam->height, per) * sizeof(unsigned);
 }
 
+__global__ void raymap_reset_kernel(double *__restrict__ dist, double *__restrict__ vert,
+                                    double *__restrict__ norm, int64_t npix);
+
 static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
                         int64_t coarse_step, const double r_wc[9], const double cam_center[3],
                         double *dist, double *vert, double *norm, void *workspace,
-                        size_t workspace_bytes, uint64_t *stats, void *stream_, int row_mod, int row_rem);
+                        size_t workspace_bytes, uint64_t *stats, void *stream_, int row_mod, int row_rem,
+                        int flags = 0);
 
 extern "C" int tf_raycast_ws(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
                              int64_t coarse_step, const double r_wc[9], const double cam_center[3],
@@ -1618,6 +1629,20 @@ extern "C" int tf_raycast_rows(const TfVolume *vols, int nvol, const TfCamera *c
                         workspace, workspace_bytes, stats, stream_, row_mod, row_rem);
 }
 
+extern "C" int tf_raycast_ex(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
+                             int64_t coarse_step, const double r_wc[9], const double cam_center[3],
+                             double *dist, double *vert, double *norm, void *workspace,
+                             size_t workspace_bytes, int row_mod, int row_rem, int flags, uint64_t *stats,
+                             void *stream_) {
+    if (!workspace && nvol > 0) return tf_set_error(TF_EINVAL, "tf_raycast_ex: null workspace");
+    if (row_mod < 1 || row_rem < 0 || row_rem >= row_mod)
+        return tf_set_error(TF_EINVAL, "tf_raycast_ex: bad row subset");
+    if ((flags & TF_RAYCAST_FRESH) && row_mod != 1)
+        return tf_set_error(TF_EINVAL, "tf_raycast_ex: TF_RAYCAST_FRESH traces every row");
+    return raycast_impl(vols, nvol, cam, tau, coarse_step, r_wc, cam_center, dist, vert, norm, workspace,
+                        workspace_bytes, stats, stream_, row_mod, row_rem, flags);
+}
+
 extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
                           int64_t coarse_step, const double r_wc[9], const double cam_center[3],
                           double *dist, double *vert, double *norm, uint64_t *stats,
@@ -1629,7 +1654,8 @@ extern "C" int tf_raycast(const TfVolume *vols, int nvol, const TfCamera *cam, d
 static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, double tau,
                         int64_t coarse_step, const double r_wc[9], const double cam_center[3],
                         double *dist, double *vert, double *norm, void *workspace,
-                        size_t workspace_bytes, uint64_t *stats, void *stream_, int row_mod, int row_rem) {
+                        size_t workspace_bytes, uint64_t *stats, void *stream_, int row_mod, int row_rem,
+                        int flags) {
     cudaStream_t stream = (cudaStream_t)stream_;
     if (nvol == 0) return TF_OK;
     if (!vols || nvol < 0 || !cam || !r_wc || !cam_center || !dist || !vert || !norm)
@@ -1664,6 +1690,14 @@ static int raycast_impl(const TfVolume *vols, int nvol, const TfCamera *cam, dou
             vt.vol[v] = vols[first + v];
             if (!vt.vol[v].voxels_dev || vt.vol[v].n < 2 || !(vt.vol[v].voxel_size > 0.0))
                 return tf_set_error(TF_EINVAL, "tf_raycast: bad volume %d", first + v);
+        }
+        // TF_RAYCAST_FRESH: the first launch writes every pixel (the map's
+        // previous contents are never read); later chunks merge into it
+        g.fresh = (flags & TF_RAYCAST_FRESH) && first == 0 ? 1 : 0;
+        if (g.fresh && g.lane0_only) {  // (a debug mode that traces a subset of the pixels)
+            const int64_t npix = cam->width * cam->height;
+            raymap_reset_kernel<<<(unsigned)((3 * npix + 255) / 256), 256, 0, stream>>>(dist, vert, norm, npix);
+            g.fresh = 0;
         }
         void *prof = tf_profile_begin(TF_PROF_RAYCAST, stream);
         static const int shape = [] {

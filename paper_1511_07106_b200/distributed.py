@@ -634,9 +634,8 @@ class ShardedFusion:
         self.frames += 1
         self._integrator(self.tiles, depth, pose, self.intr, self.params, self.stats, color=color,
                          depth_ready=depth_ready)
-        self.partial.reset()
         raycast_volumes(self.tiles, pose, self.intr, self.partial, self.params, self.stats,
-                        rows=(self.rank, self.world) if self.replicated else None)
+                        rows=(self.rank, self.world) if self.replicated else None, fresh=True)
         if self.world == 1:
             self.model, self.partial = self.partial, self.model
             return self.model

@@ -539,11 +539,15 @@ def coarse_step(params: FusionParams, voxel_size: float) -> int:
 
 def raycast_volumes(volumes: Sequence[TsdfSubvolume], pose: Pose, intr: CameraIntrinsics,
                     raymap: RayMap, params: FusionParams,
-                    stats: torch.Tensor | None = None, rows: tuple[int, int] | None = None) -> RayMap:
+                    stats: torch.Tensor | None = None, rows: tuple[int, int] | None = None,
+                    fresh: bool = False) -> RayMap:
     """Render every volume into ``raymap`` with one fused launch.
 
     ``rows`` = (rank, world): trace only the 8-pixel block rows b with
     b % world == rank (tf_raycast_rows; the rest of the map is untouched).
+    ``fresh``: render into an emptied map (``raymap.reset()`` + render) — the
+    first launch writes every pixel instead of merging (TF_RAYCAST_FRESH),
+    so the reset costs no launch.
 
     Volumes are grouped by coarse stride (the reference computes it per
     volume, tsdf.py:207); the merge is order-free so grouping is exact.
@@ -552,8 +556,12 @@ def raycast_volumes(volumes: Sequence[TsdfSubvolume], pose: Pose, intr: CameraIn
     if tuple(raymap.shape) != (intr.height, intr.width):
         raise ValueError("raymap size does not match intrinsics")
     if not volumes:
-        return raymap
-    raymap._device_read()
+        return raymap.reset() if fresh else raymap
+    if fresh and rows is not None:
+        raymap.reset()
+        fresh = False
+    if not fresh:
+        raymap._device_read()
     for v in volumes:
         v._device_read()
     groups: dict[int, list[TsdfSubvolume]] = {}
@@ -570,7 +578,14 @@ def raycast_volumes(volumes: Sequence[TsdfSubvolume], pose: Pose, intr: CameraIn
         # the cooperative pass's scratch: one workspace per stream (launches on
         # a stream are ordered; two streams never share one)
         ws = nat.workspace.get(L.tf_raycast_workspace_size(len(vols), cam), f"raycast{stream}")
-        if rows is None:
+        if fresh:  # the first group writes every pixel; later groups merge into it
+            nat.check(L.tf_raycast_ex(arr, len(vols), cam, float(params.truncation), int(coarse),
+                                      r, c, nat.ptr(raymap.distance_dev),
+                                      nat.ptr(raymap.vertices_dev), nat.ptr(raymap.normals_dev),
+                                      nat.ptr(ws), ws.numel(), 1, 0, nat.RAYCAST_FRESH, nat.ptr(st), stream),
+                      "tf_raycast_ex")
+            fresh = False
+        elif rows is None:
             nat.check(L.tf_raycast_ws(arr, len(vols), cam, float(params.truncation), int(coarse),
                                       r, c, nat.ptr(raymap.distance_dev),
                                       nat.ptr(raymap.vertices_dev), nat.ptr(raymap.normals_dev),

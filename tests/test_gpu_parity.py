@@ -846,3 +846,35 @@ def test_tma_staged_free_bricks_equal_exact():
     r = subprocess.run([sys.executable, "-c", _SCREEN_SCRIPT], env=env, cwd=root,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
+
+
+def test_fresh_raycast_ignores_previous_map():
+    """raycast_volumes(fresh=True) on a map full of stale hits (TF_RAYCAST_FRESH: the
+    map is never read, every pixel written) == reset() + raycast, bit for bit —
+    including the pixels finished by the cooperative pass (tiny per-warp budget
+    via DEBUG_COOP_ALL on a second frame)."""
+    intr = tf.RunConfig().intrinsics()
+    spec = tf.init_grid(4.08, 1020, 510)
+    params = tf.FusionParams.for_voxel_size(spec.voxel_size)
+    tiles = [tf.TsdfSubvolume.empty(k, spec.voxels_per_side, spec.subvolume_side_length)
+             for k in spec.keys]
+    scene = demo_scene()
+    poses = tf.orbit_trajectory((0.0, 0.0, 1.5), 1.5, 64)
+    for pose in poses[:6]:
+        tf.integrate_volumes(tiles, scene.render_depth(pose, intr), pose, intr, params)
+    lib = nat.load_library()
+    try:
+        for flag in (0, nat.DEBUG_COOP_ALL):
+            lib.tf_set_debug_flags(flag)
+            want = tf.RayMap.empty(intr)
+            tf.raycast_volumes(tiles, poses[5], intr, want, params)
+            stale = tf.RayMap.empty(intr)
+            tf.raycast_volumes(tiles, poses[30], intr, stale, params)   # another view's hits
+            stale.distance_dev[::7] = 0.25                               # and some nonsense
+            stale.normals_dev[::5] = 3.0
+            tf.raycast_volumes(tiles, poses[5], intr, stale, params, fresh=True)
+            assert torch.equal(stale.distance_dev, want.distance_dev)
+            assert torch.equal(stale.vertices_dev, want.vertices_dev)
+            assert torch.equal(stale.normals_dev, want.normals_dev)
+    finally:
+        lib.tf_set_debug_flags(0)
