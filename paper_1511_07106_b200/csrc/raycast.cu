@@ -603,9 +603,11 @@ __device__ bool march_fast(const FastRay &fr, const RayRef &er, int j, const int
     // observed, bit1 free space, 0 = ordinary)
     int region_end = -1, region_kind = 0, region_start = 0;
     unsigned last_s = kNoDecision;  // decisions of march point last_j
+    unsigned tick = 0;
     while (j <= j_end) {
         // the warp ran past its budget: hand the ray to the cooperative pass
-        if (clock64() > deadline) {
+        // (the clock is read every 8th step: the budget is a heuristic)
+        if ((++tick & 7u) == 0u && clock64() > deadline) {
             aborted = true;
             return false;
         }
