@@ -811,17 +811,20 @@ print("updates", sf[nat.STAT_VOXEL_UPDATES].item(), "exact_voxels", sf[nat.STAT_
 """
 
 
-@pytest.mark.parametrize("split,queue_cap", [("1", None), ("0", None), ("1", "2000"), ("0", "2000")])
-def test_screen_modes_and_queue_overflow_equal_exact(split, queue_cap):
+@pytest.mark.parametrize("split,queue_cap,stream", [("1", None, "2"), ("0", None, "2"), ("1", "2000", "2"),
+                                                    ("0", "2000", "2"), ("1", None, "0"), ("1", "2000", "1")])
+def test_screen_modes_and_queue_overflow_equal_exact(split, queue_cap, stream):
     """The general bricks' screen in the prepare phase (masks + brick_apply_kernel,
     the default) and the one-kernel screen+update (TFB200_SPLIT_SCREEN=0) equal the
     reference-order exact kernel bit for bit on config 3's busiest tiles — also with
     the exact queue capped at 2000 entries, so the overflow paths (exact updates in
-    place; in the split screen, marked in the masks) carry most undecided voxels."""
+    place; in the split screen, marked in the masks) carry most undecided voxels.
+    ``stream``: TFB200_FUSED_STREAM (2: free-space + masked updates in one kernel, the
+    exact band beside it; 1: the exact band after it; 0: separate free-space kernel)."""
     import os
     import subprocess
     import sys
-    env = dict(os.environ, TFB200_SPLIT_SCREEN=split)
+    env = dict(os.environ, TFB200_SPLIT_SCREEN=split, TFB200_FUSED_STREAM=stream)
     if queue_cap:
         env["TFB200_QUEUE_CAP"] = queue_cap
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -841,7 +844,7 @@ def test_tma_staged_free_bricks_equal_exact():
     import os
     import subprocess
     import sys
-    env = dict(os.environ, TFB200_FREE_TMA="1")
+    env = dict(os.environ, TFB200_FREE_TMA="1", TFB200_FUSED_STREAM="0")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", _SCREEN_SCRIPT], env=env, cwd=root,
                        capture_output=True, text=True, timeout=900)
