@@ -384,13 +384,21 @@ def run_ours(args) -> None:
     free_upd = int(st[nat.STAT_FREE_KERNEL_UPDATES])
     exact_upd = int(st[nat.STAT_EXACT_UPDATES])
     screen_ms, screen_launches = prof["integrate_screen"]
-    components = {
-        "brick_free_kernel (certified free-space bricks, bandwidth-bound)": comp("integrate_free", free_upd),
-        ("brick_apply_kernel (general bricks: the masked free-space updates)" if screen_launches else
-         "brick_update_kernel (general bricks: float32 screen + update in one kernel)"):
-            comp("integrate_general", updates_local - free_upd - exact_upd),
-        "exact_queue_kernel (near-surface band, reference arithmetic)": comp("integrate_exact", exact_upd),
-    }
+    if prof["integrate_free"][1] == 0:  # free-space bricks inside the streaming kernel (the default)
+        components = {
+            "brick_apply_kernel (certified free-space bricks + the general bricks' masked updates, one "
+            "streaming kernel)": comp("integrate_general", updates_local - exact_upd),
+            "exact_queue_kernel (near-surface band, reference arithmetic; beside it on the side stream, "
+            "timed only when it runs in stream order)": comp("integrate_exact", exact_upd),
+        }
+    else:
+        components = {
+            "brick_free_kernel (certified free-space bricks, bandwidth-bound)": comp("integrate_free", free_upd),
+            ("brick_apply_kernel (general bricks: the masked free-space updates)" if screen_launches else
+             "brick_update_kernel (general bricks: float32 screen + update in one kernel)"):
+                comp("integrate_general", updates_local - free_upd - exact_upd),
+            "exact_queue_kernel (near-surface band, reference arithmetic)": comp("integrate_exact", exact_upd),
+        }
     # the general bricks' screen runs in the prepare phase (no voxel traffic),
     # on the integrator's side stream next to the previous frame's raycast
     screen = ({"kernel": "brick_update_kernel<true> (float32 screen of the general bricks: masks + exact "
@@ -421,9 +429,9 @@ def run_ours(args) -> None:
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
                      "traffic_source": traffic_src,
-                     "kernel": "integrate update bracket (brick_apply_kernel + brick_free_kernel + "
-                               "exact_queue_kernel, TF_PROF_INTEGRATE_UPDATE): every voxel read/write of "
-                               "the frame's integration", "peak_source": peak_src,
+                     "kernel": "integrate update bracket (brick_apply_kernel: free-space bricks + masked "
+                               "updates, with exact_queue_kernel beside it; TF_PROF_INTEGRATE_UPDATE): every "
+                               "voxel read/write of the frame's integration", "peak_source": peak_src,
                      "screen": screen,
                      "bytes_per_update": BYTES_PER_UPDATE,
                      "launches": upd_launches, "kernel_ms_per_launch": upd_ms / max(upd_launches, 1),
