@@ -357,7 +357,7 @@ def run_ours(args) -> None:
     achieved = (BYTES_PER_UPDATE * updates_local / max(upd_launches, 1)) / (
         upd_ms / max(upd_launches, 1) / 1e3) / 1e9 if upd_ms > 0 else 0.0
     traffic = ray_traffic = traffic_src = None
-    tfile = ROOT / "profiles" / "traffic_r02c.json"
+    tfile = ROOT / "profiles" / "traffic_r02d.json"
     if tfile.exists():
         try:
             tj = json.loads(tfile.read_text())
