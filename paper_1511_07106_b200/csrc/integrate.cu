@@ -2100,7 +2100,7 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
                 return e ? atoi(e) : 0;
             }();
             void *pf = tf_profile_begin(TF_PROF_INTEGRATE_FREE, fs);
-            static BrickMaps maps;  // host staging of the kernel parameter (under the side-stream lock)
+            BrickMaps maps;  // the kernel parameter (copied at launch)
             bool maps_ok = free_tma != 0;
             if (maps_ok) {
                 using Encode = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
@@ -2131,10 +2131,10 @@ static int integrate_impl(const TfVolume *vols, int nvol, const double *depth, c
             }
             if (maps_ok) {
                 constexpr int smem = kFreeTmaWarps * 2 * 4096;
-                static bool attr = cudaFuncSetAttribute(brick_free_tma_kernel,
-                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                        smem) == cudaSuccess;
-                if (!attr) return tf_set_error(TF_ECUDA, "tf_integrate: shared memory attribute");
+                // (per device: set on every call)
+                if (cudaFuncSetAttribute(brick_free_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+                    cudaSuccess)
+                    return tf_set_error(TF_ECUDA, "tf_integrate: shared memory attribute");
                 brick_free_tma_kernel<<<(unsigned)(sms * 3), 256, smem, fs>>>(
                     vt, bt, f, maps, active_free, fcount, fixed_point, (unsigned long long *)stats, changed);
             } else
