@@ -142,6 +142,10 @@ int64_t tf_debug_weight_division_check(int64_t n, uint64_t seed);
  * through the raycast's division-free ray/box interval vs. the reference's
  * (_kernels.py:299-348); returns the number of mismatches (-1 on error). */
 int64_t tf_debug_ray_interval_check(int64_t n, uint64_t seed);
+/* Test hook (synchronous): the raycast's certified quotient by the voxel size
+ * (reciprocal + correction, proved or else IEEE) vs. IEEE division on n random
+ * and adversarial pairs; returns the number of mismatches (-1 on error). */
+int64_t tf_debug_div_check(int64_t n, uint64_t seed);
 void tf_profile_enable(int on);
 int tf_profile_read(double *ms_by_kind, int64_t *launches_by_kind, int nkinds);
 

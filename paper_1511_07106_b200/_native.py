@@ -88,6 +88,7 @@ _SIGNATURES = {
                               _c_d, _c_p, ctypes.c_size_t, _c_p, _c_p]),
     "tf_debug_weight_division_check": (_c_i64, [_c_i64, ctypes.c_uint64]),
     "tf_debug_ray_interval_check": (_c_i64, [_c_i64, ctypes.c_uint64]),
+    "tf_debug_div_check": (_c_i64, [_c_i64, ctypes.c_uint64]),
     "tf_profile_enable": (None, [_c_int]),
     "tf_profile_read": (_c_int, [_c_p, _c_p, _c_int]),
     "tf_integrate_workspace_size": (_c_sz, [_VOL, _c_int, _CAM]),

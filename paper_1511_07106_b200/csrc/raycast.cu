@@ -109,14 +109,35 @@ struct Ray {
     double htx, hty, htz, vs;
     double ox, oy, oz, dx, dy, dz;
     unsigned long long samples;
+    double ivs;  // an approximation of 1 / vs for div_vs (0: always the IEEE division)
 };
+
+// RN(x / b), the IEEE quotient, from an approximate reciprocal: a
+// Newton-corrected q1 is returned only when it is PROVED to be the correctly
+// rounded quotient — its remainder x - q1 b (one FMA; exact whenever q1 is
+// within one ulp, i.e. whenever the test can pass) is below half an ulp of q1
+// times |b|, and q1 is not a power of two (where the spacing below halves).
+// Anything else — ties, huge / tiny magnitudes, a poor reciprocal — takes
+// the IEEE division.  So the result is ddiv(x, b) bit for bit, always.
+__device__ __forceinline__ double div_vs(double x, double b, double inv) {
+    const double ax = fabs(x);
+    if (ax >= 0x1p-900 && ax <= 0x1p900) {
+        const double q0 = dmul(x, inv);
+        const double q1 = __fma_rn(__fma_rn(-q0, b, x), inv, q0);
+        const double r1 = __fma_rn(-q1, b, x);
+        const long long bits = __double_as_longlong(q1);
+        const double half_ulp = __longlong_as_double(bits & 0x7FF0000000000000ll) * 0x1p-53;
+        if ((bits & 0x000FFFFFFFFFFFFFll) != 0 && fabs(r1) < half_ulp * fabs(b)) return q1;
+    }
+    return ddiv(x, b);
+}
 
 // fine lattice point k in local voxel coordinates (:164-167, :357-359)
 __device__ __noinline__ bool sample_at(Ray &r, int64_t k, double &value) {
     const double tk = dmul((double)k, r.vs);
-    const double kx = dsub(ddiv(dadd(r.ox, dmul(tk, r.dx)), r.vs), r.htx);
-    const double ky = dsub(ddiv(dadd(r.oy, dmul(tk, r.dy)), r.vs), r.hty);
-    const double kz = dsub(ddiv(dadd(r.oz, dmul(tk, r.dz)), r.vs), r.htz);
+    const double kx = dsub(div_vs(dadd(r.ox, dmul(tk, r.dx)), r.vs, r.ivs), r.htx);
+    const double ky = dsub(div_vs(dadd(r.oy, dmul(tk, r.dy)), r.vs, r.ivs), r.hty);
+    const double kz = dsub(div_vs(dadd(r.oz, dmul(tk, r.dz)), r.vs, r.ivs), r.htz);
     r.samples++;
     return sample(r.vox, r.n, kx, ky, kz, value);
 }
@@ -138,9 +159,9 @@ __device__ __noinline__ bool accept_crossing(const Ray &r, int64_t k, double sp_
     const double hx = dadd(r.ox, dmul(tstar, r.dx));
     const double hy = dadd(r.oy, dmul(tstar, r.dy));
     const double hz = dadd(r.oz, dmul(tstar, r.dz));
-    const double qx = dsub(ddiv(hx, r.vs), r.htx);
-    const double qy = dsub(ddiv(hy, r.vs), r.hty);
-    const double qz = dsub(ddiv(hz, r.vs), r.htz);
+    const double qx = dsub(div_vs(hx, r.vs, r.ivs), r.htx);
+    const double qy = dsub(div_vs(hy, r.vs, r.ivs), r.hty);
+    const double qz = dsub(div_vs(hz, r.vs, r.ivs), r.htz);
     const double fcx = floor(qx), fcy = floor(qy), fcz = floor(qz);
     if (!(fcx >= 0.0 && fcy >= 0.0 && fcz >= 0.0 && fcx <= hi && fcy <= hi && fcz <= hi)) return false;
     Cell cell;
@@ -395,6 +416,7 @@ __device__ __forceinline__ Ray make_ray(const FastRay &fr, const RayRef &rr) {
     r.hty = (double)rr.vol->origin[1];
     r.htz = (double)rr.vol->origin[2];
     r.vs = rr.vol->voxel_size;
+    r.ivs = rr.g->uniform_vs ? rr.g->inv_vs : 0.0;
     r.ox = rr.g->cam.v[0];
     r.oy = rr.g->cam.v[1];
     r.oz = rr.g->cam.v[2];
@@ -757,6 +779,7 @@ __device__ __forceinline__ bool setup_volume(const RayGeom &g, const TfVolume &v
     r.hty = (double)vol.origin[1];
     r.htz = (double)vol.origin[2];
     r.vs = vol.voxel_size;
+    r.ivs = g.uniform_vs ? g.inv_vs : 0.0;
     r.ox = o[0];
     r.oy = o[1];
     r.oz = o[2];
@@ -1582,7 +1605,46 @@ __global__ void ray_interval_check_kernel(int64_t n, unsigned long long seed, un
     }
     if (bad) atomicAdd(&out[0], bad);
 }
+// test hook: div_vs against the IEEE division on random and adversarial
+// (x, b) pairs, with the exact reciprocal and with perturbed ones
+__global__ void div_check_kernel(int64_t n, unsigned long long seed, unsigned long long *out) {
+    const double vss[6] = {0.004, 0.001, 0.0029296875, 0.1, 0.0117647058823529, 3.0};
+    unsigned long long bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long st = seed ^ (0xA0761D6478BD642Full * (unsigned long long)(i + 1));
+        const double r = unif(st);
+        double b = r < 0.5 ? vss[(int)(unif(st) * 6.0)] : ldexp(1.0 + unif(st), (int)(unif(st) * 40.0) - 20);
+        double x;
+        const double c = unif(st);
+        if (c < 0.3) {  // near-multiples of b: quotients at or next to integers and halves
+            x = dmul((double)((int64_t)(unif(st) * 4096.0) - 2048) * 0.5, b);
+            if (unif(st) < 0.5)  // a neighbouring double (one ulp up or down in magnitude)
+                x = __longlong_as_double(__double_as_longlong(x) + (unif(st) < 0.5 ? 1 : -1));
+        } else {
+            x = ldexp(1.0 + unif(st), (int)(unif(st) * 60.0) - 40);
+            if (unif(st) < 0.5) x = -x;
+        }
+        const double exact_inv = 1.0 / b;
+        const double p = unif(st);
+        const double inv = p < 0.6 ? exact_inv
+                                   : (p < 0.8 ? __longlong_as_double(__double_as_longlong(exact_inv) + 1)
+                                              : exact_inv * (1.0 + 1e-9));
+        bad += __double_as_longlong(div_vs(x, b, inv)) != __double_as_longlong(__ddiv_rn(x, b));
+    }
+    if (bad) atomicAdd(out, bad);
+}
 }  // namespace tf
+
+extern "C" int64_t tf_debug_div_check(int64_t n, uint64_t seed) {
+    unsigned long long *d = nullptr, h = 0;
+    if (n <= 0) return 0;
+    if (cudaMalloc(&d, sizeof(h)) != cudaSuccess) return -1;
+    cudaMemset(d, 0, sizeof(h));
+    tf::div_check_kernel<<<1184, 256>>>(n, seed, d);
+    const bool ok = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(d);
+    return ok ? (int64_t)h : -1;
+}
 
 extern "C" int64_t tf_debug_ray_interval_check(int64_t n, uint64_t seed) {
     unsigned long long *d = nullptr, h = 0;

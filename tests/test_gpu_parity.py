@@ -236,6 +236,17 @@ def test_table_division_is_ieee():
         assert lib.tf_debug_weight_division_check(100_000_000, seed) == 0
 
 
+def test_certified_voxel_size_division_is_ieee():
+    """The raycast's exact path divides by the voxel size with a reciprocal, one
+    Newton correction and an exact remainder test that falls back to the IEEE
+    division whenever it cannot prove the quotient correctly rounded: equal to
+    __ddiv_rn bit for bit on 400 M random and adversarial pairs (multiples and
+    half-multiples of b and their neighbours, perturbed reciprocals)."""
+    lib = nat.load_library()
+    for seed in (1, 2, 3, 4):
+        assert lib.tf_debug_div_check(100_000_000, seed) == 0
+
+
 def test_division_free_ray_interval_is_exact():
     """The raycast's ray/box interval from products with 1/d and 1/vs (with its
     certified margins and exact fallback) equals the reference's divisions
